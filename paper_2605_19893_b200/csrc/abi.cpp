@@ -1,0 +1,434 @@
+// abi.cpp -- the C-ABI boundary (include/specsv_b200/nsa_verify.h): argument
+// validation with the reference's rules, workspace layout, TMA descriptor
+// encoding and the launch sequence of one verify call.
+//
+// One verify call == the per-layer hot section of run_target_pass
+// (src/engine.cpp:175-278):  REFRESH -> routing launches (route.cu) + fused
+// attend launch (attend.cu);  REUSE -> fused attend launch only, reading the
+// source layer's index sets and clamping them per query in-kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "attend.h"
+#include "policy.h"
+#include "specsv_b200/nsa_verify.h"
+
+namespace specsv_b200 {
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+specsv_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return SPECSV_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SPECSV_EINVAL;
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(SPECSV_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static const EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// bf16 [rows][hkv][dh] as a 3-D map (dh, hkv, rows) with 64x1x64 SWIZZLE_128B boxes
+void encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int64_t hkv, int64_t dh) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)hkv, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)(dh * 2), (cuuint64_t)(hkv * dh * 2)};
+  const cuuint32_t box[3] = {64, 1, 64};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled failed");
+}
+
+int splits_for_device() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = std::min(dev, 63);
+  int s = cache[dev].load();
+  if (s == 0) {
+    s = attend_max_cluster(16);
+    cache[dev].store(s);
+  }
+  return s;
+}
+
+struct Layout {
+  size_t attend_off = 0, attend_bytes = 0;
+  size_t E_off = 0, TM_off = 0, TD_off = 0, mass_off = 0;
+  size_t total = 0;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int qc_size_for(const specsv_nsa_config& c) {
+  const int G = static_cast<int>(c.n_q_heads / c.n_kv_heads);
+  return std::min(64 / G, kMaxChunkQ);
+}
+
+Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows, int splits) {
+  Layout L;
+  const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
+  L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
+  const int64_t maxblk = max_rows >= c.l ? (max_rows - c.l) / c.d + 1 : 0;
+  const int64_t m_pad = align_up(std::max<int64_t>(maxblk, 1), kRouteTile);
+  const int64_t ntiles = m_pad / kRouteTile;
+  size_t off = align_up(L.attend_bytes, 256);
+  L.E_off = off;
+  off = align_up(off + (size_t)nq * c.n_q_heads * m_pad * 8, 256);
+  L.TM_off = off;
+  off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
+  L.TD_off = off;
+  off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
+  L.mass_off = off;
+  off = align_up(off + (size_t)nq * m_pad * 8, 256);
+  L.total = off;
+  return L;
+}
+
+void validate_args(const specsv_nsa_config& c, const specsv_layer_kv& kv,
+                   const specsv_verify_args& a) {
+  if (a.n_queries < 1 || a.n_queries > kMaxQueries)
+    throw Error(SPECSV_EUNSUPPORTED, "n_queries must be in [1, 65] (gamma <= 64)");
+  if (a.group_size < 1) throw Error(SPECSV_EINVAL, "partition_groups: C must be >= 1");
+  if (a.mode != SPECSV_MODE_EXACT && a.mode != SPECSV_MODE_APPROX)
+    throw Error(SPECSV_EINVAL, "mode must be EXACT or APPROX");
+  if (a.role != SPECSV_ROLE_REFRESH && a.role != SPECSV_ROLE_REUSE)
+    throw Error(SPECSV_EINVAL, "role must be REFRESH or REUSE");
+  if (a.pos == nullptr || a.q == nullptr || a.gates == nullptr || a.out == nullptr ||
+      a.idx == nullptr || a.idx_count == nullptr || a.idx_forced == nullptr)
+    throw Error(SPECSV_EINVAL, "null argument");
+  if (kv.k == nullptr || kv.v == nullptr || kv.ck == nullptr || kv.ck16 == nullptr ||
+      kv.cv == nullptr)
+    throw Error(SPECSV_EINVAL, "null cache pointer");
+  if (kv.rows < 1) throw Error(SPECSV_EINVAL, "rows must be >= 1 (the pending root is committed)");
+  if (kv.rows > (int64_t)kMaxUnionWords * 32 * c.l_sel)
+    throw Error(SPECSV_EUNSUPPORTED, "context exceeds this build's selection-block bitmap");
+  const int64_t want_blocks = kv.rows >= c.l ? (kv.rows - c.l) / c.d + 1 : 0;
+  if (kv.blocks < 0 || kv.blocks > want_blocks)
+    throw Error(SPECSV_EINVAL, "compressed block count exceeds the committed rows");
+  const int32_t gamma = a.n_queries - 1;
+  if (gamma > 0 && (a.tree_k == nullptr || a.tree_v == nullptr || a.tree_mask == nullptr ||
+                    a.mask_words < (gamma + 63) / 64))
+    throw Error(SPECSV_EINVAL, "draft rows / tree mask missing");
+  if (a.pos[0] < 0 || a.pos[0] > kv.rows - 1)
+    throw Error(SPECSV_EINVAL, "root position must be a committed row");
+  for (int32_t q = 1; q < a.n_queries; ++q) {
+    if (a.pos[q] <= a.pos[0]) throw Error(SPECSV_EINVAL, "draft positions must follow the root");
+    if (a.pos[q] - a.pos[0] > c.routing_lag)  // engine.cpp:479-480
+      throw Error(SPECSV_EINVAL, "step: draft depth exceeds routing lag");
+  }
+  if (selection_block_count(c, routing_visible_len(c, a.pos[a.n_queries - 1])) > kMaxAvail)
+    throw Error(SPECSV_EUNSUPPORTED, "too many selection blocks for the Top-n kernel");
+}
+
+RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv& kv,
+                              const specsv_verify_args& a, const Layout& L, char* ws,
+                              const std::vector<int32_t>& routed) {
+  RouteParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.q = a.q;
+  p.ck = kv.ck;
+  p.idx = a.idx;
+  p.idx_count = a.idx_count;
+  p.idx_forced = a.idx_forced;
+  p.nr = static_cast<int32_t>(routed.size());
+  p.nq = a.n_queries;
+  p.Hq = (int32_t)c.n_q_heads;
+  p.Hkv = (int32_t)c.n_kv_heads;
+  p.G = (int32_t)(c.n_q_heads / c.n_kv_heads);
+  p.dh = (int32_t)c.d_head;
+  p.n = (int32_t)c.n;
+  p.l = (int32_t)c.l;
+  p.d = (int32_t)c.d;
+  p.l_sel = (int32_t)c.l_sel;
+  p.blocks = (int32_t)kv.blocks;
+  p.scale = 1.0 / std::sqrt(static_cast<double>(c.d_head));
+  int64_t mmax = 0;
+  std::vector<bool> is_routed(a.n_queries, false);
+  for (size_t s = 0; s < routed.size(); ++s) {
+    const int32_t q = routed[s];
+    is_routed[q] = true;
+    const int64_t vis = routing_visible_len(c, a.pos[q]);
+    p.slot_q[s] = q;
+    p.slot_mvis[s] = (int32_t)visible_blocks(c, kv.blocks, vis);
+    p.slot_avail[s] = (int32_t)selection_block_count(c, vis);
+    mmax = std::max<int64_t>(mmax, p.slot_mvis[s]);
+  }
+  for (int32_t q = 0; q < a.n_queries; ++q)
+    if (!is_routed[q]) p.unrouted[p.n_unrouted++] = q;
+  p.m_pad = (int32_t)align_up((size_t)mmax, kRouteTile);
+  p.ntiles = p.m_pad / kRouteTile;
+  p.E = reinterpret_cast<double*>(ws + L.E_off);
+  p.TM = reinterpret_cast<double*>(ws + L.TM_off);
+  p.TD = reinterpret_cast<double*>(ws + L.TD_off);
+  p.mass = reinterpret_cast<double*>(ws + L.mass_off);
+  return p;
+}
+
+void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+               void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const Layout L = layout_for(c, a.n_queries, kv.rows, splits_for_device());
+  if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
+  const auto routed = routed_queries(a.n_queries, a.pos, a.group_size, a.mode);
+  RouteParams p = make_route_params(c, kv, a, L, static_cast<char*>(ws), routed);
+  cuda_check(launch_route(p, stream, true), "route launch");
+}
+
+void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+                void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const int S = splits_for_device();
+  const Layout L = layout_for(c, a.n_queries, kv.rows, S);
+  if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
+  AttendParams p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t H = c.n_kv_heads, dh = c.d_head;
+  const int32_t gamma = a.n_queries - 1;
+  encode_rows_map(&p.tm_k, kv.k, kv.rows, H, dh);
+  encode_rows_map(&p.tm_v, kv.v, kv.rows, H, dh);
+  encode_rows_map(&p.tm_ck, kv.ck16, kv.blocks, H, dh);
+  encode_rows_map(&p.tm_cv, kv.cv, kv.blocks, H, dh);
+  encode_rows_map(&p.tm_tk, gamma > 0 ? a.tree_k : kv.k, std::max(gamma, 1), H, dh);
+  encode_rows_map(&p.tm_tv, gamma > 0 ? a.tree_v : kv.v, std::max(gamma, 1), H, dh);
+  p.q = a.q;
+  p.gates = a.gates;
+  p.out = a.out;
+  p.idx = a.idx;
+  p.idx_count = a.idx_count;
+  p.ws = static_cast<float*>(ws);
+  const int qc = qc_size_for(c);
+  const int nchunks = (a.n_queries + qc - 1) / qc;
+  p.ws_o_offset = (int64_t)nchunks * H * S * (3 * 64 * 2);
+  p.nq = a.n_queries;
+  p.gamma = gamma;
+  p.Hq = (int32_t)c.n_q_heads;
+  p.Hkv = (int32_t)H;
+  p.G = (int32_t)(c.n_q_heads / H);
+  p.n_sel = (int32_t)c.n;
+  p.rows = (int32_t)kv.rows;
+  p.blocks = (int32_t)kv.blocks;
+  p.l = (int32_t)c.l;
+  p.d = (int32_t)c.d;
+  p.l_sel = (int32_t)c.l_sel;
+  p.w = (int32_t)c.w;
+  p.lag = (int32_t)c.routing_lag;
+  p.qc_size = qc;
+  p.n_splits = S;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)dh));
+  const auto src = source_rows(c, a.n_queries, a.pos, a.group_size, a.mode);
+  for (int32_t q = 0; q < a.n_queries; ++q) {
+    p.pos[q] = (int32_t)a.pos[q];
+    p.src_row[q] = src[q];
+    p.tree_mask[q] = (q < gamma) ? a.tree_mask[(int64_t)q * a.mask_words] : 0ull;
+  }
+  cuda_check(launch_attend(p, nchunks, stream), "attend launch");
+}
+
+}  // namespace
+}  // namespace specsv_b200
+
+using namespace specsv_b200;
+
+extern "C" {
+
+int32_t specsv_abi_version(void) { return SPECSV_ABI_VERSION; }
+
+const char* specsv_last_error(void) { return g_last_error.c_str(); }
+
+specsv_status specsv_validate_config(const specsv_nsa_config* cfg) {
+  return guarded([&] {
+    if (cfg == nullptr) throw Error(SPECSV_EINVAL, "null config");
+    validate_config(*cfg);
+    check_build_limits(*cfg);
+  });
+}
+
+size_t specsv_verify_workspace_size(const specsv_nsa_config* cfg, int32_t n_queries,
+                                    int64_t max_rows) {
+  if (cfg == nullptr || n_queries < 1) return 0;
+  return layout_for(*cfg, n_queries, max_rows, splits_for_device()).total;
+}
+
+specsv_status specsv_nsa_route(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
+                               const specsv_verify_args* args, void* ws, size_t ws_bytes,
+                               specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !kv || !args) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    check_build_limits(*cfg);
+    validate_args(*cfg, *kv, *args);
+    run_route(*cfg, *kv, *args, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+specsv_status specsv_nsa_attend_fused(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
+                                      const specsv_verify_args* args, void* ws, size_t ws_bytes,
+                                      specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !kv || !args) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    check_build_limits(*cfg);
+    validate_args(*cfg, *kv, *args);
+    run_attend(*cfg, *kv, *args, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+specsv_status specsv_nsa_verify(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
+                                const specsv_verify_args* args, void* ws, size_t ws_bytes,
+                                specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !kv || !args) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    check_build_limits(*cfg);
+    validate_args(*cfg, *kv, *args);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (args->role == SPECSV_ROLE_REFRESH) run_route(*cfg, *kv, *args, ws, ws_bytes, s);
+    run_attend(*cfg, *kv, *args, ws, ws_bytes, s);
+  });
+}
+
+specsv_status specsv_nsa_verify_batched(const specsv_nsa_config* cfg, const specsv_layer_kv* kvs,
+                                        const specsv_verify_args* args, int32_t batch, void* ws,
+                                        size_t ws_bytes, specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !kvs || !args || batch < 0) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    check_build_limits(*cfg);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    for (int32_t b = 0; b < batch; ++b) {
+      validate_args(*cfg, kvs[b], args[b]);
+      if (args[b].role == SPECSV_ROLE_REFRESH) run_route(*cfg, kvs[b], args[b], ws, ws_bytes, s);
+      run_attend(*cfg, kvs[b], args[b], ws, ws_bytes, s);
+    }
+  });
+}
+
+specsv_status specsv_nsa_scores(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
+                                const specsv_verify_args* args, int32_t query, double* scores,
+                                void* ws, size_t ws_bytes, specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !kv || !args || !scores) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    check_build_limits(*cfg);
+    validate_args(*cfg, *kv, *args);
+    if (query < 0 || query >= args->n_queries) throw Error(SPECSV_EINVAL, "query out of range");
+    const Layout L = layout_for(*cfg, args->n_queries, kv->rows, splits_for_device());
+    if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
+    std::vector<int32_t> routed{query};
+    RouteParams p = make_route_params(*cfg, *kv, *args, L, static_cast<char*>(ws), routed);
+    cuda_check(launch_scores_only(p, scores, 0, reinterpret_cast<cudaStream_t>(stream)),
+               "scores launch");
+  });
+}
+
+specsv_status specsv_select_blocks(const specsv_nsa_config* cfg, const double* scores,
+                                   int64_t visible_len, int32_t* idx, int32_t* count,
+                                   uint32_t* forced, specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !scores || !idx || !count || !forced) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    if (cfg->n > 64) throw Error(SPECSV_EUNSUPPORTED, "n must be <= 64");
+    const int64_t avail = selection_block_count(*cfg, visible_len);
+    if (avail > kMaxAvail) throw Error(SPECSV_EUNSUPPORTED, "too many selection blocks");
+    cuda_check(launch_select(scores, (int)avail, (int)cfg->n, idx, count, forced,
+                             reinterpret_cast<cudaStream_t>(stream)),
+               "select launch");
+  });
+}
+
+specsv_status specsv_compress_append(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
+                                     int64_t first_block, int64_t last_block,
+                                     const float* pos_embed, specsv_stream_t stream) {
+  return guarded([&] {
+    if (!cfg || !kv) throw Error(SPECSV_EINVAL, "null argument");
+    validate_config(*cfg);
+    if (cfg->d_head > 1024) throw Error(SPECSV_EUNSUPPORTED, "d_head too large");
+    const int64_t want = kv->rows >= cfg->l ? (kv->rows - cfg->l) / cfg->d + 1 : 0;
+    if (first_block < 0 || last_block > want || first_block > last_block)
+      throw Error(SPECSV_EINVAL, "block range outside the committed rows");
+    if (!kv->k || !kv->v || !kv->ck || !kv->ck16 || !kv->cv)
+      throw Error(SPECSV_EINVAL, "null cache pointer");
+    cuda_check(launch_compress(kv->k, kv->v, pos_embed, kv->ck, kv->ck16, kv->cv, first_block,
+                               last_block, (int)cfg->n_kv_heads, (int)cfg->d_head, (int)cfg->l,
+                               (int)cfg->d, reinterpret_cast<cudaStream_t>(stream)),
+               "compress launch");
+  });
+}
+
+specsv_status specsv_resolve_layer_roles(const int64_t* reuse_set, int64_t n_reuse,
+                                         int64_t n_layers, int32_t* roles, int64_t* source) {
+  return guarded([&] {
+    if ((n_reuse > 0 && !reuse_set) || !roles || !source) throw Error(SPECSV_EINVAL, "null argument");
+    resolve_layer_roles(reuse_set, n_reuse, n_layers, roles, source);
+  });
+}
+
+specsv_status specsv_clamp_inherited(const specsv_nsa_config* cfg, const int32_t* src,
+                                     uint32_t src_forced, int32_t count, int64_t causal_bound,
+                                     int32_t* out, uint32_t* out_forced, int32_t* out_count) {
+  return guarded([&] {
+    if (!cfg || (count > 0 && !src) || !out || !out_count) throw Error(SPECSV_EINVAL, "null argument");
+    *out_count = clamp_inherited(*cfg, src, src_forced, count, causal_bound, out, out_forced);
+  });
+}
+
+specsv_status specsv_load_stats(const specsv_nsa_config* cfg, int64_t rows, int32_t n_queries,
+                                const int64_t* pos, const uint64_t* tree_mask, int32_t mask_words,
+                                int32_t group_size, int32_t mode, int32_t role, const int32_t* idx,
+                                const int32_t* idx_count, specsv_load_stats_t* out) {
+  return guarded([&] {
+    if (!cfg || !pos || !idx || !idx_count || !out) throw Error(SPECSV_EINVAL, "null argument");
+    if (n_queries > 1 && !tree_mask) throw Error(SPECSV_EINVAL, "null tree mask");
+    load_stats(*cfg, rows, n_queries, pos, tree_mask, mask_words, group_size, mode, role, idx,
+               idx_count, out);
+  });
+}
+
+specsv_status specsv_algorithmic_bytes(const specsv_nsa_config* cfg, int64_t rows,
+                                       int32_t n_queries, const int64_t* pos, int32_t role,
+                                       const int32_t* idx, const int32_t* idx_count, int32_t mode,
+                                       int32_t group_size, int64_t* bytes) {
+  return guarded([&] {
+    if (!cfg || !pos || !idx || !idx_count || !bytes) throw Error(SPECSV_EINVAL, "null argument");
+    *bytes = algorithmic_bytes(*cfg, rows, n_queries, pos, role, idx, idx_count, mode, group_size);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,746 @@
+// attend.cu -- fused NSA verify attention for sm_100a (compressed + selected +
+// window branches + learned-gate combine) over all queries of one request.
+//
+// Replaces verify::group_attend_exact / group_attend_approx / attend_one
+// (src/group_attend.cpp:59-139) and the branch kernels they call
+// (src/nsa_attention.cpp:138-251), for every layer (refresh layers after the
+// routing launch, reuse layers as the single fused launch).
+//
+// Design ("K2/K3 fused attend"):
+//  * One CTA cluster per (KV head, query chunk); its CTAs split the KEY tiles.
+//    A key tile is 128 keys: 128 compressed blocks (cmp branch), two 64-token
+//    selection blocks of the per-request UNION of selected and window blocks
+//    (slc and win branches from one QK^T), or the draft-tree rows (win).
+//    Every K/V tile is TMA-staged into shared memory ONCE for all queries and
+//    all GQA heads that read it -- the overlap-aware dedup of the paper.
+//  * Swap-AB: S^T = K_tile . Q^T on tcgen05 (M = 128 keys, N = queries x heads),
+//    so the key dimension fills the 128-lane MMA; O^T += V^T . P^T (M = d_head).
+//    Accumulators live in TMEM.  q and P are split hi+lo in bf16 so logits and
+//    probabilities keep ~16 mantissa bits (fp32-class accumulation).
+//  * Ownership / routing-bound / window / tree masks are applied in registers
+//    per (key, query) after tcgen05.ld; masked entries contribute exactly 0.
+//  * Online softmax with a lazily-raised running max per (branch, column): the
+//    O accumulators in TMEM are rescaled only when a tile's max exceeds the
+//    reference max by 2^8.
+//  * Split-KV partials are merged inside the cluster (cluster barrier) and the
+//    gate combine is applied in the same kernel: branch partial outputs never
+//    leave the L2-resident workspace of this launch.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "attend.h"
+#include "sm100.cuh"
+
+namespace specsv_b200 {
+namespace {
+
+using namespace sm100;
+
+constexpr int kDh = 128;
+constexpr int kTile = 128;
+constexpr int kCols = 64;      // query columns (queries x heads) per CTA
+constexpr int kWarpsSoftmax = 4;
+constexpr int kThreads = 192;  // warps 0-3 softmax/epilogue, 4 TMA, 5 MMA
+constexpr uint32_t kTmemCols = 512;
+constexpr int kTmemS = 0;      // two S buffers at cols 0, 64
+constexpr int kTmemO = 128;    // O_cmp 128, O_slc 192, O_win 256
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+
+// shared memory map (bytes from the 1024-aligned base)
+constexpr uint32_t kOffK = 0;                 // 2 stages x 32 KB (K tile; reused for P of branch A)
+constexpr uint32_t kOffV = 65536;             // 2 stages x 32 KB
+constexpr uint32_t kOffQ = 131072;            // Q hi 16 KB, Q lo 16 KB
+constexpr uint32_t kOffPB = 163840;           // P of branch B (window) hi 16 KB, lo 16 KB
+constexpr uint32_t kOffMisc = 196608;
+constexpr uint32_t kStageBytes = 32768;
+
+enum Branch { kCmp = 0, kSlc = 1, kWin = 2 };
+enum TileKind { kTileCmp = 0, kTileTok = 1, kTileTree = 2 };
+
+struct Misc {
+  uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2];
+  uint64_t p_full, pv_done, setup;
+  uint32_t tmem_base;
+  int32_t n_union, n_cmp_tiles, n_tok_tiles, n_tree_tiles;
+  int32_t vote[4];
+  float m2[3][kCols];
+  float alpha[2][kCols];
+  float tmax[4][kCols];
+  float lsum[4][3][kCols];
+  int32_t qpos[kMaxChunkQ], qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
+  uint32_t bitmap[kMaxUnionWords];
+  int32_t union_blk[kMaxUnion];
+  uint32_t union_own[kMaxUnion];
+  int32_t word_prefix[kMaxUnionWords];
+};
+static_assert(sizeof(Misc) + kOffMisc + 1024 <= 232448, "shared memory budget");
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// transpose-reduce: 64 values per lane -> lane L holds the warp reduction of
+// columns 2L and 2L+1 (62 shuffles instead of 64 x 5)
+template <bool kMax>
+__device__ __forceinline__ void reduce_scatter64(float (&v)[kCols], int lane, float& o0, float& o1) {
+#pragma unroll
+  for (int lvl = 16, half = 32; lvl >= 1; lvl >>= 1, half >>= 1) {
+    const bool up = (lane & lvl) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? v[i] : v[i + half];
+      const float keep = up ? v[i + half] : v[i];
+      const float got = __shfl_xor_sync(0xffffffffu, send, lvl);
+      v[i] = kMax ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  o0 = v[0];
+  o1 = v[1];
+}
+
+__device__ __forceinline__ int visible_blocks(int bound, const AttendParams& p) {
+  if (bound < p.l) return 0;
+  const int by_len = (bound - p.l) / p.d + 1;
+  return by_len < p.blocks ? by_len : p.blocks;
+}
+
+// ---------------------------------------------------------------------------
+// prologue: per-chunk query table, union of selected + window blocks with
+// per-block query ownership (exact: own set; approx: representative's set;
+// both clamped at the query's routing bound, layer_roles.cpp:37-50)
+__device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int tid, int nthr) {
+  const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
+  const int words = (nsel + 31) >> 5;
+  for (int i = tid; i < nqc; i += nthr) {
+    const int q = q0 + i;
+    const int pos = p.pos[q];
+    const int bound = max(0, pos + 1 - p.lag);
+    m.qpos[i] = pos;
+    m.qbound[i] = min(bound, p.rows);
+    m.qwlo[i] = max(0, pos - p.w + 1);
+    m.qwhi[i] = min(pos, p.rows - 1);
+    m.qmvis[i] = visible_blocks(bound, p);
+  }
+  for (int i = tid; i < words; i += nthr) m.bitmap[i] = 0u;
+  named_bar_sync(2, nthr);
+  // window range of the chunk
+  int wlo = 0x7fffffff, whi = -1;
+  for (int i = 0; i < nqc; ++i) {
+    wlo = min(wlo, m.qwlo[i]);
+    whi = max(whi, m.qwhi[i]);
+  }
+  for (int b = wlo / p.l_sel + tid; b <= whi / p.l_sel; b += nthr)
+    atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
+  for (int e = tid; e < nqc * p.n_sel; e += nthr) {
+    const int i = e / p.n_sel, k = e % p.n_sel;
+    const int src = p.src_row[q0 + i];
+    if (k >= p.idx_count[src]) continue;
+    const int b = p.idx[src * p.n_sel + k];
+    if (b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
+    atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
+  }
+  named_bar_sync(2, nthr);
+  // exclusive prefix of popcounts (one warp; words <= kMaxUnionWords)
+  if (tid < 32) {
+    const int per = (words + 31) / 32;
+    const int w0 = tid * per;
+    int local = 0;
+    for (int w = w0; w < min(words, w0 + per); ++w) local += __popc(m.bitmap[w]);
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (tid >= off) incl += y;
+    }
+    int run = incl - local;
+    for (int w = w0; w < min(words, w0 + per); ++w) {
+      m.word_prefix[w] = run;
+      run += __popc(m.bitmap[w]);
+    }
+    if (tid == 31) m.n_union = min(incl, kMaxUnion);
+  }
+  named_bar_sync(2, nthr);
+  for (int w = tid; w < words; w += nthr) {
+    uint32_t bits = m.bitmap[w];
+    int r = m.word_prefix[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (r < kMaxUnion) {
+        m.union_blk[r] = (w << 5) + bit;
+        m.union_own[r] = 0u;
+      }
+      ++r;
+    }
+  }
+  named_bar_sync(2, nthr);
+  for (int e = tid; e < nqc * p.n_sel; e += nthr) {
+    const int i = e / p.n_sel, k = e % p.n_sel;
+    const int src = p.src_row[q0 + i];
+    if (k >= p.idx_count[src]) continue;
+    const int b = p.idx[src * p.n_sel + k];
+    if (b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
+    const int w = b >> 5;
+    const int r = m.word_prefix[w] + __popc(m.bitmap[w] & ((1u << (b & 31)) - 1u));
+    if (r < kMaxUnion) atomicOr(&m.union_own[r], 1u << i);
+  }
+  named_bar_sync(2, nthr);
+}
+
+struct TileInfo {
+  int kind;
+  int base;      // cmp: first compressed block; tok: union index of the first half
+  bool act_a;    // branch A (cmp or slc) has work
+  bool act_b;    // branch B (win) has work
+};
+
+__device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int nqc, int wlo, int whi,
+                                              int l_sel) {
+  TileInfo ti;
+  if (t < m.n_cmp_tiles) {
+    ti.kind = kTileCmp;
+    ti.base = t * kTile;
+    ti.act_a = true;
+    ti.act_b = false;
+  } else if (t < m.n_cmp_tiles + m.n_tok_tiles) {
+    ti.kind = kTileTok;
+    ti.base = 2 * (t - m.n_cmp_tiles);
+    const uint32_t own0 = m.union_own[ti.base];
+    const int b0 = m.union_blk[ti.base];
+    bool win = (b0 * l_sel <= whi) && (b0 * l_sel + l_sel - 1 >= wlo);
+    uint32_t own = own0;
+    if (ti.base + 1 < m.n_union) {
+      const int b1 = m.union_blk[ti.base + 1];
+      own |= m.union_own[ti.base + 1];
+      win = win || ((b1 * l_sel <= whi) && (b1 * l_sel + l_sel - 1 >= wlo));
+    }
+    ti.act_a = own != 0u;
+    ti.act_b = win;
+  } else {
+    ti.kind = kTileTree;
+    ti.base = 0;
+    ti.act_a = false;
+    ti.act_b = true;
+  }
+  return ti;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    nsa_attend_kernel(const __grid_constant__ AttendParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Misc& m = *reinterpret_cast<Misc*>(smem + kOffMisc);
+  const uint32_t sbase = smem_u32(smem);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int split = blockIdx.x;  // == cluster rank (cluster dims (n_splits,1,1))
+  const int kvh = blockIdx.y;
+  const int chunk = blockIdx.z;
+  const int q0 = chunk * p.qc_size;
+  const int nqc = min(p.qc_size, p.nq - q0);
+  const int ncols = nqc * p.G;
+  const int nqk = (ncols + 15) & ~15;
+  const int S = p.n_splits;
+
+  // ---- barriers + TMEM -----------------------------------------------------
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&m.k_full[i], 1);
+      mbar_init(&m.v_full[i], 1);
+      mbar_init(&m.kv_empty[i], 1);
+      mbar_init(&m.s_full[i], 1);
+      mbar_init(&m.s_free[i], 128);
+    }
+    mbar_init(&m.p_full, 128);
+    mbar_init(&m.pv_done, 1);
+    mbar_init(&m.setup, 128);
+    fence_mbar_init();
+  }
+  if (warp == 4) {
+    tmem_alloc<kTmemCols>(&m.tmem_base);
+  }
+  if (warp == 4 && lane == 0) {
+    tma_prefetch(&p.tm_k);
+    tma_prefetch(&p.tm_v);
+    tma_prefetch(&p.tm_ck);
+    tma_prefetch(&p.tm_cv);
+  }
+  // compressed tiles do not depend on the union; every CTA can count them now
+  int mmax = 0;
+  for (int i = 0; i < nqc; ++i) mmax = max(mmax, visible_blocks(max(0, p.pos[q0 + i] + 1 - p.lag), p));
+  const int n_cmp = (mmax + kTile - 1) / kTile;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = m.tmem_base;
+
+  // chunk window range (for branch-activity flags)
+  int cwlo = 0x7fffffff, cwhi = -1;
+  for (int i = 0; i < nqc; ++i) {
+    const int pos = p.pos[q0 + i];
+    cwlo = min(cwlo, max(0, pos - p.w + 1));
+    cwhi = max(cwhi, min(pos, p.rows - 1));
+  }
+  const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
+
+  if (warp < kWarpsSoftmax) {
+    // =================== setup: union, Q (hi/lo bf16), O := 0 ===================
+    if (tid == 0) m.n_cmp_tiles = n_cmp;
+    build_union(p, m, q0, nqc, tid, 128);
+    if (tid == 0) {
+      m.n_tok_tiles = (m.n_union + 1) / 2;
+      m.n_tree_tiles = has_tree ? 1 : 0;
+    }
+    // Q: 64 rows (columns c = qlocal*G + g) x 128 dh, K-major SW128, hi + lo
+    for (int unit = tid; unit < kCols * 16; unit += 128) {
+      const int c = unit >> 4, u16 = unit & 15;  // 16 units of 8 elems per row
+      const int chunk64 = u16 >> 3, u = u16 & 7;
+      float x[8];
+      if (c < ncols) {
+        const int qg = q0 + c / p.G;
+        const int h = kvh * p.G + (c % p.G);
+        const float4* src = reinterpret_cast<const float4*>(p.q + ((int64_t)qg * p.Hq + h) * kDh + u16 * 8);
+        const float4 a = src[0], b = src[1];
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = 0.f;
+      }
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+        const float2 hf = __bfloat1622float2(h2);
+        hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+        lo[e] = pack_bf16(x[2 * e] - hf.x, x[2 * e + 1] - hf.y);
+      }
+      const uint32_t off = chunk64 * 8192 + sw128_off(c, u);
+      *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    for (int i = tid; i < 3 * kCols; i += 128) (&m.m2[0][0])[i] = -INFINITY;
+    {
+      uint32_t z[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll
+      for (int c = 0; c < 3 * kCols; c += 16)
+        tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + c, z);
+      tmem_wait_st();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    mbar_arrive(&m.setup);
+  }
+
+  if (warp == 4) {
+    // =================== TMA producer ===================
+    if (lane == 0) {
+      bool setup_seen = false;
+      int n_total = 0x7fffffff;
+      for (int j = 0;; ++j) {
+        const int t = split + j * S;
+        if (t >= n_cmp && !setup_seen) {
+          mbar_wait(&m.setup, 0);
+          setup_seen = true;
+          n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+        }
+        if (t >= n_total) break;
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&m.kv_empty[st], ((j >> 1) + 1) & 1);
+        uint8_t* kdst = smem + kOffK + st * kStageBytes;
+        uint8_t* vdst = smem + kOffV + st * kStageBytes;
+        mbar_expect_tx(&m.k_full[st], kStageBytes);
+        mbar_expect_tx(&m.v_full[st], kStageBytes);
+        const CUtensorMap *tk, *tv;
+        int r0, r1;
+        if (t < n_cmp) {
+          tk = &p.tm_ck; tv = &p.tm_cv;
+          r0 = t * kTile; r1 = r0 + 64;
+        } else if (t < m.n_cmp_tiles + m.n_tok_tiles) {
+          tk = &p.tm_k; tv = &p.tm_v;
+          const int u0 = 2 * (t - m.n_cmp_tiles);
+          r0 = m.union_blk[u0] * p.l_sel;
+          r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
+        } else {
+          tk = &p.tm_tk; tv = &p.tm_tv;
+          r0 = 0; r1 = 64;
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
+          tma_load_3d(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st]);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          tma_load_3d(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st]);
+          tma_load_3d(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // =================== MMA issuer (one thread) ===================
+    mbar_wait(&m.setup, 0);
+    tc_fence_after();
+    const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+    const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
+    if (lane == 0 && T > 0) {
+      const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
+      auto issue_qk = [&](int j) {
+        const int st = j & 1, sb = j & 1;
+        if (j >= 2) mbar_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
+        mbar_wait(&m.k_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t kaddr = sbase + kOffK + st * kStageBytes;
+        const uint32_t qaddr = sbase + kOffQ;
+        const uint32_t d = tmem + kTmemS + 64 * sb;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {  // q hi, q lo
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+            const uint32_t qoff = part * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32;
+            umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
+                     idesc_qk, (part | kk) != 0);
+          }
+        }
+        umma_commit(&m.s_full[sb]);
+      };
+      issue_qk(0);
+      for (int j = 0; j < T; ++j) {
+        if (j + 1 < T) issue_qk(j + 1);
+        const int st = j & 1;
+        const TileInfo ti = tile_info(m, split + j * S, nqc, cwlo, cwhi, p.l_sel);
+        mbar_wait(&m.p_full, j & 1);
+        mbar_wait(&m.v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
+        if (ti.act_a) {
+          const uint32_t pa = sbase + kOffK + st * kStageBytes;  // P of branch A lives in the K stage
+          const uint32_t d = tmem + kTmemO + 64 * (ti.kind == kTileCmp ? kCmp : kSlc);
+#pragma unroll
+          for (int part = 0; part < 2; ++part)
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
+                       desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024), idesc_pv, 1u);
+        }
+        if (ti.act_b) {
+          const uint32_t pb = sbase + kOffPB;
+          const uint32_t d = tmem + kTmemO + 64 * kWin;
+#pragma unroll
+          for (int part = 0; part < 2; ++part)
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
+                       desc_sw128(pb + part * 16384 + kk * 2048, 16384, 1024), idesc_pv, 1u);
+        }
+        umma_commit(&m.pv_done);
+        umma_commit(&m.kv_empty[st]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // =================== softmax / masking / P (warps 0-3) ===================
+    mbar_wait(&m.setup, 0);  // own arrival completed; makes union visible
+    const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+    const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
+    const int row = warp * 32 + lane;  // key row within the tile
+    const int gshift = __ffs(p.G) - 1;
+    float lacc[3][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    for (int j = 0; j < T; ++j) {
+      const int t = split + j * S;
+      const int st = j & 1, sb = j & 1;
+      const TileInfo ti = tile_info(m, t, nqc, cwlo, cwhi, p.l_sel);
+      // per-query masks for this key row
+      uint32_t bits_a = 0u, bits_b = 0u;
+      if (ti.kind == kTileCmp) {
+        const int i = ti.base + row;
+        for (int qi = 0; qi < nqc; ++qi) bits_a |= (i < m.qmvis[qi] ? 1u : 0u) << qi;
+      } else if (ti.kind == kTileTok) {
+        const int u = ti.base + (row >> 6);
+        if (u < m.n_union) {
+          const int tok = m.union_blk[u] * p.l_sel + (row & 63);
+          const uint32_t own = m.union_own[u];
+          for (int qi = 0; qi < nqc; ++qi) {
+            bits_a |= ((((own >> qi) & 1u) != 0u) && tok < m.qbound[qi] ? 1u : 0u) << qi;
+            bits_b |= (tok >= m.qwlo[qi] && tok <= m.qwhi[qi] ? 1u : 0u) << qi;
+          }
+        }
+      } else {
+        for (int qi = 0; qi < nqc; ++qi) {
+          const int qg = q0 + qi;
+          if (qg >= 1 && row < 64) bits_b |= (uint32_t)((p.tree_mask[qg - 1] >> row) & 1ull) << qi;
+        }
+      }
+      // S^T row from TMEM
+      mbar_wait(&m.s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s2[kCols];
+      {
+        uint32_t r[16];
+#pragma unroll
+        for (int cc = 0; cc < kCols; cc += 16) {
+          if (cc < nqk) {
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemS + 64 * sb + cc, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) s2[cc + e] = __uint_as_float(r[e]) * p.scale_log2;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) s2[cc + e] = 0.f;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&m.s_free[sb]);
+
+      // ---- lazy running max per active branch (block-wide vote) ----
+      const int br_a = ti.kind == kTileCmp ? kCmp : kSlc;
+      bool resc[2] = {false, false};
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const bool act = side == 0 ? ti.act_a : ti.act_b;
+        if (!act) continue;  // warp-uniform
+        const int br = side == 0 ? br_a : kWin;
+        const uint32_t bits = side == 0 ? bits_a : bits_b;
+        bool need = false;
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) {
+          const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
+          need |= valid && (s2[c] > m.m2[br][c] + kRescaleThresh);
+        }
+        const bool any_w = __any_sync(0xffffffffu, need);
+        if (lane == 0) m.vote[warp] = any_w ? 1 : 0;
+        named_bar_sync(1, 128);
+        const bool any = (m.vote[0] | m.vote[1] | m.vote[2] | m.vote[3]) != 0;
+        named_bar_sync(1, 128);
+        if (!any) continue;
+        resc[side] = true;
+        float tmp[kCols];
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) {
+          const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
+          tmp[c] = valid ? s2[c] : -INFINITY;
+        }
+        float mx0, mx1;
+        reduce_scatter64<true>(tmp, lane, mx0, mx1);
+        m.tmax[warp][2 * lane] = mx0;
+        m.tmax[warp][2 * lane + 1] = mx1;
+        named_bar_sync(1, 128);
+        if (tid < kCols) {
+          const float old = m.m2[br][tid];
+          const float tm = fmaxf(fmaxf(m.tmax[0][tid], m.tmax[1][tid]), fmaxf(m.tmax[2][tid], m.tmax[3][tid]));
+          const float nw = tm > old ? tm : old;
+          m.alpha[side][tid] = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
+          m.m2[br][tid] = nw;
+        }
+        named_bar_sync(1, 128);
+        // l accumulators of this branch (lane holds columns 2L, 2L+1)
+        lacc[br][0] *= m.alpha[side][2 * lane];
+        lacc[br][1] *= m.alpha[side][2 * lane + 1];
+      }
+      // PV of the previous tile must be complete before P / O are touched
+      if (j > 0) mbar_wait(&m.pv_done, (j - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        if (!resc[side]) continue;
+        const int br = side == 0 ? br_a : kWin;
+        const float* al = m.alpha[side];
+        // O^T[dh = row][col] *= alpha[col]
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + 64 * br;
+#pragma unroll
+        for (int cc = 0; cc < kCols; cc += 16) {
+          uint32_t r[16];
+          tmem_ld16(ta + cc, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[cc + e]);
+          tmem_st16(ta + cc, r);
+        }
+        tmem_wait_st();
+      }
+      // ---- probabilities -> P^T (MN-major SW128, hi + lo), row sums ----
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const bool act = side == 0 ? ti.act_a : ti.act_b;
+        if (!act) continue;
+        const int br = side == 0 ? br_a : kWin;
+        const uint32_t bits = side == 0 ? bits_a : bits_b;
+        uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
+        float pl[kCols];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float pv[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int c = u * 8 + e * 2 + k;
+              const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
+              pv[k] = valid ? fast_exp2(s2[c] - m.m2[br][c]) : 0.f;
+              pl[c] = pv[k];
+            }
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(pv[0], pv[1]);
+            const float2 hf = __bfloat1622float2(h2);
+            hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+            lo[e] = pack_bf16(pv[0] - hf.x, pv[1] - hf.y);
+          }
+          const uint32_t off = sw128_off(row, u);
+          *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        float s0, s1;
+        reduce_scatter64<false>(pl, lane, s0, s1);
+        lacc[br][0] += s0;
+        lacc[br][1] += s1;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&m.p_full);
+    }
+    // ---- epilogue: partial (m, l, O) of this split -> workspace ----
+    if (T > 0) mbar_wait(&m.pv_done, (T - 1) & 1);
+    tc_fence_after();
+#pragma unroll
+    for (int br = 0; br < 3; ++br) {
+      m.lsum[warp][br][2 * lane] = lacc[br][0];
+      m.lsum[warp][br][2 * lane + 1] = lacc[br][1];
+    }
+    named_bar_sync(1, 128);
+    const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
+    float* ws_ml = p.ws + unit * (3 * kCols * 2);
+    float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
+    for (int i = tid; i < 3 * kCols; i += 128) {
+      const int br = i / kCols, c = i % kCols;
+      const float l = m.lsum[0][br][c] + m.lsum[1][br][c] + m.lsum[2][br][c] + m.lsum[3][br][c];
+      ws_ml[2 * i] = m.m2[br][c];
+      ws_ml[2 * i + 1] = l;
+    }
+#pragma unroll
+    for (int br = 0; br < 3; ++br) {
+#pragma unroll
+      for (int cc = 0; cc < kCols; cc += 16) {
+        if (cc >= ncols) break;
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + 64 * br + cc, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (cc + e < ncols) ws_o[((int64_t)br * kCols + cc + e) * kDh + row] = __uint_as_float(r[e]);
+      }
+    }
+    __threadfence();
+  }
+
+  // ---- cluster-wide merge of the split partials + gated combine ----
+  tc_fence_before();
+  if (S > 1) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
+  if (warp < kWarpsSoftmax) {
+    const int64_t unit0 = ((int64_t)chunk * p.Hkv + kvh) * S;
+    const int dh = tid;
+    for (int c = split; c < ncols; c += S) {
+      const int qg = q0 + (c >> (__ffs(p.G) - 1));
+      const int h = kvh * p.G + (c & (p.G - 1));
+      float res = 0.f;
+#pragma unroll
+      for (int br = 0; br < 3; ++br) {
+        float M = -INFINITY;
+        for (int s = 0; s < S; ++s) M = fmaxf(M, p.ws[(unit0 + s) * (3 * kCols * 2) + 2 * (br * kCols + c)]);
+        if (M == -INFINITY) continue;  // empty branch contributes 0 (nsa_attention.cpp:244)
+        float L = 0.f, O = 0.f;
+        for (int s = 0; s < S; ++s) {
+          const float* ml = p.ws + (unit0 + s) * (3 * kCols * 2) + 2 * (br * kCols + c);
+          if (ml[0] == -INFINITY) continue;
+          const float f = fast_exp2(ml[0] - M);
+          L += ml[1] * f;
+          O += p.ws[p.ws_o_offset + (unit0 + s) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + dh] * f;
+        }
+        if (L > 0.f) res += p.gates[((int64_t)qg * p.Hq + h) * 3 + br] * (O / L);
+      }
+      p.out[((int64_t)qg * p.Hq + h) * kDh + dh] = res;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+}  // namespace
+
+size_t attend_smem_bytes() { return kOffMisc + sizeof(Misc) + 1024; }
+
+size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits) {
+  const size_t units = (size_t)n_chunks * hkv * n_splits;
+  return units * (3 * kCols * 2) + units * (3 * kCols * kDh);
+}
+
+cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream) {
+  static_assert(kDh == 128, "d_head");
+  cudaError_t e = cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)attend_smem_bytes());
+  if (e != cudaSuccess) return e;
+  if (p.n_splits > 8) {
+    e = cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_splits, p.Hkv, n_chunks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = attend_smem_bytes();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.n_splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, nsa_attend_kernel, p);
+}
+
+int attend_max_cluster(int want) {
+  cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)attend_smem_bytes());
+  cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int s = want; s >= 1; s >>= 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(s, 8, 1);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = attend_smem_bytes();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = s;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, nsa_attend_kernel, &cfg) == cudaSuccess && n >= 1) {
+      cudaGetLastError();
+      return s;
+    }
+    cudaGetLastError();
+  }
+  return 1;
+}
+
+}  // namespace specsv_b200

@@ -1,0 +1,78 @@
+// attend.h -- launch interface of the device kernels (internal to the library).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace specsv_b200 {
+
+constexpr int kMaxQueries = 65;      // 1 + gamma, gamma <= 64 (one mask word per row)
+constexpr int kMaxChunkQ = 32;       // queries per CTA column chunk (64 cols / G, G >= 2)
+constexpr int kMaxUnion = 1280;      // union blocks per chunk
+constexpr int kMaxUnionWords = 1024; // selection-block bitmap words (32768 blocks)
+
+struct AttendParams {
+  CUtensorMap tm_k, tm_v;    // committed K/V bf16, dims (dh, Hkv, rows)
+  CUtensorMap tm_ck, tm_cv;  // compressed K (bf16 copy) / V bf16, dims (dh, Hkv, blocks)
+  CUtensorMap tm_tk, tm_tv;  // draft rows bf16, dims (dh, Hkv, max(gamma, 1))
+  const float* q;            // [nq][Hq][dh]
+  const float* gates;        // [nq][Hq][3]
+  float* out;                // [nq][Hq][dh]
+  const int32_t* idx;        // [nq][n_sel]
+  const int32_t* idx_count;  // [nq]
+  float* ws;                 // split partials
+  int64_t ws_o_offset;       // float offset of the O partials inside ws
+  int32_t nq, gamma, Hq, Hkv, G, n_sel;
+  int32_t rows, blocks, l, d, l_sel, w, lag;
+  int32_t qc_size, n_splits;
+  float scale_log2;
+  int32_t pos[kMaxQueries];
+  int32_t src_row[kMaxQueries];  // index-set row each query attends with
+  uint64_t tree_mask[kMaxQueries];
+};
+
+size_t attend_smem_bytes();
+size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits);
+cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream);
+int attend_max_cluster(int want);
+
+// ---- routing (route.cu) -------------------------------------------------------
+constexpr int kRouteTile = 64;      // compressed blocks per R1 CTA
+constexpr int kRouteRows = 128;     // q rows (routed queries x G) per R1 CTA
+constexpr int kMaxAvail = 8192;     // selection blocks per query for the Top-n CTA
+
+struct RouteParams {
+  const float* q;        // [nq][Hq][dh]
+  const float* ck;       // fp32 [blocks][Hkv][dh]
+  double* E;             // [nr][Hq][m_pad] exp(logit - tile max)
+  double* TM;            // [nr][Hq][ntiles] tile max
+  double* TD;            // [nr][Hq][ntiles] tile denominators
+  double* mass;          // [nr][m_pad]
+  int32_t* idx;          // [nq][n]
+  int32_t* idx_count;    // [nq]
+  uint32_t* idx_forced;  // [nq]
+  int32_t nr, nq, Hq, Hkv, G, dh, n;
+  int32_t l, d, l_sel;
+  int32_t m_pad, ntiles;
+  int32_t blocks;        // compressed blocks present in the cache
+  double scale;          // 1 / sqrt(dh)
+  int32_t slot_q[kMaxQueries];     // routed slot -> query index
+  int32_t slot_mvis[kMaxQueries];  // visible compressed blocks
+  int32_t slot_avail[kMaxQueries]; // selection blocks available
+  int32_t unrouted[kMaxQueries];   // queries that get count = -1
+  int32_t n_unrouted;
+};
+
+cudaError_t launch_route(const RouteParams& p, cudaStream_t stream, bool write_idx);
+cudaError_t launch_scores_only(const RouteParams& p, double* scores, int slot, cudaStream_t stream);
+cudaError_t launch_select(const double* scores, int avail, int n, int32_t* idx, int32_t* count,
+                          uint32_t* forced, cudaStream_t stream);
+
+// ---- compression (compress.cu) ------------------------------------------------
+cudaError_t launch_compress(const void* k, const void* v, const float* pe, float* ck, void* ck16,
+                            void* cv, int64_t first, int64_t last, int hkv, int dh, int l, int d,
+                            cudaStream_t stream);
+
+}  // namespace specsv_b200

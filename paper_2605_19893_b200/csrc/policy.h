@@ -1,0 +1,38 @@
+// policy.h -- host-side C++ rules shared by the C-ABI and the launchers.
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "specsv_b200/nsa_verify.h"
+
+namespace specsv_b200 {
+
+struct Error : std::runtime_error {
+  specsv_status code;
+  Error(specsv_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void validate_config(const specsv_nsa_config& c);
+void check_build_limits(const specsv_nsa_config& c);
+int64_t routing_visible_len(const specsv_nsa_config& c, int64_t pos);
+int64_t visible_blocks(const specsv_nsa_config& c, int64_t blocks, int64_t visible_len);
+int64_t selection_block_count(const specsv_nsa_config& c, int64_t visible_len);
+int64_t representative(const int64_t* pos, int64_t n);
+std::vector<int32_t> source_rows(const specsv_nsa_config& c, int32_t nq, const int64_t* pos,
+                                 int32_t group_size, int32_t mode);
+std::vector<int32_t> routed_queries(int32_t nq, const int64_t* pos, int32_t group_size,
+                                    int32_t mode);
+void resolve_layer_roles(const int64_t* reuse, int64_t n_reuse, int64_t n_layers, int32_t* roles,
+                         int64_t* source);
+int32_t clamp_inherited(const specsv_nsa_config& c, const int32_t* src, uint32_t src_forced,
+                        int32_t count, int64_t bound, int32_t* out, uint32_t* out_forced);
+void load_stats(const specsv_nsa_config& c, int64_t rows, int32_t nq, const int64_t* pos,
+                const uint64_t* tree_mask, int32_t mask_words, int32_t C, int32_t mode,
+                int32_t role, const int32_t* idx, const int32_t* cnt, specsv_load_stats_t* st);
+int64_t algorithmic_bytes(const specsv_nsa_config& c, int64_t rows, int32_t nq, const int64_t* pos,
+                          int32_t role, const int32_t* idx, const int32_t* cnt, int32_t mode,
+                          int32_t C);
+
+}  // namespace specsv_b200

@@ -1,0 +1,65 @@
+"""Diagnostics for the GPU path (not a test): runs verify cases with one-hot
+gates to isolate the compressed / selected / window branches, prints index
+agreement and per-branch errors against the oracle.
+
+    python tests/debug_run.py [rows] [gamma]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from oracle import oracle as O  # noqa: E402
+from paper_2605_19893_b200 import verify as V  # noqa: E402
+from paper_2605_19893_b200.workload import LayerInputs  # noqa: E402
+from tests.gpu_harness import DeviceCase, rel_errors, sets_to_numpy  # noqa: E402
+
+
+def main():
+    rows = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+    gamma = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    lib = O.load("oracle")
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, rows, gamma, 7)
+    t0 = time.time()
+    case = DeviceCase(cfg, x)
+    print("setup", time.time() - t0, "blocks", case.cache.blocks, flush=True)
+    ck, cv = case.oracle_cache(lib)
+    got_ck = case.cache.ck[:ck.shape[0]].cpu().numpy()
+    print("ck bit-exact:", np.array_equal(got_ck.view(np.uint32), ck.view(np.uint32)), flush=True)
+    sc = V.selection_scores(case.vcfg, case.cache, case.batch, 0, case.ws).cpu().numpy()
+    rs = lib.selection_scores(cfg, x.q[0], ck, cfg.routing_visible_len(int(x.pos[0])))
+    print("scores max rel diff:", float(np.abs(sc - rs).max() / np.abs(rs).max()), flush=True)
+    for name, g in (("cmp", (1, 0, 0)), ("slc", (0, 1, 0)), ("win", (0, 0, 1)), ("all", None)):
+        if g is not None:
+            gates = np.zeros_like(x.gates)
+            gates[..., :] = np.array(g, np.float32)
+            case.batch.gates = torch.from_numpy(gates).cuda()
+            x_g = gates
+        else:
+            case.batch.gates = torch.from_numpy(x.gates).cuda()
+            x_g = x.gates
+        out, sets = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+        saved = x.gates
+        x.gates = x_g
+        ref = case.oracle(lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+        x.gates = saved
+        gi, gc, _ = sets_to_numpy(sets)
+        same = [bool(gc[q] == ref["idx_count"][q] and (gi[q, :gc[q]] == ref["idx"][q, :gc[q]]).all())
+                for q in range(1 + gamma)]
+        per, l2 = rel_errors(out, ref["out"])
+        print(f"{name}: idx_same={all(same)} per={per:.3e} l2={l2:.3e} "
+              f"gpu[0,0,:4]={out[0, 0, :4]} ref={ref['out'][0, 0, :4]}", flush=True)
+        if not all(same):
+            print("  gpu idx q0", gi[0, :gc[0]], "\n  ref idx q0", ref["idx"][0, :ref["idx_count"][0]])
+        bad = np.argwhere(np.abs(out - ref["out"]).max(-1) > 2e-3 * np.maximum(np.abs(ref["out"]).max(-1), 1e-6))
+        if len(bad):
+            print("  bad (q,h) first 10:", bad[:10].tolist())
+
+
+if __name__ == "__main__":
+    main()

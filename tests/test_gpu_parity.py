@@ -1,0 +1,196 @@
+"""GPU parity of the sm_100a verify path against the CPU oracle (the C
+restatement pinned bit-exact to the reference).  All calls go through the
+C-ABI.  Contract:
+  P1  Top-n fed the oracle's fp64 scores returns identical indices/flags.
+  P2  end-to-end indices equal the oracle's for every query whose oracle
+      boundary gap exceeds NEAR_TIE (near-ties are counted, expected 0).
+  P3  fp64 scores within 1e-13 relative of the oracle.
+  P4  outputs within 2e-3: per (query, head) inf-norm relative and global L2.
+  P5  LoadStats integers equal (test_abi_cpu covers the host accounting).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402
+from paper_2605_19893_b200 import verify as V  # noqa: E402
+from paper_2605_19893_b200.workload import LayerInputs, bf16_round  # noqa: E402
+from tests.gpu_harness import (TOL, DeviceCase, boundary_gap, forced_matrix,  # noqa: E402
+                               rel_errors, sets_to_numpy)
+
+NEAR_TIE = 1e-12
+TREE8 = [-1, -1, 0, 0, 1, 2, 2, 4]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _check_indices(oracle_lib, case, got_idx, got_cnt, got_forced, ref, routed_only=None):
+    cfg = case.cfg
+    ck, _ = case.oracle_cache(oracle_lib)
+    near = 0
+    for q in range(case.nq):
+        if ref["idx_count"][q] < 0:
+            assert got_cnt[q] == -1, f"query {q} should have no set"
+            continue
+        same = (got_cnt[q] == ref["idx_count"][q]
+                and (got_idx[q, :got_cnt[q]] == ref["idx"][q, :got_cnt[q]]).all()
+                and (forced_matrix(got_forced[q:q + 1], cfg.n)[0, :got_cnt[q]]
+                     == ref["idx_forced"][q, :got_cnt[q]]).all())
+        if not same:
+            gap = boundary_gap(oracle_lib, cfg, case.x.q[q], ck, case.x.pos[q])
+            assert gap <= NEAR_TIE, f"query {q}: indices differ with gap {gap}"
+            near += 1
+    return near
+
+
+def test_compress_append_bit_exact(oracle_lib):
+    cfg = O.llama_config(2)
+    x = LayerInputs(cfg, 3000, 0, 5)
+    case = DeviceCase(cfg, x)
+    ck, cv = oracle_lib.build_compressed(cfg, x.k, x.v, 3000, x.pos_embed)
+    nb = ck.shape[0]
+    assert case.cache.blocks == nb
+    got_ck = case.cache.ck[:nb].cpu().numpy()
+    assert np.array_equal(got_ck.view(np.uint32), ck.view(np.uint32))
+    got_cv = case.cache.cv[:nb].float().cpu().numpy()
+    assert np.array_equal(got_cv, bf16_round(cv))
+    got_ck16 = case.cache.ck16[:nb].float().cpu().numpy()
+    assert np.array_equal(got_ck16, bf16_round(ck))
+
+
+def test_compress_append_incremental(oracle_lib):
+    cfg = O.llama_config(2)
+    x = LayerInputs(cfg, 2000, 0, 6)
+    vcfg = V.NsaConfig(**cfg.__dict__)
+    cache = V.LayerCache(vcfg, 2000)
+    pe = torch.from_numpy(x.pos_embed).cuda()
+    for lo, hi in ((0, 40), (40, 47), (47, 1000), (1000, 2000)):
+        cache.append(torch.from_numpy(x.k[lo:hi]).cuda().bfloat16(),
+                     torch.from_numpy(x.v[lo:hi]).cuda().bfloat16())
+        cache.extend_compressed(pe)
+    ck, _ = oracle_lib.build_compressed(cfg, x.k, x.v, 2000, x.pos_embed)
+    assert np.array_equal(cache.ck[:ck.shape[0]].cpu().numpy().view(np.uint32), ck.view(np.uint32))
+
+
+@pytest.mark.parametrize("rows", [700, 4096, 9000])
+def test_selection_scores_fp64(oracle_lib, rows):
+    cfg = O.llama_config(2)
+    x = LayerInputs(cfg, rows, 3, 7 + rows)
+    case = DeviceCase(cfg, x)
+    ck, _ = case.oracle_cache(oracle_lib)
+    for q in range(case.nq):
+        got = V.selection_scores(case.vcfg, case.cache, case.batch, q, case.ws).cpu().numpy()
+        ref = oracle_lib.selection_scores(cfg, x.q[q], ck, cfg.routing_visible_len(int(x.pos[q])))
+        assert got.shape == ref.shape
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_select_blocks_on_reference_scores(oracle_lib):
+    cfg = O.llama_config(2)
+    vcfg = V.NsaConfig(**cfg.__dict__)
+    rng = np.random.default_rng(3)
+    for avail in (1, 2, 3, 5, 16, 17, 100, 1024, 2048):
+        for trial in range(3):
+            s = rng.random(avail)
+            if trial == 2:
+                s = np.round(s * 8) / 8  # many exact ties -> lower id wins
+            vis = avail * cfg.l_sel
+            ref = oracle_lib.select_blocks(cfg, s, cfg.n, vis)
+            got = V.select_blocks(vcfg, torch.from_numpy(s).cuda(), vis)
+            assert got == ref, (avail, trial)
+
+
+CASES = [
+    # rows, gamma, parents, mode, C
+    (1000, 0, None, O.MODE_EXACT, 1),
+    (1000, 4, None, O.MODE_EXACT, 2),
+    (4096, 4, None, O.MODE_EXACT, 4),   # C1 shape
+    (2085, 8, None, O.MODE_APPROX, 4),
+    (3001, 8, TREE8, O.MODE_EXACT, 2),
+    (3001, 8, TREE8, O.MODE_APPROX, 4),
+    (9000, 8, None, O.MODE_EXACT, 8),
+    (520, 3, None, O.MODE_EXACT, 1),    # window covers the whole context
+    (40, 2, None, O.MODE_EXACT, 1),     # almost nothing compressed / selectable
+]
+
+
+@pytest.mark.parametrize("rows,gamma,parents,mode,C", CASES)
+def test_verify_refresh_then_reuse(oracle_lib, rows, gamma, parents, mode, C):
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, rows, gamma, 100 + rows + gamma, parent_slot=parents)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(C, mode, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, C, mode, O.ROLE_REFRESH)
+    assert ref["rc"] == 0
+    gi, gc, gf = sets_to_numpy(sets)
+    near = _check_indices(oracle_lib, case, gi, gc, gf, ref)
+    assert near == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+    # reuse layer: different KV, inherits the refresh layer's sets
+    y = LayerInputs(cfg, rows, gamma, 900 + rows + gamma, parent_slot=parents)
+    case2 = DeviceCase(cfg, y)
+    out2, _ = case2.run(C, mode, V.ROLE_REUSE, sets=sets)
+    ref2 = case2.oracle(oracle_lib, C, mode, O.ROLE_REUSE, idx=ref["idx"],
+                        idx_count=ref["idx_count"], idx_forced=ref["idx_forced"])
+    assert ref2["rc"] == 0
+    per, l2 = rel_errors(out2, ref2["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_verify_64k_chain8_full_size(oracle_lib):
+    """Config C2 at full size (65536 committed rows, 8-token chain), one layer."""
+    cfg = O.llama_config(32)
+    x = LayerInputs(cfg, 65536, 8, 4242)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_verify_tree32(oracle_lib):
+    """Config C3 shape: 32-node tree (D <= 6) at 8K context, BFS flat order."""
+    cfg = O.llama_config(4)
+    parents = [-1, -1, -1, -1]
+    for i in range(4, 32):
+        parents.append(i // 4 - 1 if i // 4 - 1 < i else -1)
+    # depths stay <= 6 <= routing_lag
+    x = LayerInputs(cfg, 8192, 32, 77, parent_slot=parents)
+    case = DeviceCase(cfg, x)
+    for mode, C in ((O.MODE_EXACT, 4), (O.MODE_APPROX, 4)):
+        out, sets = case.run(C, mode, V.ROLE_REFRESH)
+        ref = case.oracle(oracle_lib, C, mode, O.ROLE_REFRESH)
+        gi, gc, gf = sets_to_numpy(sets)
+        assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+        per, l2 = rel_errors(out, ref["out"])
+        assert per <= TOL and l2 <= TOL, (mode, per, l2)
+
+
+def test_deterministic(oracle_lib):
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 5000, 8, 31)
+    case = DeviceCase(cfg, x)
+    a, _ = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    b, _ = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    assert np.array_equal(a, b)
+
+
+def test_depth_beyond_lag_rejected():
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 2000, 2, 3)
+    case = DeviceCase(cfg, x)
+    case.batch.pos = case.batch.pos.copy()
+    case.batch.pos[2] = case.batch.pos[0] + cfg.routing_lag + 1
+    with pytest.raises(V.SpecsvError) as e:
+        case.run(1, V.MODE_EXACT, V.ROLE_REFRESH)
+    assert e.value.code == 1
