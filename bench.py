@@ -1,0 +1,486 @@
+#!/usr/bin/env python3
+"""Benchmark of the sparse speculative-verification hot path on B200.
+
+Workload (BASELINE.json configs[1]): Llama-3.1-8B-shaped NSA
+(32 q / 8 KV heads, d_head 128, l=32, d=16, l_sel=64, n=16, w=512, lag 16),
+64K committed context, 8-token chain draft, bf16 KV, one request per GPU,
+one verify pass over L=32 DISTINCT layer caches per step (the layers run in
+sequence, one C-ABI verify call each, like run_target_pass).  Strategy:
+EXACT grouping (C=4) with the reference's "alt" refresh/reuse schedule
+(layers 1,3,..,31 reuse the preceding layer's index sets).
+
+A step touches ~10 GB of KV (> 126 MB L2), so successive steps never hit L2
+on the same layer.  The step is captured once in a CUDA graph and replayed.
+
+metric: verified query-tokens/s = requests * (1 + gamma) / seconds per step
+(whole job over all GPUs).  `e2e` runs the same step through the public API
+with the step's inputs copied host->device (pinned) and the last layer's
+output copied back inside the timed region.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+reference compiled from its sources) on this host's cores, same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified query-tokens/s at 64K ctx, 8-tok draft; achieved HBM GB/s vs peak"
+UNIT = "query-tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ctx", type=int, default=65536)
+    ap.add_argument("--gamma", type=int, default=8)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--mode", default="exact", choices=["exact", "approx"])
+    ap.add_argument("--group", type=int, default=4)
+    ap.add_argument("--schedule", default="alt")
+    ap.add_argument("--requests", type=int, default=1, help="requests per GPU")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def reuse_set(schedule: str, L: int):
+    if schedule in ("", "none"):
+        return []
+    if schedule == "alt":
+        return list(range(1, L, 2))
+    return [int(x) for x in schedule.split(",") if x]
+
+
+def llama_cfg(L):
+    from paper_2605_19893_b200.verify import NsaConfig
+    return NsaConfig(l=32, d=16, l_sel=64, n=16, w=512, n_q_heads=32, n_kv_heads=8, d_head=128,
+                     n_layers=L, routing_lag=16)
+
+
+def workload_config(a, extra=None):
+    cfg = {"workload": f"C2: Llama-3.1-8B-shaped NSA verify, {a.ctx // 1024}K ctx, "
+                       f"{a.gamma}-token chain draft, bf16 KV, {a.layers} layers",
+           "ctx": a.ctx, "draft": "chain", "gamma": a.gamma, "layers": a.layers,
+           "requests_per_gpu": a.requests, "mode": a.mode, "group_size": a.group,
+           "schedule": a.schedule, "heads": "32q/8kv", "d_head": 128,
+           "nsa": "l=32 d=16 l_sel=64 n=16 w=512 lag=16",
+           "l2": "inputs larger than L2 (each step streams >= 9 GB of distinct layer caches)"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# --------------------------------------------------------------------------- CPU
+class CpuReference:
+    """The reference (oracle/_ref: the reference's own C++ compiled in place) on
+    this host: independent (layer, request) verify units on host threads
+    (SPEC.md:138 allows concurrent queries/layers)."""
+
+    def __init__(self, a, threads: int):
+        from oracle import oracle as O
+        from paper_2605_19893_b200.workload import LayerInputs
+        self.O, self.a, self.threads = O, a, threads
+        self.kind = "reference" if O.ref_available() else "port"
+        self.lib = O.load("ref" if self.kind == "reference" else "oracle")
+        self.cfg = O.llama_config(a.layers)
+        self.mode = O.MODE_EXACT if a.mode == "exact" else O.MODE_APPROX
+        self.units = []
+        for u in range(2):
+            x = LayerInputs(self.cfg, a.ctx, a.gamma, 500 + u)
+            ck, cv = self.lib.build_compressed(self.cfg, x.k, x.v, a.ctx, x.pos_embed)
+            self.units.append((x, ck, cv))
+        x0, ck0, cv0 = self.units[0]
+        self.seed_sets = self.lib.verify_layer(
+            self.cfg, x0.k, x0.v, ck0, cv0, x0.q, x0.pos, x0.gates.astype(np.float64), x0.tree_k,
+            x0.tree_v, x0.tree_mask, a.group, self.mode, O.ROLE_REFRESH)
+        self.n_reuse = len(reuse_set(a.schedule, a.layers))
+
+    def measure(self, seconds: float):
+        """query-tokens/s for full L-layer steps (schedule's refresh/reuse mix),
+        all threads, plus a description of the bounded sample."""
+        O, a = self.O, self.a
+        times = {O.ROLE_REFRESH: [], O.ROLE_REUSE: []}
+        done = [0] * self.threads
+        stop = time.time() + seconds
+
+        def worker(tid):
+            k = 0
+            while k < 2 or time.time() < stop:
+                role = O.ROLE_REUSE if (k % 2 == 1 and self.n_reuse > 0) else O.ROLE_REFRESH
+                x, ck, cv = self.units[(tid + k) % 2]
+                kw = {}
+                if role == O.ROLE_REUSE:
+                    kw = dict(idx=self.seed_sets["idx"], idx_count=self.seed_sets["idx_count"],
+                              idx_forced=self.seed_sets["idx_forced"])
+                t0 = time.time()
+                self.lib.verify_layer(self.cfg, x.k, x.v, ck, cv, x.q, x.pos,
+                                      x.gates.astype(np.float64), x.tree_k, x.tree_v,
+                                      x.tree_mask, a.group, self.mode, role, **kw)
+                times[role].append(time.time() - t0)
+                done[tid] += 1
+                k += 1
+
+        t0 = time.time()
+        ths = [threading.Thread(target=worker, args=(i,)) for i in range(self.threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        el = time.time() - t0
+        tr = float(np.mean(times[O.ROLE_REFRESH]))
+        tu = float(np.mean(times[O.ROLE_REUSE])) if times[O.ROLE_REUSE] else tr
+        per_step_thread_s = (a.layers - self.n_reuse) * tr + self.n_reuse * tu
+        rate = self.threads * (1 + a.gamma) / per_step_thread_s
+        sample = (f"{sum(done)} single-layer verify calls of the workload ({a.ctx // 1024}K ctx, "
+                  f"gamma={a.gamma}, {a.mode} C={a.group}; mean refresh {tr * 1e3:.0f} ms, reuse "
+                  f"{tu * 1e3:.0f} ms per call per thread) on {self.threads} threads in {el:.1f} s, "
+                  f"scaled to {a.layers}-layer steps ({a.layers - self.n_reuse} refresh + "
+                  f"{self.n_reuse} reuse layers)")
+        return rate, sample
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = a.cpu_threads or os.cpu_count() or 1
+    ref = CpuReference(a, threads)
+    per_step = max(1.0, min(5.0, 150.0 / max(1, a.steps + a.warmup)))
+    vals, sample = [], ""
+    for s_ in range(a.warmup + a.steps):
+        rate, smp = ref.measure(per_step if s_ >= a.warmup else 0.0)
+        if s_ >= a.warmup:
+            vals.append(rate)
+            sample = sample or smp
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * (1 + a.gamma) / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (splitmix64 U[-1,1] KV/q, bf16-rounded)",
+            "config": workload_config(a),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": ref.kind,
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/specsv_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except OSError:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_19893_b200 import verify as V
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = llama_cfg(a.layers)
+    L, g, nq = a.layers, a.gamma, 1 + a.gamma
+    R = a.requests
+    mode = V.MODE_EXACT if a.mode == "exact" else V.MODE_APPROX
+    roles, source = V.resolve_layer_roles(reuse_set(a.schedule, L), L)
+    H, dh, Hq = cfg.n_kv_heads, cfg.d_head, cfg.n_q_heads
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + 1000 * rank)
+
+    def urand(*shape, dtype=torch.float32):
+        return (torch.rand(*shape, generator=gen, device=dev) * 2 - 1).to(dtype)
+
+    pos = np.array([a.ctx - 1 + i for i in range(nq)], np.int64)
+    from paper_2605_19893_b200.workload import chain_tree_mask
+    tmask = chain_tree_mask(g)
+    caches, batches, sets, outs, inbufs = [], [], [], [], []
+    for r in range(R):
+        qa = urand(L, nq, Hq, dh)
+        ga = torch.rand(L, nq, Hq, 3, generator=gen, device=dev) * 0.6 + 0.2
+        tka = urand(L, max(g, 1), H, dh, dtype=torch.bfloat16)
+        tva = urand(L, max(g, 1), H, dh, dtype=torch.bfloat16)
+        inbufs.append((qa, ga, tka, tva))
+        cr, br, sr, orr = [], [], [], []
+        for j in range(L):
+            c = V.LayerCache(cfg, a.ctx, device=dev)
+            c.k.copy_(urand(a.ctx, H, dh, dtype=torch.bfloat16))
+            c.v.copy_(urand(a.ctx, H, dh, dtype=torch.bfloat16))
+            c.rows = a.ctx
+            c.extend_compressed(urand(cfg.l, dh) * 0.1)
+            cr.append(c)
+            br.append(V.DraftBatch(pos=pos, tree_mask=tmask, q=qa[j], gates=ga[j],
+                                   tree_k=tka[j], tree_v=tva[j]))
+            sr.append(V.IndexSets.empty(nq, cfg.n, dev))
+            orr.append(torch.zeros(nq, Hq, dh, device=dev))
+        caches.append(cr)
+        batches.append(br)
+        sets.append(sr)
+        outs.append(orr)
+    ws = V.Workspace(cfg, nq, a.ctx, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        for r in range(R):
+            for j in range(L):
+                s = sets[r][j] if roles[j] == V.ROLE_REFRESH else sets[r][int(source[j])]
+                V.nsa_verify(cfg, caches[r][j], batches[r][j], s, outs[r][j], ws, a.group, mode,
+                             int(roles[j]))
+
+    n_refresh = int((roles == V.ROLE_REFRESH).sum())
+    launches_per_step = R * (n_refresh * 4 + (L - n_refresh) * 1)
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    graph = None
+    if not a.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                step()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(a.warmup):
+        run_step()
+    barrier()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(a.steps):
+            run_step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    ms = max_over_ranks(ms)
+    value = world * R * nq / (ms * 1e-3)
+
+    # ---- kernel-level roofline: the fused attend kernel and the routing
+    # launches, each captured alone over all L layers (same stream, graphs so
+    # host launch overhead does not leak into the device timing)
+    def capture(fn):
+        gph = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            fn()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gph, stream=cs):
+                fn()
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        return gph
+
+    def attend_all():
+        for j in range(L):
+            src = sets[0][j] if roles[j] == V.ROLE_REFRESH else sets[0][int(source[j])]
+            V.attend_fused(cfg, caches[0][j], batches[0][j], src, outs[0][j], ws, a.group, mode,
+                           V.ROLE_REUSE)
+
+    def route_all():
+        for j in range(L):
+            if roles[j] == V.ROLE_REFRESH:
+                V.route(cfg, caches[0][j], batches[0][j], sets[0][j], outs[0][j], ws, a.group, mode)
+
+    g_att, g_rt = capture(attend_all), capture(route_all)
+    att_ms, rt_ms = [], []
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for rep in range(6):
+        e[0].record(stream)
+        g_att.replay()
+        e[1].record(stream)
+        g_rt.replay()
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        if rep > 0:
+            att_ms.append(e[0].elapsed_time(e[1]) / L)
+            rt_ms.append(e[1].elapsed_time(e[2]) / max(1, n_refresh))
+    attend_ms = float(np.median(att_ms))
+    route_ms = float(np.median(rt_ms))
+    alg_att, alg_route, uniq = [], [], []
+    for j in range(L):
+        src = sets[0][j] if roles[j] == V.ROLE_REFRESH else sets[0][int(source[j])]
+        idx = src.idx.cpu().numpy()
+        cnt = src.count.cpu().numpy()
+        b_att = V.algorithmic_bytes(cfg, a.ctx, pos, V.ROLE_REUSE, idx, cnt, mode, a.group)
+        b_ref = V.algorithmic_bytes(cfg, a.ctx, pos, V.ROLE_REFRESH, idx, cnt, mode, a.group)
+        alg_att.append(b_att)
+        alg_route.append(b_ref - b_att)
+        uniq.append(len(set(idx[cnt > 0].ravel().tolist()) - {-1}))
+    bytes_att = float(np.mean(alg_att))
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_att / (attend_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "attend_ncu_summary.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    # step-level algorithmic bytes / time
+    step_bytes = sum(alg_att) + sum(alg_route[j] for j in range(L) if roles[j] == V.ROLE_REFRESH)
+
+    # ---- e2e through the public API with host buffers: the step's inputs
+    # (q, gates, draft K/V of every layer) arrive from pinned host memory and
+    # the last layer's output goes back, inside the timed region
+    hin = [tuple(t.cpu().pin_memory() for t in bufs) for bufs in inbufs]
+    hout = [torch.empty(nq, Hq, dh, pin_memory=True) for _ in range(R)]
+    h2d = sum(t.numel() * t.element_size() for bufs in hin for t in bufs)
+    d2h = sum(t.numel() * t.element_size() for t in hout)
+
+    def e2e_step():
+        for r in range(R):
+            for dst, src in zip(inbufs[r], hin[r]):
+                dst.copy_(src, non_blocking=True)
+        run_step()
+        for r in range(R):
+            hout[r].copy_(outs[r][L - 1], non_blocking=True)
+
+    for _ in range(max(1, a.warmup)):
+        e2e_step()
+    barrier()
+    t0w = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(a.steps):
+        e2e_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t0w) * 1e3 / a.steps
+    e2e_ms = max_over_ranks(max(ev0.elapsed_time(ev1) / a.steps, wall_ms))
+    e2e_value = world * R * nq / (e2e_ms * 1e-3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not a.skip_cpu_baseline:
+        threads = a.cpu_threads or os.cpu_count() or 1
+        ref = CpuReference(a, threads)
+        rate, sample = ref.measure(a.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": ref.kind, "sample": sample}
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (U[-1,1] KV and queries, random-init; no checkpoint)",
+        "config": workload_config(a, {"parallelism": f"replicas x{world} (request sharding)"}),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "nsa_attend_kernel (fused cmp+slc+win+gate, one launch per layer)",
+                     "alg_bytes_per_launch": bytes_att, "launch_ms": attend_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": launches_per_step * a.steps,
+        "detail": {
+            "per_layer_us_step_avg": ms * 1e3 / L,
+            "attend_us": attend_ms * 1e3, "route_us": route_ms * 1e3,
+            "route_alg_bytes": float(np.mean(alg_route)),
+            "step_alg_GBps": step_bytes / (ms * 1e-3) / 1e9,
+            "step_frac_of_peak": step_bytes / (ms * 1e-3) / 1e9 / peak,
+            "unique_selected_blocks_per_layer": float(np.mean(uniq)),
+            "refresh_layers": n_refresh, "reuse_layers": L - n_refresh,
+            "graph": graph is not None,
+        },
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -204,6 +204,13 @@ specsv_status specsv_algorithmic_bytes(const specsv_nsa_config* cfg, int64_t row
                                        const int32_t* idx, const int32_t* idx_count,
                                        int32_t mode, int32_t group_size, int64_t* bytes);
 
+/* ---- diagnostics ------------------------------------------------------- */
+/* Per-thread (host thread) debug hook: when `buf` is a device pointer, the
+ * next fused-attend launches write per-CTA globaltimer stamps [cta][8]
+ * (start, setup done, tile loop done, partials written, merge done); NULL
+ * disables.  Not used on the product path. */
+specsv_status specsv_debug_attend_trace(unsigned long long* buf);
+
 #ifdef __cplusplus
 }
 #endif

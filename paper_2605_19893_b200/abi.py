@@ -23,7 +23,7 @@ EXPORTED = (
     "specsv_verify_workspace_size", "specsv_nsa_verify", "specsv_nsa_verify_batched",
     "specsv_nsa_route", "specsv_nsa_attend_fused", "specsv_nsa_scores", "specsv_select_blocks",
     "specsv_compress_append", "specsv_resolve_layer_roles", "specsv_clamp_inherited",
-    "specsv_load_stats", "specsv_algorithmic_bytes",
+    "specsv_load_stats", "specsv_algorithmic_bytes", "specsv_debug_attend_trace",
 )
 
 
@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
                                C.POINTER(LoadStatsC)], C.c_int),
         "specsv_algorithmic_bytes": ([cfgp, i64, i32, i64p, i32, i32p, i32p, i32, i32, i64p],
                                      C.c_int),
+        "specsv_debug_attend_trace": ([vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -24,6 +24,7 @@ namespace specsv_b200 {
 namespace {
 
 thread_local std::string g_last_error;
+thread_local unsigned long long* g_trace = nullptr;
 
 template <class F>
 specsv_status guarded(F&& f) {
@@ -233,6 +234,7 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   p.idx = a.idx;
   p.idx_count = a.idx_count;
   p.ws = static_cast<float*>(ws);
+  p.trace = g_trace;
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
   p.ws_o_offset = (int64_t)nchunks * H * S * (3 * 64 * 2);
@@ -269,6 +271,11 @@ using namespace specsv_b200;
 extern "C" {
 
 int32_t specsv_abi_version(void) { return SPECSV_ABI_VERSION; }
+
+specsv_status specsv_debug_attend_trace(unsigned long long* buf) {
+  g_trace = buf;
+  return SPECSV_OK;
+}
 
 const char* specsv_last_error(void) { return g_last_error.c_str(); }
 

@@ -61,15 +61,15 @@ enum Branch { kCmp = 0, kSlc = 1, kWin = 2 };
 enum TileKind { kTileCmp = 0, kTileTok = 1, kTileTree = 2 };
 
 struct Misc {
-  uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2];
-  uint64_t p_full, pv_done, setup;
+  uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], pv_done[2];
+  uint64_t p_full, setup;
   uint32_t tmem_base;
   int32_t n_union, n_cmp_tiles, n_tok_tiles, n_tree_tiles;
   int32_t vote[4];
   float m2[3][kCols];
   float alpha[2][kCols];
   float tmax[4][kCols];
-  float lsum[4][3][kCols];
+  float lsum[4][3][kCols];  // per-warp row sums of P (the softmax denominators)
   int32_t qpos[kMaxChunkQ], qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
   uint32_t bitmap[kMaxUnionWords];
   int32_t union_blk[kMaxUnion];
@@ -78,18 +78,24 @@ struct Misc {
 };
 static_assert(sizeof(Misc) + kOffMisc + 1024 <= 232448, "shared memory budget");
 
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// transpose-reduce: 64 values per lane -> lane L holds the warp reduction of
-// columns 2L and 2L+1 (62 shuffles instead of 64 x 5)
+// transpose-reduce of 16 columns across the warp: returns, in lanes 2c and
+// 2c+1, the reduction over all 32 lanes of column c (16 shuffles)
 template <bool kMax>
-__device__ __forceinline__ void reduce_scatter64(float (&v)[kCols], int lane, float& o0, float& o1) {
+__device__ __forceinline__ float reduce16(float (&v)[16], int lane) {
 #pragma unroll
-  for (int lvl = 16, half = 32; lvl >= 1; lvl >>= 1, half >>= 1) {
+  for (int lvl = 16, half = 8; lvl >= 2; lvl >>= 1, half >>= 1) {
     const bool up = (lane & lvl) != 0;
 #pragma unroll
     for (int i = 0; i < half; ++i) {
@@ -99,8 +105,8 @@ __device__ __forceinline__ void reduce_scatter64(float (&v)[kCols], int lane, fl
       v[i] = kMax ? fmaxf(keep, got) : keep + got;
     }
   }
-  o0 = v[0];
-  o1 = v[1];
+  const float other = __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return kMax ? fmaxf(v[0], other) : v[0] + other;
 }
 
 __device__ __forceinline__ int visible_blocks(int bound, const AttendParams& p) {
@@ -247,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ncols = nqc * p.G;
   const int nqk = (ncols + 15) & ~15;
   const int S = p.n_splits;
+  const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
 
   // ---- barriers + TMEM -----------------------------------------------------
   if (tid == 0) {
@@ -256,9 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&m.kv_empty[i], 1);
       mbar_init(&m.s_full[i], 1);
       mbar_init(&m.s_free[i], 128);
+      mbar_init(&m.pv_done[i], 1);
     }
     mbar_init(&m.p_full, 128);
-    mbar_init(&m.pv_done, 1);
     mbar_init(&m.setup, 128);
     fence_mbar_init();
   }
@@ -279,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = m.tmem_base;
+  if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 0] = globaltimer();
 
   // chunk window range (for branch-activity flags)
   int cwlo = 0x7fffffff, cwhi = -1;
@@ -288,49 +296,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     cwhi = max(cwhi, min(pos, p.rows - 1));
   }
   const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
+  const int nch = nqk >> 4;  // 16-column chunks holding valid columns
 
   if (warp < kWarpsSoftmax) {
-    // =================== setup: union, Q (hi/lo bf16), O := 0 ===================
+    // =================== setup: Q (hi/lo bf16), union, O := 0 ===================
+    // Q rows c = qlocal*G + g, K-major SW128; all loads issued before use
+    {
+      float4 xa[8], xb[8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int unit = tid + it * 128;
+        const int c = unit >> 4, u16 = unit & 15;
+        if (c < ncols) {
+          const int qg = q0 + (c >> (__ffs(p.G) - 1));
+          const int h = kvh * p.G + (c & (p.G - 1));
+          const float4* src = reinterpret_cast<const float4*>(p.q + ((int64_t)qg * p.Hq + h) * kDh + u16 * 8);
+          xa[it] = src[0];
+          xb[it] = src[1];
+        } else {
+          xa[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+          xb[it] = xa[it];
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int unit = tid + it * 128;
+        const int c = unit >> 4, u16 = unit & 15;
+        const float x[8] = {xa[it].x, xa[it].y, xa[it].z, xa[it].w, xb[it].x, xb[it].y, xb[it].z, xb[it].w};
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+          const float2 hf = __bfloat1622float2(h2);
+          hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+          lo[e] = pack_bf16(x[2 * e] - hf.x, x[2 * e + 1] - hf.y);
+        }
+        const uint32_t off = (u16 >> 3) * 8192 + sw128_off(c, u16 & 7);
+        *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+    }
     if (tid == 0) m.n_cmp_tiles = n_cmp;
     build_union(p, m, q0, nqc, tid, 128);
     if (tid == 0) {
       m.n_tok_tiles = (m.n_union + 1) / 2;
       m.n_tree_tiles = has_tree ? 1 : 0;
     }
-    // Q: 64 rows (columns c = qlocal*G + g) x 128 dh, K-major SW128, hi + lo
-    for (int unit = tid; unit < kCols * 16; unit += 128) {
-      const int c = unit >> 4, u16 = unit & 15;  // 16 units of 8 elems per row
-      const int chunk64 = u16 >> 3, u = u16 & 7;
-      float x[8];
-      if (c < ncols) {
-        const int qg = q0 + c / p.G;
-        const int h = kvh * p.G + (c % p.G);
-        const float4* src = reinterpret_cast<const float4*>(p.q + ((int64_t)qg * p.Hq + h) * kDh + u16 * 8);
-        const float4 a = src[0], b = src[1];
-        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = 0.f;
-      }
-      uint32_t hi[4], lo[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
-        const float2 hf = __bfloat1622float2(h2);
-        hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
-        lo[e] = pack_bf16(x[2 * e] - hf.x, x[2 * e + 1] - hf.y);
-      }
-      const uint32_t off = chunk64 * 8192 + sw128_off(c, u);
-      *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    for (int i = tid; i < 3 * kCols; i += 128) {
+      (&m.m2[0][0])[i] = -INFINITY;
+      for (int w = 0; w < 4; ++w) (&m.lsum[w][0][0])[i] = 0.f;
     }
-    for (int i = tid; i < 3 * kCols; i += 128) (&m.m2[0][0])[i] = -INFINITY;
     {
       uint32_t z[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) z[i] = 0u;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 3 * kCols; c += 16)
         tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + c, z);
       tmem_wait_st();
@@ -424,9 +444,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&m.v_full[st], (j >> 1) & 1);
         tc_fence_after();
         const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
-        if (ti.act_a) {
-          const uint32_t pa = sbase + kOffK + st * kStageBytes;  // P of branch A lives in the K stage
-          const uint32_t d = tmem + kTmemO + 64 * (ti.kind == kTileCmp ? kCmp : kSlc);
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+          if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
+          // P of branch A lives in this tile's K stage; P of branch B in its own region
+          const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
+          const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+          const uint32_t d = tmem + kTmemO + 64 * br;
 #pragma unroll
           for (int part = 0; part < 2; ++part)
 #pragma unroll
@@ -434,17 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
                        desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024), idesc_pv, 1u);
         }
-        if (ti.act_b) {
-          const uint32_t pb = sbase + kOffPB;
-          const uint32_t d = tmem + kTmemO + 64 * kWin;
-#pragma unroll
-          for (int part = 0; part < 2; ++part)
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
-                       desc_sw128(pb + part * 16384 + kk * 2048, 16384, 1024), idesc_pv, 1u);
-        }
-        umma_commit(&m.pv_done);
+        umma_commit(&m.pv_done[j & 1]);
         umma_commit(&m.kv_empty[st]);
       }
     }
@@ -452,11 +466,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // =================== softmax / masking / P (warps 0-3) ===================
     mbar_wait(&m.setup, 0);  // own arrival completed; makes union visible
+    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 1] = globaltimer();
     const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
     const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
     const int row = warp * 32 + lane;  // key row within the tile
     const int gshift = __ffs(p.G) - 1;
-    float lacc[3][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    const uint32_t srow = tmem + ((uint32_t)(warp * 32) << 16);
+    bool prev_b = false;  // previous tile wrote the branch-B P region
+#pragma unroll 1
     for (int j = 0; j < T; ++j) {
       const int t = split + j * S;
       const int st = j & 1, sb = j & 1;
@@ -482,42 +499,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (qg >= 1 && row < 64) bits_b |= (uint32_t)((p.tree_mask[qg - 1] >> row) & 1ull) << qi;
         }
       }
-      // S^T row from TMEM
       mbar_wait(&m.s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      float s2[kCols];
-      {
-        uint32_t r[16];
-#pragma unroll
-        for (int cc = 0; cc < kCols; cc += 16) {
-          if (cc < nqk) {
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemS + 64 * sb + cc, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) s2[cc + e] = __uint_as_float(r[e]) * p.scale_log2;
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) s2[cc + e] = 0.f;
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&m.s_free[sb]);
+      const uint32_t sbuf = srow + kTmemS + 64 * sb;
 
       // ---- lazy running max per active branch (block-wide vote) ----
-      const int br_a = ti.kind == kTileCmp ? kCmp : kSlc;
       bool resc[2] = {false, false};
-#pragma unroll
+#pragma unroll 1
       for (int side = 0; side < 2; ++side) {
-        const bool act = side == 0 ? ti.act_a : ti.act_b;
-        if (!act) continue;  // warp-uniform
-        const int br = side == 0 ? br_a : kWin;
+        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
+        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
         const uint32_t bits = side == 0 ? bits_a : bits_b;
         bool need = false;
+#pragma unroll 1
+        for (int k = 0; k < nch; ++k) {
+          uint32_t r[16];
+          tmem_ld16(sbuf + 16 * k, r);
+          tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) {
-          const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
-          need |= valid && (s2[c] > m.m2[br][c] + kRescaleThresh);
+          for (int e = 0; e < 16; ++e) {
+            const int c = 16 * k + e;
+            const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
+            need |= valid && (__uint_as_float(r[e]) * p.scale_log2 > m.m2[br][c] + kRescaleThresh);
+          }
         }
         const bool any_w = __any_sync(0xffffffffu, need);
         if (lane == 0) m.vote[warp] = any_w ? 1 : 0;
@@ -526,98 +530,115 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, 128);
         if (!any) continue;
         resc[side] = true;
-        float tmp[kCols];
+#pragma unroll 1
+        for (int k = 0; k < nch; ++k) {
+          uint32_t r[16];
+          tmem_ld16(sbuf + 16 * k, r);
+          tmem_wait_ld();
+          float v[16];
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) {
-          const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
-          tmp[c] = valid ? s2[c] : -INFINITY;
+          for (int e = 0; e < 16; ++e) {
+            const int c = 16 * k + e;
+            const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
+            v[e] = valid ? __uint_as_float(r[e]) * p.scale_log2 : -INFINITY;
+          }
+          const float mx = reduce16<true>(v, lane);
+          if ((lane & 1) == 0) m.tmax[warp][16 * k + (lane >> 1)] = mx;
         }
-        float mx0, mx1;
-        reduce_scatter64<true>(tmp, lane, mx0, mx1);
-        m.tmax[warp][2 * lane] = mx0;
-        m.tmax[warp][2 * lane + 1] = mx1;
         named_bar_sync(1, 128);
-        if (tid < kCols) {
+        if (tid < 16 * nch) {
           const float old = m.m2[br][tid];
           const float tm = fmaxf(fmaxf(m.tmax[0][tid], m.tmax[1][tid]), fmaxf(m.tmax[2][tid], m.tmax[3][tid]));
           const float nw = tm > old ? tm : old;
-          m.alpha[side][tid] = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
+          const float al = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
+          m.alpha[side][tid] = al;
           m.m2[br][tid] = nw;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) m.lsum[w][br][tid] *= al;
         }
         named_bar_sync(1, 128);
-        // l accumulators of this branch (lane holds columns 2L, 2L+1)
-        lacc[br][0] *= m.alpha[side][2 * lane];
-        lacc[br][1] *= m.alpha[side][2 * lane + 1];
       }
-      // PV of the previous tile must be complete before P / O are touched
-      if (j > 0) mbar_wait(&m.pv_done, (j - 1) & 1);
+      // PV of the previous tile must be complete before O is rescaled or the
+      // shared branch-B P region is rewritten (branch-A P lives in this tile's
+      // own K stage, whose previous PV completed before the stage was reloaded)
+      if (j > 0 && (resc[0] || resc[1] || (ti.act_b && prev_b)))
+        mbar_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
       tc_fence_after();
-#pragma unroll
+#pragma unroll 1
       for (int side = 0; side < 2; ++side) {
         if (!resc[side]) continue;
-        const int br = side == 0 ? br_a : kWin;
-        const float* al = m.alpha[side];
-        // O^T[dh = row][col] *= alpha[col]
-        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + 64 * br;
-#pragma unroll
-        for (int cc = 0; cc < kCols; cc += 16) {
+        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+        const uint32_t ta = srow + kTmemO + 64 * br;
+#pragma unroll 1
+        for (int k = 0; k < nch; ++k) {
           uint32_t r[16];
-          tmem_ld16(ta + cc, r);
+          tmem_ld16(ta + 16 * k, r);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[cc + e]);
-          tmem_st16(ta + cc, r);
+          for (int e = 0; e < 16; ++e)
+            r[e] = __float_as_uint(__uint_as_float(r[e]) * m.alpha[side][16 * k + e]);
+          tmem_st16(ta + 16 * k, r);
         }
         tmem_wait_st();
       }
       // ---- probabilities -> P^T (MN-major SW128, hi + lo), row sums ----
-#pragma unroll
+#pragma unroll 1
       for (int side = 0; side < 2; ++side) {
-        const bool act = side == 0 ? ti.act_a : ti.act_b;
-        if (!act) continue;
-        const int br = side == 0 ? br_a : kWin;
+        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
+        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
         const uint32_t bits = side == 0 ? bits_a : bits_b;
         uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
-        float pl[kCols];
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+          if (k >= nch) {  // columns beyond the valid chunks: P = 0
+            const uint4 z = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float pv[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int c = u * 8 + e * 2 + k;
-              const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
-              pv[k] = valid ? fast_exp2(s2[c] - m.m2[br][c]) : 0.f;
-              pl[c] = pv[k];
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t off = sw128_off(row, 2 * k + h);
+              *reinterpret_cast<uint4*>(pdst + off) = z;
+              *reinterpret_cast<uint4*>(pdst + 16384 + off) = z;
             }
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(pv[0], pv[1]);
-            const float2 hf = __bfloat1622float2(h2);
-            hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
-            lo[e] = pack_bf16(pv[0] - hf.x, pv[1] - hf.y);
+            continue;
           }
-          const uint32_t off = sw128_off(row, u);
-          *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          uint32_t r[16];
+          tmem_ld16(sbuf + 16 * k, r);
+          tmem_wait_ld();
+          float pv[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int c = 16 * k + e;
+            const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
+            pv[e] = valid ? fast_exp2(__uint_as_float(r[e]) * p.scale_log2 - m.m2[br][c]) : 0.f;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+              const float2 hf = __bfloat1622float2(h2);
+              hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+              lo[e] = pack_bf16(a - hf.x, b - hf.y);
+            }
+            const uint32_t off = sw128_off(row, 2 * k + h);
+            *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+          const float sum = reduce16<false>(pv, lane);
+          if ((lane & 1) == 0) m.lsum[warp][br][16 * k + (lane >> 1)] += sum;
         }
-        float s0, s1;
-        reduce_scatter64<false>(pl, lane, s0, s1);
-        lacc[br][0] += s0;
-        lacc[br][1] += s1;
       }
+      prev_b = ti.act_b;
       fence_proxy_async_smem();
       tc_fence_before();
+      mbar_arrive(&m.s_free[sb]);
       mbar_arrive(&m.p_full);
     }
+    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 2] = globaltimer();
     // ---- epilogue: partial (m, l, O) of this split -> workspace ----
-    if (T > 0) mbar_wait(&m.pv_done, (T - 1) & 1);
+    if (T > 0) mbar_wait(&m.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
     tc_fence_after();
-#pragma unroll
-    for (int br = 0; br < 3; ++br) {
-      m.lsum[warp][br][2 * lane] = lacc[br][0];
-      m.lsum[warp][br][2 * lane + 1] = lacc[br][1];
-    }
     named_bar_sync(1, 128);
     const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
     float* ws_ml = p.ws + unit * (3 * kCols * 2);
@@ -628,20 +649,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       ws_ml[2 * i] = m.m2[br][c];
       ws_ml[2 * i + 1] = l;
     }
-#pragma unroll
+#pragma unroll 1
     for (int br = 0; br < 3; ++br) {
-#pragma unroll
-      for (int cc = 0; cc < kCols; cc += 16) {
-        if (cc >= ncols) break;
+#pragma unroll 1
+      for (int k = 0; k < nch; ++k) {
         uint32_t r[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + 64 * br + cc, r);
+        tmem_ld16(srow + kTmemO + 64 * br + 16 * k, r);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          if (cc + e < ncols) ws_o[((int64_t)br * kCols + cc + e) * kDh + row] = __uint_as_float(r[e]);
+          if (16 * k + e < ncols) ws_o[((int64_t)br * kCols + 16 * k + e) * kDh + row] = __uint_as_float(r[e]);
       }
     }
     __threadfence();
+    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 3] = globaltimer();
   }
 
   // ---- cluster-wide merge of the split partials + gated combine ----
@@ -675,6 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       p.out[((int64_t)qg * p.Hq + h) * kDh + dh] = res;
     }
+    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 4] = globaltimer();
   }
   tc_fence_before();
   __syncthreads();

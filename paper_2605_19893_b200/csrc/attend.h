@@ -23,6 +23,7 @@ struct AttendParams {
   const int32_t* idx;        // [nq][n_sel]
   const int32_t* idx_count;  // [nq]
   float* ws;                 // split partials
+  unsigned long long* trace; // optional per-CTA globaltimer stamps [cta][8] (debug)
   int64_t ws_o_offset;       // float offset of the O partials inside ws
   int32_t nq, gamma, Hq, Hkv, G, n_sel;
   int32_t rows, blocks, l, d, l_sel, w, lag;

@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kR3Threads)
 constexpr size_t kR3Smem = (size_t)kMaxAvail * 9;
 
 cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
+  if (p.ntiles == 0) return cudaSuccess;  // nothing compressed is visible yet: all masses 0
   const int rows_total = p.nr * p.G;
   const int rchunks = (rows_total + kRouteRows - 1) / kRouteRows;
   const int maxrows = rows_total < kRouteRows ? rows_total : kRouteRows;

@@ -61,5 +61,35 @@ def main():
             print("  bad (q,h) first 10:", bad[:10].tolist())
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) <= 3:
     main()
+
+
+def trace_attend(rows=65536, gamma=8):
+    """Per-CTA phase timeline of one fused attend launch (globaltimer, ns)."""
+    from paper_2605_19893_b200 import abi
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, rows, gamma, 9)
+    case = DeviceCase(cfg, x)
+    case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    buf = torch.zeros(4096 * 8, dtype=torch.int64, device="cuda")
+    abi.lib().specsv_debug_attend_trace(torch.cuda.LongTensor.data_ptr(buf))
+    sets = V.IndexSets.empty(case.nq, cfg.n)
+    out = torch.zeros(case.nq, cfg.n_q_heads, cfg.d_head, device="cuda")
+    V.route(case.vcfg, case.cache, case.batch, sets, out, case.ws, 4)
+    for _ in range(3):
+        V.attend_fused(case.vcfg, case.cache, case.batch, sets, out, case.ws, 4, V.MODE_EXACT, V.ROLE_REUSE)
+    torch.cuda.synchronize()
+    abi.lib().specsv_debug_attend_trace(None)
+    t = buf.view(-1, 8).cpu().numpy()
+    t = t[t[:, 0] > 0]
+    t0 = t[:, 0].min()
+    print("ctas", len(t))
+    for name, col in (("setup", 1), ("tiles", 2), ("partials", 3), ("merge", 4)):
+        d = (t[:, col] - t0) / 1e3
+        print(f"{name:9s} done at us: min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}")
+    print("start spread us:", (t[:, 0].max() - t0) / 1e3)
+
+
+if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[3] == "trace":
+    trace_attend(int(sys.argv[1]), int(sys.argv[2]))
