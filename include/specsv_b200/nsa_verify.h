@@ -127,7 +127,10 @@ const char* specsv_last_error(void);
 /* NsaConfig::validate (config.hpp:38-51) plus this build's limits. */
 specsv_status specsv_validate_config(const specsv_nsa_config* cfg);
 
-/* Bytes of device workspace one verify call needs (caller allocates). */
+/* Bytes of device workspace one verify call needs.  The caller allocates it,
+ * zero-fills it ONCE before first use and then reserves it for this library
+ * (it holds split partials and per-head barrier words that return to a
+ * consistent state after every call).  One workspace per stream. */
 size_t specsv_verify_workspace_size(const specsv_nsa_config* cfg, int32_t n_queries,
                                     int64_t max_rows);
 

@@ -78,17 +78,28 @@ void encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int64_t hkv
   if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
-int splits_for_device() {
+// co-resident CTAs of the attend kernel on this device (a device constant,
+// computed once per device)
+int coresident_for_device() {
   static std::atomic<int> cache[64];
   int dev = 0;
   cudaGetDevice(&dev);
   dev = std::min(dev, 63);
   int s = cache[dev].load();
   if (s == 0) {
-    s = attend_max_cluster(16);
+    s = std::max(1, attend_max_coresident());
     cache[dev].store(s);
   }
   return s;
+}
+
+int qc_size_for(const specsv_nsa_config& c);
+
+// split CTAs per (KV head, query chunk): all of them must be co-resident
+int splits_for(const specsv_nsa_config& c, int32_t nq) {
+  const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
+  const int groups = (int)c.n_kv_heads * nchunks;
+  return std::max(1, std::min(18, coresident_for_device() / groups));
 }
 
 struct Layout {
@@ -104,7 +115,8 @@ int qc_size_for(const specsv_nsa_config& c) {
   return std::min(64 / G, kMaxChunkQ);
 }
 
-Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows, int splits) {
+Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
+  const int splits = 18;  // upper bound of splits_for()
   Layout L;
   const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
   L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
@@ -206,7 +218,7 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
 
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                void* ws, size_t ws_bytes, cudaStream_t stream) {
-  const Layout L = layout_for(c, a.n_queries, kv.rows, splits_for_device());
+  const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   const auto routed = routed_queries(a.n_queries, a.pos, a.group_size, a.mode);
   RouteParams p = make_route_params(c, kv, a, L, static_cast<char*>(ws), routed);
@@ -215,8 +227,8 @@ void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spec
 
 void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                 void* ws, size_t ws_bytes, cudaStream_t stream) {
-  const int S = splits_for_device();
-  const Layout L = layout_for(c, a.n_queries, kv.rows, S);
+  const int S = splits_for(c, a.n_queries);
+  const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   AttendParams p;
   std::memset(&p, 0, sizeof(p));
@@ -238,6 +250,7 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
   p.ws_o_offset = (int64_t)nchunks * H * S * (3 * 64 * 2);
+  p.ws_sync_offset = (int64_t)(L.attend_bytes / sizeof(float)) - (int64_t)nchunks * H * 2;
   p.nq = a.n_queries;
   p.gamma = gamma;
   p.Hq = (int32_t)c.n_q_heads;
@@ -290,7 +303,7 @@ specsv_status specsv_validate_config(const specsv_nsa_config* cfg) {
 size_t specsv_verify_workspace_size(const specsv_nsa_config* cfg, int32_t n_queries,
                                     int64_t max_rows) {
   if (cfg == nullptr || n_queries < 1) return 0;
-  return layout_for(*cfg, n_queries, max_rows, splits_for_device()).total;
+  return layout_for(*cfg, n_queries, max_rows).total;
 }
 
 specsv_status specsv_nsa_route(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
@@ -356,7 +369,7 @@ specsv_status specsv_nsa_scores(const specsv_nsa_config* cfg, const specsv_layer
     check_build_limits(*cfg);
     validate_args(*cfg, *kv, *args);
     if (query < 0 || query >= args->n_queries) throw Error(SPECSV_EINVAL, "query out of range");
-    const Layout L = layout_for(*cfg, args->n_queries, kv->rows, splits_for_device());
+    const Layout L = layout_for(*cfg, args->n_queries, kv->rows);
     if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
     std::vector<int32_t> routed{query};
     RouteParams p = make_route_params(*cfg, *kv, *args, L, static_cast<char*>(ws), routed);

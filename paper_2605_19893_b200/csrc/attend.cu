@@ -6,25 +6,27 @@
 // (src/nsa_attention.cpp:138-251), for every layer (refresh layers after the
 // routing launch, reuse layers as the single fused launch).
 //
-// Design ("K2/K3 fused attend"):
-//  * One CTA cluster per (KV head, query chunk); its CTAs split the KEY tiles.
-//    A key tile is 128 keys: 128 compressed blocks (cmp branch), two 64-token
-//    selection blocks of the per-request UNION of selected and window blocks
-//    (slc and win branches from one QK^T), or the draft-tree rows (win).
-//    Every K/V tile is TMA-staged into shared memory ONCE for all queries and
-//    all GQA heads that read it -- the overlap-aware dedup of the paper.
+// Design ("fused attend"):
+//  * S split CTAs per (KV head, query chunk), co-resident (cooperative launch);
+//    they split the KEY tiles.  A key tile is 128 keys: 128 compressed blocks
+//    (cmp branch), two 64-token selection blocks of the per-request UNION of
+//    selected and window blocks (slc and win branches from one QK^T), or the
+//    draft-tree rows (win).  Every K/V tile is TMA-staged into shared memory
+//    ONCE for all queries and all GQA heads that read it -- the overlap-aware
+//    dedup of the paper.
 //  * Swap-AB: S^T = K_tile . Q^T on tcgen05 (M = 128 keys, N = queries x heads),
 //    so the key dimension fills the 128-lane MMA; O^T += V^T . P^T (M = d_head).
-//    Accumulators live in TMEM.  q and P are split hi+lo in bf16 so logits and
-//    probabilities keep ~16 mantissa bits (fp32-class accumulation).
-//  * Ownership / routing-bound / window / tree masks are applied in registers
-//    per (key, query) after tcgen05.ld; masked entries contribute exactly 0.
+//    Accumulators live in TMEM.  q (pre-scaled by log2(e)/sqrt(dh)) and P are
+//    split hi+lo in bf16, keeping ~16 mantissa bits (fp32-class accumulation).
+//  * 16 softmax warps: warp w owns TMEM lane quadrant w%4 (32 keys) and the
+//    16-column chunk w/4.  Ownership / routing-bound / window / tree masks are
+//    applied in registers per (key, query); masked entries contribute exactly 0.
 //  * Online softmax with a lazily-raised running max per (branch, column): the
 //    O accumulators in TMEM are rescaled only when a tile's max exceeds the
 //    reference max by 2^8.
-//  * Split-KV partials are merged inside the cluster (cluster barrier) and the
-//    gate combine is applied in the same kernel: branch partial outputs never
-//    leave the L2-resident workspace of this launch.
+//  * Split partials are merged behind a per-head global barrier among the S
+//    co-resident CTAs, and the gate combine is applied in the same kernel: the
+//    branch partial outputs never leave this launch's L2-resident workspace.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -41,19 +43,22 @@ using namespace sm100;
 
 constexpr int kDh = 128;
 constexpr int kTile = 128;
-constexpr int kCols = 64;      // query columns (queries x heads) per CTA
-constexpr int kWarpsSoftmax = 4;
-constexpr int kThreads = 192;  // warps 0-3 softmax/epilogue, 4 TMA, 5 MMA
+constexpr int kCols = 64;          // query columns (queries x heads) per CTA
+constexpr int kSoftWarps = 16;     // 4 lane quadrants x 4 column chunks
+constexpr int kSoftThreads = kSoftWarps * 32;
+constexpr int kWarpTma = 16;
+constexpr int kThreads = 18 * 32;  // + TMA warp + MMA warp
 constexpr uint32_t kTmemCols = 512;
-constexpr int kTmemS = 0;      // two S buffers at cols 0, 64
-constexpr int kTmemO = 128;    // O_cmp 128, O_slc 192, O_win 256
+constexpr int kTmemS = 0;          // two S buffers at cols 0, 64
+constexpr int kTmemO = 128;        // O_cmp 128, O_slc 192, O_win 256
 constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr uint32_t kSleepNs = 20000;
 
 // shared memory map (bytes from the 1024-aligned base)
-constexpr uint32_t kOffK = 0;                 // 2 stages x 32 KB (K tile; reused for P of branch A)
-constexpr uint32_t kOffV = 65536;             // 2 stages x 32 KB
-constexpr uint32_t kOffQ = 131072;            // Q hi 16 KB, Q lo 16 KB
-constexpr uint32_t kOffPB = 163840;           // P of branch B (window) hi 16 KB, lo 16 KB
+constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P of branch A)
+constexpr uint32_t kOffV = 65536;    // 2 stages x 32 KB
+constexpr uint32_t kOffQ = 131072;   // Q hi 16 KB, Q lo 16 KB
+constexpr uint32_t kOffPB = 163840;  // P of branch B (window): hi 16 KB, lo 16 KB
 constexpr uint32_t kOffMisc = 196608;
 constexpr uint32_t kStageBytes = 32768;
 
@@ -62,19 +67,22 @@ enum TileKind { kTileCmp = 0, kTileTok = 1, kTileTree = 2 };
 
 struct Misc {
   uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], pv_done[2];
-  uint64_t p_full, setup;
+  uint64_t p_full, q_ready, union_ready;
   uint32_t tmem_base;
   int32_t n_union, n_cmp_tiles, n_tok_tiles, n_tree_tiles;
-  int32_t vote[4];
-  float m2[3][kCols];
-  float alpha[2][kCols];
+  int32_t vote[kSoftWarps];
+  float m2[3][kCols];    // running max (log2 units) per branch and column
+  float thr[3][kCols];   // m2 + threshold
+  float alpha[kCols];
   float tmax[4][kCols];
-  float lsum[4][3][kCols];  // per-warp row sums of P (the softmax denominators)
-  int32_t qpos[kMaxChunkQ], qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
+  float lsum[4][3][kCols];  // per-quadrant row sums of P
+  int32_t qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
+  int32_t qcount[kMaxChunkQ];
+  int32_t qsel[kMaxChunkQ * 64];
   uint32_t bitmap[kMaxUnionWords];
+  int32_t word_prefix[kMaxUnionWords];
   int32_t union_blk[kMaxUnion];
   uint32_t union_own[kMaxUnion];
-  int32_t word_prefix[kMaxUnionWords];
 };
 static_assert(sizeof(Misc) + kOffMisc + 1024 <= 232448, "shared memory budget");
 
@@ -88,6 +96,20 @@ __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// waits with a hardware suspend hint (no busy spinning of the waiting warp)
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(kSleepNs)
+        : "memory");
+  } while (!ok);
 }
 
 // transpose-reduce of 16 columns across the warp: returns, in lanes 2c and
@@ -115,26 +137,50 @@ __device__ __forceinline__ int visible_blocks(int bound, const AttendParams& p) 
   return by_len < p.blocks ? by_len : p.blocks;
 }
 
+// per-(chunk, head) barrier among the S co-resident split CTAs: a counter
+// that returns to 0 plus a generation word that only grows (workspace words
+// start at 0 and are owned by this library)
+__device__ void group_barrier(int* cnt, volatile int* gen, int S, int tid) {
+  __syncthreads();
+  if (tid == 0) {
+    const int g = *gen;
+    __threadfence();
+    if (atomicAdd(cnt, 1) == S - 1) {
+      atomicExch(cnt, 0);
+      __threadfence();
+      atomicAdd(const_cast<int*>(gen), 1);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // prologue: per-chunk query table, union of selected + window blocks with
 // per-block query ownership (exact: own set; approx: representative's set;
-// both clamped at the query's routing bound, layer_roles.cpp:37-50)
+// both clamped at the query's routing bound, layer_roles.cpp:37-50).
+// Index sets are staged in shared memory first (one global round trip).
 __device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int tid, int nthr) {
   const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
   const int words = (nsel + 31) >> 5;
-  for (int i = tid; i < nqc; i += nthr) {
-    const int q = q0 + i;
-    const int pos = p.pos[q];
-    const int bound = max(0, pos + 1 - p.lag);
-    m.qpos[i] = pos;
-    m.qbound[i] = min(bound, p.rows);
-    m.qwlo[i] = max(0, pos - p.w + 1);
-    m.qwhi[i] = min(pos, p.rows - 1);
-    m.qmvis[i] = visible_blocks(bound, p);
+  const int n = p.n_sel;
+  for (int e = tid; e < nqc * n; e += nthr) {
+    const int i = e / n, k = e % n;
+    m.qsel[e] = p.idx[p.src_row[q0 + i] * n + k];
+    if (k == 0) {
+      m.qcount[i] = p.idx_count[p.src_row[q0 + i]];
+      const int pos = p.pos[q0 + i];
+      const int bound = max(0, pos + 1 - p.lag);
+      m.qbound[i] = min(bound, p.rows);
+      m.qwlo[i] = max(0, pos - p.w + 1);
+      m.qwhi[i] = min(pos, p.rows - 1);
+      m.qmvis[i] = visible_blocks(bound, p);
+    }
   }
   for (int i = tid; i < words; i += nthr) m.bitmap[i] = 0u;
   named_bar_sync(2, nthr);
-  // window range of the chunk
   int wlo = 0x7fffffff, whi = -1;
   for (int i = 0; i < nqc; ++i) {
     wlo = min(wlo, m.qwlo[i]);
@@ -142,17 +188,14 @@ __device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int
   }
   for (int b = wlo / p.l_sel + tid; b <= whi / p.l_sel; b += nthr)
     atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
-  for (int e = tid; e < nqc * p.n_sel; e += nthr) {
-    const int i = e / p.n_sel, k = e % p.n_sel;
-    const int src = p.src_row[q0 + i];
-    if (k >= p.idx_count[src]) continue;
-    const int b = p.idx[src * p.n_sel + k];
-    if (b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
+  for (int e = tid; e < nqc * n; e += nthr) {
+    const int i = e / n, k = e % n;
+    const int b = m.qsel[e];
+    if (k >= m.qcount[i] || b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
     atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
   }
   named_bar_sync(2, nthr);
-  // exclusive prefix of popcounts (one warp; words <= kMaxUnionWords)
-  if (tid < 32) {
+  if (tid < 32) {  // exclusive prefix of popcounts
     const int per = (words + 31) / 32;
     const int w0 = tid * per;
     int local = 0;
@@ -185,12 +228,10 @@ __device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int
     }
   }
   named_bar_sync(2, nthr);
-  for (int e = tid; e < nqc * p.n_sel; e += nthr) {
-    const int i = e / p.n_sel, k = e % p.n_sel;
-    const int src = p.src_row[q0 + i];
-    if (k >= p.idx_count[src]) continue;
-    const int b = p.idx[src * p.n_sel + k];
-    if (b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
+  for (int e = tid; e < nqc * n; e += nthr) {
+    const int i = e / n, k = e % n;
+    const int b = m.qsel[e];
+    if (k >= m.qcount[i] || b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
     const int w = b >> 5;
     const int r = m.word_prefix[w] + __popc(m.bitmap[w] & ((1u << (b & 31)) - 1u));
     if (r < kMaxUnion) atomicOr(&m.union_own[r], 1u << i);
@@ -200,13 +241,12 @@ __device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int
 
 struct TileInfo {
   int kind;
-  int base;      // cmp: first compressed block; tok: union index of the first half
-  bool act_a;    // branch A (cmp or slc) has work
-  bool act_b;    // branch B (win) has work
+  int base;    // cmp: first compressed block; tok: union index of the first half
+  bool act_a;  // branch A (cmp or slc) has work
+  bool act_b;  // branch B (win) has work
 };
 
-__device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int nqc, int wlo, int whi,
-                                              int l_sel) {
+__device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int wlo, int whi, int l_sel) {
   TileInfo ti;
   if (t < m.n_cmp_tiles) {
     ti.kind = kTileCmp;
@@ -216,10 +256,9 @@ __device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int nqc, int
   } else if (t < m.n_cmp_tiles + m.n_tok_tiles) {
     ti.kind = kTileTok;
     ti.base = 2 * (t - m.n_cmp_tiles);
-    const uint32_t own0 = m.union_own[ti.base];
     const int b0 = m.union_blk[ti.base];
     bool win = (b0 * l_sel <= whi) && (b0 * l_sel + l_sel - 1 >= wlo);
-    uint32_t own = own0;
+    uint32_t own = m.union_own[ti.base];
     if (ti.base + 1 < m.n_union) {
       const int b1 = m.union_blk[ti.base + 1];
       own |= m.union_own[ti.base + 1];
@@ -245,15 +284,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int split = blockIdx.x;  // == cluster rank (cluster dims (n_splits,1,1))
+  const int split = blockIdx.x;
   const int kvh = blockIdx.y;
   const int chunk = blockIdx.z;
+  const int S = p.n_splits;
+  const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   const int q0 = chunk * p.qc_size;
   const int nqc = min(p.qc_size, p.nq - q0);
   const int ncols = nqc * p.G;
   const int nqk = (ncols + 15) & ~15;
-  const int S = p.n_splits;
-  const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const int nch = nqk >> 4;  // 16-column chunks holding valid columns
+  const int gshift = __ffs(p.G) - 1;
+  const bool trace = p.trace != nullptr;
 
   // ---- barriers + TMEM -----------------------------------------------------
   if (tid == 0) {
@@ -262,33 +304,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&m.v_full[i], 1);
       mbar_init(&m.kv_empty[i], 1);
       mbar_init(&m.s_full[i], 1);
-      mbar_init(&m.s_free[i], 128);
+      mbar_init(&m.s_free[i], kSoftWarps);
       mbar_init(&m.pv_done[i], 1);
     }
-    mbar_init(&m.p_full, 128);
-    mbar_init(&m.setup, 128);
+    mbar_init(&m.p_full, kSoftWarps);
+    mbar_init(&m.q_ready, kSoftWarps);
+    mbar_init(&m.union_ready, kSoftWarps);
     fence_mbar_init();
   }
-  if (warp == 4) {
-    tmem_alloc<kTmemCols>(&m.tmem_base);
-  }
-  if (warp == 4 && lane == 0) {
-    tma_prefetch(&p.tm_k);
-    tma_prefetch(&p.tm_v);
-    tma_prefetch(&p.tm_ck);
-    tma_prefetch(&p.tm_cv);
-  }
-  // compressed tiles do not depend on the union; every CTA can count them now
-  int mmax = 0;
+  if (warp == kWarpTma) tmem_alloc<kTmemCols>(&m.tmem_base);
+  int mmax = 0;  // compressed tiles do not depend on the union
   for (int i = 0; i < nqc; ++i) mmax = max(mmax, visible_blocks(max(0, p.pos[q0 + i] + 1 - p.lag), p));
   const int n_cmp = (mmax + kTile - 1) / kTile;
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = m.tmem_base;
-  if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 0] = globaltimer();
-
-  // chunk window range (for branch-activity flags)
   int cwlo = 0x7fffffff, cwhi = -1;
   for (int i = 0; i < nqc; ++i) {
     const int pos = p.pos[q0 + i];
@@ -296,19 +323,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     cwhi = max(cwhi, min(pos, p.rows - 1));
   }
   const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
-  const int nch = nqk >> 4;  // 16-column chunks holding valid columns
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = m.tmem_base;
+  if (trace && tid == 0) p.trace[cta_id * 64 + 0] = globaltimer();
 
-  if (warp < kWarpsSoftmax) {
-    // =================== setup: Q (hi/lo bf16), union, O := 0 ===================
-    // Q rows c = qlocal*G + g, K-major SW128; all loads issued before use
+  if (warp < kSoftWarps) {
+    const int qd = warp & 3, ck = warp >> 2;  // TMEM lane quadrant, column chunk
+    // =================== setup: Q (pre-scaled, hi/lo bf16), O := 0 ===================
     {
-      float4 xa[8], xb[8];
+      // 64 rows x 16 units of 8 elements: 2 units per thread, loads first
+      float4 xa[2], xb[2];
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int unit = tid + it * 128;
+      for (int it = 0; it < 2; ++it) {
+        const int unit = tid + it * kSoftThreads;
         const int c = unit >> 4, u16 = unit & 15;
         if (c < ncols) {
-          const int qg = q0 + (c >> (__ffs(p.G) - 1));
+          const int qg = q0 + (c >> gshift);
           const int h = kvh * p.G + (c & (p.G - 1));
           const float4* src = reinterpret_cast<const float4*>(p.q + ((int64_t)qg * p.Hq + h) * kDh + u16 * 8);
           xa[it] = src[0];
@@ -319,10 +351,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int unit = tid + it * 128;
+      for (int it = 0; it < 2; ++it) {
+        const int unit = tid + it * kSoftThreads;
         const int c = unit >> 4, u16 = unit & 15;
-        const float x[8] = {xa[it].x, xa[it].y, xa[it].z, xa[it].w, xb[it].x, xb[it].y, xb[it].z, xb[it].w};
+        const float sc = p.scale_log2;
+        const float x[8] = {xa[it].x * sc, xa[it].y * sc, xa[it].z * sc, xa[it].w * sc,
+                            xb[it].x * sc, xb[it].y * sc, xb[it].z * sc, xb[it].w * sc};
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -335,48 +369,236 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
+      uint32_t z[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) z[i] = 0u;
+      const uint32_t orow = tmem + ((uint32_t)(qd * 32) << 16) + kTmemO + 16 * ck;
+#pragma unroll
+      for (int br = 0; br < 3; ++br) tmem_st16(orow + 64 * br, z);
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m.q_ready);
     }
     if (tid == 0) m.n_cmp_tiles = n_cmp;
-    build_union(p, m, q0, nqc, tid, 128);
+    for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
+      (&m.m2[0][0])[i] = -INFINITY;
+      (&m.thr[0][0])[i] = -INFINITY;
+      for (int w = 0; w < 4; ++w) (&m.lsum[w][0][0])[i] = 0.f;
+    }
+    build_union(p, m, q0, nqc, tid, kSoftThreads);
     if (tid == 0) {
       m.n_tok_tiles = (m.n_union + 1) / 2;
       m.n_tree_tiles = has_tree ? 1 : 0;
     }
-    for (int i = tid; i < 3 * kCols; i += 128) {
-      (&m.m2[0][0])[i] = -INFINITY;
-      for (int w = 0; w < 4; ++w) (&m.lsum[w][0][0])[i] = 0.f;
-    }
-    {
-      uint32_t z[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) z[i] = 0u;
-#pragma unroll 1
-      for (int c = 0; c < 3 * kCols; c += 16)
-        tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + kTmemO + c, z);
-      tmem_wait_st();
-    }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    mbar_arrive(&m.setup);
-  }
+    named_bar_sync(1, kSoftThreads);
+    if (lane == 0) mbar_arrive(&m.union_ready);
+    if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
 
-  if (warp == 4) {
+    // =================== per tile: masks, lazy max, P, row sums ===================
+    const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+    const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
+    const int row = qd * 32 + lane;  // key row within the tile
+    const uint32_t lanebase = tmem + ((uint32_t)(qd * 32) << 16);
+    const int c0 = 16 * ck;
+    bool prev_b = false;  // previous tile wrote the branch-B P region
+#pragma unroll 1
+    for (int j = 0; j < T; ++j) {
+      const int t = split + j * S;
+      const int st = j & 1, sb = j & 1;
+      const TileInfo ti = tile_info(m, t, cwlo, cwhi, p.l_sel);
+      // per-query masks of this key row -> 16-bit column masks of this chunk
+      uint32_t bits_a = 0u, bits_b = 0u;
+      if (ti.kind == kTileCmp) {
+        const int i = ti.base + row;
+        for (int qi = 0; qi < nqc; ++qi) bits_a |= (i < m.qmvis[qi] ? 1u : 0u) << qi;
+      } else if (ti.kind == kTileTok) {
+        const int u = ti.base + (row >> 6);
+        if (u < m.n_union) {
+          const int tok = m.union_blk[u] * p.l_sel + (row & 63);
+          const uint32_t own = m.union_own[u];
+          for (int qi = 0; qi < nqc; ++qi) {
+            bits_a |= ((((own >> qi) & 1u) != 0u) && tok < m.qbound[qi] ? 1u : 0u) << qi;
+            bits_b |= (tok >= m.qwlo[qi] && tok <= m.qwhi[qi] ? 1u : 0u) << qi;
+          }
+        }
+      } else {
+        for (int qi = 0; qi < nqc; ++qi) {
+          const int qg = q0 + qi;
+          if (qg >= 1 && row < 64) bits_b |= (uint32_t)((p.tree_mask[qg - 1] >> row) & 1ull) << qi;
+        }
+      }
+      uint32_t cm[2] = {0u, 0u};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int c = c0 + e;
+        const bool inb = c < ncols;
+        cm[0] |= (inb && ((bits_a >> (c >> gshift)) & 1u) ? 1u : 0u) << e;
+        cm[1] |= (inb && ((bits_b >> (c >> gshift)) & 1u) ? 1u : 0u) << e;
+      }
+      // S^T rows of this quadrant, this warp's 16 columns (log2 units)
+      float s[16];
+      mbar_sleep_wait(&m.s_full[sb], (j >> 1) & 1);
+      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 24 + j] = globaltimer();
+      tc_fence_after();
+      if (ck < nch) {
+        uint32_t r[16];
+        tmem_ld16(lanebase + kTmemS + 64 * sb + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[e] = __uint_as_float(r[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s[e] = 0.f;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m.s_free[sb]);
+
+      // ---- lazy running max per active branch (CTA-wide vote) ----
+      bool resc[2] = {false, false};
+#pragma unroll 1
+      for (int side = 0; side < 2; ++side) {
+        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
+        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+        bool need = false;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          need |= ((cm[side] >> e) & 1u) && (s[e] > m.thr[br][c0 + e]);
+        const bool any_w = __any_sync(0xffffffffu, need);
+        if (lane == 0) m.vote[warp] = any_w ? 1 : 0;
+        named_bar_sync(1, kSoftThreads);
+        int any = 0;
+#pragma unroll
+        for (int w = 0; w < kSoftWarps; ++w) any |= m.vote[w];
+        named_bar_sync(1, kSoftThreads);
+        if (!any) continue;
+        resc[side] = true;
+        float v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = ((cm[side] >> e) & 1u) ? s[e] : -INFINITY;
+        const float mx = reduce16<true>(v, lane);
+        if ((lane & 1) == 0) m.tmax[qd][c0 + (lane >> 1)] = mx;
+        named_bar_sync(1, kSoftThreads);
+        if (tid < kCols) {
+          const float old = m.m2[br][tid];
+          const float tm = fmaxf(fmaxf(m.tmax[0][tid], m.tmax[1][tid]), fmaxf(m.tmax[2][tid], m.tmax[3][tid]));
+          const float nw = tm > old ? tm : old;
+          const float al = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
+          m.alpha[tid] = al;
+          m.m2[br][tid] = nw;
+          m.thr[br][tid] = nw + kRescaleThresh;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) m.lsum[w][br][tid] *= al;
+        }
+        named_bar_sync(1, kSoftThreads);
+        // O^T[dh rows of this quadrant][this chunk] *= alpha, after the
+        // previous tile's PV is complete
+        if (j > 0) mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+        if (ck < nch) {
+          const uint32_t ta = lanebase + kTmemO + 64 * br + c0;
+          uint32_t r[16];
+          tmem_ld16(ta, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * m.alpha[c0 + e]);
+          tmem_st16(ta, r);
+          tmem_wait_st();
+        }
+        named_bar_sync(1, kSoftThreads);  // alpha is reused by the other side
+      }
+      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
+      // the shared branch-B P region is rewritten only after the previous
+      // tile's PV read it (branch-A P lives in this tile's own K stage)
+      if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
+        mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+
+      // ---- probabilities -> P^T (MN-major SW128, hi + lo), row sums ----
+#pragma unroll 1
+      for (int side = 0; side < 2; ++side) {
+        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
+        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+        uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
+        float pv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pv[e] = ((cm[side] >> e) & 1u) ? fast_exp2(s[e] - m.m2[br][c0 + e]) : 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+            const float2 hf = __bfloat1622float2(h2);
+            hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+            lo[e] = pack_bf16(a - hf.x, b - hf.y);
+          }
+          const uint32_t off = sw128_off(row, 2 * ck + h);
+          *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        if (ck < nch) {
+          const float sum = reduce16<false>(pv, lane);
+          if ((lane & 1) == 0) m.lsum[qd][br][c0 + (lane >> 1)] += sum;
+        }
+      }
+      prev_b = ti.act_b;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m.p_full);
+      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 32 + j] = globaltimer();
+    }
+    if (trace && tid == 0) p.trace[cta_id * 64 + 2] = globaltimer();
+    // ---- epilogue: partial (m, l, O) of this split -> workspace ----
+    if (T > 0) mbar_sleep_wait(&m.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
+    tc_fence_after();
+    named_bar_sync(1, kSoftThreads);
+    const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
+    float* ws_ml = p.ws + unit * (3 * kCols * 2);
+    float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
+    for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
+      const int br = i / kCols, c = i % kCols;
+      ws_ml[2 * i] = m.m2[br][c];
+      ws_ml[2 * i + 1] = m.lsum[0][br][c] + m.lsum[1][br][c] + m.lsum[2][br][c] + m.lsum[3][br][c];
+    }
+    if (ck < nch) {
+#pragma unroll 1
+      for (int br = 0; br < 3; ++br) {
+        uint32_t r[16];
+        tmem_ld16(lanebase + kTmemO + 64 * br + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (c0 + e < ncols) ws_o[((int64_t)br * kCols + c0 + e) * kDh + row] = __uint_as_float(r[e]);
+      }
+    }
+    if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
+  } else if (warp == kWarpTma) {
     // =================== TMA producer ===================
     if (lane == 0) {
-      bool setup_seen = false;
+      tma_prefetch(&p.tm_k);
+      tma_prefetch(&p.tm_v);
+      tma_prefetch(&p.tm_ck);
+      tma_prefetch(&p.tm_cv);
+      bool union_seen = false;
       int n_total = 0x7fffffff;
       for (int j = 0;; ++j) {
         const int t = split + j * S;
-        if (t >= n_cmp && !setup_seen) {
-          mbar_wait(&m.setup, 0);
-          setup_seen = true;
+        if (t >= n_cmp && !union_seen) {
+          mbar_sleep_wait(&m.union_ready, 0);
+          union_seen = true;
           n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
         }
         if (t >= n_total) break;
         const int st = j & 1;
-        if (j >= 2) mbar_wait(&m.kv_empty[st], ((j >> 1) + 1) & 1);
+        if (j >= 2) mbar_sleep_wait(&m.kv_empty[st], ((j >> 1) + 1) & 1);
         uint8_t* kdst = smem + kOffK + st * kStageBytes;
         uint8_t* vdst = smem + kOffV + st * kStageBytes;
+        if (trace && j < 8) p.trace[cta_id * 64 + 8 + j] = globaltimer();
         mbar_expect_tx(&m.k_full[st], kStageBytes);
         mbar_expect_tx(&m.v_full[st], kStageBytes);
         const CUtensorMap *tk, *tv;
@@ -406,19 +628,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else {
     // =================== MMA issuer (one thread) ===================
-    mbar_wait(&m.setup, 0);
-    tc_fence_after();
-    const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-    const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
-    if (lane == 0 && T > 0) {
+    if (lane == 0) {
+      mbar_sleep_wait(&m.q_ready, 0);
+      mbar_sleep_wait(&m.union_ready, 0);
+      tc_fence_after();
+      const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+      const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
       const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
       const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
       auto issue_qk = [&](int j) {
         const int st = j & 1, sb = j & 1;
-        if (j >= 2) mbar_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
-        mbar_wait(&m.k_full[st], (j >> 1) & 1);
+        if (j >= 2) mbar_sleep_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
+        mbar_sleep_wait(&m.k_full[st], (j >> 1) & 1);
+        if (trace && j < 8) p.trace[cta_id * 64 + 16 + j] = globaltimer();
         tc_fence_after();
         const uint32_t kaddr = sbase + kOffK + st * kStageBytes;
         const uint32_t qaddr = sbase + kOffQ;
@@ -435,19 +659,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&m.s_full[sb]);
       };
-      issue_qk(0);
+      if (T > 0) issue_qk(0);
       for (int j = 0; j < T; ++j) {
         if (j + 1 < T) issue_qk(j + 1);
         const int st = j & 1;
-        const TileInfo ti = tile_info(m, split + j * S, nqc, cwlo, cwhi, p.l_sel);
-        mbar_wait(&m.p_full, j & 1);
-        mbar_wait(&m.v_full[st], (j >> 1) & 1);
+        const TileInfo ti = tile_info(m, split + j * S, cwlo, cwhi, p.l_sel);
+        mbar_sleep_wait(&m.p_full, j & 1);
+        mbar_sleep_wait(&m.v_full[st], (j >> 1) & 1);
+        if (trace && j < 8) p.trace[cta_id * 64 + 40 + j] = globaltimer();
         tc_fence_after();
         const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
 #pragma unroll 1
         for (int side = 0; side < 2; ++side) {
           if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
-          // P of branch A lives in this tile's K stage; P of branch B in its own region
           const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
           const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
           const uint32_t d = tmem + kTmemO + 64 * br;
@@ -463,244 +687,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else {
-    // =================== softmax / masking / P (warps 0-3) ===================
-    mbar_wait(&m.setup, 0);  // own arrival completed; makes union visible
-    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 1] = globaltimer();
-    const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-    const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
-    const int row = warp * 32 + lane;  // key row within the tile
-    const int gshift = __ffs(p.G) - 1;
-    const uint32_t srow = tmem + ((uint32_t)(warp * 32) << 16);
-    bool prev_b = false;  // previous tile wrote the branch-B P region
-#pragma unroll 1
-    for (int j = 0; j < T; ++j) {
-      const int t = split + j * S;
-      const int st = j & 1, sb = j & 1;
-      const TileInfo ti = tile_info(m, t, nqc, cwlo, cwhi, p.l_sel);
-      // per-query masks for this key row
-      uint32_t bits_a = 0u, bits_b = 0u;
-      if (ti.kind == kTileCmp) {
-        const int i = ti.base + row;
-        for (int qi = 0; qi < nqc; ++qi) bits_a |= (i < m.qmvis[qi] ? 1u : 0u) << qi;
-      } else if (ti.kind == kTileTok) {
-        const int u = ti.base + (row >> 6);
-        if (u < m.n_union) {
-          const int tok = m.union_blk[u] * p.l_sel + (row & 63);
-          const uint32_t own = m.union_own[u];
-          for (int qi = 0; qi < nqc; ++qi) {
-            bits_a |= ((((own >> qi) & 1u) != 0u) && tok < m.qbound[qi] ? 1u : 0u) << qi;
-            bits_b |= (tok >= m.qwlo[qi] && tok <= m.qwhi[qi] ? 1u : 0u) << qi;
-          }
-        }
-      } else {
-        for (int qi = 0; qi < nqc; ++qi) {
-          const int qg = q0 + qi;
-          if (qg >= 1 && row < 64) bits_b |= (uint32_t)((p.tree_mask[qg - 1] >> row) & 1ull) << qi;
-        }
-      }
-      mbar_wait(&m.s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t sbuf = srow + kTmemS + 64 * sb;
-
-      // ---- lazy running max per active branch (block-wide vote) ----
-      bool resc[2] = {false, false};
-#pragma unroll 1
-      for (int side = 0; side < 2; ++side) {
-        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
-        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-        const uint32_t bits = side == 0 ? bits_a : bits_b;
-        bool need = false;
-#pragma unroll 1
-        for (int k = 0; k < nch; ++k) {
-          uint32_t r[16];
-          tmem_ld16(sbuf + 16 * k, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c = 16 * k + e;
-            const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
-            need |= valid && (__uint_as_float(r[e]) * p.scale_log2 > m.m2[br][c] + kRescaleThresh);
-          }
-        }
-        const bool any_w = __any_sync(0xffffffffu, need);
-        if (lane == 0) m.vote[warp] = any_w ? 1 : 0;
-        named_bar_sync(1, 128);
-        const bool any = (m.vote[0] | m.vote[1] | m.vote[2] | m.vote[3]) != 0;
-        named_bar_sync(1, 128);
-        if (!any) continue;
-        resc[side] = true;
-#pragma unroll 1
-        for (int k = 0; k < nch; ++k) {
-          uint32_t r[16];
-          tmem_ld16(sbuf + 16 * k, r);
-          tmem_wait_ld();
-          float v[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c = 16 * k + e;
-            const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
-            v[e] = valid ? __uint_as_float(r[e]) * p.scale_log2 : -INFINITY;
-          }
-          const float mx = reduce16<true>(v, lane);
-          if ((lane & 1) == 0) m.tmax[warp][16 * k + (lane >> 1)] = mx;
-        }
-        named_bar_sync(1, 128);
-        if (tid < 16 * nch) {
-          const float old = m.m2[br][tid];
-          const float tm = fmaxf(fmaxf(m.tmax[0][tid], m.tmax[1][tid]), fmaxf(m.tmax[2][tid], m.tmax[3][tid]));
-          const float nw = tm > old ? tm : old;
-          const float al = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
-          m.alpha[side][tid] = al;
-          m.m2[br][tid] = nw;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) m.lsum[w][br][tid] *= al;
-        }
-        named_bar_sync(1, 128);
-      }
-      // PV of the previous tile must be complete before O is rescaled or the
-      // shared branch-B P region is rewritten (branch-A P lives in this tile's
-      // own K stage, whose previous PV completed before the stage was reloaded)
-      if (j > 0 && (resc[0] || resc[1] || (ti.act_b && prev_b)))
-        mbar_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int side = 0; side < 2; ++side) {
-        if (!resc[side]) continue;
-        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-        const uint32_t ta = srow + kTmemO + 64 * br;
-#pragma unroll 1
-        for (int k = 0; k < nch; ++k) {
-          uint32_t r[16];
-          tmem_ld16(ta + 16 * k, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            r[e] = __float_as_uint(__uint_as_float(r[e]) * m.alpha[side][16 * k + e]);
-          tmem_st16(ta + 16 * k, r);
-        }
-        tmem_wait_st();
-      }
-      // ---- probabilities -> P^T (MN-major SW128, hi + lo), row sums ----
-#pragma unroll 1
-      for (int side = 0; side < 2; ++side) {
-        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
-        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-        const uint32_t bits = side == 0 ? bits_a : bits_b;
-        uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
-#pragma unroll 1
-        for (int k = 0; k < 4; ++k) {
-          if (k >= nch) {  // columns beyond the valid chunks: P = 0
-            const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t off = sw128_off(row, 2 * k + h);
-              *reinterpret_cast<uint4*>(pdst + off) = z;
-              *reinterpret_cast<uint4*>(pdst + 16384 + off) = z;
-            }
-            continue;
-          }
-          uint32_t r[16];
-          tmem_ld16(sbuf + 16 * k, r);
-          tmem_wait_ld();
-          float pv[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c = 16 * k + e;
-            const bool valid = c < ncols && ((bits >> (c >> gshift)) & 1u);
-            pv[e] = valid ? fast_exp2(__uint_as_float(r[e]) * p.scale_log2 - m.m2[br][c]) : 0.f;
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t hi[4], lo[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
-              const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-              const float2 hf = __bfloat1622float2(h2);
-              hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
-              lo[e] = pack_bf16(a - hf.x, b - hf.y);
-            }
-            const uint32_t off = sw128_off(row, 2 * k + h);
-            *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-          }
-          const float sum = reduce16<false>(pv, lane);
-          if ((lane & 1) == 0) m.lsum[warp][br][16 * k + (lane >> 1)] += sum;
-        }
-      }
-      prev_b = ti.act_b;
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&m.s_free[sb]);
-      mbar_arrive(&m.p_full);
-    }
-    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 2] = globaltimer();
-    // ---- epilogue: partial (m, l, O) of this split -> workspace ----
-    if (T > 0) mbar_wait(&m.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
-    tc_fence_after();
-    named_bar_sync(1, 128);
-    const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
-    float* ws_ml = p.ws + unit * (3 * kCols * 2);
-    float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
-    for (int i = tid; i < 3 * kCols; i += 128) {
-      const int br = i / kCols, c = i % kCols;
-      const float l = m.lsum[0][br][c] + m.lsum[1][br][c] + m.lsum[2][br][c] + m.lsum[3][br][c];
-      ws_ml[2 * i] = m.m2[br][c];
-      ws_ml[2 * i + 1] = l;
-    }
-#pragma unroll 1
-    for (int br = 0; br < 3; ++br) {
-#pragma unroll 1
-      for (int k = 0; k < nch; ++k) {
-        uint32_t r[16];
-        tmem_ld16(srow + kTmemO + 64 * br + 16 * k, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (16 * k + e < ncols) ws_o[((int64_t)br * kCols + 16 * k + e) * kDh + row] = __uint_as_float(r[e]);
-      }
-    }
-    __threadfence();
-    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 3] = globaltimer();
   }
 
-  // ---- cluster-wide merge of the split partials + gated combine ----
+  // ---- merge of the split partials (per-head barrier) + gated combine ----
   tc_fence_before();
   if (S > 1) {
-    cluster_sync_all();
+    int* sync = reinterpret_cast<int*>(p.ws + p.ws_sync_offset) + 2 * (chunk * p.Hkv + kvh);
+    group_barrier(sync, sync + 1, S, tid);
   } else {
     __syncthreads();
   }
-  if (warp < kWarpsSoftmax) {
+  if (warp < kSoftWarps) {
     const int64_t unit0 = ((int64_t)chunk * p.Hkv + kvh) * S;
-    const int dh = tid;
-    for (int c = split; c < ncols; c += S) {
-      const int qg = q0 + (c >> (__ffs(p.G) - 1));
+    const int dh = tid & (kDh - 1);
+    for (int c = split + (tid >> 7) * S; c < ncols; c += 4 * S) {
+      const int qg = q0 + (c >> gshift);
       const int h = kvh * p.G + (c & (p.G - 1));
       float res = 0.f;
 #pragma unroll
       for (int br = 0; br < 3; ++br) {
         float M = -INFINITY;
-        for (int s = 0; s < S; ++s) M = fmaxf(M, p.ws[(unit0 + s) * (3 * kCols * 2) + 2 * (br * kCols + c)]);
+        for (int s2 = 0; s2 < S; ++s2)
+          M = fmaxf(M, p.ws[(unit0 + s2) * (3 * kCols * 2) + 2 * (br * kCols + c)]);
         if (M == -INFINITY) continue;  // empty branch contributes 0 (nsa_attention.cpp:244)
         float L = 0.f, O = 0.f;
-        for (int s = 0; s < S; ++s) {
-          const float* ml = p.ws + (unit0 + s) * (3 * kCols * 2) + 2 * (br * kCols + c);
+        for (int s2 = 0; s2 < S; ++s2) {
+          const float* ml = p.ws + (unit0 + s2) * (3 * kCols * 2) + 2 * (br * kCols + c);
           if (ml[0] == -INFINITY) continue;
           const float f = fast_exp2(ml[0] - M);
           L += ml[1] * f;
-          O += p.ws[p.ws_o_offset + (unit0 + s) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + dh] * f;
+          O += p.ws[p.ws_o_offset + (unit0 + s2) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + dh] * f;
         }
         if (L > 0.f) res += p.gates[((int64_t)qg * p.Hq + h) * 3 + br] * (O / L);
       }
       p.out[((int64_t)qg * p.Hq + h) * kDh + dh] = res;
     }
-    if (p.trace != nullptr && tid == 0) p.trace[cta_id * 8 + 4] = globaltimer();
+    if (trace && tid == 0) p.trace[cta_id * 64 + 4] = globaltimer();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kWarpTma) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
@@ -712,7 +738,7 @@ size_t attend_smem_bytes() { return kOffMisc + sizeof(Misc) + 1024; }
 
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits) {
   const size_t units = (size_t)n_chunks * hkv * n_splits;
-  return units * (3 * kCols * 2) + units * (3 * kCols * kDh);
+  return units * (3 * kCols * 2) + units * (3 * kCols * kDh) + (size_t)n_chunks * hkv * 2;
 }
 
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream) {
@@ -720,49 +746,29 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
   cudaError_t e = cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)attend_smem_bytes());
   if (e != cudaSuccess) return e;
-  if (p.n_splits > 8) {
-    e = cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_splits, p.Hkv, n_chunks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = attend_smem_bytes();
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.n_splits;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeCooperative;  // split CTAs of a head meet at a barrier
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, nsa_attend_kernel, p);
 }
 
-int attend_max_cluster(int want) {
+int attend_max_coresident() {
   cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)attend_smem_bytes());
-  cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  for (int s = want; s >= 1; s >>= 1) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(s, 8, 1);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = attend_smem_bytes();
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = s;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, nsa_attend_kernel, &cfg) == cudaSuccess && n >= 1) {
-      cudaGetLastError();
-      return s;
-    }
-    cudaGetLastError();
-  }
-  return 1;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nsa_attend_kernel, kThreads,
+                                                attend_smem_bytes());
+  cudaGetLastError();
+  return sms * per_sm;
 }
 
 }  // namespace specsv_b200

@@ -25,6 +25,7 @@ struct AttendParams {
   float* ws;                 // split partials
   unsigned long long* trace; // optional per-CTA globaltimer stamps [cta][8] (debug)
   int64_t ws_o_offset;       // float offset of the O partials inside ws
+  int64_t ws_sync_offset;    // float offset of the per-head barrier words (zero-initialised)
   int32_t nq, gamma, Hq, Hkv, G, n_sel;
   int32_t rows, blocks, l, d, l_sel, w, lag;
   int32_t qc_size, n_splits;
@@ -37,7 +38,7 @@ struct AttendParams {
 size_t attend_smem_bytes();
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits);
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream);
-int attend_max_cluster(int want);
+int attend_max_coresident();
 
 // ---- routing (route.cu) -------------------------------------------------------
 constexpr int kRouteTile = 64;      // compressed blocks per R1 CTA

@@ -147,7 +147,8 @@ class Workspace:
     def __init__(self, cfg: NsaConfig, n_queries: int, max_rows: int, device="cuda"):
         c = cfg.c()
         self.nbytes = int(lib().specsv_verify_workspace_size(C.byref(c), n_queries, max_rows))
-        self.buf = torch.empty(max(self.nbytes, 256), dtype=torch.uint8, device=device)
+        # zero-filled once: the library keeps its barrier words consistent afterwards
+        self.buf = torch.zeros(max(self.nbytes, 256), dtype=torch.uint8, device=device)
 
 
 def _args(batch: DraftBatch, sets: IndexSets, out: torch.Tensor, group_size: int, mode: int,

@@ -72,7 +72,7 @@ def trace_attend(rows=65536, gamma=8):
     x = LayerInputs(cfg, rows, gamma, 9)
     case = DeviceCase(cfg, x)
     case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
-    buf = torch.zeros(4096 * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(4096 * 64, dtype=torch.int64, device="cuda")
     abi.lib().specsv_debug_attend_trace(torch.cuda.LongTensor.data_ptr(buf))
     sets = V.IndexSets.empty(case.nq, cfg.n)
     out = torch.zeros(case.nq, cfg.n_q_heads, cfg.d_head, device="cuda")
@@ -81,9 +81,20 @@ def trace_attend(rows=65536, gamma=8):
         V.attend_fused(case.vcfg, case.cache, case.batch, sets, out, case.ws, 4, V.MODE_EXACT, V.ROLE_REUSE)
     torch.cuda.synchronize()
     abi.lib().specsv_debug_attend_trace(None)
-    t = buf.view(-1, 8).cpu().numpy()
+    t = buf.view(-1, 64).cpu().numpy()
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
+    for c in (0, 1, 17, 100):
+        if c >= len(t):
+            continue
+        r = t[c]
+        print(f"cta {c}: start {(r[0]-t0)/1e3:.2f} setup {(r[1]-t0)/1e3:.2f} loop {(r[2]-t0)/1e3:.2f} part {(r[3]-t0)/1e3:.2f} merge {(r[4]-t0)/1e3:.2f}")
+        for j in range(8):
+            ev = [r[8 + j], r[16 + j], r[24 + j], r[48 + j], r[32 + j], r[40 + j]]
+            if ev[0] == 0:
+                break
+            print("   tile", j, " ".join(f"{(x - t0) / 1e3:7.2f}" if x else "   -   " for x in ev),
+                  "(tma, qk, s_full, vote, p_full, pv)")
     print("ctas", len(t))
     for name, col in (("setup", 1), ("tiles", 2), ("partials", 3), ("merge", 4)):
         d = (t[:, col] - t0) / 1e3
