@@ -46,11 +46,13 @@ constexpr int kTile = 128;
 constexpr int kCols = 64;          // query columns (queries x heads) per CTA
 constexpr int kSoftWarps = 16;     // 4 lane quadrants x 4 column chunks
 constexpr int kSoftThreads = kSoftWarps * 32;
+constexpr int kMaxSplits = 18;
 constexpr int kWarpTma = 16;
 constexpr int kThreads = 18 * 32;  // + TMA warp + MMA warp
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTmemS = 0;          // two S buffers at cols 0, 64
 constexpr int kTmemO = 128;        // O_cmp 128, O_slc 192, O_win 256
+constexpr int kTmemL = 320;        // row sums via ones-MMA: L_cmp 320, L_slc 384, L_win 448
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr uint32_t kSleepNs = 20000;
 
@@ -59,7 +61,8 @@ constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P of bran
 constexpr uint32_t kOffV = 65536;    // 2 stages x 32 KB
 constexpr uint32_t kOffQ = 131072;   // Q hi 16 KB, Q lo 16 KB
 constexpr uint32_t kOffPB = 163840;  // P of branch B (window): hi 16 KB, lo 16 KB
-constexpr uint32_t kOffMisc = 196608;
+constexpr uint32_t kOffOnes = 196608;  // 1 KB of bf16 1.0 (A operand of the row-sum MMA)
+constexpr uint32_t kOffMisc = 197632;
 constexpr uint32_t kStageBytes = 32768;
 
 enum Branch { kCmp = 0, kSlc = 1, kWin = 2 };
@@ -70,12 +73,11 @@ struct Misc {
   uint64_t p_full, q_ready, union_ready;
   uint32_t tmem_base;
   int32_t n_union, n_cmp_tiles, n_tok_tiles, n_tree_tiles;
-  int32_t vote[kSoftWarps];
   float m2[3][kCols];    // running max (log2 units) per branch and column
   float thr[3][kCols];   // m2 + threshold
   float alpha[kCols];
   float tmax[4][kCols];
-  float lsum[4][3][kCols];  // per-quadrant row sums of P
+  int32_t vote[4][kCols / 16];  // [quadrant][chunk]
   int32_t qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
   int32_t qcount[kMaxChunkQ];
   int32_t qsel[kMaxChunkQ * 64];
@@ -331,12 +333,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp < kSoftWarps) {
     const int qd = warp & 3, ck = warp >> 2;  // TMEM lane quadrant, column chunk
-    // =================== setup: Q (pre-scaled, hi/lo bf16), O := 0 ===================
+    const int c0 = 16 * ck;
+    const uint32_t lanebase = tmem + ((uint32_t)(qd * 32) << 16);
+    // =================== setup: one global round trip for q and the index sets ===================
     {
-      // 64 rows x 16 units of 8 elements: 2 units per thread, loads first
+      const int n = p.n_sel;
       float4 xa[2], xb[2];
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {
+      for (int it = 0; it < 2; ++it) {  // 64 rows x 16 units of 8 elements, 2 units per thread
         const int unit = tid + it * kSoftThreads;
         const int c = unit >> 4, u16 = unit & 15;
         if (c < ncols) {
@@ -349,6 +353,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           xa[it] = make_float4(0.f, 0.f, 0.f, 0.f);
           xb[it] = xa[it];
         }
+      }
+      for (int e = tid; e < nqc * n; e += kSoftThreads) {
+        const int i = e / n, k = e % n;
+        m.qsel[e] = p.idx[p.src_row[q0 + i] * n + k];
+        if (k == 0) m.qcount[i] = p.idx_count[p.src_row[q0 + i]];
       }
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
@@ -369,12 +378,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
+      if (tid < 64)  // bf16 ones for the row-sum MMA
+        reinterpret_cast<uint4*>(smem + kOffOnes)[tid] =
+            make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
       uint32_t z[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) z[i] = 0u;
-      const uint32_t orow = tmem + ((uint32_t)(qd * 32) << 16) + kTmemO + 16 * ck;
 #pragma unroll
-      for (int br = 0; br < 3; ++br) tmem_st16(orow + 64 * br, z);
+      for (int br = 0; br < 3; ++br) {
+        tmem_st16(lanebase + kTmemO + 64 * br + c0, z);
+        tmem_st16(lanebase + kTmemL + 64 * br + c0, z);
+      }
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
@@ -385,7 +399,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
       (&m.m2[0][0])[i] = -INFINITY;
       (&m.thr[0][0])[i] = -INFINITY;
-      for (int w = 0; w < 4; ++w) (&m.lsum[w][0][0])[i] = 0.f;
     }
     build_union(p, m, q0, nqc, tid, kSoftThreads);
     if (tid == 0) {
@@ -396,47 +409,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) mbar_arrive(&m.union_ready);
     if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
 
-    // =================== per tile: masks, lazy max, P, row sums ===================
+    // =================== per tile: masks, lazy max, P ===================
     const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
     const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
     const int row = qd * 32 + lane;  // key row within the tile
-    const uint32_t lanebase = tmem + ((uint32_t)(qd * 32) << 16);
-    const int c0 = 16 * ck;
+    // the queries whose columns this warp owns, and the column masks they map to
+    const int gw = p.G < 16 ? p.G : 16;                  // columns per query in this chunk
+    const int qa = c0 >> gshift;                         // first chunk query (chunk-local)
+    const int nqa = p.G < 16 ? (16 >> gshift) : 1;       // queries in this chunk
+    const uint32_t qmask_w = (gw == 32) ? 0xFFFFFFFFu : ((1u << gw) - 1u);
+    const uint32_t colvalid = ncols - c0 >= 16 ? 0xFFFFu : (ncols > c0 ? ((1u << (ncols - c0)) - 1u) : 0u);
+    const int bar_chunk = 3 + ck;                        // named barrier of this chunk's 4 warps
     bool prev_b = false;  // previous tile wrote the branch-B P region
 #pragma unroll 1
     for (int j = 0; j < T; ++j) {
       const int t = split + j * S;
       const int st = j & 1, sb = j & 1;
       const TileInfo ti = tile_info(m, t, cwlo, cwhi, p.l_sel);
-      // per-query masks of this key row -> 16-bit column masks of this chunk
-      uint32_t bits_a = 0u, bits_b = 0u;
+      // per-(row, query) masks for the queries of this chunk -> 16-bit column masks
+      uint32_t cm_a = 0u, cm_b = 0u;
       if (ti.kind == kTileCmp) {
         const int i = ti.base + row;
-        for (int qi = 0; qi < nqc; ++qi) bits_a |= (i < m.qmvis[qi] ? 1u : 0u) << qi;
+        for (int k = 0; k < nqa; ++k) {
+          const int qi = qa + k;
+          if (qi < nqc && i < m.qmvis[qi]) cm_a |= qmask_w << (k * gw);
+        }
       } else if (ti.kind == kTileTok) {
         const int u = ti.base + (row >> 6);
         if (u < m.n_union) {
           const int tok = m.union_blk[u] * p.l_sel + (row & 63);
           const uint32_t own = m.union_own[u];
-          for (int qi = 0; qi < nqc; ++qi) {
-            bits_a |= ((((own >> qi) & 1u) != 0u) && tok < m.qbound[qi] ? 1u : 0u) << qi;
-            bits_b |= (tok >= m.qwlo[qi] && tok <= m.qwhi[qi] ? 1u : 0u) << qi;
+          for (int k = 0; k < nqa; ++k) {
+            const int qi = qa + k;
+            if (qi >= nqc) break;
+            if (((own >> qi) & 1u) && tok < m.qbound[qi]) cm_a |= qmask_w << (k * gw);
+            if (tok >= m.qwlo[qi] && tok <= m.qwhi[qi]) cm_b |= qmask_w << (k * gw);
           }
         }
       } else {
-        for (int qi = 0; qi < nqc; ++qi) {
-          const int qg = q0 + qi;
-          if (qg >= 1 && row < 64) bits_b |= (uint32_t)((p.tree_mask[qg - 1] >> row) & 1ull) << qi;
+        for (int k = 0; k < nqa; ++k) {
+          const int qg = q0 + qa + k;
+          if (qa + k < nqc && qg >= 1 && row < 64 && ((p.tree_mask[qg - 1] >> row) & 1ull))
+            cm_b |= qmask_w << (k * gw);
         }
       }
-      uint32_t cm[2] = {0u, 0u};
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int c = c0 + e;
-        const bool inb = c < ncols;
-        cm[0] |= (inb && ((bits_a >> (c >> gshift)) & 1u) ? 1u : 0u) << e;
-        cm[1] |= (inb && ((bits_b >> (c >> gshift)) & 1u) ? 1u : 0u) << e;
-      }
+      cm_a &= colvalid;
+      cm_b &= colvalid;
       // S^T rows of this quadrant, this warp's 16 columns (log2 units)
       float s[16];
       mbar_sleep_wait(&m.s_full[sb], (j >> 1) & 1);
@@ -456,81 +474,83 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&m.s_free[sb]);
 
-      // ---- lazy running max per active branch (CTA-wide vote) ----
+      // ---- lazy running max per active branch; the 4 warps sharing this
+      // column chunk vote (columns are independent across chunks) ----
       bool resc[2] = {false, false};
 #pragma unroll 1
       for (int side = 0; side < 2; ++side) {
         if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
         const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+        const uint32_t cm = side == 0 ? cm_a : cm_b;
         bool need = false;
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          need |= ((cm[side] >> e) & 1u) && (s[e] > m.thr[br][c0 + e]);
+        for (int e = 0; e < 16; ++e) need |= ((cm >> e) & 1u) && (s[e] > m.thr[br][c0 + e]);
         const bool any_w = __any_sync(0xffffffffu, need);
-        if (lane == 0) m.vote[warp] = any_w ? 1 : 0;
-        named_bar_sync(1, kSoftThreads);
-        int any = 0;
-#pragma unroll
-        for (int w = 0; w < kSoftWarps; ++w) any |= m.vote[w];
-        named_bar_sync(1, kSoftThreads);
+        if (lane == 0) m.vote[qd][ck] = any_w ? 1 : 0;
+        named_bar_sync(bar_chunk, 128);
+        const int any = m.vote[0][ck] | m.vote[1][ck] | m.vote[2][ck] | m.vote[3][ck];
+        named_bar_sync(bar_chunk, 128);
         if (!any) continue;
         resc[side] = true;
         float v[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = ((cm[side] >> e) & 1u) ? s[e] : -INFINITY;
+        for (int e = 0; e < 16; ++e) v[e] = ((cm >> e) & 1u) ? s[e] : -INFINITY;
         const float mx = reduce16<true>(v, lane);
         if ((lane & 1) == 0) m.tmax[qd][c0 + (lane >> 1)] = mx;
-        named_bar_sync(1, kSoftThreads);
-        if (tid < kCols) {
-          const float old = m.m2[br][tid];
-          const float tm = fmaxf(fmaxf(m.tmax[0][tid], m.tmax[1][tid]), fmaxf(m.tmax[2][tid], m.tmax[3][tid]));
+        named_bar_sync(bar_chunk, 128);
+        if (qd == 0 && lane < 16) {
+          const int c = c0 + lane;
+          const float old = m.m2[br][c];
+          const float tm = fmaxf(fmaxf(m.tmax[0][c], m.tmax[1][c]), fmaxf(m.tmax[2][c], m.tmax[3][c]));
           const float nw = tm > old ? tm : old;
-          const float al = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
-          m.alpha[tid] = al;
-          m.m2[br][tid] = nw;
-          m.thr[br][tid] = nw + kRescaleThresh;
-#pragma unroll
-          for (int w = 0; w < 4; ++w) m.lsum[w][br][tid] *= al;
+          m.alpha[c] = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
+          m.m2[br][c] = nw;
+          m.thr[br][c] = nw + kRescaleThresh;
         }
-        named_bar_sync(1, kSoftThreads);
-        // O^T[dh rows of this quadrant][this chunk] *= alpha, after the
-        // previous tile's PV is complete
+        named_bar_sync(bar_chunk, 128);
+        // O^T (and the row-sum accumulator) of this chunk *= alpha, once the
+        // previous tile's MMAs into them are complete
         if (j > 0) mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
         if (ck < nch) {
-          const uint32_t ta = lanebase + kTmemO + 64 * br + c0;
-          uint32_t r[16];
-          tmem_ld16(ta, r);
-          tmem_wait_ld();
+          float al[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * m.alpha[c0 + e]);
-          tmem_st16(ta, r);
+          for (int e = 0; e < 16; ++e) al[e] = m.alpha[c0 + e];
+#pragma unroll 1
+          for (int acc = 0; acc < (qd == 0 ? 2 : 1); ++acc) {
+            const uint32_t ta = lanebase + (acc == 0 ? kTmemO : kTmemL) + 64 * br + c0;
+            uint32_t r[16];
+            tmem_ld16(ta, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
+            tmem_st16(ta, r);
+          }
           tmem_wait_st();
         }
-        named_bar_sync(1, kSoftThreads);  // alpha is reused by the other side
+        named_bar_sync(bar_chunk, 128);  // alpha is reused by the other side
       }
       if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
       // the shared branch-B P region is rewritten only after the previous
-      // tile's PV read it (branch-A P lives in this tile's own K stage)
+      // tile's MMAs read it (branch-A P lives in this tile's own K stage)
       if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
         mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
 
-      // ---- probabilities -> P^T (MN-major SW128, hi + lo), row sums ----
+      // ---- probabilities -> P^T (MN-major SW128, hi + lo) ----
 #pragma unroll 1
       for (int side = 0; side < 2; ++side) {
         if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
         const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+        const uint32_t cm = side == 0 ? cm_a : cm_b;
         uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
-        float pv[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pv[e] = ((cm[side] >> e) & 1u) ? fast_exp2(s[e] - m.m2[br][c0 + e]) : 0.f;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t hi[4], lo[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
+            const int e0 = 8 * h + 2 * e;
+            const float a = ((cm >> e0) & 1u) ? fast_exp2(s[e0] - m.m2[br][c0 + e0]) : 0.f;
+            const float b = ((cm >> (e0 + 1)) & 1u) ? fast_exp2(s[e0 + 1] - m.m2[br][c0 + e0 + 1]) : 0.f;
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
             const float2 hf = __bfloat1622float2(h2);
             hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
@@ -539,10 +559,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t off = sw128_off(row, 2 * ck + h);
           *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
           *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        if (ck < nch) {
-          const float sum = reduce16<false>(pv, lane);
-          if ((lane & 1) == 0) m.lsum[qd][br][c0 + (lane >> 1)] += sum;
         }
       }
       prev_b = ti.act_b;
@@ -556,15 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- epilogue: partial (m, l, O) of this split -> workspace ----
     if (T > 0) mbar_sleep_wait(&m.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
     tc_fence_after();
-    named_bar_sync(1, kSoftThreads);
     const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
     float* ws_ml = p.ws + unit * (3 * kCols * 2);
     float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
-    for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
-      const int br = i / kCols, c = i % kCols;
-      ws_ml[2 * i] = m.m2[br][c];
-      ws_ml[2 * i + 1] = m.lsum[0][br][c] + m.lsum[1][br][c] + m.lsum[2][br][c] + m.lsum[3][br][c];
-    }
     if (ck < nch) {
 #pragma unroll 1
       for (int br = 0; br < 3; ++br) {
@@ -574,6 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           if (c0 + e < ncols) ws_o[((int64_t)br * kCols + c0 + e) * kDh + row] = __uint_as_float(r[e]);
+        if (qd == 0) {  // row sums: every lane of L holds the column sum; lane 0 writes
+          tmem_ld16(lanebase + kTmemL + 64 * br + c0, r);
+          tmem_wait_ld();
+          if (lane == 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              ws_ml[2 * (br * kCols + c0 + e)] = m.m2[br][c0 + e];
+              ws_ml[2 * (br * kCols + c0 + e) + 1] = __uint_as_float(r[e]);
+            }
+          }
+        }
       }
     }
     if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
@@ -632,12 +653,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     // =================== MMA issuer (one thread) ===================
     if (lane == 0) {
       mbar_sleep_wait(&m.q_ready, 0);
-      mbar_sleep_wait(&m.union_ready, 0);
       tc_fence_after();
-      const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-      const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
       const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
       const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
+      const uint32_t idesc_l = idesc_bf16(128, 64, 0, 1);
+      const uint32_t ones = sbase + kOffOnes;
+      // compressed tiles come first and do not need the union; the total tile
+      // count is known once the union is built
+      bool union_seen = false;
+      int T = 0x7fffffff;
+      auto tiles = [&](int j) {
+        if (split + j * S >= n_cmp && !union_seen) {
+          mbar_sleep_wait(&m.union_ready, 0);
+          union_seen = true;
+          const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+          T = split < n_total ? (n_total - split + S - 1) / S : 0;
+        }
+        return j < T;
+      };
       auto issue_qk = [&](int j) {
         const int st = j & 1, sb = j & 1;
         if (j >= 2) mbar_sleep_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
@@ -659,12 +692,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&m.s_full[sb]);
       };
-      if (T > 0) issue_qk(0);
-      for (int j = 0; j < T; ++j) {
-        if (j + 1 < T) issue_qk(j + 1);
+      if (tiles(0)) issue_qk(0);
+      for (int j = 0; tiles(j); ++j) {
+        if (tiles(j + 1)) issue_qk(j + 1);
         const int st = j & 1;
-        const TileInfo ti = tile_info(m, split + j * S, cwlo, cwhi, p.l_sel);
+        if (!union_seen) {  // tile_info of a compressed tile needs no union state
+        }
         mbar_sleep_wait(&m.p_full, j & 1);
+        const TileInfo ti = tile_info(m, split + j * S, cwlo, cwhi, p.l_sel);
         mbar_sleep_wait(&m.v_full[st], (j >> 1) & 1);
         if (trace && j < 8) p.trace[cta_id * 64 + 40 + j] = globaltimer();
         tc_fence_after();
@@ -675,12 +710,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
           const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
           const uint32_t d = tmem + kTmemO + 64 * br;
+          const uint32_t dl = tmem + kTmemL + 64 * br;
 #pragma unroll
           for (int part = 0; part < 2; ++part)
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
-                       desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024), idesc_pv, 1u);
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
+              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
+              // row sums of P: ones[128 x 16] . P^T[16 tokens x 64 cols]; SBO = 0
+              // makes every 8-row group read the same 1 KB of ones
+              umma_f16(dl, desc_sw128(ones + (kk & 3) * 32, 16, 0), bdesc, idesc_l, 1u);
+            }
         }
         umma_commit(&m.pv_done[j & 1]);
         umma_commit(&m.kv_empty[st]);
@@ -704,19 +744,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qg = q0 + (c >> gshift);
       const int h = kvh * p.G + (c & (p.G - 1));
       float res = 0.f;
-#pragma unroll
+#pragma unroll 1
       for (int br = 0; br < 3; ++br) {
+        float mv[kMaxSplits], lv[kMaxSplits], ov[kMaxSplits];
+#pragma unroll
+        for (int s2 = 0; s2 < kMaxSplits; ++s2) {  // all loads in flight at once
+          if (s2 < S) {
+            const float2 ml = *reinterpret_cast<const float2*>(
+                p.ws + (unit0 + s2) * (3 * kCols * 2) + 2 * (br * kCols + c));
+            mv[s2] = ml.x;
+            lv[s2] = ml.y;
+            ov[s2] = p.ws[p.ws_o_offset + (unit0 + s2) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + dh];
+          } else {
+            mv[s2] = -INFINITY;
+            lv[s2] = 0.f;
+            ov[s2] = 0.f;
+          }
+        }
         float M = -INFINITY;
-        for (int s2 = 0; s2 < S; ++s2)
-          M = fmaxf(M, p.ws[(unit0 + s2) * (3 * kCols * 2) + 2 * (br * kCols + c)]);
+#pragma unroll
+        for (int s2 = 0; s2 < kMaxSplits; ++s2) M = fmaxf(M, mv[s2]);
         if (M == -INFINITY) continue;  // empty branch contributes 0 (nsa_attention.cpp:244)
         float L = 0.f, O = 0.f;
-        for (int s2 = 0; s2 < S; ++s2) {
-          const float* ml = p.ws + (unit0 + s2) * (3 * kCols * 2) + 2 * (br * kCols + c);
-          if (ml[0] == -INFINITY) continue;
-          const float f = fast_exp2(ml[0] - M);
-          L += ml[1] * f;
-          O += p.ws[p.ws_o_offset + (unit0 + s2) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + dh] * f;
+#pragma unroll
+        for (int s2 = 0; s2 < kMaxSplits; ++s2) {
+          const float f = mv[s2] == -INFINITY ? 0.f : fast_exp2(mv[s2] - M);
+          L += lv[s2] * f;
+          O += ov[s2] * f;
         }
         if (L > 0.f) res += p.gates[((int64_t)qg * p.Hq + h) * 3 + br] * (O / L);
       }
