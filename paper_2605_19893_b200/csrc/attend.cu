@@ -48,7 +48,7 @@ constexpr int kSoftWarps = 16;     // 4 lane quadrants x 4 column chunks
 constexpr int kSoftThreads = kSoftWarps * 32;
 constexpr int kMaxSplits = 18;
 constexpr int kWarpTma = 16;
-constexpr int kThreads = 18 * 32;  // + TMA warp + MMA warp
+constexpr int kThreads = 19 * 32;  // + TMA warp + QK-MMA warp + PV-MMA warp
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTmemS = 0;          // two S buffers at cols 0, 64
 constexpr int kTmemO = 128;        // O_cmp 128, O_slc 192, O_win 256
@@ -280,7 +280,9 @@ __device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int wlo, int
 __global__ void __launch_bounds__(kThreads, 1)
     nsa_attend_kernel(const __grid_constant__ AttendParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align inside the shared window without leaving the shared address space
+  // (a uintptr_t round trip would turn every Misc access into a generic load)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Misc& m = *reinterpret_cast<Misc*>(smem + kOffMisc);
   const uint32_t sbase = smem_u32(smem);
 
@@ -650,14 +652,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {
-    // =================== MMA issuer (one thread) ===================
+    // =================== MMA issuers: warp 17 = QK^T, warp 18 = PV + row sums ===================
+    // (two issuing threads so a QK waiting for its K tile never delays the PV
+    // of the previous tile; each commit tracks only its own thread's MMAs)
     if (lane == 0) {
       mbar_sleep_wait(&m.q_ready, 0);
       tc_fence_after();
-      const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
-      const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
-      const uint32_t idesc_l = idesc_bf16(128, 64, 0, 1);
-      const uint32_t ones = sbase + kOffOnes;
       // compressed tiles come first and do not need the union; the total tile
       // count is known once the union is built
       bool union_seen = false;
@@ -671,59 +671,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return j < T;
       };
-      auto issue_qk = [&](int j) {
-        const int st = j & 1, sb = j & 1;
-        if (j >= 2) mbar_sleep_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
-        mbar_sleep_wait(&m.k_full[st], (j >> 1) & 1);
-        if (trace && j < 8) p.trace[cta_id * 64 + 16 + j] = globaltimer();
-        tc_fence_after();
-        const uint32_t kaddr = sbase + kOffK + st * kStageBytes;
-        const uint32_t qaddr = sbase + kOffQ;
-        const uint32_t d = tmem + kTmemS + 64 * sb;
+      if (warp == kWarpTma + 1) {
+        const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
+        for (int j = 0; tiles(j); ++j) {
+          const int st = j & 1, sb = j & 1;
+          if (j >= 2) mbar_sleep_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
+          mbar_sleep_wait(&m.k_full[st], (j >> 1) & 1);
+          if (trace && j < 8) p.trace[cta_id * 64 + 16 + j] = globaltimer();
+          tc_fence_after();
+          const uint32_t kaddr = sbase + kOffK + st * kStageBytes;
+          const uint32_t qaddr = sbase + kOffQ;
+          const uint32_t d = tmem + kTmemS + 64 * sb;
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {  // q hi, q lo
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
-            const uint32_t qoff = part * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32;
-            umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
-                     idesc_qk, (part | kk) != 0);
-          }
-        }
-        umma_commit(&m.s_full[sb]);
-      };
-      if (tiles(0)) issue_qk(0);
-      for (int j = 0; tiles(j); ++j) {
-        if (tiles(j + 1)) issue_qk(j + 1);
-        const int st = j & 1;
-        if (!union_seen) {  // tile_info of a compressed tile needs no union state
-        }
-        mbar_sleep_wait(&m.p_full, j & 1);
-        const TileInfo ti = tile_info(m, split + j * S, cwlo, cwhi, p.l_sel);
-        mbar_sleep_wait(&m.v_full[st], (j >> 1) & 1);
-        if (trace && j < 8) p.trace[cta_id * 64 + 40 + j] = globaltimer();
-        tc_fence_after();
-        const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
-#pragma unroll 1
-        for (int side = 0; side < 2; ++side) {
-          if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
-          const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
-          const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-          const uint32_t d = tmem + kTmemO + 64 * br;
-          const uint32_t dl = tmem + kTmemL + 64 * br;
-#pragma unroll
-          for (int part = 0; part < 2; ++part)
+          for (int part = 0; part < 2; ++part) {  // q hi, q lo
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-              const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
-              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
-              // row sums of P: ones[128 x 16] . P^T[16 tokens x 64 cols]; SBO = 0
-              // makes every 8-row group read the same 1 KB of ones
-              umma_f16(dl, desc_sw128(ones + (kk & 3) * 32, 16, 0), bdesc, idesc_l, 1u);
+              const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+              const uint32_t qoff = part * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32;
+              umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
+                       idesc_qk, (part | kk) != 0);
             }
+          }
+          umma_commit(&m.s_full[sb]);
         }
-        umma_commit(&m.pv_done[j & 1]);
-        umma_commit(&m.kv_empty[st]);
+      } else {
+        const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
+        const uint32_t idesc_l = idesc_bf16(128, 64, 0, 1);
+        const uint32_t ones = sbase + kOffOnes;
+        for (int j = 0; tiles(j); ++j) {
+          const int st = j & 1;
+          mbar_sleep_wait(&m.p_full, j & 1);
+          const TileInfo ti = tile_info(m, split + j * S, cwlo, cwhi, p.l_sel);
+          mbar_sleep_wait(&m.v_full[st], (j >> 1) & 1);
+          if (trace && j < 8) p.trace[cta_id * 64 + 40 + j] = globaltimer();
+          tc_fence_after();
+          const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
+#pragma unroll 1
+          for (int side = 0; side < 2; ++side) {
+            if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
+            const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
+            const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+            const uint32_t d = tmem + kTmemO + 64 * br;
+            const uint32_t dl = tmem + kTmemL + 64 * br;
+#pragma unroll
+            for (int part = 0; part < 2; ++part)
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
+                umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
+                // row sums of P: ones[128 x 16] . P^T[16 tokens x 64 cols]; SBO = 0
+                // makes every 8-row group read the same 1 KB of ones
+                umma_f16(dl, desc_sw128(ones + (kk & 3) * 32, 16, 0), bdesc, idesc_l, 1u);
+              }
+          }
+          umma_commit(&m.pv_done[j & 1]);
+          umma_commit(&m.kv_empty[st]);
+        }
       }
     }
     __syncwarp();
