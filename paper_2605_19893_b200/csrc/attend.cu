@@ -52,17 +52,15 @@ constexpr int kThreads = 19 * 32;  // + TMA warp + QK-MMA warp + PV-MMA warp
 constexpr uint32_t kTmemCols = 512;
 constexpr int kTmemS = 0;          // two S buffers at cols 0, 64
 constexpr int kTmemO = 128;        // O_cmp 128, O_slc 192, O_win 256
-constexpr int kTmemL = 320;        // row sums via ones-MMA: L_cmp 320, L_slc 384, L_win 448
+constexpr int kTmemL = 320;        // per-lane partial row sums of P: 320, 384, 448
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-constexpr uint32_t kSleepNs = 20000;
 
 // shared memory map (bytes from the 1024-aligned base)
 constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P of branch A)
 constexpr uint32_t kOffV = 65536;    // 2 stages x 32 KB
 constexpr uint32_t kOffQ = 131072;   // Q hi 16 KB, Q lo 16 KB
 constexpr uint32_t kOffPB = 163840;  // P of branch B (window): hi 16 KB, lo 16 KB
-constexpr uint32_t kOffOnes = 196608;  // 1 KB of bf16 1.0 (A operand of the row-sum MMA)
-constexpr uint32_t kOffMisc = 197632;
+constexpr uint32_t kOffMisc = 196608;
 constexpr uint32_t kStageBytes = 32768;
 
 enum Branch { kCmp = 0, kSlc = 1, kWin = 2 };
@@ -78,6 +76,7 @@ struct Misc {
   float alpha[kCols];
   float tmax[4][kCols];
   int32_t vote[4][kCols / 16];  // [quadrant][chunk]
+  float lred[3][4][kCols];      // row sums per branch, quadrant, column
   int32_t qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
   int32_t qcount[kMaxChunkQ];
   int32_t qsel[kMaxChunkQ * 64];
@@ -100,18 +99,12 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// waits with a hardware suspend hint (no busy spinning of the waiting warp)
+// try_wait already parks the warp briefly in hardware between probes; an
+// explicit suspend-time hint delays the wake-up by up to ~1 us (measured), so
+// latency-critical waits use the plain form
 __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(kSleepNs)
-        : "memory");
-  } while (!ok);
+  while (!mbar_try_wait(bar, parity)) {
+  }
 }
 
 // transpose-reduce of 16 columns across the warp: returns, in lanes 2c and
@@ -380,9 +373,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
-      if (tid < 64)  // bf16 ones for the row-sum MMA
-        reinterpret_cast<uint4*>(smem + kOffOnes)[tid] =
-            make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
       uint32_t z[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) z[i] = 0u;
@@ -396,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&m.q_ready);
+      if (trace && tid == 0) p.trace[cta_id * 64 + 5] = globaltimer();
     }
     if (tid == 0) m.n_cmp_tiles = n_cmp;
     for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
@@ -475,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&m.s_free[sb]);
+      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 56 + j] = globaltimer();
 
       // ---- lazy running max per active branch; the 4 warps sharing this
       // column chunk vote (columns are independent across chunks) ----
@@ -518,16 +510,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           float al[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) al[e] = m.alpha[c0 + e];
-#pragma unroll 1
-          for (int acc = 0; acc < (qd == 0 ? 2 : 1); ++acc) {
-            const uint32_t ta = lanebase + (acc == 0 ? kTmemO : kTmemL) + 64 * br + c0;
-            uint32_t r[16];
-            tmem_ld16(ta, r);
-            tmem_wait_ld();
+          const uint32_t ta = lanebase + kTmemO + 64 * br + c0;
+          uint32_t r[16];
+          tmem_ld16(ta, r);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
-            tmem_st16(ta, r);
-          }
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
+          tmem_st16(ta, r);
+          const uint32_t tl = lanebase + kTmemL + 64 * br + c0;  // per-lane row sums
+          tmem_ld16(tl, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
+          tmem_st16(tl, r);
           tmem_wait_st();
         }
         named_bar_sync(bar_chunk, 128);  // alpha is reused by the other side
@@ -538,21 +533,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
         mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
 
-      // ---- probabilities -> P^T (MN-major SW128, hi + lo) ----
-#pragma unroll 1
+      // ---- probabilities -> P^T (MN-major SW128, hi + lo), per-lane row sums ----
+#pragma unroll
       for (int side = 0; side < 2; ++side) {
         if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
         const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
         const uint32_t cm = side == 0 ? cm_a : cm_b;
         uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
+        float pv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pv[e] = ((cm >> e) & 1u) ? fast_exp2(s[e] - m.m2[br][c0 + e]) : 0.f;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t hi[4], lo[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int e0 = 8 * h + 2 * e;
-            const float a = ((cm >> e0) & 1u) ? fast_exp2(s[e0] - m.m2[br][c0 + e0]) : 0.f;
-            const float b = ((cm >> (e0 + 1)) & 1u) ? fast_exp2(s[e0 + 1] - m.m2[br][c0 + e0 + 1]) : 0.f;
+            const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
             const float2 hf = __bfloat1622float2(h2);
             hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
@@ -562,7 +559,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
           *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
+        if (ck < nch) {  // per-lane row sums live in TMEM (no cross-lane work per tile)
+          const uint32_t tl = lanebase + kTmemL + 64 * br + c0;
+          uint32_t r[16];
+          tmem_ld16(tl, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + pv[e]);
+          tmem_st16(tl, r);
+        }
       }
+      tmem_wait_st();
       prev_b = ti.act_b;
       fence_proxy_async_smem();
       tc_fence_before();
@@ -573,10 +580,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (trace && tid == 0) p.trace[cta_id * 64 + 2] = globaltimer();
     // ---- epilogue: partial (m, l, O) of this split -> workspace ----
     if (T > 0) mbar_sleep_wait(&m.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
+    if (trace && tid == 0) p.trace[cta_id * 64 + 7] = globaltimer();
     tc_fence_after();
     const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
     float* ws_ml = p.ws + unit * (3 * kCols * 2);
     float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
+    // row sums: lanes -> (reduce16) -> quadrants
+#pragma unroll 1
+    for (int br = 0; br < 3; ++br) {
+      uint32_t r[16];
+      tmem_ld16(lanebase + kTmemL + 64 * br + c0, r);
+      tmem_wait_ld();
+      float v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
+      const float sum = reduce16<false>(v, lane);
+      if ((lane & 1) == 0) m.lred[br][qd][c0 + (lane >> 1)] = sum;
+    }
+    named_bar_sync(1, kSoftThreads);
+    for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
+      const int br = i / kCols, c = i % kCols;
+      ws_ml[2 * i] = m.m2[br][c];
+      ws_ml[2 * i + 1] = m.lred[br][0][c] + m.lred[br][1][c] + m.lred[br][2][c] + m.lred[br][3][c];
+    }
     if (ck < nch) {
 #pragma unroll 1
       for (int br = 0; br < 3; ++br) {
@@ -586,17 +612,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           if (c0 + e < ncols) ws_o[((int64_t)br * kCols + c0 + e) * kDh + row] = __uint_as_float(r[e]);
-        if (qd == 0) {  // row sums: every lane of L holds the column sum; lane 0 writes
-          tmem_ld16(lanebase + kTmemL + 64 * br + c0, r);
-          tmem_wait_ld();
-          if (lane == 0) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              ws_ml[2 * (br * kCols + c0 + e)] = m.m2[br][c0 + e];
-              ws_ml[2 * (br * kCols + c0 + e) + 1] = __uint_as_float(r[e]);
-            }
-          }
-        }
       }
     }
     if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
@@ -696,8 +711,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
-        const uint32_t idesc_l = idesc_bf16(128, 64, 0, 1);
-        const uint32_t ones = sbase + kOffOnes;
         for (int j = 0; tiles(j); ++j) {
           const int st = j & 1;
           mbar_sleep_wait(&m.p_full, j & 1);
@@ -712,16 +725,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
             const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
             const uint32_t d = tmem + kTmemO + 64 * br;
-            const uint32_t dl = tmem + kTmemL + 64 * br;
 #pragma unroll
             for (int part = 0; part < 2; ++part)
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk) {
                 const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
                 umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
-                // row sums of P: ones[128 x 16] . P^T[16 tokens x 64 cols]; SBO = 0
-                // makes every 8-row group read the same 1 KB of ones
-                umma_f16(dl, desc_sw128(ones + (kk & 3) * 32, 16, 0), bdesc, idesc_l, 1u);
               }
           }
           umma_commit(&m.pv_done[j & 1]);
@@ -737,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (S > 1) {
     int* sync = reinterpret_cast<int*>(p.ws + p.ws_sync_offset) + 2 * (chunk * p.Hkv + kvh);
     group_barrier(sync, sync + 1, S, tid);
+    if (trace && tid == 0) p.trace[cta_id * 64 + 6] = globaltimer();
   } else {
     __syncthreads();
   }

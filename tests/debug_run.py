@@ -88,13 +88,14 @@ def trace_attend(rows=65536, gamma=8):
         if c >= len(t):
             continue
         r = t[c]
-        print(f"cta {c}: start {(r[0]-t0)/1e3:.2f} setup {(r[1]-t0)/1e3:.2f} loop {(r[2]-t0)/1e3:.2f} part {(r[3]-t0)/1e3:.2f} merge {(r[4]-t0)/1e3:.2f}")
+        print(f"cta {c}: start {(r[0]-t0)/1e3:.2f} q_ready {(r[5]-t0)/1e3:.2f} setup {(r[1]-t0)/1e3:.2f} loop {(r[2]-t0)/1e3:.2f} "
+              f"lastpv {(r[7]-t0)/1e3:.2f} part {(r[3]-t0)/1e3:.2f} barrier {(r[6]-t0)/1e3:.2f} merge {(r[4]-t0)/1e3:.2f}")
         for j in range(8):
-            ev = [r[8 + j], r[16 + j], r[24 + j], r[48 + j], r[32 + j], r[40 + j]]
+            ev = [r[8 + j], r[16 + j], r[24 + j], r[56 + j], r[48 + j], r[32 + j], r[40 + j]]
             if ev[0] == 0:
                 break
             print("   tile", j, " ".join(f"{(x - t0) / 1e3:7.2f}" if x else "   -   " for x in ev),
-                  "(tma, qk, s_full, vote, p_full, pv)")
+                  "(tma, qk, s_full, s_ld, vote, p_full, pv)")
     print("ctas", len(t))
     for name, col in (("setup", 1), ("tiles", 2), ("partials", 3), ("merge", 4)):
         d = (t[:, col] - t0) / 1e3
