@@ -622,25 +622,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch(&p.tm_v);
       tma_prefetch(&p.tm_ck);
       tma_prefetch(&p.tm_cv);
-      bool union_seen = false;
-      int n_total = 0x7fffffff;
-      for (int j = 0;; ++j) {
-        const int t = split + j * S;
-        if (t >= n_cmp && !union_seen) {
-          mbar_sleep_wait(&m.union_ready, 0);
-          union_seen = true;
-          n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-        }
-        if (t >= n_total) break;
-        const int st = j & 1;
-        if (j >= 2) mbar_sleep_wait(&m.kv_empty[st], ((j >> 1) + 1) & 1);
-        uint8_t* kdst = smem + kOffK + st * kStageBytes;
-        uint8_t* vdst = smem + kOffV + st * kStageBytes;
-        if (trace && j < 8) p.trace[cta_id * 64 + 8 + j] = globaltimer();
-        mbar_expect_tx(&m.k_full[st], kStageBytes);
-        mbar_expect_tx(&m.v_full[st], kStageBytes);
-        const CUtensorMap *tk, *tv;
-        int r0, r1;
+      // stream this CTA's tiles into L2 ahead of the two smem stages: the
+      // stage loads below then hit L2 instead of paying HBM latency per tile
+      auto tile_rows = [&](int t, const CUtensorMap*& tk, const CUtensorMap*& tv, int& r0, int& r1) {
         if (t < n_cmp) {
           tk = &p.tm_ck; tv = &p.tm_cv;
           r0 = t * kTile; r1 = r0 + 64;
@@ -653,6 +637,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           tk = &p.tm_tk; tv = &p.tm_tv;
           r0 = 0; r1 = 64;
         }
+      };
+      auto prefetch_tile = [&](int t) {
+        const CUtensorMap *tk, *tv;
+        int r0, r1;
+        tile_rows(t, tk, tv, r0, r1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          tma_prefetch_3d(tk, c * 64, kvh, r0);
+          tma_prefetch_3d(tk, c * 64, kvh, r1);
+          tma_prefetch_3d(tv, c * 64, kvh, r0);
+          tma_prefetch_3d(tv, c * 64, kvh, r1);
+        }
+      };
+      for (int t = split + 2 * S; t < n_cmp; t += S) prefetch_tile(t);
+      bool union_seen = false;
+      int n_total = 0x7fffffff;
+      for (int j = 0;; ++j) {
+        const int t = split + j * S;
+        if (t >= n_cmp && !union_seen) {
+          mbar_sleep_wait(&m.union_ready, 0);
+          union_seen = true;
+          n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
+          for (int t2 = max(t, split + 2 * S); t2 < n_total; t2 += S) prefetch_tile(t2);
+        }
+        if (t >= n_total) break;
+        const int st = j & 1;
+        if (j >= 2) mbar_sleep_wait(&m.kv_empty[st], ((j >> 1) + 1) & 1);
+        uint8_t* kdst = smem + kOffK + st * kStageBytes;
+        uint8_t* vdst = smem + kOffV + st * kStageBytes;
+        if (trace && j < 8) p.trace[cta_id * 64 + 8 + j] = globaltimer();
+        mbar_expect_tx(&m.k_full[st], kStageBytes);
+        mbar_expect_tx(&m.v_full[st], kStageBytes);
+        const CUtensorMap *tk, *tv;
+        int r0, r1;
+        tile_rows(t, tk, tv, r0, r1);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
