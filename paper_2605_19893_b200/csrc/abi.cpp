@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -247,6 +248,7 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   p.idx_count = a.idx_count;
   p.ws = static_cast<float*>(ws);
   p.trace = g_trace;
+  p.debug_flags = g_trace != nullptr && std::getenv("SPECSV_DEBUG_NOVOTE") != nullptr ? 1 : 0;
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
   p.ws_o_offset = (int64_t)nchunks * H * S * (3 * 64 * 2);

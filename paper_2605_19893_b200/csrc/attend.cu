@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
         const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
         const uint32_t cm = side == 0 ? cm_a : cm_b;
+        if ((p.debug_flags & 1) && m.m2[br][c0] != -INFINITY) continue;  // timing experiment only
         bool need = false;
 #pragma unroll
         for (int e = 0; e < 16; ++e) need |= ((cm >> e) & 1u) && (s[e] > m.thr[br][c0 + e]);

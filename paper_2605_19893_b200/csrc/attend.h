@@ -23,7 +23,8 @@ struct AttendParams {
   const int32_t* idx;        // [nq][n_sel]
   const int32_t* idx_count;  // [nq]
   float* ws;                 // split partials
-  unsigned long long* trace; // optional per-CTA globaltimer stamps [cta][8] (debug)
+  unsigned long long* trace; // optional per-CTA globaltimer stamps [cta][64] (debug)
+  int32_t debug_flags;       // diagnostics only (bit 0: skip running-max votes after the first)
   int64_t ws_o_offset;       // float offset of the O partials inside ws
   int64_t ws_sync_offset;    // float offset of the per-head barrier words (zero-initialised)
   int32_t nq, gamma, Hq, Hkv, G, n_sel;
