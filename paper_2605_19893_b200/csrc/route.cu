@@ -4,16 +4,19 @@
 // Replaces nsa::selection_scores + nsa::select_blocks
 // (src/nsa_attention.cpp:38-136) for every query that constructs indices.
 //
-//  R1 (grid: compressed-block tiles x KV heads x row chunks): per (query, head,
+//  R1 (grid: 64-block tiles x KV heads x row chunks): per (query, head,
 //     block) logit = dot(q_h, ck_i) * 1/sqrt(dh) in fp64 with the reference's
 //     lane order (4 interleaved partial sums, (s0+s2)+(s1+s3)); fp32 x fp32
 //     products are exact in fp64, so DFMA == the reference's mul-then-add and
-//     the logits are bit-identical.  Fused: per-tile max and exp-sum.
-//  R2 (grid: block chunks x routed queries): merge tile statistics per head
-//     (online-softmax merge), then mass_i = sum_h (ascending) p_hi.
+//     the logits are bit-identical.  Register blocking: 8 query rows x 2
+//     blocks per thread (the q rows are warp-broadcast smem reads, the key
+//     rows per-lane reads), fused per-tile max and exp-sum.
+//  R2 (grid: 128-block chunks x routed queries): merge tile statistics per
+//     head (online-softmax merge), then mass_i = sum_h (ascending) p_hi.
 //  R3 (one CTA per routed query): overlap remap to selection blocks in the
 //     reference's ascending order, then Top-n: forced {0, avail-2, avail-1}
-//     plus the best remaining by (score desc, id asc), written ascending.
+//     plus the best remaining by (score desc, id asc) via an in-smem bitonic
+//     sort, written ascending.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -23,9 +26,9 @@
 namespace specsv_b200 {
 namespace {
 
-constexpr int kR1Threads = 256;
+constexpr int kRowsPerWarp = 8;
 
-__global__ void __launch_bounds__(kR1Threads)
+__global__ void __launch_bounds__(512)
     route_logits_kernel(const __grid_constant__ RouteParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int dh = p.dh;
@@ -33,103 +36,104 @@ __global__ void __launch_bounds__(kR1Threads)
   const int rows_total = p.nr * p.G;
   const int r0 = blockIdx.z * kRouteRows;
   const int nrows = min(kRouteRows, rows_total - r0);
-  double* qd = reinterpret_cast<double*>(smem);                    // [nrows][dh]
+  double* qd = reinterpret_cast<double*>(smem);                          // [nrows][dh]
   float* cks = reinterpret_cast<float*>(smem + (size_t)nrows * dh * 8);  // [64][dh + 4]
   const int ckld = dh + 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nthr = blockDim.x;
 
-  // q rows (fp32 -> fp64, exact)
-  for (int e = tid; e < nrows * dh; e += kR1Threads) {
-    const int r = e / dh, x = e % dh;
+  for (int e = tid; e < nrows * (dh / 4); e += nthr) {  // q rows, fp32 -> fp64 (exact)
+    const int r = e / (dh / 4), x4 = e % (dh / 4);
     const int rr = r0 + r;
     const int slot = rr / p.G, g = rr % p.G;
-    const int q = p.slot_q[slot];
     const int h = kvh * p.G + g;
-    qd[e] = (double)p.q[((int64_t)q * p.Hq + h) * dh + x];
+    const float4 v = *reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4);
+    double* dst = qd + (size_t)r * dh + 4 * x4;
+    dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
   }
-  // compressed keys of this tile (zero beyond the cache)
   const int i0 = tile * kRouteTile;
-  for (int e = tid; e < kRouteTile * (dh / 4); e += kR1Threads) {
+  for (int e = tid; e < kRouteTile * (dh / 4); e += nthr) {  // key tile (zero beyond the cache)
     const int b = e / (dh / 4), x4 = e % (dh / 4);
     const int i = i0 + b;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < p.blocks) {
-      v = *reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + kvh) * dh + x4 * 4);
-    }
+    if (i < p.blocks) v = *reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + kvh) * dh + x4 * 4);
     *reinterpret_cast<float4*>(cks + b * ckld + x4 * 4) = v;
   }
   __syncthreads();
 
+  const int rbase = warp * kRowsPerWarp;
+  if (rbase >= nrows) return;
   const float* k0 = cks + lane * ckld;
   const float* k1 = cks + (lane + 32) * ckld;
-  for (int rbase = warp; rbase < nrows; rbase += 8 * 4) {
-    double acc[4][2][4];
+  double acc[kRowsPerWarp][2][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < kRowsPerWarp; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 2; ++b)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-    int rowi[4];
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+  const double* qrow[kRowsPerWarp];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) rowi[a] = min(rbase + 8 * a, nrows - 1);
-    for (int x = 0; x < dh; x += 4) {
-      const float4 ka = *reinterpret_cast<const float4*>(k0 + x);
-      const float4 kb = *reinterpret_cast<const float4*>(k1 + x);
+  for (int a = 0; a < kRowsPerWarp; ++a) qrow[a] = qd + (size_t)min(rbase + a, nrows - 1) * dh;
+#pragma unroll 1
+  for (int x = 0; x < dh; x += 4) {
+    const float4 ka = *reinterpret_cast<const float4*>(k0 + x);
+    const float4 kb = *reinterpret_cast<const float4*>(k1 + x);
+    const double ka0 = ka.x, ka1 = ka.y, ka2 = ka.z, ka3 = ka.w;
+    const double kb0 = kb.x, kb1 = kb.y, kb2 = kb.z, kb3 = kb.w;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const double2 qa = *reinterpret_cast<const double2*>(qd + (size_t)rowi[a] * dh + x);
-        const double2 qb = *reinterpret_cast<const double2*>(qd + (size_t)rowi[a] * dh + x + 2);
-        acc[a][0][0] = fma(qa.x, (double)ka.x, acc[a][0][0]);
-        acc[a][0][1] = fma(qa.y, (double)ka.y, acc[a][0][1]);
-        acc[a][0][2] = fma(qb.x, (double)ka.z, acc[a][0][2]);
-        acc[a][0][3] = fma(qb.y, (double)ka.w, acc[a][0][3]);
-        acc[a][1][0] = fma(qa.x, (double)kb.x, acc[a][1][0]);
-        acc[a][1][1] = fma(qa.y, (double)kb.y, acc[a][1][1]);
-        acc[a][1][2] = fma(qb.x, (double)kb.z, acc[a][1][2]);
-        acc[a][1][3] = fma(qb.y, (double)kb.w, acc[a][1][3]);
-      }
+    for (int a = 0; a < kRowsPerWarp; ++a) {
+      const double2 qa = *reinterpret_cast<const double2*>(qrow[a] + x);
+      const double2 qb = *reinterpret_cast<const double2*>(qrow[a] + x + 2);
+      acc[a][0][0] = fma(qa.x, ka0, acc[a][0][0]);
+      acc[a][0][1] = fma(qa.y, ka1, acc[a][0][1]);
+      acc[a][0][2] = fma(qb.x, ka2, acc[a][0][2]);
+      acc[a][0][3] = fma(qb.y, ka3, acc[a][0][3]);
+      acc[a][1][0] = fma(qa.x, kb0, acc[a][1][0]);
+      acc[a][1][1] = fma(qa.y, kb1, acc[a][1][1]);
+      acc[a][1][2] = fma(qb.x, kb2, acc[a][1][2]);
+      acc[a][1][3] = fma(qb.y, kb3, acc[a][1][3]);
     }
+  }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = rbase + 8 * a;
-      if (r >= nrows) continue;  // warp-uniform
-      const int rr = r0 + r;
-      const int slot = rr / p.G, g = rr % p.G;
-      const int h = kvh * p.G + g;
-      const int mvis = p.slot_mvis[slot];
-      double lg[2];
-      bool ok[2];
+  for (int a = 0; a < kRowsPerWarp; ++a) {
+    const int r = rbase + a;
+    if (r >= nrows) break;  // warp-uniform
+    const int rr = r0 + r;
+    const int slot = rr / p.G, g = rr % p.G;
+    const int h = kvh * p.G + g;
+    const int mvis = p.slot_mvis[slot];
+    double lg[2];
+    bool ok[2];
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const double dot = __dadd_rn(__dadd_rn(acc[a][b][0], acc[a][b][2]),
-                                     __dadd_rn(acc[a][b][1], acc[a][b][3]));
-        lg[b] = __dmul_rn(dot, p.scale);
-        ok[b] = (i0 + lane + 32 * b) < mvis;
-      }
-      double mx = -INFINITY;
-      if (ok[0]) mx = lg[0];
-      if (ok[1]) mx = fmax(mx, lg[1]);
+    for (int b = 0; b < 2; ++b) {
+      const double dot = __dadd_rn(__dadd_rn(acc[a][b][0], acc[a][b][2]),
+                                   __dadd_rn(acc[a][b][1], acc[a][b][3]));
+      lg[b] = __dmul_rn(dot, p.scale);
+      ok[b] = (i0 + lane + 32 * b) < mvis;
+    }
+    double mx = -INFINITY;
+    if (ok[0]) mx = lg[0];
+    if (ok[1]) mx = fmax(mx, lg[1]);
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      double e0 = ok[0] ? exp(lg[0] - mx) : 0.0;
-      double e1 = ok[1] ? exp(lg[1] - mx) : 0.0;
-      double s = e0 + e1;
+    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    const double e0 = ok[0] ? exp(lg[0] - mx) : 0.0;
+    const double e1 = ok[1] ? exp(lg[1] - mx) : 0.0;
+    double s = e0 + e1;
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad;
-      E[i0 + lane] = e0;
-      E[i0 + lane + 32] = e1;
-      if (lane == 0) {
-        p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = mx;
-        p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = s;
-      }
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad;
+    E[i0 + lane] = e0;
+    E[i0 + lane + 32] = e1;
+    if (lane == 0) {
+      p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = mx;
+      p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = s;
     }
   }
 }
 
-constexpr int kR2Threads = 256;
-constexpr int kR2Blocks = 256;  // compressed blocks per CTA (4 R1 tiles)
+constexpr int kR2Threads = 128;
+constexpr int kR2Blocks = 128;  // compressed blocks per CTA (2 R1 tiles)
 
 __global__ void __launch_bounds__(kR2Threads)
     route_mass_kernel(const __grid_constant__ RouteParams p) {
@@ -139,18 +143,34 @@ __global__ void __launch_bounds__(kR2Threads)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * kR2Blocks;
   const int t0 = i0 / kRouteTile;
+  // per-head softmax statistics merged over the tiles (online-softmax merge)
   for (int h = warp; h < p.Hq; h += kR2Threads / 32) {
     const double* TM = p.TM + ((int64_t)slot * p.Hq + h) * p.ntiles;
     const double* TD = p.TD + ((int64_t)slot * p.Hq + h) * p.ntiles;
-    double mx = -INFINITY;
-    for (int t = lane; t < p.ntiles; t += 32) mx = fmax(mx, TM[t]);
+    double mx = -INFINITY, den = 0.0;
+    for (int t0l = 0; t0l < p.ntiles; t0l += 128) {
+      double tm[4], td[4];
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    double den = 0.0;
-    for (int t = lane; t < p.ntiles; t += 32)
-      if (TD[t] > 0.0) den += TD[t] * exp(TM[t] - mx);
+      for (int k = 0; k < 4; ++k) {
+        const int t = t0l + lane + 32 * k;
+        tm[k] = t < p.ntiles ? TM[t] : -INFINITY;
+        td[k] = t < p.ntiles ? TD[t] : 0.0;
+      }
+      double cmx = fmax(fmax(tm[0], tm[1]), fmax(tm[2], tm[3]));
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+      for (int off = 16; off >= 1; off >>= 1) cmx = fmax(cmx, __shfl_xor_sync(0xffffffffu, cmx, off));
+      double cden = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (td[k] > 0.0) cden += td[k] * exp(tm[k] - cmx);
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) cden += __shfl_xor_sync(0xffffffffu, cden, off);
+      if (cmx != -INFINITY) {
+        const double nm = fmax(mx, cmx);
+        den = (mx == -INFINITY ? 0.0 : den * exp(mx - nm)) + cden * exp(cmx - nm);
+        mx = nm;
+      }
+    }
     if (lane == 0) {
       sM[h] = mx;
       sD[h] = den;
@@ -170,11 +190,18 @@ __global__ void __launch_bounds__(kR2Threads)
   __syncthreads();
   const int i = i0 + tid;
   if (i >= p.m_pad) return;
-  const int tt = (i - i0) / kRouteTile;
+  const int tt = tid / kRouteTile;
   double mass = 0.0;
   if (i < p.slot_mvis[slot]) {
-    for (int h = 0; h < p.Hq; ++h)
-      mass += p.E[((int64_t)slot * p.Hq + h) * p.m_pad + i] * sF[h][tt];
+    const double* E = p.E + (int64_t)slot * p.Hq * p.m_pad + i;
+    for (int h0 = 0; h0 < p.Hq; h0 += 16) {  // loads in flight, then accumulate in head order
+      double e[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) e[k] = h0 + k < p.Hq ? E[(int64_t)(h0 + k) * p.m_pad] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (h0 + k < p.Hq) mass += e[k] * sF[h0 + k][tt];
+    }
   }
   p.mass[(int64_t)slot * p.m_pad + i] = mass;
 }
@@ -186,62 +213,52 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
   return sa > sb || (sa == sb && ia < ib);
 }
 
-// Top-n over sel[0, avail) in shared memory (select_blocks, nsa_attention.cpp:94-136)
-__device__ void topn_write(const double* sel, uint8_t* taken, int avail, int n, int32_t* idx_row,
-                           int32_t* count, uint32_t* forced_bits) {
-  __shared__ double wbest_s[32];
-  __shared__ int wbest_i[32];
+// Top-n over sel[0, avail) (select_blocks, nsa_attention.cpp:94-136): forced
+// blocks first, then the best remaining by (score desc, id asc).  `key` and
+// `ids` are smem scratch of pow2 >= avail entries.
+__device__ void topn_write(const double* sel, double* key, int* ids, int avail, int n,
+                           int32_t* idx_row, int32_t* count, uint32_t* forced_bits) {
   __shared__ int picks[64];
-  __shared__ int npicks;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int b = tid; b < avail; b += blockDim.x) taken[b] = 0;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int E = 1;
+  while (E < avail) E <<= 1;
+  const int f1 = avail - 2 > 0 ? avail - 2 : -1;
+  const int f2 = avail - 1 > 0 ? avail - 1 : -1;
+  for (int b = tid; b < E; b += nthr) {
+    const bool forced = b == 0 || b == f1 || b == f2;
+    key[b] = (b < avail && !forced) ? sel[b] : -INFINITY;
+    ids[b] = b < avail ? b : 0x7fffffff;
+  }
   __syncthreads();
+  // bitonic sort, "ranks_before" first
+  for (int k = 2; k <= E; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < E; i += nthr) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double ka = key[i], kb = key[ixj];
+          const int ia = ids[i], ib = ids[ixj];
+          const bool up = (i & k) == 0;
+          const bool swap = up ? ranks_before(kb, ib, ka, ia) : ranks_before(ka, ia, kb, ib);
+          if (swap) {
+            key[i] = kb; key[ixj] = ka;
+            ids[i] = ib; ids[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
   if (tid == 0) {
-    npicks = 0;
+    int cnt = 0;
     if (avail > 0) {
-      picks[npicks++] = 0;
-      taken[0] = 2;
-      if (avail - 2 > 0) { picks[npicks++] = avail - 2; taken[avail - 2] = 2; }
-      if (avail - 1 > 0) { picks[npicks++] = avail - 1; taken[avail - 1] = 2; }
+      picks[cnt++] = 0;
+      if (f1 > 0) picks[cnt++] = f1;
+      if (f2 > 0 && f2 != f1) picks[cnt++] = f2;
     }
-  }
-  __syncthreads();
-  const int target = min(n, avail);
-  const int rounds = target - npicks;
-  for (int r = 0; r < rounds; ++r) {
-    double bs = -1.0;
-    int bi = 0x7fffffff;
-    for (int b = tid; b < avail; b += blockDim.x)
-      if (!taken[b] && ranks_before(sel[b], b, bs, bi)) { bs = sel[b]; bi = b; }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ranks_before(os, oi, bs, bi)) { bs = os; bi = oi; }
-    }
-    if (lane == 0) { wbest_s[warp] = bs; wbest_i[warp] = bi; }
-    __syncthreads();
-    if (warp == 0) {
-      const int nw = blockDim.x >> 5;
-      bs = lane < nw ? wbest_s[lane] : -1.0;
-      bi = lane < nw ? wbest_i[lane] : 0x7fffffff;
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, bs, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (ranks_before(os, oi, bs, bi)) { bs = os; bi = oi; }
-      }
-      if (lane == 0 && bi != 0x7fffffff) {
-        taken[bi] = 1;
-        picks[npicks++] = bi;
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    const int cnt = npicks;
-    // ascending (insertion sort, <= n entries)
-    for (int a = 1; a < cnt; ++a) {
+    const int target = n < avail ? n : avail;
+    for (int r = 0; cnt < target; ++r) picks[cnt++] = ids[r];
+    for (int a = 1; a < cnt; ++a) {  // ascending
       const int v = picks[a];
       int b = a - 1;
       while (b >= 0 && picks[b] > v) { picks[b + 1] = picks[b]; --b; }
@@ -250,7 +267,7 @@ __device__ void topn_write(const double* sel, uint8_t* taken, int avail, int n, 
     uint32_t fb = 0u;
     for (int a = 0; a < n; ++a) {
       idx_row[a] = a < cnt ? picks[a] : -1;
-      if (a < cnt && taken[picks[a]] == 2) fb |= 1u << a;
+      if (a < cnt && (picks[a] == 0 || picks[a] == f1 || picks[a] == f2)) fb |= 1u << a;
     }
     *count = cnt;
     *forced_bits = fb;
@@ -264,14 +281,14 @@ __global__ void __launch_bounds__(kR3Threads)
   const int avail = p.slot_avail[slot];
   const int mvis = p.slot_mvis[slot];
   double* sel = reinterpret_cast<double*>(smem);
-  uint8_t* taken = smem + (size_t)kMaxAvail * 8;
+  double* key = sel + kMaxAvail;
+  int* ids = reinterpret_cast<int*>(key + kMaxAvail);
   const double inv_heads = 1.0 / (double)p.Hq;
   const double* mass = p.mass + (int64_t)slot * p.m_pad;
   // overlap remap (nsa_attention.cpp:67-78), ascending i per selection block
   for (int b = threadIdx.x; b < avail; b += blockDim.x) {
     const int64_t blo = (int64_t)b * p.l_sel, bhi = blo + p.l_sel;
-    int64_t ilo = blo - p.l < 0 ? 0 : (blo - p.l) / p.d + 1;
-    if (blo - p.l < 0) ilo = 0;
+    const int64_t ilo = blo - p.l < 0 ? 0 : (blo - p.l) / p.d + 1;
     double s = 0.0;
     for (int64_t i = ilo; i < mvis && i * p.d < bhi; ++i) {
       const int64_t lo = i * p.d, hi = lo + p.l;
@@ -295,7 +312,8 @@ __global__ void __launch_bounds__(kR3Threads)
     }
   }
   const int q = p.slot_q[slot];
-  topn_write(sel, taken, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q, p.idx_forced + q);
+  topn_write(sel, key, ids, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q,
+             p.idx_forced + q);
 }
 
 __global__ void __launch_bounds__(kR3Threads)
@@ -303,13 +321,14 @@ __global__ void __launch_bounds__(kR3Threads)
                        uint32_t* forced) {
   extern __shared__ __align__(16) uint8_t smem[];
   double* sel = reinterpret_cast<double*>(smem);
-  uint8_t* taken = smem + (size_t)kMaxAvail * 8;
+  double* key = sel + kMaxAvail;
+  int* ids = reinterpret_cast<int*>(key + kMaxAvail);
   for (int b = threadIdx.x; b < avail; b += blockDim.x) sel[b] = scores[b];
   __syncthreads();
-  topn_write(sel, taken, avail, n, idx, count, forced);
+  topn_write(sel, key, ids, avail, n, idx, count, forced);
 }
 
-constexpr size_t kR3Smem = (size_t)kMaxAvail * 9;
+constexpr size_t kR3Smem = (size_t)kMaxAvail * (8 + 8 + 4);
 
 cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   if (p.ntiles == 0) return cudaSuccess;  // nothing compressed is visible yet: all masses 0
@@ -320,7 +339,11 @@ cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(route_logits_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   if (e != cudaSuccess) return e;
-  route_logits_kernel<<<dim3(p.ntiles, p.Hkv, rchunks), kR1Threads, smem1, s>>>(p);
+  e = cudaFuncSetAttribute(route_logits_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
+  const int warps = (maxrows + kRowsPerWarp - 1) / kRowsPerWarp;
+  route_logits_kernel<<<dim3(p.ntiles, p.Hkv, rchunks), 32 * warps, smem1, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks, p.nr), kR2Threads, 0, s>>>(p);
