@@ -105,7 +105,8 @@ int splits_for(const specsv_nsa_config& c, int32_t nq) {
 
 struct Layout {
   size_t attend_off = 0, attend_bytes = 0;
-  size_t E_off = 0, TM_off = 0, TD_off = 0, mass_off = 0;
+  size_t E_off = 0, TM_off = 0, TD_off = 0, mass_off = 0, sel_off = 0;
+  int64_t sel_pad = 0;
   size_t total = 0;
 };
 
@@ -133,6 +134,9 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
   L.mass_off = off;
   off = align_up(off + (size_t)nq * m_pad * 8, 256);
+  L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
+  L.sel_off = off;
+  off = align_up(off + (size_t)nq * L.sel_pad * 8, 256);
   L.total = off;
   return L;
 }
@@ -214,6 +218,8 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
   p.TM = reinterpret_cast<double*>(ws + L.TM_off);
   p.TD = reinterpret_cast<double*>(ws + L.TD_off);
   p.mass = reinterpret_cast<double*>(ws + L.mass_off);
+  p.sel = reinterpret_cast<double*>(ws + L.sel_off);
+  p.sel_pad = (int32_t)L.sel_pad;
   return p;
 }
 

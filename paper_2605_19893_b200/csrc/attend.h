@@ -43,7 +43,7 @@ int attend_max_coresident();
 
 // ---- routing (route.cu) -------------------------------------------------------
 constexpr int kRouteTile = 64;      // compressed blocks per R1 CTA
-constexpr int kRouteRows = 128;     // q rows (routed queries x G) per R1 CTA
+constexpr int kRouteRows = 64;      // q rows (routed queries x G) per R1 CTA
 constexpr int kMaxAvail = 8192;     // selection blocks per query for the Top-n CTA
 
 struct RouteParams {
@@ -53,6 +53,8 @@ struct RouteParams {
   double* TM;            // [nr][Hq][ntiles] tile max
   double* TD;            // [nr][Hq][ntiles] tile denominators
   double* mass;          // [nr][m_pad]
+  double* sel;           // [nr][sel_pad] selection-block scores
+  int32_t sel_pad;
   int32_t* idx;          // [nq][n]
   int32_t* idx_count;    // [nq]
   uint32_t* idx_forced;  // [nq]

@@ -39,6 +39,7 @@ void check_build_limits(const specsv_nsa_config& c) {
   if (g > 32 || (g & (g - 1)) != 0) unsup("GQA group size must be a power of two <= 32");
   if (c.n > 64) unsup("n must be <= 64");
   if (c.n_q_heads > 128) unsup("n_q_heads must be <= 128");
+  if ((c.l - 1) / c.d > 7) unsup("l must be <= 8 * d (routing halo)");
 }
 
 int64_t routing_visible_len(const specsv_nsa_config& c, int64_t pos) {

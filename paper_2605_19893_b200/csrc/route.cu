@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kRowsPerWarp = 8;
 
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(256)
     route_logits_kernel(const __grid_constant__ RouteParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int dh = p.dh;
@@ -188,22 +188,66 @@ __global__ void __launch_bounds__(kR2Threads)
     sF[h][tt] = f;
   }
   __syncthreads();
-  const int i = i0 + tid;
-  if (i >= p.m_pad) return;
-  const int tt = tid / kRouteTile;
-  double mass = 0.0;
-  if (i < p.slot_mvis[slot]) {
-    const double* E = p.E + (int64_t)slot * p.Hq * p.m_pad + i;
-    for (int h0 = 0; h0 < p.Hq; h0 += 16) {  // loads in flight, then accumulate in head order
-      double e[16];
+  // mass for i in [i0 - halo, i0 + kR2Blocks): the halo covers the compressed
+  // blocks that straddle into this chunk's first selection block
+  __shared__ double smass[kR2Blocks + 8];
+  const int halo = (p.l - 1) / p.d;  // <= 7 (host-checked)
+  const int mvis = p.slot_mvis[slot];
+  for (int k = tid; k < kR2Blocks + halo; k += kR2Threads) {
+    const int i = i0 - halo + k;
+    double mass = 0.0;
+    if (i >= 0 && i < mvis) {
+      const int tt = i / kRouteTile;
+      const double* E = p.E + (int64_t)slot * p.Hq * p.m_pad + i;
+      for (int h0 = 0; h0 < p.Hq; h0 += 16) {  // loads in flight, then accumulate in head order
+        double e[16], f[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) e[k] = h0 + k < p.Hq ? E[(int64_t)(h0 + k) * p.m_pad] : 0.0;
+        for (int k2 = 0; k2 < 16; ++k2) {
+          e[k2] = h0 + k2 < p.Hq ? E[(int64_t)(h0 + k2) * p.m_pad] : 0.0;
+          f[k2] = 0.0;
+        }
+        if (tt >= t0 && tt < t0 + kR2Blocks / kRouteTile) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        if (h0 + k < p.Hq) mass += e[k] * sF[h0 + k][tt];
+          for (int k2 = 0; k2 < 16; ++k2) f[k2] = h0 + k2 < p.Hq ? sF[h0 + k2][tt - t0] : 0.0;
+        } else {  // halo block of the previous chunk: factor from the tile statistics
+#pragma unroll
+          for (int k2 = 0; k2 < 16; ++k2) {
+            const int h = h0 + k2;
+            if (h < p.Hq && sD[h] > 0.0) {
+              const double tm = p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tt];
+              f[k2] = tm == -INFINITY ? 0.0 : exp(tm - sM[h]) / sD[h];
+            }
+          }
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2)
+          if (h0 + k2 < p.Hq) mass += e[k2] * f[k2];
+      }
     }
+    smass[k] = mass;
   }
-  p.mass[(int64_t)slot * p.m_pad + i] = mass;
+  __syncthreads();
+  // selection scores (nsa_attention.cpp:67-78): block b gets, in ascending i,
+  // mass_i * (1/Hq) * overlap / l from every compressed block overlapping it
+  const double inv_heads = 1.0 / (double)p.Hq;
+  const int b_lo = (i0 * p.d + p.l_sel - 1) / p.l_sel;                  // first block starting in chunk
+  const int b_hi = ((i0 + kR2Blocks) * p.d + p.l_sel - 1) / p.l_sel;    // exclusive
+  const int avail = p.slot_avail[slot];
+  for (int b = b_lo + tid; b < b_hi && b < avail; b += kR2Threads) {
+    const int64_t blo = (int64_t)b * p.l_sel, bhi = blo + p.l_sel;
+    const int64_t ilo = blo - p.l < 0 ? 0 : (blo - p.l) / p.d + 1;
+    double sacc = 0.0;
+    for (int64_t i = ilo; i < mvis && i * p.d < bhi; ++i) {
+      const int64_t lo = i * p.d, hi = lo + p.l;
+      const int64_t olo = lo > blo ? lo : blo;
+      const int64_t ohi = hi < bhi ? hi : bhi;
+      if (ohi <= olo) continue;
+      const double mi = (i - (i0 - halo)) < kR2Blocks + halo ? smass[i - (i0 - halo)] : 0.0;
+      sacc = __dadd_rn(sacc, __ddiv_rn(__dmul_rn(__dmul_rn(mi, inv_heads), (double)(ohi - olo)),
+                                       (double)p.l));
+    }
+    p.sel[(int64_t)slot * p.sel_pad + b] = sacc;
+  }
 }
 
 constexpr int kR3Threads = 1024;
@@ -214,41 +258,33 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
 }
 
 // Top-n over sel[0, avail) (select_blocks, nsa_attention.cpp:94-136): forced
-// blocks first, then the best remaining by (score desc, id asc).  `key` and
-// `ids` are smem scratch of pow2 >= avail entries.
-__device__ void topn_write(const double* sel, double* key, int* ids, int avail, int n,
-                           int32_t* idx_row, int32_t* count, uint32_t* forced_bits) {
+// blocks first, then the best remaining by (score desc, id asc).  Each
+// candidate counts the candidates that rank before it, stopping once it
+// cannot be among the winners; a winner's count is its rank.
+__device__ void topn_write(const double* sel, int avail, int n, int32_t* idx_row, int32_t* count,
+                           uint32_t* forced_bits) {
   __shared__ int picks[64];
   const int tid = threadIdx.x, nthr = blockDim.x;
-  int E = 1;
-  while (E < avail) E <<= 1;
   const int f1 = avail - 2 > 0 ? avail - 2 : -1;
   const int f2 = avail - 1 > 0 ? avail - 1 : -1;
-  for (int b = tid; b < E; b += nthr) {
-    const bool forced = b == 0 || b == f1 || b == f2;
-    key[b] = (b < avail && !forced) ? sel[b] : -INFINITY;
-    ids[b] = b < avail ? b : 0x7fffffff;
-  }
+  const int nforced = avail > 0 ? 1 + (f1 > 0) + (f2 > 0 && f2 != f1) : 0;
+  const int target = n < avail ? n : avail;
+  const int want = target - nforced;  // picks among the non-forced blocks
+  if (tid < 64) picks[tid] = -1;
   __syncthreads();
-  // bitonic sort, "ranks_before" first
-  for (int k = 2; k <= E; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < E; i += nthr) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const double ka = key[i], kb = key[ixj];
-          const int ia = ids[i], ib = ids[ixj];
-          const bool up = (i & k) == 0;
-          const bool swap = up ? ranks_before(kb, ib, ka, ia) : ranks_before(ka, ia, kb, ib);
-          if (swap) {
-            key[i] = kb; key[ixj] = ka;
-            ids[i] = ib; ids[ixj] = ia;
-          }
-        }
+  for (int b = tid; b < avail && want > 0; b += nthr) {
+    const bool forced = b == 0 || b == f1 || b == f2;
+    int rank = 0;
+    if (!forced) {
+      const double sb = sel[b];
+      for (int c = 0; c < avail && rank < want; ++c) {
+        const bool cf = c == 0 || c == f1 || c == f2;
+        rank += (!cf && ranks_before(sel[c], c, sb, b)) ? 1 : 0;
       }
-      __syncthreads();
+      if (rank < want) picks[nforced + rank] = b;
     }
   }
+  __syncthreads();
   if (tid == 0) {
     int cnt = 0;
     if (avail > 0) {
@@ -256,8 +292,7 @@ __device__ void topn_write(const double* sel, double* key, int* ids, int avail, 
       if (f1 > 0) picks[cnt++] = f1;
       if (f2 > 0 && f2 != f1) picks[cnt++] = f2;
     }
-    const int target = n < avail ? n : avail;
-    for (int r = 0; cnt < target; ++r) picks[cnt++] = ids[r];
+    cnt = target > 0 ? target : 0;
     for (int a = 1; a < cnt; ++a) {  // ascending
       const int v = picks[a];
       int b = a - 1;
@@ -279,27 +314,11 @@ __global__ void __launch_bounds__(kR3Threads)
   extern __shared__ __align__(16) uint8_t smem[];
   const int slot = only_slot >= 0 ? only_slot : blockIdx.x;
   const int avail = p.slot_avail[slot];
-  const int mvis = p.slot_mvis[slot];
   double* sel = reinterpret_cast<double*>(smem);
-  double* key = sel + kMaxAvail;
-  int* ids = reinterpret_cast<int*>(key + kMaxAvail);
-  const double inv_heads = 1.0 / (double)p.Hq;
-  const double* mass = p.mass + (int64_t)slot * p.m_pad;
-  // overlap remap (nsa_attention.cpp:67-78), ascending i per selection block
   for (int b = threadIdx.x; b < avail; b += blockDim.x) {
-    const int64_t blo = (int64_t)b * p.l_sel, bhi = blo + p.l_sel;
-    const int64_t ilo = blo - p.l < 0 ? 0 : (blo - p.l) / p.d + 1;
-    double s = 0.0;
-    for (int64_t i = ilo; i < mvis && i * p.d < bhi; ++i) {
-      const int64_t lo = i * p.d, hi = lo + p.l;
-      const int64_t olo = lo > blo ? lo : blo;
-      const int64_t ohi = hi < bhi ? hi : bhi;
-      if (ohi <= olo) continue;
-      s = __dadd_rn(s, __ddiv_rn(__dmul_rn(__dmul_rn(mass[i], inv_heads), (double)(ohi - olo)),
-                                 (double)p.l));
-    }
-    sel[b] = s;
-    if (scores_out != nullptr) scores_out[b] = s;
+    const double v = p.ntiles > 0 ? p.sel[(int64_t)slot * p.sel_pad + b] : 0.0;
+    sel[b] = v;
+    if (scores_out != nullptr) scores_out[b] = v;
   }
   __syncthreads();
   if (scores_out != nullptr) return;
@@ -312,8 +331,7 @@ __global__ void __launch_bounds__(kR3Threads)
     }
   }
   const int q = p.slot_q[slot];
-  topn_write(sel, key, ids, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q,
-             p.idx_forced + q);
+  topn_write(sel, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q, p.idx_forced + q);
 }
 
 __global__ void __launch_bounds__(kR3Threads)
@@ -321,14 +339,12 @@ __global__ void __launch_bounds__(kR3Threads)
                        uint32_t* forced) {
   extern __shared__ __align__(16) uint8_t smem[];
   double* sel = reinterpret_cast<double*>(smem);
-  double* key = sel + kMaxAvail;
-  int* ids = reinterpret_cast<int*>(key + kMaxAvail);
   for (int b = threadIdx.x; b < avail; b += blockDim.x) sel[b] = scores[b];
   __syncthreads();
-  topn_write(sel, key, ids, avail, n, idx, count, forced);
+  topn_write(sel, avail, n, idx, count, forced);
 }
 
-constexpr size_t kR3Smem = (size_t)kMaxAvail * (8 + 8 + 4);
+constexpr size_t kR3Smem = (size_t)kMaxAvail * 8;
 
 cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   if (p.ntiles == 0) return cudaSuccess;  // nothing compressed is visible yet: all masses 0
@@ -346,7 +362,8 @@ cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   route_logits_kernel<<<dim3(p.ntiles, p.Hkv, rchunks), 32 * warps, smem1, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks, p.nr), kR2Threads, 0, s>>>(p);
+  // one extra chunk so the selection blocks that start past the last compressed block get written
+  route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
