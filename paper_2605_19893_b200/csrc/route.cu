@@ -26,33 +26,43 @@
 namespace specsv_b200 {
 namespace {
 
-constexpr int kRowsPerWarp = 8;
+constexpr int kR1Rows = 8;      // query rows per thread
+constexpr int kR1Blocks = 4;    // compressed blocks per thread
+constexpr int kR1Threads = 256; // 4 row groups x 2 block halves x 32 lanes
 
-__global__ void __launch_bounds__(256)
+// Lane (g, l) = (lane / 4, lane % 4) accumulates the elements x = l (mod 4)
+// of its 8 rows x 4 blocks: exactly the reference's lane-l partial sum s_l
+// (kernels.hpp:13-18), so two xor-shuffles rebuild (s0 + s2) + (s1 + s3)
+// bit-for-bit.  q rows are broadcast loads (same x for all groups), key rows
+// are 8 consecutive blocks per load (conflict-free with the 4-float pad).
+__global__ void __launch_bounds__(kR1Threads, 2)
     route_logits_kernel(const __grid_constant__ RouteParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ double red_m[kR1Rows * 4][2], red_s[kR1Rows * 4][2];
   const int dh = p.dh;
   const int tile = blockIdx.x, kvh = blockIdx.y;
   const int rows_total = p.nr * p.G;
   const int r0 = blockIdx.z * kRouteRows;
   const int nrows = min(kRouteRows, rows_total - r0);
-  double* qd = reinterpret_cast<double*>(smem);                          // [nrows][dh]
-  float* cks = reinterpret_cast<float*>(smem + (size_t)nrows * dh * 8);  // [64][dh + 4]
+  const int qld = dh + 2;  // doubles
+  double* qd = reinterpret_cast<double*>(smem);                                // [32][qld]
+  float* cks = reinterpret_cast<float*>(smem + (size_t)kRouteRows * qld * 8);  // [64][dh + 4]
   const int ckld = dh + 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nthr = blockDim.x;
+  const int g = lane >> 2, l = lane & 3;
+  const int rg = warp >> 1, bh = warp & 1;  // row group, block half
 
-  for (int e = tid; e < nrows * (dh / 4); e += nthr) {  // q rows, fp32 -> fp64 (exact)
+  for (int e = tid; e < nrows * (dh / 4); e += kR1Threads) {  // q rows, fp32 -> fp64 (exact)
     const int r = e / (dh / 4), x4 = e % (dh / 4);
     const int rr = r0 + r;
-    const int slot = rr / p.G, g = rr % p.G;
-    const int h = kvh * p.G + g;
+    const int slot = rr / p.G, gg = rr % p.G;
+    const int h = kvh * p.G + gg;
     const float4 v = *reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4);
-    double* dst = qd + (size_t)r * dh + 4 * x4;
+    double* dst = qd + (size_t)r * qld + 4 * x4;
     dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
   }
   const int i0 = tile * kRouteTile;
-  for (int e = tid; e < kRouteTile * (dh / 4); e += nthr) {  // key tile (zero beyond the cache)
+  for (int e = tid; e < kRouteTile * (dh / 4); e += kR1Threads) {  // key tile (zero beyond the cache)
     const int b = e / (dh / 4), x4 = e % (dh / 4);
     const int i = i0 + b;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -61,167 +71,169 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
 
-  const int rbase = warp * kRowsPerWarp;
-  if (rbase >= nrows) return;
-  const float* k0 = cks + lane * ckld;
-  const float* k1 = cks + (lane + 32) * ckld;
-  double acc[kRowsPerWarp][2][4];
+  const int rbase = rg * kR1Rows;
+  double acc[kR1Rows][kR1Blocks];
 #pragma unroll
-  for (int a = 0; a < kRowsPerWarp; ++a)
+  for (int a = 0; a < kR1Rows; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = 0.0;
+  if (rbase < nrows) {
+    const double* qrow = qd + (size_t)rbase * qld + l;
+    const float* krow = cks + (bh * 32 + g) * ckld + l;
+#pragma unroll 2
+    for (int x = 0; x < dh; x += 4) {
+      double kv[kR1Blocks];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-  const double* qrow[kRowsPerWarp];
+      for (int k = 0; k < kR1Blocks; ++k) kv[k] = krow[8 * k * ckld + x];
 #pragma unroll
-  for (int a = 0; a < kRowsPerWarp; ++a) qrow[a] = qd + (size_t)min(rbase + a, nrows - 1) * dh;
-#pragma unroll 1
-  for (int x = 0; x < dh; x += 4) {
-    const float4 ka = *reinterpret_cast<const float4*>(k0 + x);
-    const float4 kb = *reinterpret_cast<const float4*>(k1 + x);
-    const double ka0 = ka.x, ka1 = ka.y, ka2 = ka.z, ka3 = ka.w;
-    const double kb0 = kb.x, kb1 = kb.y, kb2 = kb.z, kb3 = kb.w;
+      for (int a = 0; a < kR1Rows; ++a) {
+        const double qv = qrow[a * qld + x];
 #pragma unroll
-    for (int a = 0; a < kRowsPerWarp; ++a) {
-      const double2 qa = *reinterpret_cast<const double2*>(qrow[a] + x);
-      const double2 qb = *reinterpret_cast<const double2*>(qrow[a] + x + 2);
-      acc[a][0][0] = fma(qa.x, ka0, acc[a][0][0]);
-      acc[a][0][1] = fma(qa.y, ka1, acc[a][0][1]);
-      acc[a][0][2] = fma(qb.x, ka2, acc[a][0][2]);
-      acc[a][0][3] = fma(qb.y, ka3, acc[a][0][3]);
-      acc[a][1][0] = fma(qa.x, kb0, acc[a][1][0]);
-      acc[a][1][1] = fma(qa.y, kb1, acc[a][1][1]);
-      acc[a][1][2] = fma(qb.x, kb2, acc[a][1][2]);
-      acc[a][1][3] = fma(qb.y, kb3, acc[a][1][3]);
+        for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = fma(qv, kv[k], acc[a][k]);
+      }
     }
   }
+  // rebuild the reference's dot: (s0 + s2) + (s1 + s3), then * 1/sqrt(dh)
 #pragma unroll
-  for (int a = 0; a < kRowsPerWarp; ++a) {
+  for (int a = 0; a < kR1Rows; ++a)
+#pragma unroll
+    for (int k = 0; k < kR1Blocks; ++k) {
+      const double t = __dadd_rn(acc[a][k], __shfl_xor_sync(0xffffffffu, acc[a][k], 2));
+      acc[a][k] = __dmul_rn(__dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 1)), p.scale);
+    }
+  // per-row tile max and exp-sum over the 64 blocks (2 warps x 8 groups x 4)
+#pragma unroll
+  for (int a = 0; a < kR1Rows; ++a) {
     const int r = rbase + a;
-    if (r >= nrows) break;  // warp-uniform
-    const int rr = r0 + r;
-    const int slot = rr / p.G, g = rr % p.G;
-    const int h = kvh * p.G + g;
-    const int mvis = p.slot_mvis[slot];
-    double lg[2];
-    bool ok[2];
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const double dot = __dadd_rn(__dadd_rn(acc[a][b][0], acc[a][b][2]),
-                                   __dadd_rn(acc[a][b][1], acc[a][b][3]));
-      lg[b] = __dmul_rn(dot, p.scale);
-      ok[b] = (i0 + lane + 32 * b) < mvis;
-    }
+    const bool rowok = r < nrows;
+    const int rr = r0 + (rowok ? r : 0);
+    const int mvis = p.slot_mvis[rr / p.G];
     double mx = -INFINITY;
-    if (ok[0]) mx = lg[0];
-    if (ok[1]) mx = fmax(mx, lg[1]);
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const double e0 = ok[0] ? exp(lg[0] - mx) : 0.0;
-    const double e1 = ok[1] ? exp(lg[1] - mx) : 0.0;
-    double s = e0 + e1;
+    for (int k = 0; k < kR1Blocks; ++k)
+      if (rowok && i0 + bh * 32 + g + 8 * k < mvis) mx = fmax(mx, acc[a][k]);
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad;
-    E[i0 + lane] = e0;
-    E[i0 + lane + 32] = e1;
-    if (lane == 0) {
-      p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = mx;
-      p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = s;
+    for (int off = 4; off <= 16; off <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (lane == 0) red_m[rbase + a][bh] = mx;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < kR1Rows; ++a) {
+    const int r = rbase + a;
+    const bool rowok = r < nrows;
+    const int rr = r0 + (rowok ? r : 0);
+    const int slot = rr / p.G, gg = rr % p.G;
+    const int h = kvh * p.G + gg;
+    const int mvis = p.slot_mvis[slot];
+    const double mx = fmax(red_m[rbase + a][0], red_m[rbase + a][1]);
+    double sum = 0.0;
+    double ev[kR1Blocks];
+#pragma unroll
+    for (int k = 0; k < kR1Blocks; ++k) {
+      const bool ok = rowok && i0 + bh * 32 + g + 8 * k < mvis;
+      ev[k] = ok ? exp(acc[a][k] - mx) : 0.0;
+      sum += ev[k];
     }
+#pragma unroll
+    for (int off = 4; off <= 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (lane == 0) red_s[rbase + a][bh] = sum;
+    if (rowok && l == 0) {
+      double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad + i0 + bh * 32 + g;
+#pragma unroll
+      for (int k = 0; k < kR1Blocks; ++k) E[8 * k] = ev[k];
+    }
+  }
+  __syncthreads();
+  if (tid < nrows) {
+    const int rr = r0 + tid;
+    const int slot = rr / p.G, gg = rr % p.G;
+    const int h = kvh * p.G + gg;
+    p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = fmax(red_m[tid][0], red_m[tid][1]);
+    p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = red_s[tid][0] + red_s[tid][1];
   }
 }
 
 constexpr int kR2Threads = 128;
-constexpr int kR2Blocks = 128;  // compressed blocks per CTA (2 R1 tiles)
+constexpr int kR2Blocks = 128;     // compressed blocks per CTA (2 R1 tiles)
+constexpr int kR2TileChunk = 64;   // tile statistics staged per pass
 
 __global__ void __launch_bounds__(kR2Threads)
     route_mass_kernel(const __grid_constant__ RouteParams p) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  double* sTM = reinterpret_cast<double*>(dsm);            // [Hq][kR2TileChunk]
+  double* sTD = sTM + (size_t)p.Hq * kR2TileChunk;
   __shared__ double sM[128], sD[128];
-  __shared__ double sF[128][kR2Blocks / kRouteTile];
+  __shared__ double sF[128][kR2Blocks / kRouteTile + 1];
+  __shared__ double smass[kR2Blocks + 8];
   const int slot = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * kR2Blocks;
   const int t0 = i0 / kRouteTile;
-  // per-head softmax statistics merged over the tiles (online-softmax merge)
-  for (int h = warp; h < p.Hq; h += kR2Threads / 32) {
-    const double* TM = p.TM + ((int64_t)slot * p.Hq + h) * p.ntiles;
-    const double* TD = p.TD + ((int64_t)slot * p.Hq + h) * p.ntiles;
-    double mx = -INFINITY, den = 0.0;
-    for (int t0l = 0; t0l < p.ntiles; t0l += 128) {
-      double tm[4], td[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int t = t0l + lane + 32 * k;
-        tm[k] = t < p.ntiles ? TM[t] : -INFINITY;
-        td[k] = t < p.ntiles ? TD[t] : 0.0;
-      }
-      double cmx = fmax(fmax(tm[0], tm[1]), fmax(tm[2], tm[3]));
+  const int halo = (p.l - 1) / p.d;  // <= 7 (host-checked)
+  const int ttlo = (i0 - halo) < 0 ? t0 : (i0 - halo) / kRouteTile;  // first tile touched
+  // per-head softmax statistics, merged over the tiles in passes of
+  // kR2TileChunk (all loads of a pass issued together)
+  for (int h = tid; h < p.Hq; h += kR2Threads) {
+    sM[h] = -INFINITY;
+    sD[h] = 0.0;
+  }
+  for (int tc = 0; tc < p.ntiles; tc += kR2TileChunk) {
+    const int nt = min(kR2TileChunk, p.ntiles - tc);
+    __syncthreads();
+    for (int e = tid; e < p.Hq * kR2TileChunk; e += kR2Threads) {
+      const int h = e / kR2TileChunk, t = e % kR2TileChunk;
+      const int64_t o = ((int64_t)slot * p.Hq + h) * p.ntiles + tc + t;
+      sTM[e] = t < nt ? p.TM[o] : -INFINITY;
+      sTD[e] = t < nt ? p.TD[o] : 0.0;
+    }
+    __syncthreads();
+    for (int h = warp; h < p.Hq; h += kR2Threads / 32) {
+      const double* tm = sTM + h * kR2TileChunk;
+      const double* td = sTD + h * kR2TileChunk;
+      double cmx = fmax(tm[lane], tm[lane + 32]);
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) cmx = fmax(cmx, __shfl_xor_sync(0xffffffffu, cmx, off));
       double cden = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (td[k] > 0.0) cden += td[k] * exp(tm[k] - cmx);
+      if (td[lane] > 0.0) cden += td[lane] * exp(tm[lane] - cmx);
+      if (td[lane + 32] > 0.0) cden += td[lane + 32] * exp(tm[lane + 32] - cmx);
 #pragma unroll
       for (int off = 16; off >= 1; off >>= 1) cden += __shfl_xor_sync(0xffffffffu, cden, off);
-      if (cmx != -INFINITY) {
-        const double nm = fmax(mx, cmx);
-        den = (mx == -INFINITY ? 0.0 : den * exp(mx - nm)) + cden * exp(cmx - nm);
-        mx = nm;
+      if (lane == 0 && cmx != -INFINITY) {
+        const double mx = sM[h], nm = fmax(mx, cmx);
+        sD[h] = (mx == -INFINITY ? 0.0 : sD[h] * exp(mx - nm)) + cden * exp(cmx - nm);
+        sM[h] = nm;
       }
-    }
-    if (lane == 0) {
-      sM[h] = mx;
-      sD[h] = den;
     }
   }
   __syncthreads();
-  for (int e = tid; e < p.Hq * (kR2Blocks / kRouteTile); e += kR2Threads) {
-    const int h = e / (kR2Blocks / kRouteTile), tt = e % (kR2Blocks / kRouteTile);
-    const int t = t0 + tt;
+  // per-(head, tile) factors exp(m_t - M_h) / DEN_h for the tiles this chunk touches
+  const int ntt = kR2Blocks / kRouteTile + 1;
+  for (int e = tid; e < p.Hq * ntt; e += kR2Threads) {
+    const int h = e / ntt, k = e % ntt;
+    const int t = ttlo + k;
     double f = 0.0;
     if (t < p.ntiles && sD[h] > 0.0) {
       const double tm = p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + t];
       if (tm != -INFINITY) f = exp(tm - sM[h]) / sD[h];
     }
-    sF[h][tt] = f;
+    sF[h][k] = f;
   }
   __syncthreads();
-  // mass for i in [i0 - halo, i0 + kR2Blocks): the halo covers the compressed
-  // blocks that straddle into this chunk's first selection block
-  __shared__ double smass[kR2Blocks + 8];
-  const int halo = (p.l - 1) / p.d;  // <= 7 (host-checked)
+  // mass for i in [i0 - halo, i0 + kR2Blocks): mass_i = sum_h (ascending) p_hi
   const int mvis = p.slot_mvis[slot];
   for (int k = tid; k < kR2Blocks + halo; k += kR2Threads) {
     const int i = i0 - halo + k;
     double mass = 0.0;
     if (i >= 0 && i < mvis) {
-      const int tt = i / kRouteTile;
+      const int tk = i / kRouteTile - ttlo;
       const double* E = p.E + (int64_t)slot * p.Hq * p.m_pad + i;
-      for (int h0 = 0; h0 < p.Hq; h0 += 16) {  // loads in flight, then accumulate in head order
-        double e[16], f[16];
+      for (int h0 = 0; h0 < p.Hq; h0 += 32) {
+        double ev[32];
 #pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) {
-          e[k2] = h0 + k2 < p.Hq ? E[(int64_t)(h0 + k2) * p.m_pad] : 0.0;
-          f[k2] = 0.0;
-        }
-        if (tt >= t0 && tt < t0 + kR2Blocks / kRouteTile) {
+        for (int k2 = 0; k2 < 32; ++k2) ev[k2] = h0 + k2 < p.Hq ? E[(int64_t)(h0 + k2) * p.m_pad] : 0.0;
 #pragma unroll
-          for (int k2 = 0; k2 < 16; ++k2) f[k2] = h0 + k2 < p.Hq ? sF[h0 + k2][tt - t0] : 0.0;
-        } else {  // halo block of the previous chunk: factor from the tile statistics
-#pragma unroll
-          for (int k2 = 0; k2 < 16; ++k2) {
-            const int h = h0 + k2;
-            if (h < p.Hq && sD[h] > 0.0) {
-              const double tm = p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tt];
-              f[k2] = tm == -INFINITY ? 0.0 : exp(tm - sM[h]) / sD[h];
-            }
-          }
-        }
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2)
-          if (h0 + k2 < p.Hq) mass += e[k2] * f[k2];
+        for (int k2 = 0; k2 < 32; ++k2)
+          if (h0 + k2 < p.Hq) mass += ev[k2] * sF[h0 + k2][tk];
       }
     }
     smass[k] = mass;
@@ -230,8 +242,8 @@ __global__ void __launch_bounds__(kR2Threads)
   // selection scores (nsa_attention.cpp:67-78): block b gets, in ascending i,
   // mass_i * (1/Hq) * overlap / l from every compressed block overlapping it
   const double inv_heads = 1.0 / (double)p.Hq;
-  const int b_lo = (i0 * p.d + p.l_sel - 1) / p.l_sel;                  // first block starting in chunk
-  const int b_hi = ((i0 + kR2Blocks) * p.d + p.l_sel - 1) / p.l_sel;    // exclusive
+  const int b_lo = (i0 * p.d + p.l_sel - 1) / p.l_sel;
+  const int b_hi = ((i0 + kR2Blocks) * p.d + p.l_sel - 1) / p.l_sel;
   const int avail = p.slot_avail[slot];
   for (int b = b_lo + tid; b < b_hi && b < avail; b += kR2Threads) {
     const int64_t blo = (int64_t)b * p.l_sel, bhi = blo + p.l_sel;
@@ -242,7 +254,8 @@ __global__ void __launch_bounds__(kR2Threads)
       const int64_t olo = lo > blo ? lo : blo;
       const int64_t ohi = hi < bhi ? hi : bhi;
       if (ohi <= olo) continue;
-      const double mi = (i - (i0 - halo)) < kR2Blocks + halo ? smass[i - (i0 - halo)] : 0.0;
+      const int64_t k = i - (i0 - halo);
+      const double mi = (k >= 0 && k < kR2Blocks + halo) ? smass[k] : 0.0;
       sacc = __dadd_rn(sacc, __ddiv_rn(__dmul_rn(__dmul_rn(mi, inv_heads), (double)(ohi - olo)),
                                        (double)p.l));
     }
@@ -258,28 +271,77 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
 }
 
 // Top-n over sel[0, avail) (select_blocks, nsa_attention.cpp:94-136): forced
-// blocks first, then the best remaining by (score desc, id asc).  Each
-// candidate counts the candidates that rank before it, stopping once it
-// cannot be among the winners; a winner's count is its rank.
-__device__ void topn_write(const double* sel, int avail, int n, int32_t* idx_row, int32_t* count,
-                           uint32_t* forced_bits) {
+// blocks first, then the best remaining by (score desc, id asc).
+//  1. every warp's best candidate -> the K-th best of those is a lower bound
+//     of the K-th best overall (K = picks needed, <= number of warps);
+//  2. candidates ranking at or before that bound survive (typically ~K);
+//  3. exact rank among the survivors.
+__device__ void topn_write(const double* sel, int* surv, int avail, int n, int32_t* idx_row,
+                           int32_t* count, uint32_t* forced_bits) {
+  __shared__ double wbest_s[32];
+  __shared__ int wbest_i[32];
+  __shared__ double lb_s;
+  __shared__ int lb_i, nsurv;
   __shared__ int picks[64];
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int nwarps = nthr >> 5;
   const int f1 = avail - 2 > 0 ? avail - 2 : -1;
   const int f2 = avail - 1 > 0 ? avail - 1 : -1;
   const int nforced = avail > 0 ? 1 + (f1 > 0) + (f2 > 0 && f2 != f1) : 0;
   const int target = n < avail ? n : avail;
-  const int want = target - nforced;  // picks among the non-forced blocks
-  if (tid < 64) picks[tid] = -1;
-  __syncthreads();
-  for (int b = tid; b < avail && want > 0; b += nthr) {
+  const int want = target - nforced;
+  auto cand = [&](int b, double& sc) {
     const bool forced = b == 0 || b == f1 || b == f2;
-    int rank = 0;
-    if (!forced) {
+    sc = (b < avail && !forced) ? sel[b] : -INFINITY;
+    return b < avail && !forced;
+  };
+  if (tid == 0) nsurv = 0;
+  if (want > 0) {
+    // 1. per-warp best over the warp's candidates (b = warp*32 + lane + k*nthr)
+    double bs = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int b = warp * 32 + lane; b < avail; b += nthr) {
+      double sc;
+      if (cand(b, sc) && ranks_before(sc, b, bs, bi)) { bs = sc; bi = b; }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ranks_before(os, oi, bs, bi)) { bs = os; bi = oi; }
+    }
+    if (lane == 0) { wbest_s[warp] = bs; wbest_i[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {  // K-th best warp maximum (rank counting among <= 32)
+      const double ms = lane < nwarps ? wbest_s[lane] : -INFINITY;
+      const int mi = lane < nwarps ? wbest_i[lane] : 0x7fffffff;
+      int rank = 0;
+      for (int o = 0; o < nwarps; ++o) rank += ranks_before(wbest_s[o], wbest_i[o], ms, mi) ? 1 : 0;
+      const int kk = want <= nwarps ? want - 1 : -1;
+      if (lane == 0 && kk < 0) { lb_s = -INFINITY; lb_i = 0x7fffffff; }  // no bound: all survive
+      if (kk >= 0 && lane < nwarps && rank == kk) { lb_s = ms; lb_i = mi; }
+    }
+    __syncthreads();
+    // 2. survivors: rank at or before the bound
+    const double ls = lb_s;
+    const int li = lb_i;
+    for (int b = tid; b < avail; b += nthr) {
+      double sc;
+      if (cand(b, sc) && (ranks_before(sc, b, ls, li) || (sc == ls && b == li))) {
+        const int slotn = atomicAdd(&nsurv, 1);
+        surv[slotn] = b;
+      }
+    }
+    __syncthreads();
+    // 3. exact rank among survivors
+    const int ns = nsurv;
+    for (int k = tid; k < ns; k += nthr) {
+      const int b = surv[k];
       const double sb = sel[b];
-      for (int c = 0; c < avail && rank < want; ++c) {
-        const bool cf = c == 0 || c == f1 || c == f2;
-        rank += (!cf && ranks_before(sel[c], c, sb, b)) ? 1 : 0;
+      int rank = 0;
+      for (int o = 0; o < ns; ++o) {
+        const int c = surv[o];
+        rank += ranks_before(sel[c], c, sb, b) ? 1 : 0;
       }
       if (rank < want) picks[nforced + rank] = b;
     }
@@ -315,6 +377,7 @@ __global__ void __launch_bounds__(kR3Threads)
   const int slot = only_slot >= 0 ? only_slot : blockIdx.x;
   const int avail = p.slot_avail[slot];
   double* sel = reinterpret_cast<double*>(smem);
+  int* surv = reinterpret_cast<int*>(sel + kMaxAvail);
   for (int b = threadIdx.x; b < avail; b += blockDim.x) {
     const double v = p.ntiles > 0 ? p.sel[(int64_t)slot * p.sel_pad + b] : 0.0;
     sel[b] = v;
@@ -331,7 +394,7 @@ __global__ void __launch_bounds__(kR3Threads)
     }
   }
   const int q = p.slot_q[slot];
-  topn_write(sel, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q, p.idx_forced + q);
+  topn_write(sel, surv, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q, p.idx_forced + q);
 }
 
 __global__ void __launch_bounds__(kR3Threads)
@@ -339,31 +402,35 @@ __global__ void __launch_bounds__(kR3Threads)
                        uint32_t* forced) {
   extern __shared__ __align__(16) uint8_t smem[];
   double* sel = reinterpret_cast<double*>(smem);
+  int* surv = reinterpret_cast<int*>(sel + kMaxAvail);
   for (int b = threadIdx.x; b < avail; b += blockDim.x) sel[b] = scores[b];
   __syncthreads();
-  topn_write(sel, avail, n, idx, count, forced);
+  topn_write(sel, surv, avail, n, idx, count, forced);
 }
 
-constexpr size_t kR3Smem = (size_t)kMaxAvail * 8;
+constexpr size_t kR3Smem = (size_t)kMaxAvail * 8 + (size_t)kMaxAvail * 4;
 
 cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   if (p.ntiles == 0) return cudaSuccess;  // nothing compressed is visible yet: all masses 0
   const int rows_total = p.nr * p.G;
   const int rchunks = (rows_total + kRouteRows - 1) / kRouteRows;
   const int maxrows = rows_total < kRouteRows ? rows_total : kRouteRows;
-  const size_t smem1 = (size_t)maxrows * p.dh * 8 + (size_t)kRouteTile * (p.dh + 4) * 4;
+  const size_t smem1 = (size_t)kRouteRows * (p.dh + 2) * 8 + (size_t)kRouteTile * (p.dh + 4) * 4;
   cudaError_t e = cudaFuncSetAttribute(route_logits_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(route_logits_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
-  const int warps = (maxrows + kRowsPerWarp - 1) / kRowsPerWarp;
-  route_logits_kernel<<<dim3(p.ntiles, p.Hkv, rchunks), 32 * warps, smem1, s>>>(p);
+  (void)maxrows;
+  route_logits_kernel<<<dim3(p.ntiles, p.Hkv, rchunks), kR1Threads, smem1, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // one extra chunk so the selection blocks that start past the last compressed block get written
-  route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, 0, s>>>(p);
+  const size_t smem2 = (size_t)p.Hq * kR2TileChunk * 16;
+  e = cudaFuncSetAttribute(route_mass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  if (e != cudaSuccess) return e;
+  route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, smem2, s>>>(p);
   return cudaGetLastError();
 }
 
