@@ -29,6 +29,7 @@ namespace {
 constexpr int kR1Rows = 8;      // query rows per thread
 constexpr int kR1Blocks = 4;    // compressed blocks per thread
 constexpr int kR1Threads = 256; // 4 row groups x 2 block halves x 32 lanes
+constexpr int kDhRoute = 128;   // d_head of this build (host-checked)
 
 // Lane (g, l) = (lane / 4, lane % 4) accumulates the elements x = l (mod 4)
 // of its 8 rows x 4 blocks: exactly the reference's lane-l partial sum s_l
@@ -52,22 +53,44 @@ __global__ void __launch_bounds__(kR1Threads, 2)
   const int g = lane >> 2, l = lane & 3;
   const int rg = warp >> 1, bh = warp & 1;  // row group, block half
 
-  for (int e = tid; e < nrows * (dh / 4); e += kR1Threads) {  // q rows, fp32 -> fp64 (exact)
-    const int r = e / (dh / 4), x4 = e % (dh / 4);
-    const int rr = r0 + r;
-    const int slot = rr / p.G, gg = rr % p.G;
-    const int h = kvh * p.G + gg;
-    const float4 v = *reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4);
-    double* dst = qd + (size_t)r * qld + 4 * x4;
-    dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
-  }
+  // staging: every thread issues all of its loads before storing any (one
+  // round trip instead of one per loop iteration)
+  constexpr int kQPer = kRouteRows * (kDhRoute / 4) / kR1Threads;   // 4
+  constexpr int kKPer = kRouteTile * (kDhRoute / 4) / kR1Threads;   // 8
   const int i0 = tile * kRouteTile;
-  for (int e = tid; e < kRouteTile * (dh / 4); e += kR1Threads) {  // key tile (zero beyond the cache)
-    const int b = e / (dh / 4), x4 = e % (dh / 4);
+  float4 qv4[kQPer], kv4[kKPer];
+#pragma unroll
+  for (int it = 0; it < kQPer; ++it) {
+    const int e = tid + it * kR1Threads;
+    const int r = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
+    const int rr = r0 + r;
+    qv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < nrows) {
+      const int slot = rr / p.G, gg = rr % p.G;
+      const int h = kvh * p.G + gg;
+      qv4[it] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4));
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < kKPer; ++it) {
+    const int e = tid + it * kR1Threads;
+    const int b = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
     const int i = i0 + b;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < p.blocks) v = *reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + kvh) * dh + x4 * 4);
-    *reinterpret_cast<float4*>(cks + b * ckld + x4 * 4) = v;
+    kv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < p.blocks) kv4[it] = __ldg(reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + kvh) * dh + x4 * 4));
+  }
+#pragma unroll
+  for (int it = 0; it < kQPer; ++it) {
+    const int e = tid + it * kR1Threads;
+    const int r = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
+    double* dst = qd + (size_t)r * qld + 4 * x4;
+    dst[0] = qv4[it].x; dst[1] = qv4[it].y; dst[2] = qv4[it].z; dst[3] = qv4[it].w;
+  }
+#pragma unroll
+  for (int it = 0; it < kKPer; ++it) {
+    const int e = tid + it * kR1Threads;
+    const int b = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
+    *reinterpret_cast<float4*>(cks + b * ckld + x4 * 4) = kv4[it];
   }
   __syncthreads();
 
@@ -180,11 +203,29 @@ __global__ void __launch_bounds__(kR2Threads)
   for (int tc = 0; tc < p.ntiles; tc += kR2TileChunk) {
     const int nt = min(kR2TileChunk, p.ntiles - tc);
     __syncthreads();
-    for (int e = tid; e < p.Hq * kR2TileChunk; e += kR2Threads) {
-      const int h = e / kR2TileChunk, t = e % kR2TileChunk;
-      const int64_t o = ((int64_t)slot * p.Hq + h) * p.ntiles + tc + t;
-      sTM[e] = t < nt ? p.TM[o] : -INFINITY;
-      sTD[e] = t < nt ? p.TD[o] : 0.0;
+    constexpr int kBatch = 8;  // loads in flight per thread per round trip
+    for (int base = 0; base < p.Hq * kR2TileChunk; base += kBatch * kR2Threads) {
+      double vm[kBatch], vd[kBatch];
+#pragma unroll
+      for (int it = 0; it < kBatch; ++it) {
+        const int e = base + tid + it * kR2Threads;
+        const int h = e / kR2TileChunk, t = e % kR2TileChunk;
+        vm[it] = -INFINITY;
+        vd[it] = 0.0;
+        if (h < p.Hq && t < nt) {
+          const int64_t o = ((int64_t)slot * p.Hq + h) * p.ntiles + tc + t;
+          vm[it] = p.TM[o];
+          vd[it] = p.TD[o];
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kBatch; ++it) {
+        const int e = base + tid + it * kR2Threads;
+        if (e < p.Hq * kR2TileChunk) {
+          sTM[e] = vm[it];
+          sTD[e] = vd[it];
+        }
+      }
     }
     __syncthreads();
     for (int h = warp; h < p.Hq; h += kR2Threads / 32) {
@@ -295,7 +336,11 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
     sc = (b < avail && !forced) ? sel[b] : -INFINITY;
     return b < avail && !forced;
   };
-  if (tid == 0) nsurv = 0;
+  if (tid == 0) {
+    nsurv = 0;
+    lb_s = -INFINITY;  // no bound unless a warp maximum holds rank K-1
+    lb_i = 0x7fffffff;
+  }
   if (want > 0) {
     // 1. per-warp best over the warp's candidates (b = warp*32 + lane + k*nthr)
     double bs = -INFINITY;
@@ -318,8 +363,7 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
       int rank = 0;
       for (int o = 0; o < nwarps; ++o) rank += ranks_before(wbest_s[o], wbest_i[o], ms, mi) ? 1 : 0;
       const int kk = want <= nwarps ? want - 1 : -1;
-      if (lane == 0 && kk < 0) { lb_s = -INFINITY; lb_i = 0x7fffffff; }  // no bound: all survive
-      if (kk >= 0 && lane < nwarps && rank == kk) { lb_s = ms; lb_i = mi; }
+      if (kk >= 0 && lane < nwarps && rank == kk && ms != -INFINITY) { lb_s = ms; lb_i = mi; }
     }
     __syncthreads();
     // 2. survivors: rank at or before the bound
