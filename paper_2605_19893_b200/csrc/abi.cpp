@@ -105,7 +105,7 @@ int splits_for(const specsv_nsa_config& c, int32_t nq) {
 
 struct Layout {
   size_t attend_off = 0, attend_bytes = 0;
-  size_t E_off = 0, TM_off = 0, TD_off = 0, mass_off = 0, sel_off = 0;
+  size_t E_off = 0, TM_off = 0, TD_off = 0, mass_off = 0, sel_off = 0, cnt_off = 0;
   int64_t sel_pad = 0;
   size_t total = 0;
 };
@@ -137,6 +137,9 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
   L.sel_off = off;
   off = align_up(off + (size_t)nq * L.sel_pad * 8, 256);
+  L.cnt_off = off;  // R1 tile counters: [row chunks][Hkv], zero-filled with the workspace
+  off = align_up(off + (size_t)((nq * c.n_q_heads / c.n_kv_heads + kRouteRows - 1) / kRouteRows) *
+                           c.n_kv_heads * sizeof(int32_t), 256);
   L.total = off;
   return L;
 }
@@ -220,6 +223,7 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
   p.mass = reinterpret_cast<double*>(ws + L.mass_off);
   p.sel = reinterpret_cast<double*>(ws + L.sel_off);
   p.sel_pad = (int32_t)L.sel_pad;
+  p.counters = reinterpret_cast<int32_t*>(ws + L.cnt_off);
   return p;
 }
 

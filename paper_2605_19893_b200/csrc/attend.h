@@ -51,7 +51,8 @@ struct RouteParams {
   const float* ck;       // fp32 [blocks][Hkv][dh]
   double* E;             // [nr][Hq][m_pad] exp(logit - tile max)
   double* TM;            // [nr][Hq][ntiles] tile max
-  double* TD;            // [nr][Hq][ntiles] tile denominators
+  double* TD;            // [nr][Hq][ntiles] tile denominators, then per-tile factors
+  int32_t* counters;     // [row chunks][Hkv] zero-initialised, self-resetting
   double* mass;          // [nr][m_pad]
   double* sel;           // [nr][sel_pad] selection-block scores
   int32_t sel_pad;

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kR1Threads, 2)
       const double t = __dadd_rn(acc[a][k], __shfl_xor_sync(0xffffffffu, acc[a][k], 2));
       acc[a][k] = __dmul_rn(__dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 1)), p.scale);
     }
-  // per-row tile max and exp-sum over the 64 blocks (2 warps x 8 groups x 4)
+  // per-row tile max over the 64 blocks (2 warps x 8 groups x 4)
 #pragma unroll
   for (int a = 0; a < kR1Rows; ++a) {
     const int r = rbase + a;
@@ -140,8 +140,10 @@ __global__ void __launch_bounds__(kR1Threads, 2)
     if (lane == 0) red_m[rbase + a][bh] = mx;
   }
   __syncthreads();
+  // exp: the 4 lanes of a group hold identical logits; lane l takes rows l, l+4
 #pragma unroll
-  for (int a = 0; a < kR1Rows; ++a) {
+  for (int a2 = 0; a2 < kR1Rows / 4; ++a2) {
+    const int a = a2 * 4 + l;
     const int r = rbase + a;
     const bool rowok = r < nrows;
     const int rr = r0 + (rowok ? r : 0);
@@ -153,14 +155,16 @@ __global__ void __launch_bounds__(kR1Threads, 2)
     double ev[kR1Blocks];
 #pragma unroll
     for (int k = 0; k < kR1Blocks; ++k) {
+      const double v = l == 0 ? acc[a2 * 4][k] : l == 1 ? acc[a2 * 4 + 1][k]
+                     : l == 2 ? acc[a2 * 4 + 2][k] : acc[a2 * 4 + 3][k];
       const bool ok = rowok && i0 + bh * 32 + g + 8 * k < mvis;
-      ev[k] = ok ? exp(acc[a][k] - mx) : 0.0;
+      ev[k] = ok ? exp(v - mx) : 0.0;
       sum += ev[k];
     }
 #pragma unroll
     for (int off = 4; off <= 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-    if (lane == 0) red_s[rbase + a][bh] = sum;
-    if (rowok && l == 0) {
+    if (g == 0) red_s[rbase + a][bh] = sum;
+    if (rowok) {
       double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad + i0 + bh * 32 + g;
 #pragma unroll
       for (int k = 0; k < kR1Blocks; ++k) E[8 * k] = ev[k];
@@ -174,114 +178,81 @@ __global__ void __launch_bounds__(kR1Threads, 2)
     p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = fmax(red_m[tid][0], red_m[tid][1]);
     p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = red_s[tid][0] + red_s[tid][1];
   }
+  // the last tile CTA of this (row chunk, KV head) folds the tile statistics
+  // into per-tile factors F_t = exp(m_t - M) / DEN (online-softmax merge),
+  // written over TD; the counter returns to 0 for the next launch
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    int* cnt = p.counters + blockIdx.z * p.Hkv + kvh;
+    is_last = atomicAdd(cnt, 1) == p.ntiles - 1;
+    if (is_last) atomicExch(cnt, 0);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int r = warp; r < nrows; r += kR1Threads / 32) {
+    const int rr = r0 + r;
+    const int slot = rr / p.G, gg = rr % p.G;
+    const int h = kvh * p.G + gg;
+    volatile double* TM = p.TM + ((int64_t)slot * p.Hq + h) * p.ntiles;
+    volatile double* TD = p.TD + ((int64_t)slot * p.Hq + h) * p.ntiles;
+    double mx = -INFINITY;
+    for (int t = lane; t < p.ntiles; t += 32) mx = fmax(mx, TM[t]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    double den = 0.0;
+    for (int t = lane; t < p.ntiles; t += 32)
+      if (TD[t] > 0.0) den += TD[t] * exp(TM[t] - mx);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+    for (int t = lane; t < p.ntiles; t += 32) {
+      const double tm = TM[t];
+      TD[t] = (den > 0.0 && tm != -INFINITY) ? exp(tm - mx) / den : 0.0;
+    }
+  }
 }
 
 constexpr int kR2Threads = 128;
-constexpr int kR2Blocks = 128;     // compressed blocks per CTA (2 R1 tiles)
-constexpr int kR2TileChunk = 64;   // tile statistics staged per pass
+constexpr int kR2Blocks = 128;     // compressed blocks per CTA
 
+// mass_i = sum_h (ascending) E[h][i] * F[h][tile(i)] for i in [i0 - halo,
+// i0 + 128), then the selection scores of the blocks starting in this chunk
+// (nsa_attention.cpp:67-78: block b gets, in ascending i, mass_i * (1/Hq) *
+// overlap / l from every compressed block overlapping it)
 __global__ void __launch_bounds__(kR2Threads)
     route_mass_kernel(const __grid_constant__ RouteParams p) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  double* sTM = reinterpret_cast<double*>(dsm);            // [Hq][kR2TileChunk]
-  double* sTD = sTM + (size_t)p.Hq * kR2TileChunk;
-  __shared__ double sM[128], sD[128];
-  __shared__ double sF[128][kR2Blocks / kRouteTile + 1];
   __shared__ double smass[kR2Blocks + 8];
   const int slot = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int i0 = blockIdx.x * kR2Blocks;
-  const int t0 = i0 / kRouteTile;
   const int halo = (p.l - 1) / p.d;  // <= 7 (host-checked)
-  const int ttlo = (i0 - halo) < 0 ? t0 : (i0 - halo) / kRouteTile;  // first tile touched
-  // per-head softmax statistics, merged over the tiles in passes of
-  // kR2TileChunk (all loads of a pass issued together)
-  for (int h = tid; h < p.Hq; h += kR2Threads) {
-    sM[h] = -INFINITY;
-    sD[h] = 0.0;
-  }
-  for (int tc = 0; tc < p.ntiles; tc += kR2TileChunk) {
-    const int nt = min(kR2TileChunk, p.ntiles - tc);
-    __syncthreads();
-    constexpr int kBatch = 8;  // loads in flight per thread per round trip
-    for (int base = 0; base < p.Hq * kR2TileChunk; base += kBatch * kR2Threads) {
-      double vm[kBatch], vd[kBatch];
-#pragma unroll
-      for (int it = 0; it < kBatch; ++it) {
-        const int e = base + tid + it * kR2Threads;
-        const int h = e / kR2TileChunk, t = e % kR2TileChunk;
-        vm[it] = -INFINITY;
-        vd[it] = 0.0;
-        if (h < p.Hq && t < nt) {
-          const int64_t o = ((int64_t)slot * p.Hq + h) * p.ntiles + tc + t;
-          vm[it] = p.TM[o];
-          vd[it] = p.TD[o];
-        }
-      }
-#pragma unroll
-      for (int it = 0; it < kBatch; ++it) {
-        const int e = base + tid + it * kR2Threads;
-        if (e < p.Hq * kR2TileChunk) {
-          sTM[e] = vm[it];
-          sTD[e] = vd[it];
-        }
-      }
-    }
-    __syncthreads();
-    for (int h = warp; h < p.Hq; h += kR2Threads / 32) {
-      const double* tm = sTM + h * kR2TileChunk;
-      const double* td = sTD + h * kR2TileChunk;
-      double cmx = fmax(tm[lane], tm[lane + 32]);
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) cmx = fmax(cmx, __shfl_xor_sync(0xffffffffu, cmx, off));
-      double cden = 0.0;
-      if (td[lane] > 0.0) cden += td[lane] * exp(tm[lane] - cmx);
-      if (td[lane + 32] > 0.0) cden += td[lane + 32] * exp(tm[lane + 32] - cmx);
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) cden += __shfl_xor_sync(0xffffffffu, cden, off);
-      if (lane == 0 && cmx != -INFINITY) {
-        const double mx = sM[h], nm = fmax(mx, cmx);
-        sD[h] = (mx == -INFINITY ? 0.0 : sD[h] * exp(mx - nm)) + cden * exp(cmx - nm);
-        sM[h] = nm;
-      }
-    }
-  }
-  __syncthreads();
-  // per-(head, tile) factors exp(m_t - M_h) / DEN_h for the tiles this chunk touches
-  const int ntt = kR2Blocks / kRouteTile + 1;
-  for (int e = tid; e < p.Hq * ntt; e += kR2Threads) {
-    const int h = e / ntt, k = e % ntt;
-    const int t = ttlo + k;
-    double f = 0.0;
-    if (t < p.ntiles && sD[h] > 0.0) {
-      const double tm = p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + t];
-      if (tm != -INFINITY) f = exp(tm - sM[h]) / sD[h];
-    }
-    sF[h][k] = f;
-  }
-  __syncthreads();
-  // mass for i in [i0 - halo, i0 + kR2Blocks): mass_i = sum_h (ascending) p_hi
   const int mvis = p.slot_mvis[slot];
+  const double* F = p.TD;  // per-tile factors written by the last R1 CTA
   for (int k = tid; k < kR2Blocks + halo; k += kR2Threads) {
     const int i = i0 - halo + k;
     double mass = 0.0;
     if (i >= 0 && i < mvis) {
-      const int tk = i / kRouteTile - ttlo;
+      const int t = i / kRouteTile;
       const double* E = p.E + (int64_t)slot * p.Hq * p.m_pad + i;
-      for (int h0 = 0; h0 < p.Hq; h0 += 32) {
-        double ev[32];
+      const double* Fs = F + (int64_t)slot * p.Hq * p.ntiles + t;
+      for (int h0 = 0; h0 < p.Hq; h0 += 16) {
+        double ev[16], fv[16];
 #pragma unroll
-        for (int k2 = 0; k2 < 32; ++k2) ev[k2] = h0 + k2 < p.Hq ? E[(int64_t)(h0 + k2) * p.m_pad] : 0.0;
+        for (int k2 = 0; k2 < 16; ++k2) {
+          const bool ok = h0 + k2 < p.Hq;
+          ev[k2] = ok ? E[(int64_t)(h0 + k2) * p.m_pad] : 0.0;
+          fv[k2] = ok ? Fs[(int64_t)(h0 + k2) * p.ntiles] : 0.0;
+        }
 #pragma unroll
-        for (int k2 = 0; k2 < 32; ++k2)
-          if (h0 + k2 < p.Hq) mass += ev[k2] * sF[h0 + k2][tk];
+        for (int k2 = 0; k2 < 16; ++k2)
+          if (h0 + k2 < p.Hq) mass += ev[k2] * fv[k2];
       }
     }
     smass[k] = mass;
   }
   __syncthreads();
-  // selection scores (nsa_attention.cpp:67-78): block b gets, in ascending i,
-  // mass_i * (1/Hq) * overlap / l from every compressed block overlapping it
   const double inv_heads = 1.0 / (double)p.Hq;
   const int b_lo = (i0 * p.d + p.l_sel - 1) / p.l_sel;
   const int b_hi = ((i0 + kR2Blocks) * p.d + p.l_sel - 1) / p.l_sel;
@@ -471,10 +442,7 @@ cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // one extra chunk so the selection blocks that start past the last compressed block get written
-  const size_t smem2 = (size_t)p.Hq * kR2TileChunk * 16;
-  e = cudaFuncSetAttribute(route_mass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-  if (e != cudaSuccess) return e;
-  route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, smem2, s>>>(p);
+  route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
