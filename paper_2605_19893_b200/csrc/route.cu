@@ -19,6 +19,7 @@
 //     sort, written ascending.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "attend.h"
@@ -26,167 +27,186 @@
 namespace specsv_b200 {
 namespace {
 
-constexpr int kR1Rows = 8;      // query rows per thread
 constexpr int kR1Blocks = 4;    // compressed blocks per thread
 constexpr int kR1Threads = 256; // 4 row groups x 2 block halves x 32 lanes
 constexpr int kDhRoute = 128;   // d_head of this build (host-checked)
 
 // Lane (g, l) = (lane / 4, lane % 4) accumulates the elements x = l (mod 4)
-// of its 8 rows x 4 blocks: exactly the reference's lane-l partial sum s_l
+// of its R rows x 4 blocks: exactly the reference's lane-l partial sum s_l
 // (kernels.hpp:13-18), so two xor-shuffles rebuild (s0 + s2) + (s1 + s3)
 // bit-for-bit.  q rows are broadcast loads (same x for all groups), key rows
 // are 8 consecutive blocks per load (conflict-free with the 4-float pad).
-__global__ void __launch_bounds__(kR1Threads, 2)
+// Persistent over tiles: the next tile's keys are prefetched into registers
+// while the current tile is multiplied.
+template <int R>
+__global__ void __launch_bounds__(kR1Threads, 1)
     route_logits_kernel(const __grid_constant__ RouteParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ double red_m[kR1Rows * 4][2], red_s[kR1Rows * 4][2];
-  const int dh = p.dh;
-  const int tile = blockIdx.x, kvh = blockIdx.y;
+  __shared__ double red_m[4 * R][2], red_s[4 * R][2];
+  __shared__ int is_last;
+  constexpr int kRows = 4 * R;
+  constexpr int dh = kDhRoute;
+  constexpr int qld = dh + 2;  // doubles
+  constexpr int ckld = dh + 4; // floats
+  const int kvh = blockIdx.y;
   const int rows_total = p.nr * p.G;
-  const int r0 = blockIdx.z * kRouteRows;
-  const int nrows = min(kRouteRows, rows_total - r0);
-  const int qld = dh + 2;  // doubles
-  double* qd = reinterpret_cast<double*>(smem);                                // [32][qld]
-  float* cks = reinterpret_cast<float*>(smem + (size_t)kRouteRows * qld * 8);  // [64][dh + 4]
-  const int ckld = dh + 4;
+  const int r0 = blockIdx.z * kRows;
+  const int nrows = min(kRows, rows_total - r0);
+  double* qd = reinterpret_cast<double*>(smem);                                    // [kRows][qld]
+  float* ckbuf = reinterpret_cast<float*>(smem + (size_t)kRows * qld * 8);         // 2 x [64][ckld]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, l = lane & 3;
   const int rg = warp >> 1, bh = warp & 1;  // row group, block half
+  constexpr int kKPer = kRouteTile * (dh / 4) / kR1Threads;  // 8 float4 per thread
 
-  // staging: every thread issues all of its loads before storing any (one
-  // round trip instead of one per loop iteration)
-  constexpr int kQPer = kRouteRows * (kDhRoute / 4) / kR1Threads;   // 4
-  constexpr int kKPer = kRouteTile * (kDhRoute / 4) / kR1Threads;   // 8
-  const int i0 = tile * kRouteTile;
-  float4 qv4[kQPer], kv4[kKPer];
+  auto load_tile = [&](int t, float4 (&kv4)[kKPer]) {
 #pragma unroll
-  for (int it = 0; it < kQPer; ++it) {
-    const int e = tid + it * kR1Threads;
-    const int r = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
-    const int rr = r0 + r;
-    qv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < nrows) {
-      const int slot = rr / p.G, gg = rr % p.G;
-      const int h = kvh * p.G + gg;
-      qv4[it] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4));
+    for (int it = 0; it < kKPer; ++it) {
+      const int e = tid + it * kR1Threads;
+      const int b = e / (dh / 4), x4 = e % (dh / 4);
+      const int i = t * kRouteTile + b;
+      kv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < p.ntiles && i < p.blocks)
+        kv4[it] = __ldg(reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + kvh) * dh + x4 * 4));
     }
-  }
+  };
+  auto store_tile = [&](float* dst, const float4 (&kv4)[kKPer]) {
 #pragma unroll
-  for (int it = 0; it < kKPer; ++it) {
-    const int e = tid + it * kR1Threads;
-    const int b = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
-    const int i = i0 + b;
-    kv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < p.blocks) kv4[it] = __ldg(reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + kvh) * dh + x4 * 4));
-  }
-#pragma unroll
-  for (int it = 0; it < kQPer; ++it) {
-    const int e = tid + it * kR1Threads;
-    const int r = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
-    double* dst = qd + (size_t)r * qld + 4 * x4;
-    dst[0] = qv4[it].x; dst[1] = qv4[it].y; dst[2] = qv4[it].z; dst[3] = qv4[it].w;
-  }
-#pragma unroll
-  for (int it = 0; it < kKPer; ++it) {
-    const int e = tid + it * kR1Threads;
-    const int b = e / (kDhRoute / 4), x4 = e % (kDhRoute / 4);
-    *reinterpret_cast<float4*>(cks + b * ckld + x4 * 4) = kv4[it];
-  }
-  __syncthreads();
+    for (int it = 0; it < kKPer; ++it) {
+      const int e = tid + it * kR1Threads;
+      const int b = e / (dh / 4), x4 = e % (dh / 4);
+      *reinterpret_cast<float4*>(dst + b * ckld + x4 * 4) = kv4[it];
+    }
+  };
 
-  const int rbase = rg * kR1Rows;
-  double acc[kR1Rows][kR1Blocks];
+  {  // q rows, fp32 -> fp64 (exact), all loads in flight
+    constexpr int kQPer = (kRows * (dh / 4) + kR1Threads - 1) / kR1Threads;
+    float4 qv4[kQPer];
 #pragma unroll
-  for (int a = 0; a < kR1Rows; ++a)
+    for (int it = 0; it < kQPer; ++it) {
+      const int e = tid + it * kR1Threads;
+      const int r = e / (dh / 4), x4 = e % (dh / 4);
+      qv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nrows) {
+        const int rr = r0 + r;
+        const int slot = rr / p.G, gg = rr % p.G;
+        const int h = kvh * p.G + gg;
+        qv4[it] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4));
+      }
+    }
 #pragma unroll
-    for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = 0.0;
-  if (rbase < nrows) {
-    const double* qrow = qd + (size_t)rbase * qld + l;
-    const float* krow = cks + (bh * 32 + g) * ckld + l;
-#pragma unroll 2
-    for (int x = 0; x < dh; x += 4) {
-      double kv[kR1Blocks];
-#pragma unroll
-      for (int k = 0; k < kR1Blocks; ++k) kv[k] = krow[8 * k * ckld + x];
-#pragma unroll
-      for (int a = 0; a < kR1Rows; ++a) {
-        const double qv = qrow[a * qld + x];
-#pragma unroll
-        for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = fma(qv, kv[k], acc[a][k]);
+    for (int it = 0; it < kQPer; ++it) {
+      const int e = tid + it * kR1Threads;
+      const int r = e / (dh / 4), x4 = e % (dh / 4);
+      if (r < kRows) {
+        double* dst = qd + (size_t)r * qld + 4 * x4;
+        dst[0] = qv4[it].x; dst[1] = qv4[it].y; dst[2] = qv4[it].z; dst[3] = qv4[it].w;
       }
     }
   }
-  // rebuild the reference's dot: (s0 + s2) + (s1 + s3), then * 1/sqrt(dh)
-#pragma unroll
-  for (int a = 0; a < kR1Rows; ++a)
-#pragma unroll
-    for (int k = 0; k < kR1Blocks; ++k) {
-      const double t = __dadd_rn(acc[a][k], __shfl_xor_sync(0xffffffffu, acc[a][k], 2));
-      acc[a][k] = __dmul_rn(__dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 1)), p.scale);
-    }
-  // per-row tile max over the 64 blocks (2 warps x 8 groups x 4)
-#pragma unroll
-  for (int a = 0; a < kR1Rows; ++a) {
-    const int r = rbase + a;
-    const bool rowok = r < nrows;
-    const int rr = r0 + (rowok ? r : 0);
-    const int mvis = p.slot_mvis[rr / p.G];
-    double mx = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < kR1Blocks; ++k)
-      if (rowok && i0 + bh * 32 + g + 8 * k < mvis) mx = fmax(mx, acc[a][k]);
-#pragma unroll
-    for (int off = 4; off <= 16; off <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if (lane == 0) red_m[rbase + a][bh] = mx;
-  }
+  float4 kv4[kKPer];
+  int t = blockIdx.x;
+  load_tile(t, kv4);
+  store_tile(ckbuf, kv4);
   __syncthreads();
-  // exp: the 4 lanes of a group hold identical logits; lane l takes rows l, l+4
+  const int rbase = rg * R;
+  for (int it_t = 0; t < p.ntiles; t += gridDim.x, ++it_t) {
+    const float* cks = ckbuf + (it_t & 1) * kRouteTile * ckld;
+    load_tile(t + gridDim.x, kv4);  // next tile, lands while this one is multiplied
+    const int i0 = t * kRouteTile;
+    double acc[R][kR1Blocks];
 #pragma unroll
-  for (int a2 = 0; a2 < kR1Rows / 4; ++a2) {
-    const int a = a2 * 4 + l;
-    const int r = rbase + a;
-    const bool rowok = r < nrows;
-    const int rr = r0 + (rowok ? r : 0);
-    const int slot = rr / p.G, gg = rr % p.G;
-    const int h = kvh * p.G + gg;
-    const int mvis = p.slot_mvis[slot];
-    const double mx = fmax(red_m[rbase + a][0], red_m[rbase + a][1]);
-    double sum = 0.0;
-    double ev[kR1Blocks];
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-    for (int k = 0; k < kR1Blocks; ++k) {
-      const double v = l == 0 ? acc[a2 * 4][k] : l == 1 ? acc[a2 * 4 + 1][k]
-                     : l == 2 ? acc[a2 * 4 + 2][k] : acc[a2 * 4 + 3][k];
-      const bool ok = rowok && i0 + bh * 32 + g + 8 * k < mvis;
-      ev[k] = ok ? exp(v - mx) : 0.0;
-      sum += ev[k];
+      for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = 0.0;
+    if (rbase < nrows) {
+      const double* qrow = qd + (size_t)rbase * qld + l;
+      const float* krow = cks + (bh * 32 + g) * ckld + l;
+#pragma unroll 2
+      for (int x = 0; x < dh; x += 4) {
+        double kv[kR1Blocks];
+#pragma unroll
+        for (int k = 0; k < kR1Blocks; ++k) kv[k] = krow[8 * k * ckld + x];
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          const double qv = qrow[a * qld + x];
+#pragma unroll
+          for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = fma(qv, kv[k], acc[a][k]);
+        }
+      }
     }
+    // rebuild the reference's dot: (s0 + s2) + (s1 + s3), then * 1/sqrt(dh)
 #pragma unroll
-    for (int off = 4; off <= 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-    if (g == 0) red_s[rbase + a][bh] = sum;
-    if (rowok) {
-      double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad + i0 + bh * 32 + g;
+    for (int a = 0; a < R; ++a)
 #pragma unroll
-      for (int k = 0; k < kR1Blocks; ++k) E[8 * k] = ev[k];
+      for (int k = 0; k < kR1Blocks; ++k) {
+        const double tt = __dadd_rn(acc[a][k], __shfl_xor_sync(0xffffffffu, acc[a][k], 2));
+        acc[a][k] = __dmul_rn(__dadd_rn(tt, __shfl_xor_sync(0xffffffffu, tt, 1)), p.scale);
+      }
+    // per-row tile max over the 64 blocks (2 warps x 8 groups x 4)
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      const int r = rbase + a;
+      const bool rowok = r < nrows;
+      const int mvis = p.slot_mvis[(r0 + (rowok ? r : 0)) / p.G];
+      double mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kR1Blocks; ++k)
+        if (rowok && i0 + bh * 32 + g + 8 * k < mvis) mx = fmax(mx, acc[a][k]);
+#pragma unroll
+      for (int off = 4; off <= 16; off <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      if (lane == 0) red_m[rbase + a][bh] = mx;
     }
+    __syncthreads();
+    // exp: the 4 lanes of a group hold identical logits; lane l takes rows l, l+4, ...
+#pragma unroll
+    for (int a2 = 0; a2 < R / 4; ++a2) {
+      const int a = a2 * 4 + l;
+      const int r = rbase + a;
+      const bool rowok = r < nrows;
+      const int rr = r0 + (rowok ? r : 0);
+      const int slot = rr / p.G, gg = rr % p.G;
+      const int h = kvh * p.G + gg;
+      const int mvis = p.slot_mvis[slot];
+      const double mx = fmax(red_m[rbase + a][0], red_m[rbase + a][1]);
+      double sum = 0.0;
+      double ev[kR1Blocks];
+#pragma unroll
+      for (int k = 0; k < kR1Blocks; ++k) {
+        const double v = l == 0 ? acc[a2 * 4][k] : l == 1 ? acc[a2 * 4 + 1][k]
+                       : l == 2 ? acc[a2 * 4 + 2][k] : acc[a2 * 4 + 3][k];
+        const bool ok = rowok && i0 + bh * 32 + g + 8 * k < mvis;
+        ev[k] = ok ? exp(v - mx) : 0.0;
+        sum += ev[k];
+      }
+#pragma unroll
+      for (int off = 4; off <= 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (g == 0) red_s[rbase + a][bh] = sum;
+      if (rowok) {
+        double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad + i0 + bh * 32 + g;
+#pragma unroll
+        for (int k = 0; k < kR1Blocks; ++k) E[8 * k] = ev[k];
+      }
+    }
+    __syncthreads();
+    if (tid < nrows) {
+      const int rr = r0 + tid;
+      const int slot = rr / p.G, gg = rr % p.G;
+      const int h = kvh * p.G + gg;
+      p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + t] = fmax(red_m[tid][0], red_m[tid][1]);
+      p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + t] = red_s[tid][0] + red_s[tid][1];
+    }
+    store_tile(ckbuf + ((it_t + 1) & 1) * kRouteTile * ckld, kv4);
+    __syncthreads();
   }
-  __syncthreads();
-  if (tid < nrows) {
-    const int rr = r0 + tid;
-    const int slot = rr / p.G, gg = rr % p.G;
-    const int h = kvh * p.G + gg;
-    p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = fmax(red_m[tid][0], red_m[tid][1]);
-    p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + tile] = red_s[tid][0] + red_s[tid][1];
-  }
-  // the last tile CTA of this (row chunk, KV head) folds the tile statistics
-  // into per-tile factors F_t = exp(m_t - M) / DEN (online-softmax merge),
-  // written over TD; the counter returns to 0 for the next launch
-  __shared__ int is_last;
+  // the last CTA of this (row chunk, KV head) folds the tile statistics into
+  // per-tile factors F_t = exp(m_t - M) / DEN (online-softmax merge), written
+  // over TD; the counter returns to 0 for the next launch
   __threadfence();
   __syncthreads();
   if (tid == 0) {
     int* cnt = p.counters + blockIdx.z * p.Hkv + kvh;
-    is_last = atomicAdd(cnt, 1) == p.ntiles - 1;
+    is_last = atomicAdd(cnt, 1) == (int)gridDim.x - 1;
     if (is_last) atomicExch(cnt, 0);
   }
   __syncthreads();
@@ -199,19 +219,36 @@ __global__ void __launch_bounds__(kR1Threads, 2)
     volatile double* TM = p.TM + ((int64_t)slot * p.Hq + h) * p.ntiles;
     volatile double* TD = p.TD + ((int64_t)slot * p.Hq + h) * p.ntiles;
     double mx = -INFINITY;
-    for (int t = lane; t < p.ntiles; t += 32) mx = fmax(mx, TM[t]);
+    for (int tt = lane; tt < p.ntiles; tt += 32) mx = fmax(mx, TM[tt]);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     double den = 0.0;
-    for (int t = lane; t < p.ntiles; t += 32)
-      if (TD[t] > 0.0) den += TD[t] * exp(TM[t] - mx);
+    for (int tt = lane; tt < p.ntiles; tt += 32)
+      if (TD[tt] > 0.0) den += TD[tt] * exp(TM[tt] - mx);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-    for (int t = lane; t < p.ntiles; t += 32) {
-      const double tm = TM[t];
-      TD[t] = (den > 0.0 && tm != -INFINITY) ? exp(tm - mx) / den : 0.0;
+    for (int tt = lane; tt < p.ntiles; tt += 32) {
+      const double tm = TM[tt];
+      TD[tt] = (den > 0.0 && tm != -INFINITY) ? exp(tm - mx) / den : 0.0;
     }
   }
+}
+
+template <int R>
+cudaError_t launch_r1(const RouteParams& p, cudaStream_t s) {
+  constexpr int kRows = 4 * R;
+  const int rows_total = p.nr * p.G;
+  const int rchunks = (rows_total + kRows - 1) / kRows;
+  const size_t smem1 = (size_t)kRows * (kDhRoute + 2) * 8 + 2 * (size_t)kRouteTile * (kDhRoute + 4) * 4;
+  cudaError_t e = cudaFuncSetAttribute(route_logits_kernel<R>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ctas = std::max(1, std::min(p.ntiles, sms / (p.Hkv * rchunks)));
+  route_logits_kernel<R><<<dim3(ctas, p.Hkv, rchunks), kR1Threads, smem1, s>>>(p);
+  return cudaGetLastError();
 }
 
 constexpr int kR2Threads = 128;
@@ -427,21 +464,9 @@ constexpr size_t kR3Smem = (size_t)kMaxAvail * 8 + (size_t)kMaxAvail * 4;
 
 cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   if (p.ntiles == 0) return cudaSuccess;  // nothing compressed is visible yet: all masses 0
-  const int rows_total = p.nr * p.G;
-  const int rchunks = (rows_total + kRouteRows - 1) / kRouteRows;
-  const int maxrows = rows_total < kRouteRows ? rows_total : kRouteRows;
-  const size_t smem1 = (size_t)kRouteRows * (p.dh + 2) * 8 + (size_t)kRouteTile * (p.dh + 4) * 4;
-  cudaError_t e = cudaFuncSetAttribute(route_logits_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  // rows per thread: 4 for the approx (few representatives) shapes, 12 otherwise
+  const cudaError_t e = (p.nr * p.G <= 16) ? launch_r1<4>(p, s) : launch_r1<12>(p, s);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(route_logits_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
-  if (e != cudaSuccess) return e;
-  (void)maxrows;
-  route_logits_kernel<<<dim3(p.ntiles, p.Hkv, rchunks), kR1Threads, smem1, s>>>(p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  // one extra chunk so the selection blocks that start past the last compressed block get written
   route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, 0, s>>>(p);
   return cudaGetLastError();
 }
