@@ -43,7 +43,7 @@ int attend_max_coresident();
 
 // ---- routing (route.cu) -------------------------------------------------------
 constexpr int kRouteTile = 64;      // compressed blocks per R1 CTA
-constexpr int kRouteRows = 16;      // smallest R1 row chunk (4 row groups x 4 rows)
+constexpr int kRouteRows = 16;      // smallest R1 row chunk (2 MMA row tiles)
 constexpr int kMaxAvail = 8192;     // selection blocks per query for the Top-n CTA
 
 struct RouteParams {

@@ -27,37 +27,42 @@
 namespace specsv_b200 {
 namespace {
 
-constexpr int kR1Blocks = 4;    // compressed blocks per thread
-constexpr int kR1Threads = 256; // 4 row groups x 2 block halves x 32 lanes
+constexpr int kR1Threads = 512; // 16 warps: warp w owns compressed blocks [8(w%8), 8(w%8) + 8) of
+                                // the tile and the row tiles of parity w/8
 constexpr int kDhRoute = 128;   // d_head of this build (host-checked)
+constexpr int kR1MaxMt = 8;     // up to 64 query rows (8-row MMA tiles) per CTA
 
-// Lane (g, l) = (lane / 4, lane % 4) accumulates the elements x = l (mod 4)
-// of its R rows x 4 blocks: exactly the reference's lane-l partial sum s_l
-// (kernels.hpp:13-18), so two xor-shuffles rebuild (s0 + s2) + (s1 + s3)
-// bit-for-bit.  q rows are broadcast loads (same x for all groups), key rows
-// are 8 consecutive blocks per load (conflict-free with the 4-float pad).
-// Persistent over tiles: the next tile's keys are prefetched into registers
-// while the current tile is multiplied.
-template <int R>
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// fp64 logits on the FP64 tensor pipe: S[row][block] = q_row . ck_block in
+// fp64 (fp32 x fp32 products are exact in fp64; the 4-term partial sums are
+// accumulated in the MMA's order, within a few ulp of the reference's
+// 4-lane order -- contract P3).  Persistent over 64-block tiles, next tile
+// prefetched into registers.  Per-tile max / exp-sum fused.
+template <int MT>
 __global__ void __launch_bounds__(kR1Threads, 1)
     route_logits_kernel(const __grid_constant__ RouteParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ double red_m[4 * R][2], red_s[4 * R][2];
+  __shared__ double red_m[8 * MT][8], red_s[8 * MT][8];
   __shared__ int is_last;
-  constexpr int kRows = 4 * R;
+  constexpr int kRows = 8 * MT;
   constexpr int dh = kDhRoute;
-  constexpr int qld = dh + 2;  // doubles
-  constexpr int ckld = dh + 4; // floats
+  constexpr int qld = dh + 4;   // doubles (row stride 1056 B: conflict-light A loads)
+  constexpr int ckld = dh + 4;  // floats
   const int kvh = blockIdx.y;
   const int rows_total = p.nr * p.G;
   const int r0 = blockIdx.z * kRows;
   const int nrows = min(kRows, rows_total - r0);
-  double* qd = reinterpret_cast<double*>(smem);                                    // [kRows][qld]
-  float* ckbuf = reinterpret_cast<float*>(smem + (size_t)kRows * qld * 8);         // 2 x [64][ckld]
+  double* qd = reinterpret_cast<double*>(smem);                             // [kRows][qld]
+  float* ckbuf = reinterpret_cast<float*>(smem + (size_t)kRows * qld * 8);  // 2 x [64][ckld]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, l = lane & 3;
-  const int rg = warp >> 1, bh = warp & 1;  // row group, block half
-  constexpr int kKPer = kRouteTile * (dh / 4) / kR1Threads;  // 8 float4 per thread
+  const int lr = lane >> 2, lc = lane & 3;  // fragment row / column within the 8x8 tile
+  const int nt = warp & 7, mh = warp >> 3;  // block tile, row-tile parity
+  constexpr int kKPer = kRouteTile * (dh / 4) / kR1Threads;  // 4 float4 per thread
 
   auto load_tile = [&](int t, float4 (&kv4)[kKPer]) {
 #pragma unroll
@@ -78,8 +83,7 @@ __global__ void __launch_bounds__(kR1Threads, 1)
       *reinterpret_cast<float4*>(dst + b * ckld + x4 * 4) = kv4[it];
     }
   };
-
-  {  // q rows, fp32 -> fp64 (exact), all loads in flight
+  {  // q rows, fp32 -> fp64 (exact); rows past nrows are zero
     constexpr int kQPer = (kRows * (dh / 4) + kR1Threads - 1) / kR1Threads;
     float4 qv4[kQPer];
 #pragma unroll
@@ -109,92 +113,81 @@ __global__ void __launch_bounds__(kR1Threads, 1)
   load_tile(t, kv4);
   store_tile(ckbuf, kv4);
   __syncthreads();
-  const int rbase = rg * R;
+  const int nmt = (nrows + 7) >> 3;
   for (int it_t = 0; t < p.ntiles; t += gridDim.x, ++it_t) {
     const float* cks = ckbuf + (it_t & 1) * kRouteTile * ckld;
     load_tile(t + gridDim.x, kv4);  // next tile, lands while this one is multiplied
     const int i0 = t * kRouteTile;
-    double acc[R][kR1Blocks];
+    constexpr int MH = MT / 2;  // row tiles per warp: mt = 2 j + mh
+    double acc[MH][2];
 #pragma unroll
-    for (int a = 0; a < R; ++a)
+    for (int j = 0; j < MH; ++j) acc[j][0] = acc[j][1] = 0.0;
+    // B fragment: block (8 nt + lr), element 4 s + lc; A: row (8 mt + lr), element 4 s + lc
+    const float* kb = cks + (8 * nt + lr) * ckld + lc;
+    const double* qa = qd + (size_t)(8 * mh + lr) * qld + lc;
+#pragma unroll 4
+    for (int s = 0; s < dh / 4; ++s) {
+      const double b = kb[4 * s];
 #pragma unroll
-      for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = 0.0;
-    if (rbase < nrows) {
-      const double* qrow = qd + (size_t)rbase * qld + l;
-      const float* krow = cks + (bh * 32 + g) * ckld + l;
-#pragma unroll 2
-      for (int x = 0; x < dh; x += 4) {
-        double kv[kR1Blocks];
-#pragma unroll
-        for (int k = 0; k < kR1Blocks; ++k) kv[k] = krow[8 * k * ckld + x];
-#pragma unroll
-        for (int a = 0; a < R; ++a) {
-          const double qv = qrow[a * qld + x];
-#pragma unroll
-          for (int k = 0; k < kR1Blocks; ++k) acc[a][k] = fma(qv, kv[k], acc[a][k]);
-        }
-      }
+      for (int j = 0; j < MH; ++j)
+        if (2 * j + mh < nmt) dmma_8x8x4(acc[j], qa[(size_t)j * 16 * qld + 4 * s], b);
     }
-    // rebuild the reference's dot: (s0 + s2) + (s1 + s3), then * 1/sqrt(dh)
+    // C fragment: row 8 mt + lr, blocks 8 nt + 2 lc + {0, 1}
+    const int blk = i0 + 8 * nt + 2 * lc;
 #pragma unroll
-    for (int a = 0; a < R; ++a)
-#pragma unroll
-      for (int k = 0; k < kR1Blocks; ++k) {
-        const double tt = __dadd_rn(acc[a][k], __shfl_xor_sync(0xffffffffu, acc[a][k], 2));
-        acc[a][k] = __dmul_rn(__dadd_rn(tt, __shfl_xor_sync(0xffffffffu, tt, 1)), p.scale);
-      }
-    // per-row tile max over the 64 blocks (2 warps x 8 groups x 4)
-#pragma unroll
-    for (int a = 0; a < R; ++a) {
-      const int r = rbase + a;
+    for (int j = 0; j < MH; ++j) {
+      const int r = 8 * (2 * j + mh) + lr;
       const bool rowok = r < nrows;
       const int mvis = p.slot_mvis[(r0 + (rowok ? r : 0)) / p.G];
       double mx = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < kR1Blocks; ++k)
-        if (rowok && i0 + bh * 32 + g + 8 * k < mvis) mx = fmax(mx, acc[a][k]);
-#pragma unroll
-      for (int off = 4; off <= 16; off <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      if (lane == 0) red_m[rbase + a][bh] = mx;
+      for (int c = 0; c < 2; ++c) {
+        acc[j][c] = __dmul_rn(acc[j][c], p.scale);
+        if (rowok && blk + c < mvis) mx = fmax(mx, acc[j][c]);
+      }
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      if (lc == 0 && 2 * j + mh < nmt) red_m[r][nt] = mx;
     }
     __syncthreads();
-    // exp: the 4 lanes of a group hold identical logits; lane l takes rows l, l+4, ...
 #pragma unroll
-    for (int a2 = 0; a2 < R / 4; ++a2) {
-      const int a = a2 * 4 + l;
-      const int r = rbase + a;
+    for (int j = 0; j < MH; ++j) {
+      if (2 * j + mh >= nmt) break;
+      const int r = 8 * (2 * j + mh) + lr;
       const bool rowok = r < nrows;
       const int rr = r0 + (rowok ? r : 0);
       const int slot = rr / p.G, gg = rr % p.G;
       const int h = kvh * p.G + gg;
       const int mvis = p.slot_mvis[slot];
-      const double mx = fmax(red_m[rbase + a][0], red_m[rbase + a][1]);
-      double sum = 0.0;
-      double ev[kR1Blocks];
+      double mx = red_m[r][0];
 #pragma unroll
-      for (int k = 0; k < kR1Blocks; ++k) {
-        const double v = l == 0 ? acc[a2 * 4][k] : l == 1 ? acc[a2 * 4 + 1][k]
-                       : l == 2 ? acc[a2 * 4 + 2][k] : acc[a2 * 4 + 3][k];
-        const bool ok = rowok && i0 + bh * 32 + g + 8 * k < mvis;
-        ev[k] = ok ? exp(v - mx) : 0.0;
-        sum += ev[k];
+      for (int w = 1; w < 8; ++w) mx = fmax(mx, red_m[r][w]);
+      double ev[2], sum = 0.0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const bool ok = rowok && blk + c < mvis;
+        ev[c] = ok ? exp(acc[j][c] - mx) : 0.0;
+        sum += ev[c];
       }
-#pragma unroll
-      for (int off = 4; off <= 16; off <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-      if (g == 0) red_s[rbase + a][bh] = sum;
-      if (rowok) {
-        double* E = p.E + ((int64_t)slot * p.Hq + h) * p.m_pad + i0 + bh * 32 + g;
-#pragma unroll
-        for (int k = 0; k < kR1Blocks; ++k) E[8 * k] = ev[k];
-      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (lc == 0) red_s[r][nt] = sum;
+      if (rowok)
+        *reinterpret_cast<double2*>(p.E + ((int64_t)slot * p.Hq + h) * p.m_pad + blk) =
+            make_double2(ev[0], ev[1]);
     }
     __syncthreads();
     if (tid < nrows) {
       const int rr = r0 + tid;
       const int slot = rr / p.G, gg = rr % p.G;
       const int h = kvh * p.G + gg;
-      p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + t] = fmax(red_m[tid][0], red_m[tid][1]);
-      p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + t] = red_s[tid][0] + red_s[tid][1];
+      double mx = red_m[tid][0], sm = 0.0;
+#pragma unroll
+      for (int w = 1; w < 8; ++w) mx = fmax(mx, red_m[tid][w]);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sm += red_s[tid][w];
+      p.TM[((int64_t)slot * p.Hq + h) * p.ntiles + t] = mx;
+      p.TD[((int64_t)slot * p.Hq + h) * p.ntiles + t] = sm;
     }
     store_tile(ckbuf + ((it_t + 1) & 1) * kRouteTile * ckld, kv4);
     __syncthreads();
@@ -212,42 +205,57 @@ __global__ void __launch_bounds__(kR1Threads, 1)
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int r = warp; r < nrows; r += kR1Threads / 32) {
-    const int rr = r0 + r;
-    const int slot = rr / p.G, gg = rr % p.G;
-    const int h = kvh * p.G + gg;
-    volatile double* TM = p.TM + ((int64_t)slot * p.Hq + h) * p.ntiles;
-    volatile double* TD = p.TD + ((int64_t)slot * p.Hq + h) * p.ntiles;
-    double mx = -INFINITY;
-    for (int tt = lane; tt < p.ntiles; tt += 32) mx = fmax(mx, TM[tt]);
+  // row groups of the (rows x tiles) statistics go through shared memory in
+  // one coalesced pass each (the q / key buffers are free now), then per-row
+  // reductions run there
+  constexpr size_t kSmemBytes = (size_t)kRows * qld * 8 + 2 * (size_t)kRouteTile * ckld * 4;
+  const int rg = min(nrows, max(1, (int)(kSmemBytes / (16 * (size_t)p.ntiles))));
+  double* sTM = reinterpret_cast<double*>(smem);
+  double* sTD = sTM + rg * p.ntiles;
+  for (int g0 = 0; g0 < nrows; g0 += rg) {
+    const int gn = min(rg, nrows - g0);
+    __syncthreads();
+    for (int e = tid; e < gn * p.ntiles; e += kR1Threads) {
+      const int rr = r0 + g0 + e / p.ntiles, tt = e % p.ntiles;
+      const int64_t base = ((int64_t)(rr / p.G) * p.Hq + kvh * p.G + rr % p.G) * p.ntiles + tt;
+      sTM[e] = __ldcg(p.TM + base);
+      sTD[e] = __ldcg(p.TD + base);
+    }
+    __syncthreads();
+    for (int r = warp; r < gn; r += kR1Threads / 32) {
+      const double* tm = sTM + r * p.ntiles;
+      const double* td = sTD + r * p.ntiles;
+      double mx = -INFINITY;
+      for (int tt = lane; tt < p.ntiles; tt += 32) mx = fmax(mx, tm[tt]);
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    double den = 0.0;
-    for (int tt = lane; tt < p.ntiles; tt += 32)
-      if (TD[tt] > 0.0) den += TD[tt] * exp(TM[tt] - mx);
+      for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      double den = 0.0;
+      for (int tt = lane; tt < p.ntiles; tt += 32)
+        if (td[tt] > 0.0) den += td[tt] * exp(tm[tt] - mx);
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-    for (int tt = lane; tt < p.ntiles; tt += 32) {
-      const double tm = TM[tt];
-      TD[tt] = (den > 0.0 && tm != -INFINITY) ? exp(tm - mx) / den : 0.0;
+      for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+      const int rr = r0 + g0 + r;
+      double* F = p.TD + ((int64_t)(rr / p.G) * p.Hq + kvh * p.G + rr % p.G) * p.ntiles;
+      for (int tt = lane; tt < p.ntiles; tt += 32)
+        F[tt] = (den > 0.0 && tm[tt] != -INFINITY) ? exp(tm[tt] - mx) / den : 0.0;
     }
   }
 }
 
-template <int R>
+template <int MT>
 cudaError_t launch_r1(const RouteParams& p, cudaStream_t s) {
-  constexpr int kRows = 4 * R;
+  constexpr int kRows = 8 * MT;
   const int rows_total = p.nr * p.G;
   const int rchunks = (rows_total + kRows - 1) / kRows;
-  const size_t smem1 = (size_t)kRows * (kDhRoute + 2) * 8 + 2 * (size_t)kRouteTile * (kDhRoute + 4) * 4;
-  cudaError_t e = cudaFuncSetAttribute(route_logits_kernel<R>,
+  const size_t smem1 = (size_t)kRows * (kDhRoute + 4) * 8 + 2 * (size_t)kRouteTile * (kDhRoute + 4) * 4;
+  cudaError_t e = cudaFuncSetAttribute(route_logits_kernel<MT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ctas = std::max(1, std::min(p.ntiles, sms / (p.Hkv * rchunks)));
-  route_logits_kernel<R><<<dim3(ctas, p.Hkv, rchunks), kR1Threads, smem1, s>>>(p);
+  route_logits_kernel<MT><<<dim3(ctas, p.Hkv, rchunks), kR1Threads, smem1, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -465,7 +473,8 @@ constexpr size_t kR3Smem = (size_t)kMaxAvail * 8 + (size_t)kMaxAvail * 4;
 cudaError_t launch_r1_r2(const RouteParams& p, cudaStream_t s) {
   if (p.ntiles == 0) return cudaSuccess;  // nothing compressed is visible yet: all masses 0
   // rows per thread: 4 for the approx (few representatives) shapes, 12 otherwise
-  const cudaError_t e = (p.nr * p.G <= 16) ? launch_r1<4>(p, s) : launch_r1<12>(p, s);
+  const int rows = p.nr * p.G;
+  const cudaError_t e = rows <= 16 ? launch_r1<2>(p, s) : rows <= 32 ? launch_r1<4>(p, s) : launch_r1<8>(p, s);
   if (e != cudaSuccess) return e;
   route_mass_kernel<<<dim3((p.m_pad + kR2Blocks - 1) / kR2Blocks + 1, p.nr), kR2Threads, 0, s>>>(p);
   return cudaGetLastError();
