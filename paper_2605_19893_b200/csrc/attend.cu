@@ -135,19 +135,19 @@ __device__ __forceinline__ int visible_blocks(int bound, const AttendParams& p) 
 // per-(chunk, head) barrier among the S co-resident split CTAs: a counter
 // that returns to 0 plus a generation word that only grows (workspace words
 // start at 0 and are owned by this library)
-__device__ void group_barrier(int* cnt, volatile int* gen, int S, int tid) {
+__device__ void group_barrier(int* cnt, int* gen, int S, int tid) {
   __syncthreads();
   if (tid == 0) {
-    const int g = *gen;
-    __threadfence();
-    if (atomicAdd(cnt, 1) == S - 1) {
+    // the generation cannot advance before this CTA arrives, so reading it
+    // first is race-free; acq_rel arrivals publish the CTA's partials (the
+    // bar.sync above orders them before thread 0) and acquire the others'
+    const int g = sm100::ld_acquire_gpu(gen);
+    if (sm100::atom_add_acq_rel_gpu(cnt, 1) == S - 1) {
       atomicExch(cnt, 0);
-      __threadfence();
-      atomicAdd(const_cast<int*>(gen), 1);
+      sm100::atom_add_acq_rel_gpu(gen, 1);
     } else {
-      while (*gen == g) __nanosleep(64);
+      while (sm100::ld_acquire_gpu(gen) == g) __nanosleep(32);
     }
-    __threadfence();
   }
   __syncthreads();
 }

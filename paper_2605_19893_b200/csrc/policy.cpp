@@ -40,6 +40,8 @@ void check_build_limits(const specsv_nsa_config& c) {
   if (c.n > 64) unsup("n must be <= 64");
   if (c.n_q_heads > 128) unsup("n_q_heads must be <= 128");
   if ((c.l - 1) / c.d > 7) unsup("l must be <= 8 * d (routing halo)");
+  if ((63 + 7 * c.d + c.l - 1) / c.l_sel + 1 > 4)
+    unsup("7 d + l must be <= 194 (selection blocks per 8 compressed blocks)");
 }
 
 int64_t routing_visible_len(const specsv_nsa_config& c, int64_t pos) {
