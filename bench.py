@@ -241,8 +241,9 @@ def run_ours(a):
     mode = V.MODE_EXACT if a.mode == "exact" else V.MODE_APPROX
     roles, source = V.resolve_layer_roles(reuse_set(a.schedule, L), L)
     H, dh, Hq = cfg.n_kv_heads, cfg.d_head, cfg.n_q_heads
+    from paper_2605_19893_b200 import sharding
+    my_requests = sharding.request_shard(world * R, world, rank)  # global ids of this rank
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + 1000 * rank)
 
     def urand(*shape, dtype=torch.float32):
         return (torch.rand(*shape, generator=gen, device=dev) * 2 - 1).to(dtype)
@@ -252,6 +253,7 @@ def run_ours(a):
     tmask = chain_tree_mask(g)
     caches, batches, sets, outs, inbufs = [], [], [], [], []
     for r in range(R):
+        gen.manual_seed(sharding.request_seed(my_requests[r]))
         qa = urand(L, nq, Hq, dh)
         ga = torch.rand(L, nq, Hq, 3, generator=gen, device=dev) * 0.6 + 0.2
         tka = urand(L, max(g, 1), H, dh, dtype=torch.bfloat16)
@@ -311,11 +313,7 @@ def run_ours(a):
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return sharding.max_over_ranks(x, dev)
 
     for _ in range(a.warmup):
         run_step()
