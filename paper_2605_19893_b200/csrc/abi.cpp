@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <climits>
+
 #include "attend.h"
 #include "policy.h"
 #include "specsv_b200/nsa_verify.h"
@@ -112,9 +114,13 @@ struct Layout {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// queries per column chunk: 64 columns / G, and few enough that the chunk's
+// union (n selected blocks per query + the window blocks) fits kMaxUnion
 int qc_size_for(const specsv_nsa_config& c) {
   const int G = static_cast<int>(c.n_q_heads / c.n_kv_heads);
-  return std::min(64 / G, kMaxChunkQ);
+  const int64_t win_blocks = c.w / c.l_sel + 2;
+  const int64_t by_union = (kMaxUnion - win_blocks) / std::max<int64_t>(c.n, 1);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min(64 / G, kMaxChunkQ), by_union));
 }
 
 Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
@@ -254,6 +260,7 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   encode_rows_map(&p.tm_cv, kv.cv, kv.blocks, H, dh);
   encode_rows_map(&p.tm_tk, gamma > 0 ? a.tree_k : kv.k, std::max(gamma, 1), H, dh);
   encode_rows_map(&p.tm_tv, gamma > 0 ? a.tree_v : kv.v, std::max(gamma, 1), H, dh);
+  p.k_raw = static_cast<const uint16_t*>(kv.k);
   p.q = a.q;
   p.gates = a.gates;
   p.out = a.out;
@@ -261,7 +268,7 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   p.idx_count = a.idx_count;
   p.ws = static_cast<float*>(ws);
   p.trace = g_trace;
-  p.debug_flags = g_trace != nullptr && std::getenv("SPECSV_DEBUG_NOVOTE") != nullptr ? 1 : 0;
+  p.debug_flags = std::getenv("SPECSV_ATTEND_FORCE_ROBUST") != nullptr ? 1 : 0;
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
   p.ws_o_offset = (int64_t)nchunks * H * S * (3 * 64 * 2);
@@ -287,6 +294,22 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
     p.pos[q] = (int32_t)a.pos[q];
     p.src_row[q] = src[q];
     p.tree_mask[q] = (q < gamma) ? a.tree_mask[(int64_t)q * a.mask_words] : 0ull;
+    const int64_t vis = routing_visible_len(c, a.pos[q]);
+    p.qbound[q] = (int32_t)std::min<int64_t>(vis, kv.rows);
+    p.qwlo[q] = (int32_t)std::max<int64_t>(0, a.pos[q] - c.w + 1);
+    p.qwhi[q] = (int32_t)std::min<int64_t>(a.pos[q], kv.rows - 1);
+    p.qmvis[q] = (int32_t)visible_blocks(c, kv.blocks, vis);
+  }
+  for (int ch = 0; ch < nchunks; ++ch) {
+    int32_t mv = 0, wlo = INT32_MAX, whi = -1;
+    for (int32_t q = ch * qc; q < std::min<int32_t>(a.n_queries, (ch + 1) * qc); ++q) {
+      mv = std::max(mv, p.qmvis[q]);
+      wlo = std::min(wlo, p.qwlo[q]);
+      whi = std::max(whi, p.qwhi[q]);
+    }
+    p.ch_ncmp[ch] = (mv + 127) / 128;
+    p.ch_wlo[ch] = wlo;
+    p.ch_whi[ch] = whi;
   }
   cuda_check(launch_attend(p, nchunks, stream), "attend launch");
 }

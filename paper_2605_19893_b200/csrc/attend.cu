@@ -54,6 +54,8 @@ constexpr int kTmemS = 0;          // two S buffers at cols 0, 64
 constexpr int kTmemO = 128;        // O_cmp 128, O_slc 192, O_win 256
 constexpr int kTmemL = 320;        // per-lane partial row sums of P: 320, 384, 448
 constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr int kBarPassEnd = 7;     // named barriers (1: softmax warps, 3-6: column chunks)
+constexpr int kBarRedo = 8;
 
 // shared memory map (bytes from the 1024-aligned base)
 constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P of branch A)
@@ -70,13 +72,16 @@ struct Misc {
   uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], pv_done[2];
   uint64_t p_full, q_ready, union_ready;
   uint32_t tmem_base;
-  int32_t n_union, n_cmp_tiles, n_tok_tiles, n_tree_tiles;
+  int32_t n_union, n_tok_tiles;
+  int32_t flag;          // end-of-pass check failed: redo the tiles in the robust pass
+  alignas(16) float mref[kCols];  // fast-pass reference logit per column (log2 units)
   float m2[3][kCols];    // running max (log2 units) per branch and column
   float thr[3][kCols];   // m2 + threshold
   float alpha[kCols];
   float tmax[4][kCols];
   int32_t vote[4][kCols / 16];  // [quadrant][chunk]
   float lred[3][4][kCols];      // row sums per branch, quadrant, column
+  uint32_t actw[kSoftWarps][2]; // fast pass: active (branch, column) bits per warp
   int32_t qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
   int32_t qcount[kMaxChunkQ];
   int32_t qsel[kMaxChunkQ * 64];
@@ -126,12 +131,6 @@ __device__ __forceinline__ float reduce16(float (&v)[16], int lane) {
   return kMax ? fmaxf(v[0], other) : v[0] + other;
 }
 
-__device__ __forceinline__ int visible_blocks(int bound, const AttendParams& p) {
-  if (bound < p.l) return 0;
-  const int by_len = (bound - p.l) / p.d + 1;
-  return by_len < p.blocks ? by_len : p.blocks;
-}
-
 // per-(chunk, head) barrier among the S co-resident split CTAs: a counter
 // that returns to 0 plus a generation word that only grows (workspace words
 // start at 0 and are owned by this library)
@@ -153,63 +152,60 @@ __device__ void group_barrier(int* cnt, int* gen, int S, int tid) {
 }
 
 // ---------------------------------------------------------------------------
-// prologue: per-chunk query table, union of selected + window blocks with
-// per-block query ownership (exact: own set; approx: representative's set;
-// both clamped at the query's routing bound, layer_roles.cpp:37-50).
-// Index sets are staged in shared memory first (one global round trip).
-__device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int tid, int nthr) {
+// union of selected + window blocks with per-block query ownership (exact:
+// own set; approx: representative's set; both clamped at the query's routing
+// bound, layer_roles.cpp:37-50).  Built by the 32 lanes of the TMA warp while
+// the compressed tiles (which do not need it) are already in flight; the
+// index rows are staged with fire-and-forget cp.async (one round trip).
+__device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc, int lane, int wlo,
+                                 int whi, unsigned long long* tr) {
   const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
   const int words = (nsel + 31) >> 5;
   const int n = p.n_sel;
-  for (int e = tid; e < nqc * n; e += nthr) {
-    const int i = e / n, k = e % n;
-    m.qsel[e] = p.idx[p.src_row[q0 + i] * n + k];
-    if (k == 0) {
-      m.qcount[i] = p.idx_count[p.src_row[q0 + i]];
-      const int pos = p.pos[q0 + i];
-      const int bound = max(0, pos + 1 - p.lag);
-      m.qbound[i] = min(bound, p.rows);
-      m.qwlo[i] = max(0, pos - p.w + 1);
-      m.qwhi[i] = min(pos, p.rows - 1);
-      m.qmvis[i] = visible_blocks(bound, p);
-    }
+  for (int e = lane; e < nqc * n; e += 32) {
+    const int i = e / n, k = e - i * n;
+    const int r = p.src_row[q0 + i];
+    cp_async4(&m.qsel[e], p.idx + r * n + k);
+    if (k == 0) cp_async4(&m.qcount[i], p.idx_count + r);
   }
-  for (int i = tid; i < words; i += nthr) m.bitmap[i] = 0u;
-  named_bar_sync(2, nthr);
-  int wlo = 0x7fffffff, whi = -1;
-  for (int i = 0; i < nqc; ++i) {
-    wlo = min(wlo, m.qwlo[i]);
-    whi = max(whi, m.qwhi[i]);
+  for (int w = lane; w < words; w += 32) m.bitmap[w] = 0u;
+  cp_async_wait_all();
+  __syncwarp();
+  if (tr && lane == 0) tr[56] = globaltimer();
+  for (int b = wlo / p.l_sel + lane; b <= whi / p.l_sel; b += 32) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
+  for (int e = lane; e < nqc * n; e += 32) {
+    const int i = e / n, k = e - i * n;
+    int b = m.qsel[e];
+    if (k >= m.qcount[i] || b < 0 || (int64_t)b * p.l_sel >= p.qbound[q0 + i] || b >= nsel) b = -1;
+    m.qsel[e] = b;
+    if (b >= 0) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
   }
-  for (int b = wlo / p.l_sel + tid; b <= whi / p.l_sel; b += nthr)
-    atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
-  for (int e = tid; e < nqc * n; e += nthr) {
-    const int i = e / n, k = e % n;
-    const int b = m.qsel[e];
-    if (k >= m.qcount[i] || b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
-    atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
-  }
-  named_bar_sync(2, nthr);
-  if (tid < 32) {  // exclusive prefix of popcounts
-    const int per = (words + 31) / 32;
-    const int w0 = tid * per;
+  __syncwarp();
+  {  // exclusive prefix of popcounts, contiguous word ranges per lane
+    const int per = (words + 31) >> 5;
+    const int w0 = lane * per;
     int local = 0;
     for (int w = w0; w < min(words, w0 + per); ++w) local += __popc(m.bitmap[w]);
     int incl = local;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (tid >= off) incl += y;
+      if (lane >= off) incl += y;
     }
     int run = incl - local;
     for (int w = w0; w < min(words, w0 + per); ++w) {
       m.word_prefix[w] = run;
       run += __popc(m.bitmap[w]);
     }
-    if (tid == 31) m.n_union = min(incl, kMaxUnion);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 0) {
+      m.n_union = min(total, kMaxUnion);
+      m.n_tok_tiles = (min(total, kMaxUnion) + 1) / 2;
+    }
   }
-  named_bar_sync(2, nthr);
-  for (int w = tid; w < words; w += nthr) {
+  __syncwarp();
+  if (tr && lane == 0) tr[57] = globaltimer();
+  for (int w = lane; w < words; w += 32) {
     uint32_t bits = m.bitmap[w];
     int r = m.word_prefix[w];
     while (bits) {
@@ -222,16 +218,16 @@ __device__ void build_union(const AttendParams& p, Misc& m, int q0, int nqc, int
       ++r;
     }
   }
-  named_bar_sync(2, nthr);
-  for (int e = tid; e < nqc * n; e += nthr) {
-    const int i = e / n, k = e % n;
+  __syncwarp();
+  if (tr && lane == 0) tr[58] = globaltimer();
+  for (int e = lane; e < nqc * n; e += 32) {
     const int b = m.qsel[e];
-    if (k >= m.qcount[i] || b < 0 || (int64_t)b * p.l_sel >= m.qbound[i] || b >= nsel) continue;
+    if (b < 0) continue;
     const int w = b >> 5;
     const int r = m.word_prefix[w] + __popc(m.bitmap[w] & ((1u << (b & 31)) - 1u));
-    if (r < kMaxUnion) atomicOr(&m.union_own[r], 1u << i);
+    if (r < kMaxUnion) atomicOr(&m.union_own[r], 1u << (e / n));
   }
-  named_bar_sync(2, nthr);
+  __syncwarp();
 }
 
 struct TileInfo {
@@ -241,16 +237,17 @@ struct TileInfo {
   bool act_b;  // branch B (win) has work
 };
 
-__device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int wlo, int whi, int l_sel) {
+__device__ __forceinline__ TileInfo tile_info(const Misc& m, int n_cmp, int t, int wlo, int whi,
+                                              int l_sel) {
   TileInfo ti;
-  if (t < m.n_cmp_tiles) {
+  if (t < n_cmp) {
     ti.kind = kTileCmp;
     ti.base = t * kTile;
     ti.act_a = true;
     ti.act_b = false;
-  } else if (t < m.n_cmp_tiles + m.n_tok_tiles) {
+  } else if (t < n_cmp + m.n_tok_tiles) {
     ti.kind = kTileTok;
-    ti.base = 2 * (t - m.n_cmp_tiles);
+    ti.base = 2 * (t - n_cmp);
     const int b0 = m.union_blk[ti.base];
     bool win = (b0 * l_sel <= whi) && (b0 * l_sel + l_sel - 1 >= wlo);
     uint32_t own = m.union_own[ti.base];
@@ -269,6 +266,47 @@ __device__ __forceinline__ TileInfo tile_info(const Misc& m, int t, int wlo, int
   }
   return ti;
 }
+
+// P^T of one branch for this warp's 16 columns x its 32 key rows: masked
+// probabilities -> SW128 MN-major hi + lo bf16 planes, and the per-lane
+// partial row sums in TMEM (no cross-lane work per tile)
+__device__ __forceinline__ void write_p(uint8_t* pdst, int row, int ck, uint32_t cm, const float (&pe)[16],
+                                        uint32_t tl) {
+  float pv[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) pv[e] = ((cm >> e) & 1u) ? pe[e] : 0.f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+      const float2 hf = __bfloat1622float2(h2);
+      hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+      lo[e] = pack_bf16(a - hf.x, b - hf.y);
+    }
+    const uint32_t off = sw128_off(row, 2 * ck + h);
+    *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+  uint32_t r[16];
+  tmem_ld16(tl, r);
+  tmem_wait_ld();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + pv[e]);
+  tmem_st16(tl, r);
+}
+
+// Softmax reference.  Pass 0 (fast) uses ONE fixed reference logit per column,
+// mref = the column's logit against the newest committed key (a key inside
+// every query's window), for all tiles and branches: P = 2^(s - mref) needs no
+// running max, no cross-warp votes and no O rescales.  fp32/bf16 share the
+// same exponent range, so P keeps its relative precision while
+// s - mref <= kFastHi; the pass is checked at its end (no active logit above
+// mref + kFastHi, every active branch sum >= 2^-kFastHi) and otherwise redone
+// in pass 1 (robust) with the classic lazily-raised running max.
+constexpr float kFastHi = 48.0f;
 
 __global__ void __launch_bounds__(kThreads, 1)
     nsa_attend_kernel(const __grid_constant__ AttendParams p) {
@@ -293,6 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nch = nqk >> 4;  // 16-column chunks holding valid columns
   const int gshift = __ffs(p.G) - 1;
   const bool trace = p.trace != nullptr;
+  const int n_cmp = p.ch_ncmp[chunk];  // compressed tiles do not depend on the union
+  const int cwlo = p.ch_wlo[chunk], cwhi = p.ch_whi[chunk];
+  const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
 
   // ---- barriers + TMEM -----------------------------------------------------
   if (tid == 0) {
@@ -301,39 +342,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&m.v_full[i], 1);
       mbar_init(&m.kv_empty[i], 1);
       mbar_init(&m.s_full[i], 1);
-      mbar_init(&m.s_free[i], kSoftWarps);
+      mbar_init(&m.s_free[i], 4 * nch);  // the warps of the active column chunks
       mbar_init(&m.pv_done[i], 1);
     }
-    mbar_init(&m.p_full, kSoftWarps);
+    mbar_init(&m.p_full, 4 * nch);
     mbar_init(&m.q_ready, kSoftWarps);
-    mbar_init(&m.union_ready, kSoftWarps);
+    mbar_init(&m.union_ready, 32);
+    m.flag = (p.debug_flags & 1) ? 1 : 0;  // bit 0: force the robust redo (tests)
     fence_mbar_init();
   }
   if (warp == kWarpTma) tmem_alloc<kTmemCols>(&m.tmem_base);
-  int mmax = 0;  // compressed tiles do not depend on the union
-  for (int i = 0; i < nqc; ++i) mmax = max(mmax, visible_blocks(max(0, p.pos[q0 + i] + 1 - p.lag), p));
-  const int n_cmp = (mmax + kTile - 1) / kTile;
-  int cwlo = 0x7fffffff, cwhi = -1;
-  for (int i = 0; i < nqc; ++i) {
-    const int pos = p.pos[q0 + i];
-    cwlo = min(cwlo, max(0, pos - p.w + 1));
-    cwhi = max(cwhi, min(pos, p.rows - 1));
-  }
-  const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = m.tmem_base;
   if (trace && tid == 0) p.trace[cta_id * 64 + 0] = globaltimer();
 
+  // tile count once the union is known (identical in every role)
+  auto tile_count = [&]() {
+    const int n_total = n_cmp + m.n_tok_tiles + (has_tree ? 1 : 0);
+    return split < n_total ? (n_total - split + S - 1) / S : 0;
+  };
+
   if (warp < kSoftWarps) {
     const int qd = warp & 3, ck = warp >> 2;  // TMEM lane quadrant, column chunk
     const int c0 = 16 * ck;
+    const bool active = ck < nch;             // this warp's columns hold queries
     const uint32_t lanebase = tmem + ((uint32_t)(qd * 32) << 16);
-    // =================== setup: one global round trip for q and the index sets ===================
+    // =================== setup: q (hi/lo bf16) and the reference logits ===================
     {
-      const int n = p.n_sel;
+      const uint4* kref = reinterpret_cast<const uint4*>(
+          p.k_raw + ((int64_t)(p.rows - 1) * p.Hkv + kvh) * kDh);
       float4 xa[2], xb[2];
+      const uint4 kr = kref[tid & 15];
 #pragma unroll
       for (int it = 0; it < 2; ++it) {  // 64 rows x 16 units of 8 elements, 2 units per thread
         const int unit = tid + it * kSoftThreads;
@@ -349,11 +390,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           xb[it] = xa[it];
         }
       }
-      for (int e = tid; e < nqc * n; e += kSoftThreads) {
-        const int i = e / n, k = e % n;
-        m.qsel[e] = p.idx[p.src_row[q0 + i] * n + k];
-        if (k == 0) m.qcount[i] = p.idx_count[p.src_row[q0 + i]];
+      if (tid < nqc) {
+        m.qbound[tid] = p.qbound[q0 + tid];
+        m.qwlo[tid] = p.qwlo[q0 + tid];
+        m.qwhi[tid] = p.qwhi[q0 + tid];
+        m.qmvis[tid] = p.qmvis[q0 + tid];
       }
+      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kr);
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
         const int unit = tid + it * kSoftThreads;
@@ -361,250 +404,293 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sc = p.scale_log2;
         const float x[8] = {xa[it].x * sc, xa[it].y * sc, xa[it].z * sc, xa[it].w * sc,
                             xb[it].x * sc, xb[it].y * sc, xb[it].z * sc, xb[it].w * sc};
+        float dot = 0.f;
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
+          const float2 kf = __bfloat1622float2(k2[e]);
+          dot = fmaf(x[2 * e], kf.x, fmaf(x[2 * e + 1], kf.y, dot));
           const __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
           const float2 hf = __bfloat1622float2(h2);
           hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
           lo[e] = pack_bf16(x[2 * e] - hf.x, x[2 * e + 1] - hf.y);
         }
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+        if (u16 == 0) m.mref[c] = dot;
         const uint32_t off = (u16 >> 3) * 8192 + sw128_off(c, u16 & 7);
         *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
-      uint32_t z[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) z[i] = 0u;
-#pragma unroll
-      for (int br = 0; br < 3; ++br) {
-        tmem_st16(lanebase + kTmemO + 64 * br + c0, z);
-        tmem_st16(lanebase + kTmemL + 64 * br + c0, z);
-      }
-      tmem_wait_st();
+      if (trace && tid == 0) p.trace[cta_id * 64 + 61] = globaltimer();
       fence_proxy_async_smem();
-      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&m.q_ready);
       if (trace && tid == 0) p.trace[cta_id * 64 + 5] = globaltimer();
     }
-    if (tid == 0) m.n_cmp_tiles = n_cmp;
-    for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
-      (&m.m2[0][0])[i] = -INFINITY;
-      (&m.thr[0][0])[i] = -INFINITY;
-    }
-    build_union(p, m, q0, nqc, tid, kSoftThreads);
-    if (tid == 0) {
-      m.n_tok_tiles = (m.n_union + 1) / 2;
-      m.n_tree_tiles = has_tree ? 1 : 0;
-    }
-    named_bar_sync(1, kSoftThreads);
-    if (lane == 0) mbar_arrive(&m.union_ready);
-    if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
 
-    // =================== per tile: masks, lazy max, P ===================
-    const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-    const int T = split < n_total ? (n_total - split + S - 1) / S : 0;
+    // =================== passes over this CTA's tiles ===================
     const int row = qd * 32 + lane;  // key row within the tile
-    // the queries whose columns this warp owns, and the column masks they map to
     const int gw = p.G < 16 ? p.G : 16;                  // columns per query in this chunk
     const int qa = c0 >> gshift;                         // first chunk query (chunk-local)
     const int nqa = p.G < 16 ? (16 >> gshift) : 1;       // queries in this chunk
     const uint32_t qmask_w = (gw == 32) ? 0xFFFFFFFFu : ((1u << gw) - 1u);
     const uint32_t colvalid = ncols - c0 >= 16 ? 0xFFFFu : (ncols > c0 ? ((1u << (ncols - c0)) - 1u) : 0u);
     const int bar_chunk = 3 + ck;                        // named barrier of this chunk's 4 warps
-    bool prev_b = false;  // previous tile wrote the branch-B P region
+    bool union_seen = false;
+    int T = 0x7fffffff;
+    int J0 = 0;  // tiles of earlier passes (mbarrier phase base)
 #pragma unroll 1
-    for (int j = 0; j < T; ++j) {
-      const int t = split + j * S;
-      const int st = j & 1, sb = j & 1;
-      const TileInfo ti = tile_info(m, t, cwlo, cwhi, p.l_sel);
-      // per-(row, query) masks for the queries of this chunk -> 16-bit column masks
-      uint32_t cm_a = 0u, cm_b = 0u;
-      if (ti.kind == kTileCmp) {
-        const int i = ti.base + row;
-        for (int k = 0; k < nqa; ++k) {
-          const int qi = qa + k;
-          if (qi < nqc && i < m.qmvis[qi]) cm_a |= qmask_w << (k * gw);
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool robust = pass > 0;
+      if (robust) {
+        named_bar_sync(kBarRedo, kThreads);  // every role has seen the redo decision
+        if (tid == 0) m.flag = 0;
+      }
+      named_bar_sync(1, kSoftThreads);  // every column's mref is written
+      // running max / threshold: fast = fixed reference, robust = -inf (lazy raise)
+      for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
+        const float r = m.mref[i % kCols];
+        (&m.m2[0][0])[i] = robust ? -INFINITY : r;
+        (&m.thr[0][0])[i] = robust ? -INFINITY : r + kFastHi;
+      }
+      {  // zero the O and row-sum accumulators of this warp's lanes / columns
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+#pragma unroll
+        for (int br = 0; br < 3; ++br) {
+          tmem_st16(lanebase + kTmemO + 64 * br + c0, z);
+          tmem_st16(lanebase + kTmemL + 64 * br + c0, z);
         }
-      } else if (ti.kind == kTileTok) {
-        const int u = ti.base + (row >> 6);
-        if (u < m.n_union) {
-          const int tok = m.union_blk[u] * p.l_sel + (row & 63);
-          const uint32_t own = m.union_own[u];
+        tmem_wait_st();
+      }
+      named_bar_sync(1, kSoftThreads);
+      bool ovf = false;       // fast pass: an active logit above mref + kFastHi
+      uint32_t act_ab = 0u;   // fast pass: active columns, cmp (bits 0-15) / slc (16-31)
+      uint32_t act_w = 0u;    //            and win (bits 0-15), of this lane
+      bool prev_b = false;    // previous tile wrote the branch-B P region
+#pragma unroll 1
+      for (int j = 0; active; ++j) {
+        const int t = split + j * S;
+        if (!union_seen && t >= n_cmp) {
+          mbar_sleep_wait(&m.union_ready, 0);
+          union_seen = true;
+          T = tile_count();
+        }
+        if (union_seen && j >= T) break;
+        const int J = J0 + j;
+        const int sb = J & 1;
+        const TileInfo ti = tile_info(m, n_cmp, t, cwlo, cwhi, p.l_sel);
+        // per-(row, query) masks for the queries of this chunk -> 16-bit column masks
+        uint32_t cm_a = 0u, cm_b = 0u;
+        if (ti.kind == kTileCmp) {
+          const int i = ti.base + row;
+#pragma unroll 4
           for (int k = 0; k < nqa; ++k) {
             const int qi = qa + k;
-            if (qi >= nqc) break;
-            if (((own >> qi) & 1u) && tok < m.qbound[qi]) cm_a |= qmask_w << (k * gw);
-            if (tok >= m.qwlo[qi] && tok <= m.qwhi[qi]) cm_b |= qmask_w << (k * gw);
+            if (qi < nqc && i < m.qmvis[qi]) cm_a |= qmask_w << (k * gw);
+          }
+        } else if (ti.kind == kTileTok) {
+          const int u = ti.base + (row >> 6);
+          if (u < m.n_union) {
+            const int tok = m.union_blk[u] * p.l_sel + (row & 63);
+            const uint32_t own = m.union_own[u];
+#pragma unroll 4
+            for (int k = 0; k < nqa; ++k) {
+              const int qi = qa + k;
+              if (qi >= nqc) break;
+              if (((own >> qi) & 1u) && tok < m.qbound[qi]) cm_a |= qmask_w << (k * gw);
+              if (tok >= m.qwlo[qi] && tok <= m.qwhi[qi]) cm_b |= qmask_w << (k * gw);
+            }
+          }
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < nqa; ++k) {
+            const int qg = q0 + qa + k;
+            if (qa + k < nqc && qg >= 1 && row < 64 && ((p.tree_mask[qg - 1] >> row) & 1ull))
+              cm_b |= qmask_w << (k * gw);
           }
         }
-      } else {
-        for (int k = 0; k < nqa; ++k) {
-          const int qg = q0 + qa + k;
-          if (qa + k < nqc && qg >= 1 && row < 64 && ((p.tree_mask[qg - 1] >> row) & 1ull))
-            cm_b |= qmask_w << (k * gw);
+        cm_a &= colvalid;
+        cm_b &= colvalid;
+        if (!ti.act_a) cm_a = 0u;
+        if (!ti.act_b) cm_b = 0u;
+        // S^T rows of this quadrant, this warp's 16 columns (log2 units)
+        float s[16];
+        mbar_sleep_wait(&m.s_full[sb], (J >> 1) & 1);
+        if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 24 + j] = globaltimer();
+        tc_fence_after();
+        {
+          uint32_t r[16];
+          tmem_ld16(lanebase + kTmemS + 64 * sb + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) s[e] = __uint_as_float(r[e]);
         }
-      }
-      cm_a &= colvalid;
-      cm_b &= colvalid;
-      // S^T rows of this quadrant, this warp's 16 columns (log2 units)
-      float s[16];
-      mbar_sleep_wait(&m.s_full[sb], (j >> 1) & 1);
-      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 24 + j] = globaltimer();
-      tc_fence_after();
-      if (ck < nch) {
-        uint32_t r[16];
-        tmem_ld16(lanebase + kTmemS + 64 * sb + c0, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) s[e] = __uint_as_float(r[e]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) s[e] = 0.f;
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&m.s_free[sb]);
-      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 56 + j] = globaltimer();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&m.s_free[sb]);
 
-      // ---- lazy running max per active branch; the 4 warps sharing this
-      // column chunk vote (columns are independent across chunks) ----
-      bool resc[2] = {false, false};
-#pragma unroll 1
-      for (int side = 0; side < 2; ++side) {
-        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
-        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-        const uint32_t cm = side == 0 ? cm_a : cm_b;
-        if ((p.debug_flags & 1) && m.m2[br][c0] != -INFINITY) continue;  // timing experiment only
-        bool need = false;
+        if (!robust) {
+          // ---- fast pass: one exp per element, shared by both branches ----
+          float pe[16];
+          const uint32_t cm = cm_a | cm_b;
+          float mx = -INFINITY;
+          const float4* mr4 = reinterpret_cast<const float4*>(&m.mref[c0]);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) need |= ((cm >> e) & 1u) && (s[e] > m.thr[br][c0 + e]);
-        const bool any_w = __any_sync(0xffffffffu, need);
-        if (lane == 0) m.vote[qd][ck] = any_w ? 1 : 0;
-        named_bar_sync(bar_chunk, 128);
-        const int any = m.vote[0][ck] | m.vote[1][ck] | m.vote[2][ck] | m.vote[3][ck];
-        named_bar_sync(bar_chunk, 128);
-        if (!any) continue;
-        resc[side] = true;
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const float4 r4 = mr4[e4];
+            const float mr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float d = s[4 * e4 + e] - mr[e];
+              mx = fmaxf(mx, ((cm >> (4 * e4 + e)) & 1u) ? d : -INFINITY);
+              pe[4 * e4 + e] = fast_exp2(d);
+            }
+          }
+          ovf |= mx > kFastHi;
+          if (ti.kind == kTileCmp) act_ab |= cm_a; else act_ab |= cm_a << 16;
+          act_w |= cm_b;
+          if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
+          if (ti.act_a)
+            write_p(smem + kOffK + sb * kStageBytes, row, ck, cm_a, pe,
+                    lanebase + kTmemL + 64 * (ti.kind == kTileCmp ? kCmp : kSlc) + c0);
+          if (ti.act_b) {
+            // the shared branch-B P region is rewritten only after the previous
+            // tile's MMAs read it (branch-A P lives in this tile's own K stage)
+            if (j > 0 && prev_b) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
+            write_p(smem + kOffPB, row, ck, cm_b, pe, lanebase + kTmemL + 64 * kWin + c0);
+          }
+        } else {
+          // ---- robust pass: lazy running max per active branch; the 4 warps
+          // sharing this column chunk vote (columns are independent across chunks)
+          bool resc[2] = {false, false};
+#pragma unroll 1
+          for (int side = 0; side < 2; ++side) {
+            if (!(side == 0 ? ti.act_a : ti.act_b)) continue;  // CTA-uniform
+            const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+            const uint32_t cm = side == 0 ? cm_a : cm_b;
+            bool need = false;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) need |= ((cm >> e) & 1u) && (s[e] > m.thr[br][c0 + e]);
+            const bool any_w = __any_sync(0xffffffffu, need);
+            if (lane == 0) m.vote[qd][ck] = any_w ? 1 : 0;
+            named_bar_sync(bar_chunk, 128);
+            const int any = m.vote[0][ck] | m.vote[1][ck] | m.vote[2][ck] | m.vote[3][ck];
+            named_bar_sync(bar_chunk, 128);
+            if (!any) continue;
+            resc[side] = true;
+            float v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = ((cm >> e) & 1u) ? s[e] : -INFINITY;
+            const float mx = reduce16<true>(v, lane);
+            if ((lane & 1) == 0) m.tmax[qd][c0 + (lane >> 1)] = mx;
+            named_bar_sync(bar_chunk, 128);
+            if (qd == 0 && lane < 16) {
+              const int c = c0 + lane;
+              const float old = m.m2[br][c];
+              const float tm = fmaxf(fmaxf(m.tmax[0][c], m.tmax[1][c]), fmaxf(m.tmax[2][c], m.tmax[3][c]));
+              const float nw = tm > old ? tm : old;
+              m.alpha[c] = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
+              m.m2[br][c] = nw;
+              m.thr[br][c] = nw + kRescaleThresh;
+            }
+            named_bar_sync(bar_chunk, 128);
+            // O^T (and the row-sum accumulator) of this chunk *= alpha, once the
+            // previous tile's MMAs into them are complete
+            if (j > 0) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
+            tc_fence_after();
+            float al[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) al[e] = m.alpha[c0 + e];
+            const uint32_t ta = lanebase + kTmemO + 64 * br + c0;
+            uint32_t r[16];
+            tmem_ld16(ta, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
+            tmem_st16(ta, r);
+            const uint32_t tl = lanebase + kTmemL + 64 * br + c0;  // per-lane row sums
+            tmem_ld16(tl, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
+            tmem_st16(tl, r);
+            tmem_wait_st();
+            named_bar_sync(bar_chunk, 128);  // alpha is reused by the other side
+          }
+          if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
+            mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
+#pragma unroll 1
+          for (int side = 0; side < 2; ++side) {
+            if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
+            const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+            float pe[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pe[e] = fast_exp2(s[e] - m.m2[br][c0 + e]);
+            write_p(side == 0 ? smem + kOffK + sb * kStageBytes : smem + kOffPB, row, ck,
+                    side == 0 ? cm_a : cm_b, pe, lanebase + kTmemL + 64 * br + c0);
+          }
+        }
+        tmem_wait_st();
+        prev_b = ti.act_b;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&m.p_full);
+        if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 32 + j] = globaltimer();
+      }
+      if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 2] = globaltimer();
+      // ---- end of pass: branch row sums, then the fast-pass check ----
+      if (active && T > 0) mbar_sleep_wait(&m.pv_done[(J0 + T - 1) & 1], ((J0 + T - 1) >> 1) & 1);
+      if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 7] = globaltimer();
+      tc_fence_after();
+#pragma unroll 1
+      for (int br = 0; br < 3; ++br) {
+        uint32_t r[16];
+        tmem_ld16(lanebase + kTmemL + 64 * br + c0, r);
+        tmem_wait_ld();
         float v[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = ((cm >> e) & 1u) ? s[e] : -INFINITY;
-        const float mx = reduce16<true>(v, lane);
-        if ((lane & 1) == 0) m.tmax[qd][c0 + (lane >> 1)] = mx;
-        named_bar_sync(bar_chunk, 128);
-        if (qd == 0 && lane < 16) {
-          const int c = c0 + lane;
-          const float old = m.m2[br][c];
-          const float tm = fmaxf(fmaxf(m.tmax[0][c], m.tmax[1][c]), fmaxf(m.tmax[2][c], m.tmax[3][c]));
-          const float nw = tm > old ? tm : old;
-          m.alpha[c] = (nw == old) ? 1.f : (old == -INFINITY ? 0.f : fast_exp2(old - nw));
-          m.m2[br][c] = nw;
-          m.thr[br][c] = nw + kRescaleThresh;
-        }
-        named_bar_sync(bar_chunk, 128);
-        // O^T (and the row-sum accumulator) of this chunk *= alpha, once the
-        // previous tile's MMAs into them are complete
-        if (j > 0) mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-        if (ck < nch) {
-          float al[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) al[e] = m.alpha[c0 + e];
-          const uint32_t ta = lanebase + kTmemO + 64 * br + c0;
-          uint32_t r[16];
-          tmem_ld16(ta, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
-          tmem_st16(ta, r);
-          const uint32_t tl = lanebase + kTmemL + 64 * br + c0;  // per-lane row sums
-          tmem_ld16(tl, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
-          tmem_st16(tl, r);
-          tmem_wait_st();
-        }
-        named_bar_sync(bar_chunk, 128);  // alpha is reused by the other side
+        for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
+        const float sum = reduce16<false>(v, lane);
+        if ((lane & 1) == 0) m.lred[br][qd][c0 + (lane >> 1)] = sum;
       }
-      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
-      // the shared branch-B P region is rewritten only after the previous
-      // tile's MMAs read it (branch-A P lives in this tile's own K stage)
-      if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
-        mbar_sleep_wait(&m.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-
-      // ---- probabilities -> P^T (MN-major SW128, hi + lo), per-lane row sums ----
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
-        const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-        const uint32_t cm = side == 0 ? cm_a : cm_b;
-        uint8_t* pdst = side == 0 ? smem + kOffK + st * kStageBytes : smem + kOffPB;
-        float pv[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pv[e] = ((cm >> e) & 1u) ? fast_exp2(s[e] - m.m2[br][c0 + e]) : 0.f;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-            const float2 hf = __bfloat1622float2(h2);
-            hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
-            lo[e] = pack_bf16(a - hf.x, b - hf.y);
-          }
-          const uint32_t off = sw128_off(row, 2 * ck + h);
-          *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (!robust) {
+        const uint32_t ab = __reduce_or_sync(0xffffffffu, act_ab);
+        const uint32_t wb = __reduce_or_sync(0xffffffffu, act_w);
+        if (lane == 0) {
+          m.actw[warp][0] = ab;
+          m.actw[warp][1] = wb;
         }
-        if (ck < nch) {  // per-lane row sums live in TMEM (no cross-lane work per tile)
-          const uint32_t tl = lanebase + kTmemL + 64 * br + c0;
-          uint32_t r[16];
-          tmem_ld16(tl, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + pv[e]);
-          tmem_st16(tl, r);
-        }
+        if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(&m.flag, 2);
       }
-      tmem_wait_st();
-      prev_b = ti.act_b;
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&m.p_full);
-      if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 32 + j] = globaltimer();
+      named_bar_sync(1, kSoftThreads);
+      if (!robust && tid < 3 * kCols) {  // one (branch, column) per thread
+        const int br = tid / kCols, c = tid % kCols, ckc = c >> 4;
+        const int bit = (br == kWin ? 0 : 16 * br) + (c & 15);
+        const int wd = br == kWin ? 1 : 0;
+        const uint32_t a = m.actw[4 * ckc][wd] | m.actw[4 * ckc + 1][wd] | m.actw[4 * ckc + 2][wd] |
+                           m.actw[4 * ckc + 3][wd];
+        const float L = m.lred[br][0][c] + m.lred[br][1][c] + m.lred[br][2][c] + m.lred[br][3][c];
+        if (((a >> bit) & 1u) && !(L >= 0x1p-48f && L < 0x1p+100f)) atomicOr(&m.flag, 4);
+      }
+      named_bar_sync(kBarPassEnd, kThreads);  // pass end: the redo decision is visible to every role
+      if (trace && tid == 0) p.trace[cta_id * 64 + 62 + pass] = (unsigned long long)m.flag;
+      if (!m.flag) break;
+      J0 += T;
     }
-    if (trace && tid == 0) p.trace[cta_id * 64 + 2] = globaltimer();
     // ---- epilogue: partial (m, l, O) of this split -> workspace ----
-    if (T > 0) mbar_sleep_wait(&m.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
-    if (trace && tid == 0) p.trace[cta_id * 64 + 7] = globaltimer();
-    tc_fence_after();
     const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
     float* ws_ml = p.ws + unit * (3 * kCols * 2);
     float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
-    // row sums: lanes -> (reduce16) -> quadrants
-#pragma unroll 1
-    for (int br = 0; br < 3; ++br) {
-      uint32_t r[16];
-      tmem_ld16(lanebase + kTmemL + 64 * br + c0, r);
-      tmem_wait_ld();
-      float v[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
-      const float sum = reduce16<false>(v, lane);
-      if ((lane & 1) == 0) m.lred[br][qd][c0 + (lane >> 1)] = sum;
-    }
-    named_bar_sync(1, kSoftThreads);
     for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
       const int br = i / kCols, c = i % kCols;
       ws_ml[2 * i] = m.m2[br][c];
       ws_ml[2 * i + 1] = m.lred[br][0][c] + m.lred[br][1][c] + m.lred[br][2][c] + m.lred[br][3][c];
     }
-    if (ck < nch) {
+    if (active) {
 #pragma unroll 1
       for (int br = 0; br < 3; ++br) {
         uint32_t r[16];
@@ -617,148 +703,176 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
   } else if (warp == kWarpTma) {
-    // =================== TMA producer ===================
-    if (lane == 0) {
-      tma_prefetch(&p.tm_k);
-      tma_prefetch(&p.tm_v);
-      tma_prefetch(&p.tm_ck);
-      tma_prefetch(&p.tm_cv);
-      // stream this CTA's tiles into L2 ahead of the two smem stages: the
-      // stage loads below then hit L2 instead of paying HBM latency per tile
-      auto tile_rows = [&](int t, const CUtensorMap*& tk, const CUtensorMap*& tv, int& r0, int& r1) {
-        if (t < n_cmp) {
-          tk = &p.tm_ck; tv = &p.tm_cv;
-          r0 = t * kTile; r1 = r0 + 64;
-        } else if (t < m.n_cmp_tiles + m.n_tok_tiles) {
-          tk = &p.tm_k; tv = &p.tm_v;
-          const int u0 = 2 * (t - m.n_cmp_tiles);
-          r0 = m.union_blk[u0] * p.l_sel;
-          r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
-        } else {
-          tk = &p.tm_tk; tv = &p.tm_tv;
-          r0 = 0; r1 = 64;
-        }
-      };
-      auto prefetch_tile = [&](int t) {
-        const CUtensorMap *tk, *tv;
-        int r0, r1;
-        tile_rows(t, tk, tv, r0, r1);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          tma_prefetch_3d(tk, c * 64, kvh, r0);
-          tma_prefetch_3d(tk, c * 64, kvh, r1);
-          tma_prefetch_3d(tv, c * 64, kvh, r0);
-          tma_prefetch_3d(tv, c * 64, kvh, r1);
-        }
-      };
-      for (int t = split + 2 * S; t < n_cmp; t += S) prefetch_tile(t);
-      bool union_seen = false;
-      int n_total = 0x7fffffff;
-      for (int j = 0;; ++j) {
-        const int t = split + j * S;
-        if (t >= n_cmp && !union_seen) {
-          mbar_sleep_wait(&m.union_ready, 0);
-          union_seen = true;
-          n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-          for (int t2 = max(t, split + 2 * S); t2 < n_total; t2 += S) prefetch_tile(t2);
-        }
-        if (t >= n_total) break;
-        const int st = j & 1;
-        if (j >= 2) mbar_sleep_wait(&m.kv_empty[st], ((j >> 1) + 1) & 1);
-        uint8_t* kdst = smem + kOffK + st * kStageBytes;
-        uint8_t* vdst = smem + kOffV + st * kStageBytes;
-        if (trace && j < 8) p.trace[cta_id * 64 + 8 + j] = globaltimer();
-        mbar_expect_tx(&m.k_full[st], kStageBytes);
-        mbar_expect_tx(&m.v_full[st], kStageBytes);
-        const CUtensorMap *tk, *tv;
-        int r0, r1;
-        tile_rows(t, tk, tv, r0, r1);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
-          tma_load_3d(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st]);
-        }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          tma_load_3d(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st]);
-          tma_load_3d(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st]);
-        }
+    // =================== TMA producer (+ the union build) ===================
+    auto tile_rows = [&](int t, const CUtensorMap*& tk, const CUtensorMap*& tv, int& r0, int& r1) {
+      if (t < n_cmp) {
+        tk = &p.tm_ck; tv = &p.tm_cv;
+        r0 = t * kTile; r1 = r0 + 64;
+      } else if (t < n_cmp + m.n_tok_tiles) {
+        tk = &p.tm_k; tv = &p.tm_v;
+        const int u0 = 2 * (t - n_cmp);
+        r0 = m.union_blk[u0] * p.l_sel;
+        r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
+      } else {
+        tk = &p.tm_tk; tv = &p.tm_tv;
+        r0 = 0; r1 = 64;
       }
+    };
+    // stream this CTA's tiles into L2 ahead of the two smem stages: the
+    // stage loads below then hit L2 instead of paying HBM latency per tile
+    auto prefetch_tile = [&](int t) {
+      const CUtensorMap *tk, *tv;
+      int r0, r1;
+      tile_rows(t, tk, tv, r0, r1);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tma_prefetch_3d(tk, c * 64, kvh, r0);
+        tma_prefetch_3d(tk, c * 64, kvh, r1);
+        tma_prefetch_3d(tv, c * 64, kvh, r0);
+        tma_prefetch_3d(tv, c * 64, kvh, r1);
+      }
+    };
+    auto issue = [&](int t, int J) {
+      const int st = J & 1;
+      if (J >= 2) mbar_sleep_wait(&m.kv_empty[st], ((J >> 1) + 1) & 1);
+      uint8_t* kdst = smem + kOffK + st * kStageBytes;
+      uint8_t* vdst = smem + kOffV + st * kStageBytes;
+      if (trace && J < 8) p.trace[cta_id * 64 + 8 + J] = globaltimer();
+      mbar_expect_tx(&m.k_full[st], kStageBytes);
+      mbar_expect_tx(&m.v_full[st], kStageBytes);
+      const CUtensorMap *tk, *tv;
+      int r0, r1;
+      tile_rows(t, tk, tv, r0, r1);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
+        tma_load_3d(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st]);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tma_load_3d(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st]);
+        tma_load_3d(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st]);
+      }
+    };
+    // pass 0: the first compressed stages go out before the union is built
+    int pre = 0;
+    if (lane == 0) {
+      while (pre < 2 && split + pre * S < n_cmp) {
+        issue(split + pre * S, pre);
+        ++pre;
+      }
+      for (int t = split + 2 * S; t < n_cmp; t += S) prefetch_tile(t);
+    }
+    if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
+    build_union_warp(p, m, q0, nqc, lane, cwlo, cwhi, trace ? p.trace + cta_id * 64 : nullptr);
+    mbar_arrive(&m.union_ready);  // every lane: releases its own union writes
+    if (trace && lane == 0) p.trace[cta_id * 64 + 1] = globaltimer();
+    const int T = tile_count();
+    if (lane == 0) {
+      for (int j = max(pre, 2); j < T; ++j)
+        if (split + j * S >= n_cmp) prefetch_tile(split + j * S);
+      if (trace) p.trace[cta_id * 64 + 60] = globaltimer();
+      for (int j = pre; j < T; ++j) issue(split + j * S, j);
     }
     __syncwarp();
+    named_bar_sync(kBarPassEnd, kThreads);
+    if (m.flag) {  // robust redo: the same tiles again
+      named_bar_sync(kBarRedo, kThreads);
+      if (lane == 0)
+        for (int j = 0; j < T; ++j) issue(split + j * S, T + j);
+      __syncwarp();
+      named_bar_sync(kBarPassEnd, kThreads);
+    }
   } else {
-    // =================== MMA issuers: warp 17 = QK^T, warp 18 = PV + row sums ===================
+    // =================== MMA issuers: warp 17 = QK^T, warp 18 = PV ===================
     // (two issuing threads so a QK waiting for its K tile never delays the PV
     // of the previous tile; each commit tracks only its own thread's MMAs)
-    if (lane == 0) {
-      mbar_sleep_wait(&m.q_ready, 0);
-      tc_fence_after();
-      // compressed tiles come first and do not need the union; the total tile
-      // count is known once the union is built
-      bool union_seen = false;
-      int T = 0x7fffffff;
-      auto tiles = [&](int j) {
-        if (split + j * S >= n_cmp && !union_seen) {
-          mbar_sleep_wait(&m.union_ready, 0);
-          union_seen = true;
-          const int n_total = m.n_cmp_tiles + m.n_tok_tiles + m.n_tree_tiles;
-          T = split < n_total ? (n_total - split + S - 1) / S : 0;
-        }
-        return j < T;
-      };
-      if (warp == kWarpTma + 1) {
-        const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
-        for (int j = 0; tiles(j); ++j) {
-          const int st = j & 1, sb = j & 1;
-          if (j >= 2) mbar_sleep_wait(&m.s_free[sb], ((j >> 1) + 1) & 1);
-          mbar_sleep_wait(&m.k_full[st], (j >> 1) & 1);
-          if (trace && j < 8) p.trace[cta_id * 64 + 16 + j] = globaltimer();
-          tc_fence_after();
-          const uint32_t kaddr = sbase + kOffK + st * kStageBytes;
-          const uint32_t qaddr = sbase + kOffQ;
-          const uint32_t d = tmem + kTmemS + 64 * sb;
+    bool union_seen = false;
+    int T = 0x7fffffff;
+    auto tiles = [&](int j) {
+      if (split + j * S >= n_cmp && !union_seen) {
+        mbar_sleep_wait(&m.union_ready, 0);
+        union_seen = true;
+        T = tile_count();
+      }
+      return j < T;
+    };
+    auto qk_pass = [&](int J0) {
+      const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
+      for (int j = 0; tiles(j); ++j) {
+        const int J = J0 + j;
+        const int sb = J & 1;
+        if (J >= 2) mbar_sleep_wait(&m.s_free[sb], ((J >> 1) + 1) & 1);
+        mbar_sleep_wait(&m.k_full[sb], (J >> 1) & 1);
+        if (trace && J < 8) p.trace[cta_id * 64 + 16 + J] = globaltimer();
+        tc_fence_after();
+        const uint32_t kaddr = sbase + kOffK + sb * kStageBytes;
+        const uint32_t qaddr = sbase + kOffQ;
+        const uint32_t d = tmem + kTmemS + 64 * sb;
 #pragma unroll
-          for (int part = 0; part < 2; ++part) {  // q hi, q lo
+        for (int part = 0; part < 2; ++part) {  // q hi, q lo
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+            const uint32_t qoff = part * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32;
+            umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
+                     idesc_qk, (part | kk) != 0);
+          }
+        }
+        umma_commit(&m.s_full[sb]);
+      }
+    };
+    auto pv_pass = [&](int J0) {
+      const uint32_t idesc_pv = idesc_bf16(128, nqk, 1, 1);
+      for (int j = 0; tiles(j); ++j) {
+        const int J = J0 + j;
+        const int st = J & 1;
+        mbar_sleep_wait(&m.p_full, J & 1);
+        const TileInfo ti = tile_info(m, n_cmp, split + j * S, cwlo, cwhi, p.l_sel);
+        mbar_sleep_wait(&m.v_full[st], (J >> 1) & 1);
+        if (trace && J < 8) p.trace[cta_id * 64 + 40 + J] = globaltimer();
+        tc_fence_after();
+        const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+          if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
+          const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
+          const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+          const uint32_t d = tmem + kTmemO + 64 * br;
+#pragma unroll
+          for (int part = 0; part < 2; ++part)
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
-              const uint32_t qoff = part * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32;
-              umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
-                       idesc_qk, (part | kk) != 0);
+              const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
+              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
             }
-          }
-          umma_commit(&m.s_full[sb]);
         }
-      } else {
-        const uint32_t idesc_pv = idesc_bf16(128, 64, 1, 1);
-        for (int j = 0; tiles(j); ++j) {
-          const int st = j & 1;
-          mbar_sleep_wait(&m.p_full, j & 1);
-          const TileInfo ti = tile_info(m, split + j * S, cwlo, cwhi, p.l_sel);
-          mbar_sleep_wait(&m.v_full[st], (j >> 1) & 1);
-          if (trace && j < 8) p.trace[cta_id * 64 + 40 + j] = globaltimer();
-          tc_fence_after();
-          const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
-#pragma unroll 1
-          for (int side = 0; side < 2; ++side) {
-            if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
-            const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
-            const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-            const uint32_t d = tmem + kTmemO + 64 * br;
-#pragma unroll
-            for (int part = 0; part < 2; ++part)
-#pragma unroll
-              for (int kk = 0; kk < 8; ++kk) {
-                const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
-                umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
-              }
-          }
-          umma_commit(&m.pv_done[j & 1]);
-          umma_commit(&m.kv_empty[st]);
-        }
+        umma_commit(&m.pv_done[J & 1]);
+        umma_commit(&m.kv_empty[st]);
       }
+    };
+    if (lane == 0) {
+      if (warp == kWarpTma + 1) {
+        tma_prefetch(&p.tm_k);
+        tma_prefetch(&p.tm_v);
+        tma_prefetch(&p.tm_tk);
+        tma_prefetch(&p.tm_tv);
+      }
+      mbar_sleep_wait(&m.q_ready, 0);
+      tc_fence_after();
+      if (warp == kWarpTma + 1) qk_pass(0); else pv_pass(0);
     }
     __syncwarp();
+    named_bar_sync(kBarPassEnd, kThreads);
+    if (m.flag) {
+      named_bar_sync(kBarRedo, kThreads);
+      if (lane == 0) {
+        tc_fence_after();
+        if (warp == kWarpTma + 1) qk_pass(T); else pv_pass(T);
+      }
+      __syncwarp();
+      named_bar_sync(kBarPassEnd, kThreads);
+    }
   }
 
   // ---- merge of the split partials (per-head barrier) + gated combine ----
@@ -776,6 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = split + (tid >> 7) * S; c < ncols; c += 4 * S) {
       const int qg = q0 + (c >> gshift);
       const int h = kvh * p.G + (c & (p.G - 1));
+      const float* gate = p.gates + ((int64_t)qg * p.Hq + h) * 3;
       float res = 0.f;
 #pragma unroll 1
       for (int br = 0; br < 3; ++br) {
@@ -794,18 +909,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             ov[s2] = 0.f;
           }
         }
+        const float g = gate[br];
         float M = -INFINITY;
 #pragma unroll
-        for (int s2 = 0; s2 < kMaxSplits; ++s2) M = fmaxf(M, mv[s2]);
+        for (int s2 = 0; s2 < kMaxSplits; ++s2)
+          if (lv[s2] > 0.f) M = fmaxf(M, mv[s2]);
         if (M == -INFINITY) continue;  // empty branch contributes 0 (nsa_attention.cpp:244)
         float L = 0.f, O = 0.f;
 #pragma unroll
         for (int s2 = 0; s2 < kMaxSplits; ++s2) {
-          const float f = mv[s2] == -INFINITY ? 0.f : fast_exp2(mv[s2] - M);
+          const float f = lv[s2] > 0.f ? fast_exp2(mv[s2] - M) : 0.f;
           L += lv[s2] * f;
           O += ov[s2] * f;
         }
-        if (L > 0.f) res += p.gates[((int64_t)qg * p.Hq + h) * 3 + br] * (O / L);
+        if (L > 0.f) res += g * (O / L);
       }
       p.out[((int64_t)qg * p.Hq + h) * kDh + dh] = res;
     }

@@ -17,6 +17,7 @@ struct AttendParams {
   CUtensorMap tm_k, tm_v;    // committed K/V bf16, dims (dh, Hkv, rows)
   CUtensorMap tm_ck, tm_cv;  // compressed K (bf16 copy) / V bf16, dims (dh, Hkv, blocks)
   CUtensorMap tm_tk, tm_tv;  // draft rows bf16, dims (dh, Hkv, max(gamma, 1))
+  const uint16_t* k_raw;     // committed K bf16 (the fast-pass reference key row)
   const float* q;            // [nq][Hq][dh]
   const float* gates;        // [nq][Hq][3]
   float* out;                // [nq][Hq][dh]
@@ -24,7 +25,7 @@ struct AttendParams {
   const int32_t* idx_count;  // [nq]
   float* ws;                 // split partials
   unsigned long long* trace; // optional per-CTA globaltimer stamps [cta][64] (debug)
-  int32_t debug_flags;       // diagnostics only (bit 0: skip running-max votes after the first)
+  int32_t debug_flags;       // tests only (bit 0: force the robust softmax redo pass)
   int64_t ws_o_offset;       // float offset of the O partials inside ws
   int64_t ws_sync_offset;    // float offset of the per-head barrier words (zero-initialised)
   int32_t nq, gamma, Hq, Hkv, G, n_sel;
@@ -34,6 +35,15 @@ struct AttendParams {
   int32_t pos[kMaxQueries];
   int32_t src_row[kMaxQueries];  // index-set row each query attends with
   uint64_t tree_mask[kMaxQueries];
+  // per-query tables (host-computed from pos; config.hpp:55-58, nsa_attention.cpp:161-222)
+  int32_t qbound[kMaxQueries];   // min(routing bound, rows): selected tokens < qbound
+  int32_t qwlo[kMaxQueries];     // committed window [qwlo, qwhi]
+  int32_t qwhi[kMaxQueries];
+  int32_t qmvis[kMaxQueries];    // visible compressed blocks
+  // per-chunk tables
+  int32_t ch_ncmp[kMaxQueries];  // compressed tiles of the chunk (widest visible range)
+  int32_t ch_wlo[kMaxQueries];   // union of the chunk's windows
+  int32_t ch_whi[kMaxQueries];
 };
 
 size_t attend_smem_bytes();

@@ -39,6 +39,7 @@ void check_build_limits(const specsv_nsa_config& c) {
   if (g > 32 || (g & (g - 1)) != 0) unsup("GQA group size must be a power of two <= 32");
   if (c.n > 64) unsup("n must be <= 64");
   if (c.n_q_heads > 128) unsup("n_q_heads must be <= 128");
+  if (c.w / c.l_sel + 2 + c.n > 1280) unsup("w / l_sel + n must be <= 1278 (per-chunk block union)");
   if ((c.l - 1) / c.d > 7) unsup("l must be <= 8 * d (routing halo)");
   if ((63 + 7 * c.d + c.l - 1) / c.l_sel + 1 > 4)
     unsup("7 d + l must be <= 194 (selection blocks per 8 compressed blocks)");

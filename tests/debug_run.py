@@ -90,13 +90,16 @@ def trace_attend(rows=65536, gamma=8):
         r = t[c]
         print(f"cta {c}: start {(r[0]-t0)/1e3:.2f} q_ready {(r[5]-t0)/1e3:.2f} setup {(r[1]-t0)/1e3:.2f} loop {(r[2]-t0)/1e3:.2f} "
               f"lastpv {(r[7]-t0)/1e3:.2f} part {(r[3]-t0)/1e3:.2f} barrier {(r[6]-t0)/1e3:.2f} merge {(r[4]-t0)/1e3:.2f}")
+        print("   union: start %.2f staged %.2f prefix %.2f scatter %.2f done %.2f prefetched %.2f; q math %.2f" % tuple(
+            (r[k] - t0) / 1e3 for k in (59, 56, 57, 58, 1, 60, 61)))
         for j in range(8):
             ev = [r[8 + j], r[16 + j], r[24 + j], r[56 + j], r[48 + j], r[32 + j], r[40 + j]]
             if ev[0] == 0:
                 break
             print("   tile", j, " ".join(f"{(x - t0) / 1e3:7.2f}" if x else "   -   " for x in ev),
                   "(tma, qk, s_full, s_ld, vote, p_full, pv)")
-    print("ctas", len(t))
+    print("ctas", len(t), "fast-pass flags", np.unique(t[:, 62], return_counts=True),
+          "robust-pass flags", np.unique(t[:, 63], return_counts=True))
     for name, col in (("setup", 1), ("tiles", 2), ("partials", 3), ("merge", 4)):
         d = (t[:, col] - t0) / 1e3
         print(f"{name:9s} done at us: min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}")

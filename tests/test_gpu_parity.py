@@ -194,3 +194,34 @@ def test_depth_beyond_lag_rejected():
     with pytest.raises(V.SpecsvError) as e:
         case.run(1, V.MODE_EXACT, V.ROLE_REFRESH)
     assert e.value.code == 1
+
+
+def test_robust_redo_pass_forced(oracle_lib, monkeypatch):
+    """The attend kernel's robust (running-max) pass, forced for every CTA,
+    matches the oracle like the fast fixed-reference pass does."""
+    monkeypatch.setenv("SPECSV_ATTEND_FORCE_ROBUST", "1")
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 3001, 8, 3109, parent_slot=TREE8)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(2, V.MODE_EXACT, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 2, O.MODE_EXACT, O.ROLE_REFRESH)
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+@pytest.mark.parametrize("scale", [30.0, 0.001])
+def test_extreme_logit_ranges(oracle_lib, scale):
+    """Queries scaled so logits span far more than the fast pass's +-48
+    (log2) window around its reference key (scale 30), or are nearly flat
+    (0.001): the end-of-pass check must route the first through the robust
+    pass and both must stay within tolerance."""
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 6000, 8, 555)
+    x.q = (x.q * scale).astype(np.float32)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
