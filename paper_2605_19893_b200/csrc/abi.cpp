@@ -120,7 +120,7 @@ int qc_size_for(const specsv_nsa_config& c) {
   const int G = static_cast<int>(c.n_q_heads / c.n_kv_heads);
   const int64_t win_blocks = c.w / c.l_sel + 2;
   const int64_t by_union = (kMaxUnion - win_blocks) / std::max<int64_t>(c.n, 1);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min(64 / G, kMaxChunkQ), by_union));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min(kAttendCols / G, kMaxChunkQ), by_union));
 }
 
 Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
@@ -261,6 +261,9 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   encode_rows_map(&p.tm_tk, gamma > 0 ? a.tree_k : kv.k, std::max(gamma, 1), H, dh);
   encode_rows_map(&p.tm_tv, gamma > 0 ? a.tree_v : kv.v, std::max(gamma, 1), H, dh);
   p.k_raw = static_cast<const uint16_t*>(kv.k);
+  p.v_raw = static_cast<const uint16_t*>(kv.v);
+  p.ck_raw = static_cast<const uint16_t*>(kv.ck16);
+  p.cv_raw = static_cast<const uint16_t*>(kv.cv);
   p.q = a.q;
   p.gates = a.gates;
   p.out = a.out;
@@ -271,7 +274,7 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   p.debug_flags = std::getenv("SPECSV_ATTEND_FORCE_ROBUST") != nullptr ? 1 : 0;
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
-  p.ws_o_offset = (int64_t)nchunks * H * S * (3 * 64 * 2);
+  p.ws_o_offset = (int64_t)nchunks * H * S * (3 * kAttendCols * 2);
   p.ws_sync_offset = (int64_t)(L.attend_bytes / sizeof(float)) - (int64_t)nchunks * H * 2;
   p.nq = a.n_queries;
   p.gamma = gamma;

@@ -14,16 +14,19 @@
 //    draft-tree rows (win).  Every K/V tile is TMA-staged into shared memory
 //    ONCE for all queries and all GQA heads that read it -- the overlap-aware
 //    dedup of the paper.
-//  * Swap-AB: S^T = K_tile . Q^T on tcgen05 (M = 128 keys, N = queries x heads),
+//  * Swap-AB: S^T = K_tile . Q^T on tcgen05 (M = 128 keys, N = query columns),
 //    so the key dimension fills the 128-lane MMA; O^T += V^T . P^T (M = d_head).
-//    Accumulators live in TMEM.  q (pre-scaled by log2(e)/sqrt(dh)) and P are
-//    split hi+lo in bf16, keeping ~16 mantissa bits (fp32-class accumulation).
-//  * 16 softmax warps: warp w owns TMEM lane quadrant w%4 (32 keys) and the
-//    16-column chunk w/4.  Ownership / routing-bound / window / tree masks are
-//    applied in registers per (key, query); masked entries contribute exactly 0.
-//  * Online softmax with a lazily-raised running max per (branch, column): the
-//    O accumulators in TMEM are rescaled only when a tile's max exceeds the
-//    reference max by 2^8.
+//    q (pre-scaled by log2(e)/sqrt(dh)) and P are split hi+lo in bf16 (~16
+//    mantissa bits).  The hi and lo halves are stacked along N (N = 2 x cols),
+//    so each MMA reads its K or V tile from shared memory ONCE: the MMAs are
+//    bound by that operand read, not by the tensor pipe.
+//  * 12 softmax warps: warp w owns TMEM lane quadrant w%4 (32 keys) and the
+//    16-column chunk w/4 (<= 48 columns).  Ownership / routing-bound / window /
+//    tree masks are applied in registers per (key, query); masked entries
+//    contribute exactly 0.  Row sums stay in registers.
+//  * Fast pass: one fixed reference logit per column, no running max (checked
+//    at the end of the pass; a robust running-max pass redoes the rare CTA
+//    whose logits fall outside the window, see kFastHi).
 //  * Split partials are merged behind a per-head global barrier among the S
 //    co-resident CTAs, and the gate combine is applied in the same kernel: the
 //    branch partial outputs never leave this launch's L2-resident workspace.
@@ -43,26 +46,33 @@ using namespace sm100;
 
 constexpr int kDh = 128;
 constexpr int kTile = 128;
-constexpr int kCols = 64;          // query columns (queries x heads) per CTA
-constexpr int kSoftWarps = 16;     // 4 lane quadrants x 4 column chunks
+constexpr int kCols = kAttendCols;  // query columns (queries x heads) per CTA
+constexpr int kSoftWarps = 12;      // 4 lane quadrants x 3 column chunks
 constexpr int kSoftThreads = kSoftWarps * 32;
 constexpr int kMaxSplits = 18;
-constexpr int kWarpTma = 16;
-constexpr int kThreads = 19 * 32;  // + TMA warp + QK-MMA warp + PV-MMA warp
+constexpr int kWarpTma = 12;
+constexpr int kWarpQk = 13;
+constexpr int kWarpPv = 14;
+constexpr int kWarpUnion = 15;
+static_assert(kWarpPv == kWarpQk + 1 && kWarpUnion == kWarpPv + 1, "warp roles");
+constexpr int kThreads = 16 * 32;
 constexpr uint32_t kTmemCols = 512;
-constexpr int kTmemS = 0;          // two S buffers at cols 0, 64
-constexpr int kTmemO = 128;        // O_cmp 128, O_slc 192, O_win 256
-constexpr int kTmemL = 320;        // per-lane partial row sums of P: 320, 384, 448
-constexpr float kRescaleThresh = 8.0f;  // log2 units
-constexpr int kBarPassEnd = 7;     // named barriers (1: softmax warps, 3-6: column chunks)
+constexpr int kTmemS = 0;           // two S buffers of [hi | lo] x 48: cols 0, 96
+constexpr int kTmemO = 192;         // O_cmp 192, O_slc 288, O_win 384, each [hi | lo] x 48
+constexpr int kTmemStride = 2 * kCols;
+constexpr float kRescaleThresh = 8.0f;  // log2 units (robust pass)
+constexpr int kBarSoft = 1;         // named barriers: softmax warps
+constexpr int kBarChunk0 = 3;       // 3..5: the 4 warps of one column chunk
+constexpr int kBarPassEnd = 7;
 constexpr int kBarRedo = 8;
 
 // shared memory map (bytes from the 1024-aligned base)
-constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P of branch A)
+constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P^T of branch A)
 constexpr uint32_t kOffV = 65536;    // 2 stages x 32 KB
-constexpr uint32_t kOffQ = 131072;   // Q hi 16 KB, Q lo 16 KB
-constexpr uint32_t kOffPB = 163840;  // P of branch B (window): hi 16 KB, lo 16 KB
-constexpr uint32_t kOffMisc = 196608;
+constexpr uint32_t kOffQ = 131072;   // Q^T [hi | lo] rows, two 64-element K halves of 96 x 128 B
+constexpr uint32_t kQHalf = 2 * kCols * 128;
+constexpr uint32_t kOffPB = kOffQ + 2 * kQHalf;  // P^T of branch B (window): 2 MN atoms x 16 KB
+constexpr uint32_t kOffMisc = kOffPB + 32768;
 constexpr uint32_t kStageBytes = 32768;
 
 enum Branch { kCmp = 0, kSlc = 1, kWin = 2 };
@@ -73,15 +83,15 @@ struct Misc {
   uint64_t p_full, q_ready, union_ready;
   uint32_t tmem_base;
   int32_t n_union, n_tok_tiles;
-  int32_t flag;          // end-of-pass check failed: redo the tiles in the robust pass
+  int32_t flag;                   // end-of-pass check failed: redo the tiles in the robust pass
   alignas(16) float mref[kCols];  // fast-pass reference logit per column (log2 units)
-  float m2[3][kCols];    // running max (log2 units) per branch and column
-  float thr[3][kCols];   // m2 + threshold
+  float m2[3][kCols];             // running max (log2 units) per branch and column
+  float thr[3][kCols];            // m2 + threshold
   float alpha[kCols];
   float tmax[4][kCols];
-  int32_t vote[4][kCols / 16];  // [quadrant][chunk]
-  float lred[3][4][kCols];      // row sums per branch, quadrant, column
-  uint32_t actw[kSoftWarps][2]; // fast pass: active (branch, column) bits per warp
+  int32_t vote[4][kCols / 16];    // [quadrant][chunk]
+  float lred[3][4][kCols];        // row sums per branch, quadrant, column
+  uint32_t actw[kSoftWarps][2];   // fast pass: active (branch, column) bits per warp
   int32_t qbound[kMaxChunkQ], qwlo[kMaxChunkQ], qwhi[kMaxChunkQ], qmvis[kMaxChunkQ];
   int32_t qcount[kMaxChunkQ];
   int32_t qsel[kMaxChunkQ * 64];
@@ -91,6 +101,7 @@ struct Misc {
   uint32_t union_own[kMaxUnion];
 };
 static_assert(sizeof(Misc) + kOffMisc + 1024 <= 232448, "shared memory budget");
+static_assert(kTmemO + 3 * kTmemStride <= (int)kTmemCols, "TMEM budget");
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -154,13 +165,11 @@ __device__ void group_barrier(int* cnt, int* gen, int S, int tid) {
 // ---------------------------------------------------------------------------
 // union of selected + window blocks with per-block query ownership (exact:
 // own set; approx: representative's set; both clamped at the query's routing
-// bound, layer_roles.cpp:37-50).  Built by the 32 lanes of the TMA warp while
-// the compressed tiles (which do not need it) are already in flight; the
-// index rows are staged with fire-and-forget cp.async (one round trip).
-__device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc, int lane, int wlo,
-                                 int whi, unsigned long long* tr) {
-  const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
-  const int words = (nsel + 31) >> 5;
+// bound, layer_roles.cpp:37-50).  Built by the union warp while the
+// compressed tiles (which do not need it) are already in flight; the index
+// rows are staged with fire-and-forget cp.async (one round trip).
+// index rows of the chunk's queries -> smem, fire-and-forget (one round trip)
+__device__ __forceinline__ void stage_index_rows(const AttendParams& p, Misc& m, int q0, int nqc, int lane) {
   const int n = p.n_sel;
   for (int e = lane; e < nqc * n; e += 32) {
     const int i = e / n, k = e - i * n;
@@ -168,6 +177,13 @@ __device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc
     cp_async4(&m.qsel[e], p.idx + r * n + k);
     if (k == 0) cp_async4(&m.qcount[i], p.idx_count + r);
   }
+}
+
+__device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc, int lane, int wlo,
+                                 int whi, unsigned long long* tr) {
+  const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
+  const int words = (nsel + 31) >> 5;
+  const int n = p.n_sel;
   for (int w = lane; w < words; w += 32) m.bitmap[w] = 0u;
   cp_async_wait_all();
   __syncwarp();
@@ -267,35 +283,35 @@ __device__ __forceinline__ TileInfo tile_info(const Misc& m, int n_cmp, int t, i
   return ti;
 }
 
+// 16 bf16x2 words (this thread's key row, 16 consecutive N columns from n0)
+// into an MN-major SW128 operand of 128 keys whose 64-column atoms are 16 KB apart
+__device__ __forceinline__ void store_cols(uint8_t* base, int row, int n0, const uint32_t (&w)[8]) {
+  uint8_t* atom = base + (n0 >> 6) * 16384;
+  const int u0 = (n0 & 63) >> 3;
+  *reinterpret_cast<uint4*>(atom + sw128_off(row, u0)) = make_uint4(w[0], w[1], w[2], w[3]);
+  *reinterpret_cast<uint4*>(atom + sw128_off(row, u0 + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 // P^T of one branch for this warp's 16 columns x its 32 key rows: masked
-// probabilities -> SW128 MN-major hi + lo bf16 planes, and the per-lane
-// partial row sums in TMEM (no cross-lane work per tile)
-__device__ __forceinline__ void write_p(uint8_t* pdst, int row, int ck, uint32_t cm, const float (&pe)[16],
-                                        uint32_t tl) {
+// probabilities -> hi at N = c0.., lo at N = nqk + c0.. (bf16), and the
+// warp's column sums added to lacc (lanes 2c, 2c+1 hold column c)
+__device__ __forceinline__ void write_p(uint8_t* pdst, int row, int c0, int nqk, uint32_t cm,
+                                        const float (&pe)[16], float& lacc, int lane) {
   float pv[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) pv[e] = ((cm >> e) & 1u) ? pe[e] : 0.f;
+  uint32_t hi[8], lo[8];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t hi[4], lo[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float a = pv[8 * h + 2 * e], b = pv[8 * h + 2 * e + 1];
-      const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-      const float2 hf = __bfloat1622float2(h2);
-      hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
-      lo[e] = pack_bf16(a - hf.x, b - hf.y);
-    }
-    const uint32_t off = sw128_off(row, 2 * ck + h);
-    *reinterpret_cast<uint4*>(pdst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4*>(pdst + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  for (int e = 0; e < 8; ++e) {
+    const float a = pv[2 * e], b = pv[2 * e + 1];
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+    const float2 hf = __bfloat1622float2(h2);
+    hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
+    lo[e] = pack_bf16(a - hf.x, b - hf.y);
   }
-  uint32_t r[16];
-  tmem_ld16(tl, r);
-  tmem_wait_ld();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + pv[e]);
-  tmem_st16(tl, r);
+  store_cols(pdst, row, c0, hi);
+  store_cols(pdst, row, nqk + c0, lo);
+  lacc += reduce16<false>(pv, lane);
 }
 
 // Softmax reference.  Pass 0 (fast) uses ONE fixed reference logit per column,
@@ -327,69 +343,120 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int q0 = chunk * p.qc_size;
   const int nqc = min(p.qc_size, p.nq - q0);
   const int ncols = nqc * p.G;
-  const int nqk = (ncols + 15) & ~15;
-  const int nch = nqk >> 4;  // 16-column chunks holding valid columns
+  const int nqk = (ncols + 15) & ~15;  // hi columns; lo columns follow at nqk
+  const int nch = nqk >> 4;            // 16-column chunks holding valid columns
   const int gshift = __ffs(p.G) - 1;
   const bool trace = p.trace != nullptr;
   const int n_cmp = p.ch_ncmp[chunk];  // compressed tiles do not depend on the union
   const int cwlo = p.ch_wlo[chunk], cwhi = p.ch_whi[chunk];
   const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
 
-  // ---- barriers + TMEM -----------------------------------------------------
-  if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&m.k_full[i], 1);
-      mbar_init(&m.v_full[i], 1);
-      mbar_init(&m.kv_empty[i], 1);
-      mbar_init(&m.s_full[i], 1);
-      mbar_init(&m.s_free[i], 4 * nch);  // the warps of the active column chunks
-      mbar_init(&m.pv_done[i], 1);
+  // ---- TMA issue helpers (compressed tiles need no union) ------------------
+  auto tile_rows = [&](int t, const CUtensorMap*& tk, const CUtensorMap*& tv, int& r0, int& r1) {
+    if (t < n_cmp) {
+      tk = &p.tm_ck; tv = &p.tm_cv;
+      r0 = t * kTile; r1 = r0 + 64;
+    } else if (t < n_cmp + m.n_tok_tiles) {
+      tk = &p.tm_k; tv = &p.tm_v;
+      const int u0 = 2 * (t - n_cmp);
+      r0 = m.union_blk[u0] * p.l_sel;
+      r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
+    } else {
+      tk = &p.tm_tk; tv = &p.tm_tv;
+      r0 = 0; r1 = 64;
     }
-    mbar_init(&m.p_full, 4 * nch);
-    mbar_init(&m.q_ready, kSoftWarps);
-    mbar_init(&m.union_ready, 32);
-    m.flag = (p.debug_flags & 1) ? 1 : 0;  // bit 0: force the robust redo (tests)
-    fence_mbar_init();
-  }
-  if (warp == kWarpTma) tmem_alloc<kTmemCols>(&m.tmem_base);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = m.tmem_base;
-  if (trace && tid == 0) p.trace[cta_id * 64 + 0] = globaltimer();
-
+  };
+  auto issue = [&](int t, int J) {
+    const int st = J & 1;
+    if (J >= 2) mbar_sleep_wait(&m.kv_empty[st], ((J >> 1) + 1) & 1);
+    uint8_t* kdst = smem + kOffK + st * kStageBytes;
+    uint8_t* vdst = smem + kOffV + st * kStageBytes;
+    if (trace && J < 8) p.trace[cta_id * 64 + 8 + J] = globaltimer();
+    mbar_expect_tx(&m.k_full[st], kStageBytes);
+    mbar_expect_tx(&m.v_full[st], kStageBytes);
+    const CUtensorMap *tk, *tv;
+    int r0, r1;
+    tile_rows(t, tk, tv, r0, r1);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
+      tma_load_3d(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st]);
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      tma_load_3d(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st]);
+      tma_load_3d(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st]);
+    }
+  };
+  // stages issued before the CTA-wide barrier (compressed tiles only)
+  int pre = 0;
+  while (pre < 2 && split + pre * S < n_cmp) ++pre;
   // tile count once the union is known (identical in every role)
   auto tile_count = [&]() {
     const int n_total = n_cmp + m.n_tok_tiles + (has_tree ? 1 : 0);
     return split < n_total ? (n_total - split + S - 1) / S : 0;
   };
 
+  // ---- prologue: everything that needs no other warp goes out first --------
+  float4 xa[2], xb[2];  // softmax warps: this thread's q units, in flight over the barrier
+  uint4 kr;             //                and its slice of the reference key row
+  if (warp == kWarpTma) {
+    if (lane == 0) {
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&m.k_full[i], 1);
+        mbar_init(&m.v_full[i], 1);
+        mbar_init(&m.kv_empty[i], 1);
+        mbar_init(&m.s_full[i], 1);
+        mbar_init(&m.s_free[i], 4 * nch);  // the warps of the active column chunks
+        mbar_init(&m.pv_done[i], 1);
+      }
+      mbar_init(&m.p_full, 4 * nch);
+      mbar_init(&m.q_ready, kSoftWarps);
+      mbar_init(&m.union_ready, 32);
+      m.flag = (p.debug_flags & 1) ? 1 : 0;  // bit 0: force the robust redo (tests)
+      fence_mbar_init();
+      for (int j = 0; j < pre; ++j) issue(split + j * S, j);
+    }
+    __syncwarp();
+    tmem_alloc<kTmemCols>(&m.tmem_base);
+  } else if (warp < kSoftWarps) {
+    kr = reinterpret_cast<const uint4*>(p.k_raw + ((int64_t)(p.rows - 1) * p.Hkv + kvh) * kDh)[tid & 15];
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {  // 48 columns x 16 units of 8 elements, 2 units per thread
+      const int unit = tid + it * kSoftThreads;
+      const int c = unit >> 4, u16 = unit & 15;
+      if (c < ncols) {
+        const int qg = q0 + (c >> gshift);
+        const int h = kvh * p.G + (c & (p.G - 1));
+        const float4* src = reinterpret_cast<const float4*>(p.q + ((int64_t)qg * p.Hq + h) * kDh + u16 * 8);
+        xa[it] = src[0];
+        xb[it] = src[1];
+      } else {
+        xa[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+        xb[it] = xa[it];
+      }
+    }
+  } else if (warp == kWarpUnion) {
+    stage_index_rows(p, m, q0, nqc, lane);
+  } else if (warp == kWarpQk && lane == 0) {
+    tma_prefetch(&p.tm_k);
+    tma_prefetch(&p.tm_v);
+    tma_prefetch(&p.tm_tk);
+    tma_prefetch(&p.tm_tv);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = m.tmem_base;
+  if (trace && tid == 0) p.trace[cta_id * 64 + 0] = globaltimer();
+
   if (warp < kSoftWarps) {
     const int qd = warp & 3, ck = warp >> 2;  // TMEM lane quadrant, column chunk
     const int c0 = 16 * ck;
     const bool active = ck < nch;             // this warp's columns hold queries
     const uint32_t lanebase = tmem + ((uint32_t)(qd * 32) << 16);
-    // =================== setup: q (hi/lo bf16) and the reference logits ===================
+    // =================== setup: Q^T (hi rows, then lo rows) and the reference logits ===================
     {
-      const uint4* kref = reinterpret_cast<const uint4*>(
-          p.k_raw + ((int64_t)(p.rows - 1) * p.Hkv + kvh) * kDh);
-      float4 xa[2], xb[2];
-      const uint4 kr = kref[tid & 15];
-#pragma unroll
-      for (int it = 0; it < 2; ++it) {  // 64 rows x 16 units of 8 elements, 2 units per thread
-        const int unit = tid + it * kSoftThreads;
-        const int c = unit >> 4, u16 = unit & 15;
-        if (c < ncols) {
-          const int qg = q0 + (c >> gshift);
-          const int h = kvh * p.G + (c & (p.G - 1));
-          const float4* src = reinterpret_cast<const float4*>(p.q + ((int64_t)qg * p.Hq + h) * kDh + u16 * 8);
-          xa[it] = src[0];
-          xb[it] = src[1];
-        } else {
-          xa[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-          xb[it] = xa[it];
-        }
-      }
       if (tid < nqc) {
         m.qbound[tid] = p.qbound[q0 + tid];
         m.qwlo[tid] = p.qwlo[q0 + tid];
@@ -418,9 +485,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int off = 8; off >= 1; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
         if (u16 == 0) m.mref[c] = dot;
-        const uint32_t off = (u16 >> 3) * 8192 + sw128_off(c, u16 & 7);
-        *reinterpret_cast<uint4*>(smem + kOffQ + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(smem + kOffQ + 16384 + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        uint8_t* half = smem + kOffQ + (u16 >> 3) * kQHalf;
+        if (c < nqk) {
+          *reinterpret_cast<uint4*>(half + sw128_off(c, u16 & 7)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(half + sw128_off(nqk + c, u16 & 7)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
       }
       if (trace && tid == 0) p.trace[cta_id * 64 + 61] = globaltimer();
       fence_proxy_async_smem();
@@ -436,10 +505,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nqa = p.G < 16 ? (16 >> gshift) : 1;       // queries in this chunk
     const uint32_t qmask_w = (gw == 32) ? 0xFFFFFFFFu : ((1u << gw) - 1u);
     const uint32_t colvalid = ncols - c0 >= 16 ? 0xFFFFu : (ncols > c0 ? ((1u << (ncols - c0)) - 1u) : 0u);
-    const int bar_chunk = 3 + ck;                        // named barrier of this chunk's 4 warps
+    const int bar_chunk = kBarChunk0 + ck;               // named barrier of this chunk's 4 warps
     bool union_seen = false;
     int T = 0x7fffffff;
     int J0 = 0;  // tiles of earlier passes (mbarrier phase base)
+    float lacc[3];  // row sums of this warp's quadrant: lanes 2c, 2c+1 hold column c0 + c
 #pragma unroll 1
     for (int pass = 0; pass < 2; ++pass) {
       const bool robust = pass > 0;
@@ -447,25 +517,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(kBarRedo, kThreads);  // every role has seen the redo decision
         if (tid == 0) m.flag = 0;
       }
-      named_bar_sync(1, kSoftThreads);  // every column's mref is written
+      named_bar_sync(kBarSoft, kSoftThreads);  // every column's mref is written
       // running max / threshold: fast = fixed reference, robust = -inf (lazy raise)
       for (int i = tid; i < 3 * kCols; i += kSoftThreads) {
         const float r = m.mref[i % kCols];
         (&m.m2[0][0])[i] = robust ? -INFINITY : r;
         (&m.thr[0][0])[i] = robust ? -INFINITY : r + kFastHi;
       }
-      {  // zero the O and row-sum accumulators of this warp's lanes / columns
+      {  // zero the O accumulators (hi and lo columns) of this warp's lanes / columns
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
+        if (active) {
 #pragma unroll
-        for (int br = 0; br < 3; ++br) {
-          tmem_st16(lanebase + kTmemO + 64 * br + c0, z);
-          tmem_st16(lanebase + kTmemL + 64 * br + c0, z);
+          for (int br = 0; br < 3; ++br) {
+            tmem_st16(lanebase + kTmemO + kTmemStride * br + c0, z);
+            tmem_st16(lanebase + kTmemO + kTmemStride * br + nqk + c0, z);
+          }
         }
         tmem_wait_st();
       }
-      named_bar_sync(1, kSoftThreads);
+#pragma unroll
+      for (int br = 0; br < 3; ++br) lacc[br] = 0.f;
+      named_bar_sync(kBarSoft, kSoftThreads);
       bool ovf = false;       // fast pass: an active logit above mref + kFastHi
       uint32_t act_ab = 0u;   // fast pass: active columns, cmp (bits 0-15) / slc (16-31)
       uint32_t act_w = 0u;    //            and win (bits 0-15), of this lane
@@ -516,17 +590,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         cm_b &= colvalid;
         if (!ti.act_a) cm_a = 0u;
         if (!ti.act_b) cm_b = 0u;
-        // S^T rows of this quadrant, this warp's 16 columns (log2 units)
+        // S^T rows of this quadrant, this warp's 16 columns (log2 units): hi + lo halves
         float s[16];
         mbar_sleep_wait(&m.s_full[sb], (J >> 1) & 1);
         if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 24 + j] = globaltimer();
         tc_fence_after();
         {
-          uint32_t r[16];
-          tmem_ld16(lanebase + kTmemS + 64 * sb + c0, r);
+          uint32_t rh[16], rl[16];
+          const uint32_t sa = lanebase + kTmemS + kTmemStride * sb + c0;
+          tmem_ld16(sa, rh);
+          tmem_ld16(sa + nqk, rl);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) s[e] = __uint_as_float(r[e]);
+          for (int e = 0; e < 16; ++e) s[e] = __uint_as_float(rh[e]) + __uint_as_float(rl[e]);
         }
         tc_fence_before();
         __syncwarp();
@@ -554,13 +630,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           act_w |= cm_b;
           if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
           if (ti.act_a)
-            write_p(smem + kOffK + sb * kStageBytes, row, ck, cm_a, pe,
-                    lanebase + kTmemL + 64 * (ti.kind == kTileCmp ? kCmp : kSlc) + c0);
+            write_p(smem + kOffK + sb * kStageBytes, row, c0, nqk, cm_a, pe,
+                    lacc[ti.kind == kTileCmp ? kCmp : kSlc], lane);
           if (ti.act_b) {
             // the shared branch-B P region is rewritten only after the previous
             // tile's MMAs read it (branch-A P lives in this tile's own K stage)
             if (j > 0 && prev_b) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
-            write_p(smem + kOffPB, row, ck, cm_b, pe, lanebase + kTmemL + 64 * kWin + c0);
+            write_p(smem + kOffPB, row, c0, nqk, cm_b, pe, lacc[kWin], lane);
           }
         } else {
           // ---- robust pass: lazy running max per active branch; the 4 warps
@@ -584,8 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             float v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = ((cm >> e) & 1u) ? s[e] : -INFINITY;
-            const float mx = reduce16<true>(v, lane);
-            if ((lane & 1) == 0) m.tmax[qd][c0 + (lane >> 1)] = mx;
+            const float mxv = reduce16<true>(v, lane);
+            if ((lane & 1) == 0) m.tmax[qd][c0 + (lane >> 1)] = mxv;
             named_bar_sync(bar_chunk, 128);
             if (qd == 0 && lane < 16) {
               const int c = c0 + lane;
@@ -597,27 +673,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               m.thr[br][c] = nw + kRescaleThresh;
             }
             named_bar_sync(bar_chunk, 128);
-            // O^T (and the row-sum accumulator) of this chunk *= alpha, once the
-            // previous tile's MMAs into them are complete
+            // O^T (hi and lo columns) and the row sums of this chunk *= alpha,
+            // once the previous tile's MMAs into them are complete
             if (j > 0) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
             tc_fence_after();
             float al[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) al[e] = m.alpha[c0 + e];
-            const uint32_t ta = lanebase + kTmemO + 64 * br + c0;
-            uint32_t r[16];
-            tmem_ld16(ta, r);
-            tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
-            tmem_st16(ta, r);
-            const uint32_t tl = lanebase + kTmemL + 64 * br + c0;  // per-lane row sums
-            tmem_ld16(tl, r);
-            tmem_wait_ld();
+            for (int hl = 0; hl < 2; ++hl) {
+              const uint32_t ta = lanebase + kTmemO + kTmemStride * br + (hl ? nqk : 0) + c0;
+              uint32_t r[16];
+              tmem_ld16(ta, r);
+              tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
-            tmem_st16(tl, r);
+              for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * al[e]);
+              tmem_st16(ta, r);
+            }
             tmem_wait_st();
+            lacc[br] *= m.alpha[c0 + (lane >> 1)];
             named_bar_sync(bar_chunk, 128);  // alpha is reused by the other side
           }
           if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
@@ -629,11 +703,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             float pe[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) pe[e] = fast_exp2(s[e] - m.m2[br][c0 + e]);
-            write_p(side == 0 ? smem + kOffK + sb * kStageBytes : smem + kOffPB, row, ck,
-                    side == 0 ? cm_a : cm_b, pe, lanebase + kTmemL + 64 * br + c0);
+            write_p(side == 0 ? smem + kOffK + sb * kStageBytes : smem + kOffPB, row, c0, nqk,
+                    side == 0 ? cm_a : cm_b, pe, lacc[br], lane);
           }
         }
-        tmem_wait_st();
         prev_b = ti.act_b;
         fence_proxy_async_smem();
         tc_fence_before();
@@ -643,19 +716,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 2] = globaltimer();
       // ---- end of pass: branch row sums, then the fast-pass check ----
-      if (active && T > 0) mbar_sleep_wait(&m.pv_done[(J0 + T - 1) & 1], ((J0 + T - 1) >> 1) & 1);
-      if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 7] = globaltimer();
-      tc_fence_after();
-#pragma unroll 1
-      for (int br = 0; br < 3; ++br) {
-        uint32_t r[16];
-        tmem_ld16(lanebase + kTmemL + 64 * br + c0, r);
-        tmem_wait_ld();
-        float v[16];
+      if ((lane & 1) == 0) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
-        const float sum = reduce16<false>(v, lane);
-        if ((lane & 1) == 0) m.lred[br][qd][c0 + (lane >> 1)] = sum;
+        for (int br = 0; br < 3; ++br) m.lred[br][qd][c0 + (lane >> 1)] = lacc[br];
       }
       if (!robust) {
         const uint32_t ab = __reduce_or_sync(0xffffffffu, act_ab);
@@ -666,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(&m.flag, 2);
       }
-      named_bar_sync(1, kSoftThreads);
+      named_bar_sync(kBarSoft, kSoftThreads);
       if (!robust && tid < 3 * kCols) {  // one (branch, column) per thread
         const int br = tid / kCols, c = tid % kCols, ckc = c >> 4;
         const int bit = (br == kWin ? 0 : 16 * br) + (c & 15);
@@ -676,12 +739,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float L = m.lred[br][0][c] + m.lred[br][1][c] + m.lred[br][2][c] + m.lred[br][3][c];
         if (((a >> bit) & 1u) && !(L >= 0x1p-48f && L < 0x1p+100f)) atomicOr(&m.flag, 4);
       }
+      // the O accumulators are final once the last PV of the pass completed
+      if (active && T > 0) mbar_sleep_wait(&m.pv_done[(J0 + T - 1) & 1], ((J0 + T - 1) >> 1) & 1);
+      if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 7] = globaltimer();
       named_bar_sync(kBarPassEnd, kThreads);  // pass end: the redo decision is visible to every role
       if (trace && tid == 0) p.trace[cta_id * 64 + 62 + pass] = (unsigned long long)m.flag;
       if (!m.flag) break;
       J0 += T;
     }
-    // ---- epilogue: partial (m, l, O) of this split -> workspace ----
+    // ---- epilogue: partial (m, l, O = O_hi + O_lo) of this split -> workspace ----
+    tc_fence_after();
     const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
     float* ws_ml = p.ws + unit * (3 * kCols * 2);
     float* ws_o = p.ws + p.ws_o_offset + unit * (3 * kCols * kDh);
@@ -693,87 +760,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (active) {
 #pragma unroll 1
       for (int br = 0; br < 3; ++br) {
-        uint32_t r[16];
-        tmem_ld16(lanebase + kTmemO + 64 * br + c0, r);
+        uint32_t rh[16], rl[16];
+        const uint32_t ta = lanebase + kTmemO + kTmemStride * br + c0;
+        tmem_ld16(ta, rh);
+        tmem_ld16(ta + nqk, rl);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          if (c0 + e < ncols) ws_o[((int64_t)br * kCols + c0 + e) * kDh + row] = __uint_as_float(r[e]);
+          if (c0 + e < ncols)
+            ws_o[((int64_t)br * kCols + c0 + e) * kDh + row] = __uint_as_float(rh[e]) + __uint_as_float(rl[e]);
       }
     }
     if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
   } else if (warp == kWarpTma) {
-    // =================== TMA producer (+ the union build) ===================
-    auto tile_rows = [&](int t, const CUtensorMap*& tk, const CUtensorMap*& tv, int& r0, int& r1) {
-      if (t < n_cmp) {
-        tk = &p.tm_ck; tv = &p.tm_cv;
-        r0 = t * kTile; r1 = r0 + 64;
-      } else if (t < n_cmp + m.n_tok_tiles) {
-        tk = &p.tm_k; tv = &p.tm_v;
-        const int u0 = 2 * (t - n_cmp);
-        r0 = m.union_blk[u0] * p.l_sel;
-        r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
-      } else {
-        tk = &p.tm_tk; tv = &p.tm_tv;
-        r0 = 0; r1 = 64;
-      }
-    };
-    // stream this CTA's tiles into L2 ahead of the two smem stages: the
-    // stage loads below then hit L2 instead of paying HBM latency per tile
-    auto prefetch_tile = [&](int t) {
-      const CUtensorMap *tk, *tv;
-      int r0, r1;
-      tile_rows(t, tk, tv, r0, r1);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tma_prefetch_3d(tk, c * 64, kvh, r0);
-        tma_prefetch_3d(tk, c * 64, kvh, r1);
-        tma_prefetch_3d(tv, c * 64, kvh, r0);
-        tma_prefetch_3d(tv, c * 64, kvh, r1);
-      }
-    };
-    auto issue = [&](int t, int J) {
-      const int st = J & 1;
-      if (J >= 2) mbar_sleep_wait(&m.kv_empty[st], ((J >> 1) + 1) & 1);
-      uint8_t* kdst = smem + kOffK + st * kStageBytes;
-      uint8_t* vdst = smem + kOffV + st * kStageBytes;
-      if (trace && J < 8) p.trace[cta_id * 64 + 8 + J] = globaltimer();
-      mbar_expect_tx(&m.k_full[st], kStageBytes);
-      mbar_expect_tx(&m.v_full[st], kStageBytes);
-      const CUtensorMap *tk, *tv;
-      int r0, r1;
-      tile_rows(t, tk, tv, r0, r1);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
-        tma_load_3d(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st]);
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st]);
-        tma_load_3d(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st]);
-      }
-    };
-    // pass 0: the first compressed stages go out before the union is built
-    int pre = 0;
+    // =================== TMA producer ===================
+    // the first compressed stages went out in the prologue; token tiles wait
+    // for the union warp
+    int T = 0x7fffffff;
     if (lane == 0) {
-      while (pre < 2 && split + pre * S < n_cmp) {
-        issue(split + pre * S, pre);
-        ++pre;
+      for (int j = pre;; ++j) {
+        if (T == 0x7fffffff && split + j * S >= n_cmp) {
+          mbar_sleep_wait(&m.union_ready, 0);
+          T = tile_count();
+        }
+        if (j >= T) break;
+        issue(split + j * S, j);
       }
-      for (int t = split + 2 * S; t < n_cmp; t += S) prefetch_tile(t);
     }
-    if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
-    build_union_warp(p, m, q0, nqc, lane, cwlo, cwhi, trace ? p.trace + cta_id * 64 : nullptr);
-    mbar_arrive(&m.union_ready);  // every lane: releases its own union writes
-    if (trace && lane == 0) p.trace[cta_id * 64 + 1] = globaltimer();
-    const int T = tile_count();
-    if (lane == 0) {
-      for (int j = max(pre, 2); j < T; ++j)
-        if (split + j * S >= n_cmp) prefetch_tile(split + j * S);
-      if (trace) p.trace[cta_id * 64 + 60] = globaltimer();
-      for (int j = pre; j < T; ++j) issue(split + j * S, j);
-    }
+    T = __shfl_sync(0xffffffffu, T, 0);
     __syncwarp();
     named_bar_sync(kBarPassEnd, kThreads);
     if (m.flag) {  // robust redo: the same tiles again
@@ -783,8 +797,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       named_bar_sync(kBarPassEnd, kThreads);
     }
-  } else {
-    // =================== MMA issuers: warp 17 = QK^T, warp 18 = PV ===================
+  } else if (warp != kWarpUnion) {
+    // =================== MMA issuers: QK^T warp and PV warp ===================
     // (two issuing threads so a QK waiting for its K tile never delays the PV
     // of the previous tile; each commit tracks only its own thread's MMAs)
     bool union_seen = false;
@@ -797,8 +811,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return j < T;
     };
+    // one MMA per 16-element K step, hi and lo stacked along N
+    const uint32_t idesc_qk = idesc_bf16(128, 2 * nqk, 0, 0);
+    const uint32_t idesc_pv = idesc_bf16(128, 2 * nqk, 1, 1);
     auto qk_pass = [&](int J0) {
-      const uint32_t idesc_qk = idesc_bf16(128, nqk, 0, 0);
       for (int j = 0; tiles(j); ++j) {
         const int J = J0 + j;
         const int sb = J & 1;
@@ -808,22 +824,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t kaddr = sbase + kOffK + sb * kStageBytes;
         const uint32_t qaddr = sbase + kOffQ;
-        const uint32_t d = tmem + kTmemS + 64 * sb;
+        const uint32_t d = tmem + kTmemS + kTmemStride * sb;
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {  // q hi, q lo
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
-            const uint32_t qoff = part * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32;
-            umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
-                     idesc_qk, (part | kk) != 0);
-          }
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t qoff = (kk >> 2) * kQHalf + (kk & 3) * 32;
+          umma_f16(d, desc_sw128(kaddr + koff, 16, 1024), desc_sw128(qaddr + qoff, 16, 1024),
+                   idesc_qk, kk != 0);
         }
         umma_commit(&m.s_full[sb]);
       }
     };
     auto pv_pass = [&](int J0) {
-      const uint32_t idesc_pv = idesc_bf16(128, nqk, 1, 1);
       for (int j = 0; tiles(j); ++j) {
         const int J = J0 + j;
         const int st = J & 1;
@@ -838,29 +850,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
           const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
           const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
-          const uint32_t d = tmem + kTmemO + 64 * br;
+          const uint32_t d = tmem + kTmemO + kTmemStride * br;
 #pragma unroll
-          for (int part = 0; part < 2; ++part)
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint64_t bdesc = desc_sw128(pa + part * 16384 + kk * 2048, 16384, 1024);
-              umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024), bdesc, idesc_pv, 1u);
-            }
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
+                     desc_sw128(pa + kk * 2048, 16384, 1024), idesc_pv, 1u);
         }
         umma_commit(&m.pv_done[J & 1]);
         umma_commit(&m.kv_empty[st]);
       }
     };
     if (lane == 0) {
-      if (warp == kWarpTma + 1) {
-        tma_prefetch(&p.tm_k);
-        tma_prefetch(&p.tm_v);
-        tma_prefetch(&p.tm_tk);
-        tma_prefetch(&p.tm_tv);
-      }
       mbar_sleep_wait(&m.q_ready, 0);
       tc_fence_after();
-      if (warp == kWarpTma + 1) qk_pass(0); else pv_pass(0);
+      if (warp == kWarpQk) qk_pass(0); else pv_pass(0);
     }
     __syncwarp();
     named_bar_sync(kBarPassEnd, kThreads);
@@ -868,9 +871,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(kBarRedo, kThreads);
       if (lane == 0) {
         tc_fence_after();
-        if (warp == kWarpTma + 1) qk_pass(T); else pv_pass(T);
+        if (warp == kWarpQk) qk_pass(T); else pv_pass(T);
       }
       __syncwarp();
+      named_bar_sync(kBarPassEnd, kThreads);
+    }
+  } else {
+    // =================== union warp: block union, then L2 prefetch ===================
+    // L2 prefetch of this CTA's tiles beyond the two smem stages (LSU
+    // prefetches: they do not occupy the TMA unit the stage loads use)
+    auto prefetch_tile = [&](int t) {
+      const uint16_t *bk, *bv;
+      int r0, r1, lim;
+      if (t < n_cmp) {
+        bk = p.ck_raw; bv = p.cv_raw; r0 = t * kTile; r1 = r0 + 64; lim = p.blocks - 1;
+      } else {
+        const int u0 = 2 * (t - n_cmp);
+        bk = p.k_raw; bv = p.v_raw; lim = p.rows - 1;
+        r0 = m.union_blk[u0] * p.l_sel;
+        r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
+      }
+#pragma unroll 4
+      for (int i = lane; i < 256; i += 32) {  // 128 rows x 2 lines of 128 B, K and V
+        const int rr = i >> 1;
+        const int r = min(rr < 64 ? r0 + rr : r1 + rr - 64, lim);
+        const int64_t off = ((int64_t)r * p.Hkv + kvh) * kDh + (i & 1) * 64;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(bk + off));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(bv + off));
+      }
+    };
+    for (int j = 2; split + j * S < n_cmp; ++j) prefetch_tile(split + j * S);
+    if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
+    build_union_warp(p, m, q0, nqc, lane, cwlo, cwhi, trace ? p.trace + cta_id * 64 : nullptr);
+    mbar_arrive(&m.union_ready);  // every lane: releases its own union writes
+    if (trace && lane == 0) p.trace[cta_id * 64 + 1] = globaltimer();
+    const int T = tile_count();
+    const int n_tok_end = n_cmp + m.n_tok_tiles;
+    for (int j = 2; j < T; ++j)
+      if (split + j * S >= n_cmp && split + j * S < n_tok_end) prefetch_tile(split + j * S);
+    if (trace && lane == 0) p.trace[cta_id * 64 + 60] = globaltimer();
+    named_bar_sync(kBarPassEnd, kThreads);
+    if (m.flag) {
+      named_bar_sync(kBarRedo, kThreads);
       named_bar_sync(kBarPassEnd, kThreads);
     }
   }
@@ -887,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < kSoftWarps) {
     const int64_t unit0 = ((int64_t)chunk * p.Hkv + kvh) * S;
     const int dh = tid & (kDh - 1);
-    for (int c = split + (tid >> 7) * S; c < ncols; c += 4 * S) {
+    for (int c = split + (tid >> 7) * S; c < ncols; c += (kSoftThreads / kDh) * S) {
       const int qg = q0 + (c >> gshift);
       const int h = kvh * p.G + (c & (p.G - 1));
       const float* gate = p.gates + ((int64_t)qg * p.Hq + h) * 3;
