@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libspecsv_b200.so")
+# SPECSV_LIB: diagnostics only (A/B timing of build variants); the default is the in-tree build
+LIB_PATH = os.environ.get("SPECSV_LIB") or os.path.join(PKG, "lib", "libspecsv_b200.so")
 
 OK, EINVAL, ESTATE, EUNSUPPORTED, ECUDA, ENOSPACE = range(6)
 MODE_EXACT, MODE_APPROX = 0, 1

@@ -107,7 +107,7 @@ int splits_for(const specsv_nsa_config& c, int32_t nq) {
 
 struct Layout {
   size_t attend_off = 0, attend_bytes = 0;
-  size_t E_off = 0, TM_off = 0, TD_off = 0, part_off = 0, sel_off = 0, cnt_off = 0;
+  size_t E_off = 0, TM_off = 0, TD_off = 0, F_off = 0, sel_off = 0, cnt_off = 0;
   int64_t sel_pad = 0;
   size_t total = 0;
 };
@@ -139,13 +139,11 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
   L.TD_off = off;
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
-  L.part_off = off;  // per-KV-head score shares [nq][Hkv][ntiles][gs]
-  off = align_up(off + (size_t)nq * c.n_kv_heads * ntiles * gs * 8, 256);
   L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
-  L.sel_off = off;
-  off = align_up(off + (size_t)nq * L.sel_pad * 8, 256);
-  L.cnt_off = off;  // routing barrier words, zero-filled with the workspace, self-resetting
-  off = align_up(off + 4 * sizeof(int32_t), 256);
+  L.F_off = off;  // per-KV-head score shares [nq][Hkv][sel_pad]
+  off = align_up(off + (size_t)nq * c.n_kv_heads * L.sel_pad * 8, 256);
+  L.cnt_off = off;  // routing barrier words + per-slot unit counters, zero-filled, self-resetting
+  off = align_up(off + (4 + kMaxQueries) * sizeof(int32_t), 256);
   L.total = off;
   return L;
 }
@@ -193,7 +191,6 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
   std::memset(&p, 0, sizeof(p));
   p.q = a.q;
   p.ck = kv.ck;
-  if (const char* dbg = std::getenv("SPECSV_ROUTE_DEBUG")) p.debug_flags = std::atoi(dbg);
   p.trace = g_trace;
   p.idx = a.idx;
   p.idx_count = a.idx_count;
@@ -229,10 +226,10 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
   p.g_stride = (int32_t)(((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 1);
   p.TM = reinterpret_cast<double*>(ws + L.TM_off);
   p.TD = reinterpret_cast<double*>(ws + L.TD_off);
-  p.part = reinterpret_cast<double*>(ws + L.part_off);
-  p.sel = reinterpret_cast<double*>(ws + L.sel_off);
+  p.part = reinterpret_cast<double*>(ws + L.F_off);
   p.sel_pad = (int32_t)L.sel_pad;
   p.counters = reinterpret_cast<int32_t*>(ws + L.cnt_off);
+  p.slot_done = p.counters + 4;
   return p;
 }
 

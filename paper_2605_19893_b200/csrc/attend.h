@@ -56,9 +56,7 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
 int attend_max_coresident();
 
 // ---- routing (route.cu) -------------------------------------------------------
-constexpr int kRouteTile = 64;      // compressed blocks per R1 CTA
-constexpr int kRouteRows = 16;      // smallest routing row chunk (2 MMA row tiles)
-constexpr int kRouteSpan = 4;       // selection blocks 8 consecutive compressed blocks may touch
+constexpr int kRouteTile = 16;      // compressed blocks per routing statistics tile
 constexpr int kMaxAvail = 8192;     // selection blocks per query for the Top-n CTA
 
 struct RouteParams {
@@ -67,14 +65,12 @@ struct RouteParams {
   double* gsh;           // [nr][ntiles][Hq][g_stride] per-tile selection-block shares
   int32_t g_stride;      // selection blocks one 64-block tile touches
   double* TM;            // [nr][Hq][ntiles] tile max
-  double* TD;            // [nr][Hq][ntiles] tile denominators, then per-tile factors
-  int32_t* counters;     // [3] barrier words; zero-initialised, self-resetting
-  double* part;          // [nr][Hkv][ntiles][g_stride] per-KV-head score shares
-  int32_t chunk_rows;    // (slot, head) rows per row chunk, a multiple of G (set at launch)
-  int32_t shares_rows;   // rows whose tile statistics are staged in smem at once (set at launch)
-  int32_t tail_stage;    // doubles of shares the tail stages per round (set at launch)
-  double* sel;           // [nr][sel_pad] selection-block scores
+  double* TD;            // [nr][Hq][ntiles] tile denominators
+  double* part;          // [nr][Hkv][sel_pad] per-KV-head score shares
   int32_t sel_pad;
+  int32_t* counters;     // [3] barrier words; zero-initialised, self-resetting
+  int32_t* slot_done;    // [nr] finished units per slot; zero-initialised, self-resetting
+  int32_t chunk_rows;    // (slot, head) rows per row chunk, a multiple of G (set at launch)
   int32_t* idx;          // [nq][n]
   int32_t* idx_count;    // [nq]
   uint32_t* idx_forced;  // [nq]
@@ -88,7 +84,6 @@ struct RouteParams {
   int32_t slot_avail[kMaxQueries]; // selection blocks available
   int32_t unrouted[kMaxQueries];   // queries that get count = -1
   int32_t n_unrouted;
-  int32_t debug_flags;  // diagnostics only (SPECSV_ROUTE_DEBUG): skip R1 phases, breaks parity
   unsigned long long* trace;  // diagnostics only: per-CTA phase stamps at kRouteTraceBase
 };
 constexpr int kRouteTraceBase = 196608;  // route stamps: trace[kRouteTraceBase + cta * 16 + k]

@@ -7,6 +7,7 @@
 //   representative       src/group_attend.cpp:112-119
 //   load_stats           src/group_attend.cpp:87-139 + engine.cpp:272-275
 #include "policy.h"
+#include "attend.h"
 
 #include <algorithm>
 #include <cstring>
@@ -41,8 +42,10 @@ void check_build_limits(const specsv_nsa_config& c) {
   if (c.n_q_heads > 128) unsup("n_q_heads must be <= 128");
   if (c.w / c.l_sel + 2 + c.n > 1280) unsup("w / l_sel + n must be <= 1278 (per-chunk block union)");
   if ((c.l - 1) / c.d > 7) unsup("l must be <= 8 * d (routing halo)");
-  if ((63 + 7 * c.d + c.l - 1) / c.l_sel + 1 > 4)
-    unsup("7 d + l must be <= 194 (selection blocks per 8 compressed blocks)");
+  if ((kRouteTile * c.d) % c.l_sel != 0)
+    unsup("d must be a multiple of 4 (16-block routing tiles start on selection-block boundaries)");
+  if (((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 2 > 8)
+    unsup("15 d + l must be <= 448 (selection blocks one 16-block routing tile touches)");
 }
 
 int64_t routing_visible_len(const specsv_nsa_config& c, int64_t pos) {

@@ -4,20 +4,26 @@
 // Replaces nsa::selection_scores + nsa::select_blocks
 // (src/nsa_attention.cpp:38-136) for every query that constructs indices.
 //
-// One cooperative persistent kernel (one 512-thread CTA per SM), two phases
+// One cooperative persistent kernel (one 320-thread CTA per SM), two phases
 // and a single grid-wide arrival barrier:
-//  1. tiles (all CTAs): per (routed query, head, compressed block i) logit =
-//     dot(q_h, ck_i) / sqrt(dh) in fp64 on the FP64 tensor pipe (DMMA
-//     m8n8k4; fp32 x fp32 products are exact in fp64).  Per 64-block tile t
-//     and row: TM = max logit, TD = sum e^(logit - TM), and for every
-//     selection block b the tile touches G[t][b] = sum_i overlap(i, b) *
-//     e^(logit_i - TM) -- the tile's share of b's score before the softmax
-//     normalisation is known, so no per-block probabilities reach HBM.
-//  2. tail (one CTA per routed query): per head M = max_t TM, DEN = sum_t TD
-//     e^(TM - M), F_t = e^(TM_t - M) / DEN; score_b = sum_t sum_h (ascending)
-//     F_ht G_ht[b] / (Hq l)  (= the reference's sum over blocks and heads of
-//     p_hi * overlap / l, nsa_attention.cpp:52-78, regrouped -- contract P3);
-//     then Top-n: forced {0, avail-2, avail-1} plus the best remaining by
+//  1. tiles (all CTAs).  Work item = (KV head, <= 40 (query, head) rows, 2
+//     key tiles of 64 compressed blocks).  Warp (m, t) owns 8 rows x tile t:
+//     logit = dot(q_h, ck_i) / sqrt(dh) in fp64 on the FP64 tensor pipe (DMMA
+//     m8n8k4; fp32 x fp32 products are exact in fp64).  The key rows are
+//     permuted in shared memory so that lane column c of the MMA fragment
+//     holds the 16 consecutive blocks [16c, 16c + 16): the whole per-row
+//     epilogue stays inside the warp (no cross-warp reductions).  Per row and
+//     tile it writes TM = max logit and, through a second small DMMA against
+//     the tile-invariant overlap matrix W[block][selection block] (plus a
+//     ones column), TD = sum e^(logit - TM) and G[b] = sum_i overlap(i, b)
+//     e^(logit_i - TM): the tile's share of selection block b before the
+//     softmax normalisation is known, so no per-block probability reaches HBM.
+//  2. units (one CTA per (routed query, KV head)): per head M = max_t TM,
+//     DEN = sum_t TD e^(TM - M), F_t = e^(TM_t - M) / DEN and the KV head's
+//     share of every selection-block score; the query's last unit sums the
+//     shares, score_b = sum_kvh sum_t sum_g F G / (Hq l)  (= the reference's
+//     sum over blocks and heads of p_hi * overlap / l, nsa_attention.cpp:52-78,
+//     regrouped -- contract P3), then Top-n: forced {0, avail-2, avail-1} plus the best remaining by
 //     (score desc, id asc), written ascending (nsa_attention.cpp:94-136).
 #include <cuda_runtime.h>
 
@@ -30,28 +36,41 @@
 namespace specsv_b200 {
 namespace {
 
-constexpr int kR1Threads = 512;  // two groups of 8 warps; warp w of a group owns the
-                                 // compressed blocks [8w, 8w + 8) of that group's tile
-constexpr int kR1GroupThreads = kR1Threads / 2;
-constexpr int kDhRoute = 128;    // d_head of this build (host-checked)
-constexpr int kQld = kDhRoute + 4;   // q row stride, doubles (1056 B: conflict-light A loads)
-constexpr int kCkld = kDhRoute + 4;  // key row stride, floats (528 B: conflict-free B loads)
-constexpr int kW = kRouteSpan;       // selection blocks one warp's 8 compressed blocks touch
+constexpr int kMT = 5;                    // 8-row m-tiles per row chunk (40 rows)
+constexpr int kTB = kRouteTile;           // compressed blocks per statistics tile (16)
+constexpr int kSuper = 128;               // compressed blocks per work item (staged at once)
+constexpr int kTilesPerItem = kSuper / kTB;
+constexpr int kRouteThreads = 32 * kTilesPerItem;  // one warp per 16-block tile, all 40 rows
+constexpr int kDhRoute = 128;             // d_head of this build (host-checked)
+constexpr int kLd = kDhRoute + 4;         // fp64 row stride (== 4 mod 16: conflict-free fragment loads)
+constexpr int kWLd = 12;                  // overlap-matrix row stride, doubles (== 4 mod 8)
+constexpr int kWCols = 8;                 // overlap matrix columns: g_stride + the ones column <= 8
 constexpr size_t kTopnSmem = (size_t)kMaxAvail * 8 + (size_t)kMaxAvail * 4;
+constexpr size_t kUnitSmem = 150 * 1024;  // phase-2 staging (see slot_unit)
+constexpr size_t kTailSmem = kTopnSmem;
+static_assert(kTB == 16, "lane column c of the MMA fragment owns blocks 4c .. 4c + 3");
 
+#ifndef ROUTE_UNROLL
+#define ROUTE_UNROLL 4
+#endif
+constexpr int kRouteUnroll = ROUTE_UNROLL;  // k steps of the logit loop unrolled (A/B builds)
+
+struct TileSmem {
+  static constexpr size_t q = 0;                                  // [40][kLd] f64
+  static constexpr size_t ck = q + (size_t)8 * kMT * kLd * 8;     // [kSuper][kLd] f64 (permuted rows)
+  static constexpr size_t w = ck + (size_t)kSuper * kLd * 8;      // [16][kWLd] f64 (K-chunk-major)
+  static constexpr size_t bytes = w + (size_t)kTB * kWLd * 8;
+  static_assert(bytes <= 227 * 1024, "tile-phase shared memory");
+};
+
+// (not volatile: a pure function of its operands, so the compiler may hoist the
+// next k step's fragment loads above it)
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void tstamp_any(unsigned long long* tr, int k) {
-  if (tr != nullptr) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    tr[k] = t;
-  }
-}
 __device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
   if (tr != nullptr && threadIdx.x == 0) {
     unsigned long long t;
@@ -60,230 +79,211 @@ __device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
   }
 }
 
+// e^x for x <= 0 (x = logit - tile max), ~2 ulp: x = n ln2 + r, |r| <= ln2/2,
+// Taylor to degree 12 (truncation < 2e-16 relative), scaled by 2^n through the
+// exponent bits.  x < -708 (including -inf) flushes to 0.
+__device__ __forceinline__ double exp_nonpos(double x) {
+  if (!(x >= -708.0)) return 0.0;
+  const double n = rint(x * 1.4426950408889634);
+  double r = fma(n, -6.93147180369123816490e-01, x);
+  r = fma(n, -1.90821492927058770002e-10, r);
+  double p = 2.08767569878680989792e-09;  // 1/12!
+  p = fma(p, r, 2.50521083854417187751e-08);
+  p = fma(p, r, 2.75573192239858906526e-07);
+  p = fma(p, r, 2.75573192239858906526e-06);
+  p = fma(p, r, 2.48015873015873015873e-05);
+  p = fma(p, r, 1.98412698412698412698e-04);
+  p = fma(p, r, 1.38888888888888888889e-03);
+  p = fma(p, r, 8.33333333333333333333e-03);
+  p = fma(p, r, 4.16666666666666666667e-02);
+  p = fma(p, r, 1.66666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  return __hiloint2double(__double2hiint(p) + (static_cast<int>(n) << 20), __double2loint(p));
+}
+
 // tokens shared by compressed block i ([i d, i d + l)) and selection block b
 __device__ __forceinline__ int overlap(int i, int b, int d, int l, int l_sel) {
   const int lo = max(i * d, b * l_sel), hi = min(i * d + l, (b + 1) * l_sel);
   return hi > lo ? hi - lo : 0;
 }
 
-// dynamic shared memory of phase 1 (MT row tiles)
-template <int MT>
-struct TileSmem {
-  static constexpr int kRows = 8 * MT;
-  static constexpr size_t q = 0;                                            // [kRows][kQld] f64
-  static constexpr size_t ck = q + (size_t)kRows * kQld * 8;                // [2 grp][2 buf][64][kCkld] f32
-  static constexpr size_t red_m = ck + 4 * (size_t)kRouteTile * kCkld * 4;  // [2][kRows][8]
-  static constexpr size_t red_s = red_m + 2 * (size_t)kRows * 8 * 8;        // [2][kRows][8]
-  static constexpr size_t gpart = red_s + 2 * (size_t)kRows * 8 * 8;        // [2][kRows][8][kW]
-  static constexpr size_t bytes = gpart + 2 * (size_t)kRows * 8 * kW * 8;
-  static_assert(bytes <= 227 * 1024, "tile-phase shared memory");
+// shared-memory key row of tile-local block i (0..15): MMA n-tile nt, column
+// n holds block 4 (n / 2) + 2 nt + n % 2, so C-fragment lane column c covers
+// the consecutive blocks [4 c, 4 c + 4)
+__device__ __forceinline__ int perm_row(int i) {
+  return 8 * ((i >> 1) & 1) + 2 * (i >> 2) + (i & 1);
+}
+
+// Phase 1.  A work item is rows [r0, r0 + nrows) of KV head kvh x the 128
+// compressed blocks of super tile st (8 statistics tiles of 16 blocks; warp w
+// owns tile 8 st + w for all 40 rows: per k step 5 A + 2 B fragment loads
+// feed 10 DMMAs).  Keys and q are converted to fp64 once, while staging (a
+// conversion per fragment load would share the FP64 pipe with the DMMAs).
+// The next item's global loads are issued into registers before the current
+// item is multiplied, so they land meanwhile.
+constexpr int kStageUnits = kSuper * (kDhRoute / 4) + 8 * kMT * (kDhRoute / 4);  // float4s
+constexpr int kStagePer = (kStageUnits + kRouteThreads - 1) / kRouteThreads;
+
+struct Item {
+  int kvh, r0, nrows, st;
 };
 
-// Phase 1.  S[row][block] = q_row . ck_block in fp64 on the FP64 tensor pipe;
-// the 4-term partial sums are accumulated in the MMA's order, within a few
-// ulp of the reference's 4-lane order (contract P3).
-//
-// The CTA's two warp groups ping-pong over alternate 64-block tiles
-// (group-local named barriers), so one group's softmax epilogue overlaps the
-// other's MMAs on the shared FP64 pipe.  Each group keeps its next tile in
-// registers while the current one is multiplied.  Per-tile statistics go
-// through shared buffers guarded by a group barrier at the end of each tile.
-template <int MT>
-__device__ __forceinline__ void tiles_phase(const RouteParams& p, uint8_t* smem,
-                                            unsigned long long* trc) {
-  using L = TileSmem<MT>;
-  constexpr int kRows = L::kRows;
-  constexpr int dh = kDhRoute;
-  constexpr int qld = kQld, ckld = kCkld;
-  const int kvh = blockIdx.y;
+__device__ __forceinline__ Item item_of(const RouteParams& p, int it) {
   const int rows_total = p.nr * p.G;
-  const int r0 = blockIdx.z * p.chunk_rows;
-  const int nrows = min(p.chunk_rows, rows_total - r0);
-  const int nmt = (nrows + 7) >> 3;
-  double* qd = reinterpret_cast<double*>(smem + L::q);
-  float* ckbuf = reinterpret_cast<float*>(smem + L::ck);
-  const int tid = threadIdx.x;
-  const int grp = tid / kR1GroupThreads, gtid = tid % kR1GroupThreads;
-  const int warp = gtid >> 5, lane = tid & 31;
-  const int lr = lane >> 2, lc = lane & 3;  // fragment row / column within the 8x8 tile
-  const int vstride = 2 * gridDim.x;  // tiles of this group: t = 2 blockIdx.x + grp + k vstride
-  float* cks0 = ckbuf + grp * 2 * kRouteTile * ckld;  // this group's two key buffers
-  const uint32_t gbar = 1 + grp;
-  const int l = p.l, d = p.d, l_sel = p.l_sel;
+  const int nst = (p.ntiles + kTilesPerItem - 1) / kTilesPerItem;
+  const int rest = it / nst;
+  Item I;
+  I.st = it % nst;
+  I.kvh = rest % p.Hkv;
+  I.r0 = (rest / p.Hkv) * p.chunk_rows;
+  I.nrows = min(p.chunk_rows, rows_total - I.r0);
+  return I;
+}
 
-  // key tile t -> buffer, fire-and-forget (cp.async, blocks past the cache zero-filled)
-  auto issue_tile = [&](int t, float* dst) {
-    constexpr int kPer = kRouteTile * (dh / 4) / kR1GroupThreads;  // 8 x 16 B per thread
+// this thread's staging units of an item -> registers (zero past the cache / rows)
+__device__ __forceinline__ void load_item(const RouteParams& p, const Item& I, float4 (&v)[kStagePer]) {
+  constexpr int dh = kDhRoute;
 #pragma unroll
-    for (int it = 0; it < kPer; ++it) {
-      const int e = gtid + it * kR1GroupThreads;
-      const int b = e / (dh / 4), x4 = e % (dh / 4);
-      const int i = t * kRouteTile + b;
-      const bool ok = t < p.ntiles && i < p.blocks;
-      sm100::cp_async16_zfill(dst + b * ckld + x4 * 4,
-                              p.ck + ((int64_t)(ok ? i : 0) * p.Hkv + kvh) * dh + x4 * 4, ok ? 16u : 0u);
-    }
-    sm100::cp_async_commit();
-  };
-  int t = 2 * blockIdx.x + grp;
-  issue_tile(t, cks0);  // in flight while the q rows are converted
-  {  // q rows, fp32 -> fp64 (exact); rows past nrows are zero
-    constexpr int kQPer = (kRows * (dh / 4) + kR1Threads - 1) / kR1Threads;
-    float4 qv4[kQPer];
-#pragma unroll
-    for (int it = 0; it < kQPer; ++it) {
-      const int e = tid + it * kR1Threads;
-      const int r = e / (dh / 4), x4 = e % (dh / 4);
-      qv4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < nrows) {
-        const int rr = r0 + r;
-        const int slot = rr / p.G, gg = rr % p.G;
-        const int h = kvh * p.G + gg;
-        qv4[it] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[slot] * p.Hq + h) * dh + 4 * x4));
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < kQPer; ++it) {
-      const int e = tid + it * kR1Threads;
-      const int r = e / (dh / 4), x4 = e % (dh / 4);
-      if (r < kRows) {
-        double* dst = qd + (size_t)r * qld + 4 * x4;
-        dst[0] = qv4[it].x; dst[1] = qv4[it].y; dst[2] = qv4[it].z; dst[3] = qv4[it].w;
+  for (int k = 0; k < kStagePer; ++k) {
+    const int e = threadIdx.x + k * kRouteThreads;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e < kSuper * (dh / 4)) {
+      const int i = I.st * kSuper + e / (dh / 4), x4 = e % (dh / 4);
+      if (i < p.blocks)
+        v[k] = __ldg(reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + I.kvh) * dh) + x4);
+    } else if (e < kStageUnits) {
+      const int e2 = e - kSuper * (dh / 4);
+      const int r = e2 / (dh / 4), x4 = e2 % (dh / 4);
+      if (r < I.nrows) {
+        const int rr = I.r0 + r;
+        const int h = I.kvh * p.G + (rr & (p.G - 1));
+        v[k] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[rr / p.G] * p.Hq + h) * dh) + x4);
       }
     }
   }
-  __syncthreads();
-  // diagnostics: group leader stamps [16 + 8 grp + ...]: prologue, then per tile (mma, epilogue)
-  unsigned long long* tg = trc != nullptr && gtid == 0 ? trc + 16 + 16 * grp : nullptr;
-  tstamp_any(tg, 0);
-  // tile-invariant epilogue constants: tile t starts at selection block t d
-  // (l_sel == 64 == tile width), so the overlap weights of this thread's two
-  // blocks with the warp's kW selection blocks do not depend on t
-  const int gshift = __ffs(p.G) - 1;  // G is a power of two (host-checked)
-  __shared__ double s_wgt[8][4][2][kW];  // [warp][lane column][block][selection block]
-  if (grp == 0)
-    for (int e = lane; e < 4 * 2 * kW; e += 32) {
-      const int c4 = e / (2 * kW), c = (e / kW) % 2, k = e % kW;
-      s_wgt[warp][c4][c][k] = (double)overlap(8 * warp + 2 * c4 + c, (8 * warp * d) / l_sel + k, d, l, l_sel);
+}
+
+// registers -> fp64 shared memory (key rows permuted within each tile, see perm_row)
+__device__ __forceinline__ void store_item(uint8_t* smem, const float4 (&v)[kStagePer]) {
+  constexpr int dh = kDhRoute;
+  double* qs = reinterpret_cast<double*>(smem + TileSmem::q);
+  double* cks = reinterpret_cast<double*>(smem + TileSmem::ck);
+#pragma unroll
+  for (int k = 0; k < kStagePer; ++k) {
+    const int e = threadIdx.x + k * kRouteThreads;
+    double* dst;
+    if (e < kSuper * (dh / 4)) {
+      const int b = e / (dh / 4), x4 = e % (dh / 4);
+      dst = cks + (size_t)((b & ~(kTB - 1)) + perm_row(b & (kTB - 1))) * kLd + x4 * 4;
+    } else if (e < kStageUnits) {
+      const int e2 = e - kSuper * (dh / 4);
+      dst = qs + (e2 / (dh / 4)) * kLd + (e2 % (dh / 4)) * 4;
+    } else {
+      continue;
     }
-  __syncthreads();
-  const double (*wgt)[kW] = s_wgt[warp][lc];
-  int mvis_mt[MT];
+    reinterpret_cast<double2*>(dst)[0] = make_double2(v[k].x, v[k].y);
+    reinterpret_cast<double2*>(dst)[1] = make_double2(v[k].z, v[k].w);
+  }
+}
+
+// one warp's statistics tile of a staged item: logits for all rows, TM, TD, G
+__device__ void tile_compute(const RouteParams& p, const uint8_t* smem, const Item& I,
+                             unsigned long long* tr) {
+  constexpr int dh = kDhRoute;
+  const double* qs = reinterpret_cast<const double*>(smem + TileSmem::q);
+  const double* cks = reinterpret_cast<const double*>(smem + TileSmem::ck);
+  const double* W = reinterpret_cast<const double*>(smem + TileSmem::w);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int t = I.st * kTilesPerItem + warp;  // statistics tile
+  const int nrows = I.nrows;
+  if (t >= p.ntiles) return;
+  // ---- logits: 40 rows x 16 blocks, fp64 DMMA ----
+  double acc[kMT][2][2];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-    mvis_mt[mt] = 8 * mt + lr < nrows ? p.slot_mvis[(r0 + 8 * mt + lr) >> gshift] : 0;
-  int tile_no = 0;
-  for (int par = 0; t < p.ntiles; t += vstride, par ^= 1, ++tile_no) {
-    double (*rm)[8] = reinterpret_cast<double (*)[8]>(smem + L::red_m) + grp * kRows;
-    double (*rs)[8] = reinterpret_cast<double (*)[8]>(smem + L::red_s) + grp * kRows;
-    double (*gp)[8][kW] =
-        reinterpret_cast<double (*)[8][kW]>(smem + L::gpart) + grp * kRows;
-    const float* cks = cks0 + (tile_no & 1) * kRouteTile * ckld;
-    issue_tile(t + vstride, cks0 + ((tile_no + 1) & 1) * kRouteTile * ckld);  // lands meanwhile
-    sm100::cp_async_wait<1>();  // this thread's copies of the current tile are done
-    sm100::named_bar_sync(gbar, kR1GroupThreads);  // ... and every thread's
-    // stagger: group 1 starts its first MMAs when group 0 is done with its
-    // own, so from then on one group's epilogue overlaps the other's MMAs
-    if (tile_no == 0 && grp == 1 && 2 * blockIdx.x < p.ntiles) sm100::named_bar_sync(5, kR1Threads);
-    const int i0 = t * kRouteTile;
-    double acc[MT][2];
+  for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-    // B fragment: block (8 warp + lr), element 4 s + lc; A: row (8 mt + lr), element 4 s + lc
-    const float* kb = cks + (8 * warp + lr) * ckld + lc;
-    const double* qa = qd + (size_t)lr * qld + lc;
-    // all MT row tiles unconditionally (rows past nrows are zero in smem and
-    // masked in the epilogue): no predicates, so the A loads of a k step are
-    // all issued before its MMAs instead of one load-use pair at a time
-#pragma unroll 2
-    for (int s = 0; s < dh / 4; ++s) {
-      const double b = kb[4 * s];
-      double a[MT];
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const double* qa = qs + lr * kLd + lc;
+  const double* kb = cks + (size_t)(warp * kTB + lr) * kLd + lc;
+#pragma unroll kRouteUnroll
+  for (int s = 0; s < dh / 4; ++s) {
+    double a[kMT], b[2];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) a[mt] = qa[(size_t)mt * 8 * qld + 4 * s];
+    for (int mt = 0; mt < kMT; ++mt) a[mt] = qa[mt * 8 * kLd + 4 * s];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(acc[mt], a[mt], b);
-    }
-    // C fragment: row 8 mt + lr, blocks 8 warp + 2 lc + {0, 1}
-    const int blk = i0 + 8 * warp + 2 * lc;
+    for (int nt = 0; nt < 2; ++nt) b[nt] = kb[nt * 8 * kLd + 4 * s];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      if (mt >= nmt) break;
-      const int r = 8 * mt + lr;
-      double mx = -INFINITY;
+    for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt], a[mt], b[nt]);
+  }
+  tstamp(tr, 0);
+  // ---- per row: max over the tile (lane column c holds blocks 4 c .. 4 c + 3),
+  // e = exp(logit - max), then TD and G through e x W ----
+  const int ib = t * kTB + 4 * lc;  // first block of this lane column
+  const double* wl = W + lc * kWLd + lr;
+  // every m-tile unconditionally (rows past nrows have mvis 0 and are not
+  // stored): the 5 rows' exps and G chains are independent, so they interleave
+  int mvis[kMT], slot[kMT];
+  double mx[kMT];
+#pragma unroll
+  for (int mt = 0; mt < kMT; ++mt) {
+    const int r = 8 * mt + lr;
+    slot[mt] = (I.r0 + min(r, nrows - 1)) / p.G;
+    mvis[mt] = r < nrows ? p.slot_mvis[slot[mt]] : 0;
+    mx[mt] = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        acc[mt][c] = __dmul_rn(acc[mt][c], p.scale);
-        if (blk + c < mvis_mt[mt]) mx = fmax(mx, acc[mt][c]);
+        acc[mt][nt][c] = __dmul_rn(acc[mt][nt][c], p.scale);
+        if (ib + 2 * nt + c < mvis[mt]) mx[mt] = fmax(mx[mt], acc[mt][nt][c]);
       }
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      if (lc == 0) rm[r][warp] = mx;
+  }
+#pragma unroll
+  for (int mt = 0; mt < kMT; ++mt) {
+    mx[mt] = fmax(mx[mt], __shfl_xor_sync(0xffffffffu, mx[mt], 1));
+    mx[mt] = fmax(mx[mt], __shfl_xor_sync(0xffffffffu, mx[mt], 2));
+  }
+#pragma unroll
+  for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        acc[mt][nt][c] = ib + 2 * nt + c < mvis[mt] ? exp_nonpos(acc[mt][nt][c] - mx[mt]) : 0.0;
+  // K chunk (nt, c) = blocks {4 k + 2 nt + c : k < 4}: exactly the value lane
+  // column k holds, so the A fragment is the exp as it stands; W is stored
+  // K-chunk-major (row 4 (2 nt + c) + k) for conflict-free B fragments
+  double g[kMT][2];
+#pragma unroll
+  for (int mt = 0; mt < kMT; ++mt) g[mt][0] = g[mt][1] = 0.0;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double w = wl[4 * (2 * nt + c) * kWLd];
+#pragma unroll
+      for (int mt = 0; mt < kMT; ++mt) dmma_8x8x4(g[mt], acc[mt][nt][c], w);
     }
-    if (tile_no == 0 && grp == 0 && 2 * blockIdx.x + 1 < p.ntiles) sm100::named_bar_arrive(5, kR1Threads);
-    sm100::named_bar_sync(gbar, kR1GroupThreads);  // also: every warp is done reading cks
-    if (tile_no < 3) tstamp_any(tg, 1 + 5 * tile_no);
-    if (tile_no < 3) tstamp_any(tg, 2 + 5 * tile_no);
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      if (mt >= nmt) break;
-      const int r = 8 * mt + lr;
-      double mx = rm[r][0];
+  for (int mt = 0; mt < kMT; ++mt) {
+    const int r = 8 * mt + lr;
+    if (r >= nrows) continue;
+    const int rr = I.r0 + r;
+    const int h = I.kvh * p.G + (rr & (p.G - 1));
+    const int64_t srow = ((int64_t)slot[mt] * p.Hq + h) * p.ntiles + t;
+    const int64_t grow = ((int64_t)slot[mt] * p.ntiles + t) * p.Hq + h;
 #pragma unroll
-      for (int w = 1; w < 8; ++w) mx = fmax(mx, rm[r][w]);
-      double sum = 0.0, g[kW];
-#pragma unroll
-      for (int k = 0; k < kW; ++k) g[k] = 0.0;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const double ev = blk + c < mvis_mt[mt] ? exp(acc[mt][c] - mx) : 0.0;
-        sum += ev;
-#pragma unroll
-        for (int k = 0; k < kW; ++k) g[k] += ev * wgt[c][k];
-      }
-#pragma unroll
-      for (int off = 1; off <= 2; off <<= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, off);
-#pragma unroll
-        for (int k = 0; k < kW; ++k) g[k] += __shfl_xor_sync(0xffffffffu, g[k], off);
-      }
-      if (lc == 0) {
-        rs[r][warp] = sum;
-#pragma unroll
-        for (int k = 0; k < kW; ++k) gp[r][warp][k] = g[k];
-      }
+    for (int c = 0; c < 2; ++c) {
+      const int j = 2 * lc + c;
+      if (j < p.g_stride) p.gsh[grow * p.g_stride + j] = g[mt][c];
+      if (j == p.g_stride) p.TD[srow] = g[mt][c];
     }
-    if (tile_no < 3) tstamp_any(tg, 3 + 5 * tile_no);
-    sm100::named_bar_sync(gbar, kR1GroupThreads);
-    if (gtid < nrows) {
-      const int rr = r0 + gtid;
-      const int64_t row = (int64_t)(rr >> gshift) * p.Hq + kvh * p.G + (rr & (p.G - 1));
-      double mx = rm[gtid][0], sm = 0.0;
-#pragma unroll
-      for (int w = 1; w < 8; ++w) mx = fmax(mx, rm[gtid][w]);
-#pragma unroll
-      for (int w = 0; w < 8; ++w) sm += rs[gtid][w];
-      p.TM[row * p.ntiles + t] = mx;
-      p.TD[row * p.ntiles + t] = sm;
-    }
-    if (tile_no < 3) tstamp_any(tg, 4 + 5 * tile_no);
-    // G[slot][t][h][j] for the selection blocks t d + j the tile touches (lane
-    // j < g_stride <= 32), summed over the 8 warps in ascending order
-    if (lane < p.g_stride) {
-      for (int r = warp; r < nrows; r += 8) {
-        const int rr = r0 + r;
-        const int slot = rr >> gshift, h = kvh * p.G + (rr & (p.G - 1));
-        double v = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const int k = lane - (8 * w * d) / l_sel;
-          if (k >= 0 && k < kW) v += gp[r][w][k];
-        }
-        p.gsh[(((int64_t)slot * p.ntiles + t) * p.Hq + h) * p.g_stride + lane] = v;
-      }
-    }
-    if (tile_no < 3) tstamp_any(tg, 5 + 5 * tile_no);
-    sm100::named_bar_sync(gbar, kR1GroupThreads);  // red_* / gpart are rewritten by the next tile
+    if (lc == 0) p.TM[srow] = mx[mt];
   }
 }
 
@@ -294,19 +294,20 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
 
 // Top-n over sel[0, avail) (select_blocks, nsa_attention.cpp:94-136): forced
 // blocks first, then the best remaining by (score desc, id asc).
-//  1. every warp's best candidate -> the K-th best of those is a lower bound
-//     of the K-th best overall (K = picks needed, <= number of warps);
+//  1. the best candidate of every 4-lane group -> the K-th best of those is a
+//     lower bound of the K-th best overall (K = picks needed <= groups);
 //  2. candidates ranking at or before that bound survive (typically ~K);
 //  3. exact rank among the survivors.
 __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32_t* idx_row,
                            int32_t* count, uint32_t* forced_bits, unsigned long long* tr = nullptr) {
-  __shared__ double wbest_s[32];
-  __shared__ int wbest_i[32];
+  constexpr int kMaxGroups = 256;  // blockDim.x / 4 <= 256
+  __shared__ double gbest_s[kMaxGroups];
+  __shared__ int gbest_i[kMaxGroups];
   __shared__ double lb_s;
   __shared__ int lb_i, nsurv;
   __shared__ int picks[64];
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;  // whole CTA
-  const int nwarps = nthr >> 5;
+  const int ngroups = nthr >> 2;
   const int f1 = avail - 2 > 0 ? avail - 2 : -1;
   const int f2 = avail - 1 > 0 ? avail - 1 : -1;
   const int nforced = avail > 0 ? 1 + (f1 > 0) + (f2 > 0 && f2 != f1) : 0;
@@ -319,33 +320,32 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
   };
   if (tid == 0) {
     nsurv = 0;
-    lb_s = -INFINITY;  // no bound unless a warp maximum holds rank K-1
+    lb_s = -INFINITY;  // no bound unless a group maximum holds rank K-1
     lb_i = 0x7fffffff;
   }
   if (want > 0) {
-    // 1. per-warp best over the warp's candidates (b = warp*32 + lane + k*nthr)
+    // 1. per-group best over the group's candidates (b = tid + k nthr)
     double bs = -INFINITY;
     int bi = 0x7fffffff;
-    for (int b = warp * 32 + lane; b < avail; b += nthr) {
+    for (int b = tid; b < avail; b += nthr) {
       double sc;
       if (cand(b, sc) && ranks_before(sc, b, bs, bi)) { bs = sc; bi = b; }
     }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
+    for (int off = 1; off <= 2; off <<= 1) {
       const double os = __shfl_xor_sync(0xffffffffu, bs, off);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (ranks_before(os, oi, bs, bi)) { bs = os; bi = oi; }
     }
-    if (lane == 0) { wbest_s[warp] = bs; wbest_i[warp] = bi; }
+    if ((lane & 3) == 0) { gbest_s[tid >> 2] = bs; gbest_i[tid >> 2] = bi; }
     __syncthreads();
     tstamp(tr, 9);
-    if (warp == 0) {  // K-th best warp maximum (rank counting among <= 32)
-      const double ms = lane < nwarps ? wbest_s[lane] : -INFINITY;
-      const int mi = lane < nwarps ? wbest_i[lane] : 0x7fffffff;
+    if (tid < ngroups) {  // the group maximum of rank K-1 (rank counting among the groups)
+      const double ms = gbest_s[tid];
+      const int mi = gbest_i[tid];
       int rank = 0;
-      for (int o = 0; o < nwarps; ++o) rank += ranks_before(wbest_s[o], wbest_i[o], ms, mi) ? 1 : 0;
-      const int kk = want <= nwarps ? want - 1 : -1;
-      if (kk >= 0 && lane < nwarps && rank == kk && ms != -INFINITY) { lb_s = ms; lb_i = mi; }
+      for (int o = 0; o < ngroups; ++o) rank += ranks_before(gbest_s[o], gbest_i[o], ms, mi) ? 1 : 0;
+      if (want <= ngroups && rank == want - 1 && ms != -INFINITY) { lb_s = ms; lb_i = mi; }
     }
     __syncthreads();
     tstamp(tr, 10);
@@ -405,137 +405,128 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
   }
 }
 
-
-
-// Phase 2 (every CTA, after all tile statistics are out).  For each of the
-// CTA's rows: M = max_t TM, DEN = sum_t TD e^(TM - M) (warp per row, the
-// row's statistics in registers) and F_t = e^(TM_t - M) / DEN for the CTA's
-// own tiles.  Then for each (slot of the chunk, own tile, j):
-// part[slot][kvh][t][j] = sum_g (ascending) F[slot, g][t] G[slot][t][g][j] --
-// the KV head's share of the tile's selection-block scores.
-__device__ __noinline__ void shares_phase(const RouteParams& p, uint8_t* smem, unsigned long long* tr) {
-  // Runs once per launch, so it is bound by instruction fetch unless small:
-  // every global read is a fire-and-forget cp.async into shared memory
-  // (one round trip per stage), the arithmetic runs from there.
-  const int kvh = blockIdx.y;
-  const int r0 = blockIdx.z * p.chunk_rows;
-  const int nrows = min(p.chunk_rows, p.nr * p.G - r0);
-  const int tid = threadIdx.x;
-  const int vstride = 2 * gridDim.x;
-  const int t0 = 2 * blockIdx.x;  // own tiles: t0 + {0, 1} + m vstride
-  const int nt = p.ntiles, G = p.G, gs = p.g_stride;
-  const int ct = nt > t0 ? 2 * ((nt - t0 + vstride - 1) / vstride) : 0;
-  double* sF = reinterpret_cast<double*>(smem);  // [chunk_rows][ct]
-  double* sMD = sF + p.chunk_rows * ct;          // [chunk_rows][2]: M, DEN
-  double* sT = sMD + 2 * p.chunk_rows;           // staging
-  // statistics, rg rows at a time: M, DEN per row (8 lanes per row), F for own tiles
-  const int rg = min(nrows, p.shares_rows);
-  for (int g0 = 0; g0 < nrows; g0 += rg) {
-    const int gn = min(rg, nrows - g0);
-    __syncthreads();
-    for (int e = tid; e < gn * nt; e += kR1Threads) {
-      const int rr = r0 + g0 + e / nt;
-      const int64_t src = ((int64_t)(rr / G) * p.Hq + kvh * G + rr % G) * nt + e % nt;
-      sm100::cp_async8(sT + 2 * e, p.TM + src);
-      sm100::cp_async8(sT + 2 * e + 1, p.TD + src);
-    }
-    sm100::cp_async_wait_all();
-    __syncthreads();
-    constexpr int kL = 8;
-    for (int rb = 0; rb < gn; rb += kR1Threads / kL) {  // CTA-uniform rounds
-      const int r = min(rb + tid / kL, gn - 1), l8 = tid % kL;
-      const double* st = sT + 2 * r * nt;
-      double mx = -INFINITY, den = 0.0;
-      for (int t = l8; t < nt; t += kL) mx = fmax(mx, st[2 * t]);
-#pragma unroll
-      for (int off = kL / 2; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      for (int t = l8; t < nt; t += kL)
-        if (st[2 * t + 1] > 0.0) den += st[2 * t + 1] * exp(st[2 * t] - mx);
-#pragma unroll
-      for (int off = kL / 2; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-      if (l8 == 0) {
-        sMD[2 * (g0 + r)] = mx;
-        sMD[2 * (g0 + r) + 1] = den;
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < gn * ct; e += kR1Threads) {
-      const int r = e / ct, k = e % ct;
-      const int t = t0 + (k >> 1) * vstride + (k & 1);
-      const double mx = sMD[2 * (g0 + r)], den = sMD[2 * (g0 + r) + 1];
-      const double tm = t < nt ? sT[2 * (r * nt + t)] : -INFINITY;
-      sF[(g0 + r) * ct + k] = (den > 0.0 && tm != -INFINITY) ? exp(tm - mx) / den : 0.0;
-    }
-  }
-  tstamp(tr, 13);
-  // shares of the KV group for own tiles, kc own tiles at a time:
-  // part[slot][kvh][t][j] = sum_g (ascending) F[slot, g][t] G[slot][t][kvh G + g][j]
-  const int nslots = nrows / G;
-  const int kc = max(1, min(ct, p.shares_rows * 2 * nt / max(1, nslots * G * gs)));
-  for (int k0 = 0; k0 < ct; k0 += kc) {
-    const int kn = min(kc, ct - k0);
-    __syncthreads();
-    for (int e = tid; e < nslots * kn * G * gs; e += kR1Threads) {
-      const int sk = e / (G * gs), rem = e % (G * gs);
-      const int sl = sk / kn, k = k0 + sk % kn;
-      const int t = min(t0 + (k >> 1) * vstride + (k & 1), nt - 1);
-      sm100::cp_async8(sT + e, p.gsh + (((int64_t)(r0 / G + sl) * nt + t) * p.Hq + kvh * G) * gs + rem);
-    }
-    sm100::cp_async_wait_all();
-    __syncthreads();
-    for (int e = tid; e < nslots * kn * gs; e += kR1Threads) {
-      const int sk = e / gs, j = e % gs;
-      const int sl = sk / kn, k = k0 + sk % kn;
-      const int t = t0 + (k >> 1) * vstride + (k & 1);
-      if (t >= nt) continue;
-      const double* gsm = sT + (size_t)sk * G * gs + j;
-      double v = 0.0;
-      for (int g = 0; g < G; ++g) v += sF[(sl * G + g) * ct + k] * gsm[g * gs];
-      p.part[(((int64_t)(r0 / G + sl) * p.Hkv + kvh) * nt + t) * gs + j] = v;
-    }
-  }
-}
-
-// Phase 3 for one routed slot (whole CTA): score_b = sum_t (ascending) sum_kvh
-// (ascending) part[kvh][t][b - t step] / (Hq l), then Top-n.  The slot's
-// shares are staged tc tiles at a time with cp.async (one round trip each).
-__device__ __noinline__ void slot_tail(const RouteParams& p, int slot, uint8_t* smem,
-                                       double* scores_out, unsigned long long* tr = nullptr) {
-  const int tid = threadIdx.x;
+// Phase 2, one unit = (routed slot, KV head), whole CTA.  Per head g of the
+// group (a warp each): M = max_t TM, E_t = e^(TM_t - M), DEN = sum_t TD_t
+// E_t, F_t = E_t / DEN.  Then the KV head's share of every selection-block
+// score, part[b] = sum_t (ascending) sum_g (ascending) F_gt G_gt[b - t step]
+// over the <= 2 tiles touching b.  The last unit of a slot to finish sums the
+// Hkv shares in ascending head order -- score_b = sum part / (Hq l), the
+// reference's sum over blocks and heads regrouped (contract P3) -- and runs
+// the Top-n.
+__device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, uint8_t* smem,
+                                       double* scores_out, unsigned long long* tr) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int nthr = blockDim.x;
   const int avail = p.slot_avail[slot];
-  double* sel = reinterpret_cast<double*>(smem);        // [kMaxAvail]
-  int* surv = reinterpret_cast<int*>(sel + kMaxAvail);  // [kMaxAvail]
-  double* st = reinterpret_cast<double*>(surv + kMaxAvail);  // [Hkv][tc][gs]
-  const int nt = p.ntiles, gs = p.g_stride, hkv = p.Hkv;
+  const int nt = p.ntiles, gs = p.g_stride, G = p.G;
   const int step = kRouteTile * p.d / p.l_sel;  // first selection block of tile t = t step
-  const int tc = max(1, min(nt, p.tail_stage / (hkv * gs)));
-  __syncthreads();  // smem reuse across slots
-  for (int b = tid; b < avail; b += blockDim.x) sel[b] = 0.0;
-  for (int tb = 0; tb < nt; tb += tc) {
-    const int tn = min(tc, nt - tb);
-    __syncthreads();
-    for (int e = tid; e < hkv * tn * gs; e += blockDim.x) {
-      const int kv = e / (tn * gs), rem = e % (tn * gs);
-      sm100::cp_async8(st + e, p.part + (((int64_t)slot * hkv + kv) * nt + tb) * gs + rem);
+  // smem: F [G][nt] | TM, TD staging [G][nt] each | G staging [tiles][G][gs]
+  double* sF = reinterpret_cast<double*>(smem);
+  double* sTM = sF + G * nt;
+  double* sTD = sTM + G * nt;
+  double* sG = sTD + G * nt;
+  const int gbudget = (int)((150 * 1024) / sizeof(double)) - 3 * G * nt;  // doubles for G tiles
+  const int tc = max(2, min(nt + 1, gbudget / (G * gs)));                 // staged tiles per round
+  __syncthreads();  // smem reuse across units
+  // TM, TD of the unit's G heads: fire-and-forget (other CTAs' writes of this
+  // launch; this SM never read those lines, so L1 holds no stale copies)
+  for (int e = tid; e < G * nt; e += nthr) {
+    const int64_t src = ((int64_t)slot * p.Hq + kvh * G + e / nt) * nt + e % nt;
+    sm100::cp_async8(sTM + e, p.TM + src);
+    sm100::cp_async8(sTD + e, p.TD + src);
+  }
+  sm100::cp_async_wait_all();
+  __syncthreads();
+  for (int g = warp; g < G; g += nwarps) {
+    double mx = -INFINITY;
+    for (int t = lane; t < nt; t += 32) mx = fmax(mx, sTM[g * nt + t]);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    double den = 0.0;
+    for (int t = lane; t < nt; t += 32) {
+      const double tm = sTM[g * nt + t];
+      const double e = tm == -INFINITY ? 0.0 : exp_nonpos(tm - mx);
+      sF[g * nt + t] = e;
+      den += sTD[g * nt + t] * e;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+    const double inv = den > 0.0 ? 1.0 / den : 0.0;
+    for (int t = lane; t < nt; t += 32) sF[g * nt + t] *= inv;
+  }
+  tstamp(tr, 7);
+  // part[b] over rounds of staged tiles: round [T0, T1) computes the blocks
+  // [T0 step, T1 step) (the last round: up to avail), staging tiles T0 - 1 ..
+  // T1 - 1 (tile T0 - 1 overhangs into block T0 step)
+  double* part = p.part + ((int64_t)slot * p.Hkv + kvh) * p.sel_pad;
+  for (int T0 = 0; T0 < nt; T0 += tc - 1) {
+    const int T1 = min(nt, T0 + tc - 1);
+    const int Ts = max(0, T0 - 1);
+    __syncthreads();  // F is complete / the previous round's readers are done
+    for (int e = tid; e < (T1 - Ts) * G * gs; e += nthr) {
+      const int tt = e / (G * gs), rem = e % (G * gs);
+      sm100::cp_async8(sG + e, p.gsh + (((int64_t)slot * nt + Ts + tt) * p.Hq + kvh * G) * gs + rem);
     }
     sm100::cp_async_wait_all();
     __syncthreads();
-    const int b_hi = min(avail, (tb + tn - 1) * step + gs);
-    for (int b = tb * step + tid; b < b_hi; b += blockDim.x) {
-      double v = sel[b];
-      for (int t = max(tb, (b - gs + step) / step); t <= min(tb + tn - 1, b / step); ++t)
-        for (int kv = 0; kv < hkv; ++kv) v += st[(kv * tn + t - tb) * gs + b - t * step];
-      sel[b] = v;
+    const int b_end = T1 == nt ? avail : min(avail, T1 * step);
+    for (int b = T0 * step + tid; b < b_end; b += nthr) {
+      const int t_lo = max(0, (b - gs + step) / step), t_hi = min(nt - 1, b / step);
+      double v = 0.0;
+      for (int t = t_lo; t <= t_hi; ++t) {
+        const double* gp = sG + (size_t)(t - Ts) * G * gs + (b - t * step);
+        for (int g = 0; g < G; ++g) v += sF[g * nt + t] * gp[g * gs];
+      }
+      part[b] = v;
     }
   }
+  if (nt == 0)
+    for (int b = tid; b < avail; b += nthr) part[b] = 0.0;
+  // ---- the slot's last unit: scores and Top-n ----
+  __shared__ int last;
   __syncthreads();
-  const double scale = 1.0 / ((double)p.Hq * (double)p.l);
-  for (int b = tid; b < avail; b += blockDim.x) {
-    sel[b] *= scale;
-    if (scores_out != nullptr) scores_out[b] = sel[b];
+  if (tid == 0) {
+    __threadfence();
+    const int done = atomicAdd(p.slot_done + slot, 1);
+    last = done == p.Hkv - 1;
+    if (last) {
+      p.slot_done[slot] = 0;  // self-resetting for the next launch
+      __threadfence();
+    }
   }
   __syncthreads();
   tstamp(tr, 8);
+  if (!last) return;
+  double* sel = reinterpret_cast<double*>(smem);        // [kMaxAvail]
+  int* surv = reinterpret_cast<int*>(sel + kMaxAvail);  // [kMaxAvail]
+  const double scale = 1.0 / ((double)p.Hq * (double)p.l);
+  const double* parts = p.part + (int64_t)slot * p.Hkv * p.sel_pad;
+  for (int b2 = tid; 2 * b2 < avail; b2 += nthr) {  // pairs of blocks; sel_pad is even
+    double2 v = make_double2(0.0, 0.0);
+    double2 pk[16];
+#pragma unroll
+    for (int kv = 0; kv < 16; ++kv)  // every head's loads in flight (other CTAs' data: L2)
+      if (kv < p.Hkv) pk[kv] = __ldcg(reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + b2);
+#pragma unroll
+    for (int kv = 0; kv < 16; ++kv)
+      if (kv < p.Hkv) {
+        v.x += pk[kv].x;
+        v.y += pk[kv].y;
+      }
+    for (int kv = 16; kv < p.Hkv; ++kv) {
+      const double2 w = __ldcg(reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + b2);
+      v.x += w.x;
+      v.y += w.y;
+    }
+    sel[2 * b2] = v.x * scale;
+    if (2 * b2 + 1 < avail) sel[2 * b2 + 1] = v.y * scale;
+    if (scores_out != nullptr) {
+      scores_out[2 * b2] = sel[2 * b2];
+      if (2 * b2 + 1 < avail) scores_out[2 * b2 + 1] = sel[2 * b2 + 1];
+    }
+  }
+  __syncthreads();
+  tstamp(tr, 6);
   if (scores_out != nullptr) return;
   const int q = p.slot_q[slot];
   topn_write(sel, surv, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q, p.idx_forced + q, tr);
@@ -552,38 +543,54 @@ __device__ __forceinline__ void wait_all(int* w, int n) {
   __syncthreads();
 }
 
-template <int MT>
-__global__ void __launch_bounds__(kR1Threads, 1)
+__global__ void __launch_bounds__(kRouteThreads, 1)
     route_fused_kernel(const __grid_constant__ RouteParams p, double* scores_out, int scores_slot) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const int nctas = gridDim.x * gridDim.y * gridDim.z;
-  int* bar = p.counters;  // [0] tiles done, [1] shares done, [2] tail CTAs done; all return to 0
+  const int cta = blockIdx.x, nctas = gridDim.x;
+  int* bar = p.counters;  // [0] tiles done, [2] tail CTAs done; both return to 0
   unsigned long long* tr =
       p.trace != nullptr && threadIdx.x == 0 ? p.trace + kRouteTraceBase + cta * 16 * 4 : nullptr;
-  auto stamp = [&](int k) {
-    if (tr != nullptr) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      tr[k] = t;
-    }
-  };
-  stamp(0);
-  if (tr != nullptr) tr[14] = clock64();
+  tstamp(tr, 0);
+  // ---- phase 1: work items (KV head, row chunk, tile set) over the grid ----
   if (p.ntiles > 0) {
-    tiles_phase<MT>(p, smem, p.trace != nullptr ? p.trace + kRouteTraceBase + cta * 16 * 4 : nullptr);
-    stamp(1);
-    arrive(bar);
-    wait_all(bar, nctas);
-    stamp(2);
-    shares_phase(p, smem, tr);
-    stamp(3);
+    {  // tile-invariant overlap matrix (+ the ones column for TD), K-chunk-major rows
+      double* W = reinterpret_cast<double*>(smem + TileSmem::w);
+      for (int e = threadIdx.x; e < kTB * kWCols; e += kRouteThreads) {
+        const int i = e / kWCols, j = e % kWCols;  // block i = 4 k + 2 nt + c -> row 4 (2 nt + c) + k
+        const int wr = 4 * (i & 3) + (i >> 2);
+        W[wr * kWLd + j] = j < p.g_stride ? (double)overlap(i, j, p.d, p.l, p.l_sel)
+                                          : (j == p.g_stride ? 1.0 : 0.0);
+      }
+    }
+    const int rows_total = p.nr * p.G;
+    const int rchunks = (rows_total + p.chunk_rows - 1) / p.chunk_rows;
+    const int items = p.Hkv * rchunks * ((p.ntiles + kTilesPerItem - 1) / kTilesPerItem);
+    float4 stage[kStagePer];
+    if (cta < items) load_item(p, item_of(p, cta), stage);
+    int round = 0;
+    for (int it = cta; it < items; it += nctas, ++round) {
+      __syncthreads();  // every warp is done with the previous item's tiles
+      if (round < 4) tstamp(tr, 32 + 3 * round);
+      store_item(smem, stage);
+      __syncthreads();
+      if (round < 4) tstamp(tr, 33 + 3 * round);
+#ifndef ROUTE_PREFETCH
+#define ROUTE_PREFETCH 1
+#endif
+      if (ROUTE_PREFETCH && it + nctas < items) load_item(p, item_of(p, it + nctas), stage);  // lands during the MMAs
+      tile_compute(p, smem, item_of(p, it), round < 4 && tr != nullptr ? tr + 48 + round : nullptr);
+      if (!ROUTE_PREFETCH && it + nctas < items) load_item(p, item_of(p, it + nctas), stage);
+      if (round < 4) tstamp(tr, 34 + 3 * round);
+    }
+    tstamp(tr, 1);
   }
-  const int ntail = scores_out != nullptr ? 1 : p.nr;
-  arrive(bar + 1);
-  if (cta >= ntail) return;  // no tail work: leave without waiting
-  wait_all(bar + 1, nctas);
-  stamp(4);
+  // ---- phase 2: (slot, KV head) units after every tile statistic is out ----
+  const int nslots = scores_out != nullptr ? 1 : p.nr;
+  const int units = nslots * p.Hkv;
+  arrive(bar);
+  if (cta >= units) return;  // no unit: leave without waiting
+  wait_all(bar, nctas);
+  tstamp(tr, 4);
   if (cta == 0 && scores_out == nullptr) {
     for (int u = threadIdx.x; u < p.n_unrouted; u += blockDim.x) {
       const int q = p.unrouted[u];
@@ -592,17 +599,14 @@ __global__ void __launch_bounds__(kR1Threads, 1)
       for (int a = 0; a < p.n; ++a) p.idx[(int64_t)q * p.n + a] = -1;
     }
   }
-  for (int slot = cta; slot < ntail; slot += nctas)
-    slot_tail(p, scores_out != nullptr ? scores_slot : slot, smem, scores_out,
-              threadIdx.x == 0 ? tr : nullptr);
-  stamp(5);
-  if (tr != nullptr) tr[15] = clock64();
+  for (int u = cta; u < units; u += nctas)
+    slot_unit(p, scores_out != nullptr ? scores_slot : u / p.Hkv, u % p.Hkv, smem, scores_out, tr);
+  tstamp(tr, 5);
   __syncthreads();
-  if (threadIdx.x == 0) {  // the last tail CTA resets the words for the next launch
-    const int tail_ctas = min(ntail, nctas);
-    if (sm100::atom_add_acq_rel_gpu(bar + 2, 1) == tail_ctas - 1) {
+  if (threadIdx.x == 0) {  // the last unit CTA resets the barrier words for the next launch
+    const int unit_ctas = min(units, nctas);
+    if (sm100::atom_add_acq_rel_gpu(bar + 2, 1) == unit_ctas - 1) {
       atomicExch(bar, 0);
-      atomicExch(bar + 1, 0);
       atomicExch(bar + 2, 0);
     }
   }
@@ -619,12 +623,10 @@ __global__ void __launch_bounds__(1024)
   topn_write(sel, surv, avail, n, idx, count, forced);
 }
 
-template <int MT>
-cudaError_t launch_fused(const RouteParams& p, double* scores_out, int scores_slot,
-                         cudaStream_t s) {
-  constexpr int kRows = 8 * MT;
+cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_slot, cudaStream_t s) {
   RouteParams pc = p;
-  pc.chunk_rows = (kRows / p.G) * p.G;  // whole slots per row chunk (G <= kRows)
+  pc.chunk_rows = (8 * kMT / p.G) * p.G;  // whole slots per row chunk (G <= 32 <= 40)
+  if (pc.chunk_rows < 1) return cudaErrorInvalidValue;
   const int rows_total = p.nr * p.G;
   const int rchunks = (rows_total + pc.chunk_rows - 1) / pc.chunk_rows;
   static int sms = 0;
@@ -633,37 +635,15 @@ cudaError_t launch_fused(const RouteParams& p, double* scores_out, int scores_sl
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // CTAs per (KV head, row chunk): as many as fit one wave (each CTA takes
-  // two tiles per round), trimmed so every CTA runs the same number of rounds
-  const int max_ctas = std::max(1, std::min((p.ntiles + 1) / 2, sms / (p.Hkv * rchunks)));
-  const int per = std::max(1, (p.ntiles + 2 * max_ctas - 1) / (2 * max_ctas));
-  const int ctas = std::max(1, (p.ntiles + 2 * per - 1) / (2 * per));
-  if (ctas * p.Hkv * rchunks > sms) return cudaErrorInvalidConfiguration;  // not co-resident
-  // shares phase: F [rows][2 per] + M/DEN [rows][2] + staged statistics [rg][2][ntiles]
-  const size_t fixed = ((size_t)pc.chunk_rows * (2 * per + 2)) * sizeof(double);
-  const size_t budget = 200 * 1024;
-  pc.shares_rows = (int)std::max<size_t>(
-      1, std::min<size_t>(pc.chunk_rows, (budget - fixed) / (2 * sizeof(double) * std::max(p.ntiles, 1))));
-  const size_t shares_smem = fixed + (size_t)pc.shares_rows * 2 * p.ntiles * sizeof(double);
-  pc.tail_stage = (int)(96 * 1024 / sizeof(double));  // staged shares per tail round, doubles
-  const size_t smem =
-      std::max({TileSmem<MT>::bytes, kTopnSmem + (size_t)pc.tail_stage * sizeof(double), shares_smem});
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = route_fused_kernel<MT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int items = p.Hkv * rchunks * ((p.ntiles + kTilesPerItem - 1) / kTilesPerItem);
+  const int units = (scores_out != nullptr ? 1 : p.nr) * p.Hkv;
+  const int ctas = std::min(sms, std::max(items, units));  // one CTA per SM: co-resident
+  const size_t smem = std::max({TileSmem::bytes, kUnitSmem, kTailSmem});
+  cudaError_t e = cudaFuncSetAttribute(route_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&pc, &scores_out, &scores_slot};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(ctas, p.Hkv, rchunks),
-                                     dim3(kR1Threads), args, smem, s);
-}
-
-cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_slot,
-                         cudaStream_t s) {
-  const int rows = p.nr * p.G;
-  return (rows <= 16 && p.G <= 16) ? launch_fused<2>(p, scores_out, scores_slot, s)
-         : rows <= 32               ? launch_fused<4>(p, scores_out, scores_slot, s)
-         : (rows <= 40 && p.G <= 8) ? launch_fused<5>(p, scores_out, scores_slot, s)
-                                    : launch_fused<6>(p, scores_out, scores_slot, s);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(route_fused_kernel), dim3(ctas),
+                                     dim3(kRouteThreads), args, smem, s);
 }
 
 }  // namespace

@@ -16,9 +16,9 @@ from paper_2605_19893_b200 import abi  # noqa: E402
 from paper_2605_19893_b200 import verify as V  # noqa: E402
 
 BASE = 196608
-NAMES = ["start", "tiles", "bar1", "shares", "bar2", "tail", "shares2", "tail2",
-         "t:scores", "t:warpbest", "t:bound", "t:surv", "t:rank",
-         "s:stats"]
+NAMES = {32: "item0 stage", 33: "item0 staged", 48: "item0 mma done", 49: "item1 mma done", 34: "item0 computed", 35: "item1 stage",
+         36: "item1 staged", 37: "item1 computed", 0: "start", 1: "tiles done", 4: "barrier passed", 7: "F written", 8: "scores",
+         9: "topn warp-best", 10: "topn bound", 11: "topn survivors", 12: "topn rank", 5: "tail done"}
 
 
 def main():
@@ -32,26 +32,15 @@ def main():
     V.route(cfg, c, b, s, out, ws)
     torch.cuda.synchronize()
     abi.lib().specsv_debug_attend_trace(None)
-    full = buf[BASE:BASE + 1024 * 64].view(-1, 64).cpu().numpy()
-    for row in full[:9]:
-        if row[15] > row[14] > 0 and row[5] > row[0]:
-            print("tail CTA effective SM clock MHz:", (row[15] - row[14]) / ((row[5] - row[0]) / 1e3) / 1e6 * 1e3 / 1e3)
-    t = full[:, :14]
+    t = buf[BASE:BASE + 1024 * 64].view(-1, 64).cpu().numpy()
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
     print("ctas", len(t))
-    names = ["prologue"] + [f"{n}{i}" for i in range(3) for n in ("mma", "store", "exp", "bar2", "gw")]
-    for gname, off in (("grp0", 16), ("grp1", 32)):
-        for k, name in enumerate(names):
-            d = full[:len(t), off + k]
-            d = (d[d > 0] - t0) / 1e3
-            if len(d):
-                print(f"{gname}.{name:9s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}")
-    for k, name in enumerate(NAMES):
+    for k, name in NAMES.items():
         d = t[:, k]
         d = (d[d > 0] - t0) / 1e3
         if len(d):
-            print(f"{name:7s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}  (n={len(d)})")
+            print(f"{name:16s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}  (n={len(d)})")
 
 
 if __name__ == "__main__":
