@@ -427,13 +427,25 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   double* sG = sTD + G * nt;
   const int gbudget = (int)((150 * 1024) / sizeof(double)) - 3 * G * nt;  // doubles for G tiles
   const int tc = max(2, min(nt + 1, gbudget / (G * gs)));                 // staged tiles per round
+  // one fire-and-forget batch (16-byte copies) for TM, TD and the first G round
+  // (other CTAs' writes of this launch; this SM never read those lines)
+  auto stage_g = [&](int Ts, int T1) {
+    const int per = G * gs / 2;  // 16-byte units of one tile's group rows (G gs is even)
+    for (int e = tid; e < (T1 - Ts) * per; e += nthr) {
+      const int tt = e / per, rem = e % per;
+      sm100::cp_async16_zfill(sG + (size_t)tt * G * gs + 2 * rem,
+                              p.gsh + (((int64_t)slot * nt + Ts + tt) * p.Hq + kvh * G) * gs + 2 * rem, 16u);
+    }
+  };
   __syncthreads();  // smem reuse across units
-  // TM, TD of the unit's G heads: fire-and-forget (other CTAs' writes of this
-  // launch; this SM never read those lines, so L1 holds no stale copies)
-  for (int e = tid; e < G * nt; e += nthr) {
-    const int64_t src = ((int64_t)slot * p.Hq + kvh * G + e / nt) * nt + e % nt;
-    sm100::cp_async8(sTM + e, p.TM + src);
-    sm100::cp_async8(sTD + e, p.TD + src);
+  {
+    const double* tm = p.TM + ((int64_t)slot * p.Hq + kvh * G) * nt;  // the group's rows are contiguous
+    const double* td = p.TD + ((int64_t)slot * p.Hq + kvh * G) * nt;
+    for (int e = tid; e < G * nt / 2; e += nthr) {
+      sm100::cp_async16_zfill(sTM + 2 * e, tm + 2 * e, 16u);
+      sm100::cp_async16_zfill(sTD + 2 * e, td + 2 * e, 16u);
+    }
+    stage_g(0, min(nt, tc - 1));
   }
   sm100::cp_async_wait_all();
   __syncthreads();
@@ -456,19 +468,18 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   }
   tstamp(tr, 7);
   // part[b] over rounds of staged tiles: round [T0, T1) computes the blocks
-  // [T0 step, T1 step) (the last round: up to avail), staging tiles T0 - 1 ..
-  // T1 - 1 (tile T0 - 1 overhangs into block T0 step)
+  // [T0 step, T1 step) (the last round: up to avail), from tiles T0 - 1 .. T1 - 1
+  // (tile T0 - 1 overhangs into block T0 step)
   double* part = p.part + ((int64_t)slot * p.Hkv + kvh) * p.sel_pad;
   for (int T0 = 0; T0 < nt; T0 += tc - 1) {
     const int T1 = min(nt, T0 + tc - 1);
     const int Ts = max(0, T0 - 1);
-    __syncthreads();  // F is complete / the previous round's readers are done
-    for (int e = tid; e < (T1 - Ts) * G * gs; e += nthr) {
-      const int tt = e / (G * gs), rem = e % (G * gs);
-      sm100::cp_async8(sG + e, p.gsh + (((int64_t)slot * nt + Ts + tt) * p.Hq + kvh * G) * gs + rem);
+    if (T0 > 0) {  // later rounds (long contexts): stage this round's tiles
+      __syncthreads();  // the previous round's readers are done
+      stage_g(Ts, T1);
+      sm100::cp_async_wait_all();
     }
-    sm100::cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // F and the staged tiles are visible
     const int b_end = T1 == nt ? avail : min(avail, T1 * step);
     for (int b = T0 * step + tid; b < b_end; b += nthr) {
       const int t_lo = max(0, (b - gs + step) / step), t_hi = min(nt - 1, b / step);
@@ -501,29 +512,38 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   int* surv = reinterpret_cast<int*>(sel + kMaxAvail);  // [kMaxAvail]
   const double scale = 1.0 / ((double)p.Hq * (double)p.l);
   const double* parts = p.part + (int64_t)slot * p.Hkv * p.sel_pad;
-  for (int b2 = tid; 2 * b2 < avail; b2 += nthr) {  // pairs of blocks; sel_pad is even
-    double2 v = make_double2(0.0, 0.0);
-    double2 pk[16];
+  for (int b4 = tid; 4 * b4 < avail; b4 += nthr) {  // 4 blocks per thread; sel_pad % 4 == 0
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 pk[16][2];
 #pragma unroll
     for (int kv = 0; kv < 16; ++kv)  // every head's loads in flight (other CTAs' data: L2)
-      if (kv < p.Hkv) pk[kv] = __ldcg(reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + b2);
+      if (kv < p.Hkv) {
+        const double2* src = reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + 2 * b4;
+        pk[kv][0] = __ldcg(src);
+        pk[kv][1] = __ldcg(src + 1);
+      }
 #pragma unroll
     for (int kv = 0; kv < 16; ++kv)
       if (kv < p.Hkv) {
-        v.x += pk[kv].x;
-        v.y += pk[kv].y;
+        v[0] += pk[kv][0].x;
+        v[1] += pk[kv][0].y;
+        v[2] += pk[kv][1].x;
+        v[3] += pk[kv][1].y;
       }
     for (int kv = 16; kv < p.Hkv; ++kv) {
-      const double2 w = __ldcg(reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + b2);
-      v.x += w.x;
-      v.y += w.y;
+      const double2* src = reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + 2 * b4;
+      const double2 w0 = __ldcg(src), w1 = __ldcg(src + 1);
+      v[0] += w0.x;
+      v[1] += w0.y;
+      v[2] += w1.x;
+      v[3] += w1.y;
     }
-    sel[2 * b2] = v.x * scale;
-    if (2 * b2 + 1 < avail) sel[2 * b2 + 1] = v.y * scale;
-    if (scores_out != nullptr) {
-      scores_out[2 * b2] = sel[2 * b2];
-      if (2 * b2 + 1 < avail) scores_out[2 * b2 + 1] = sel[2 * b2 + 1];
-    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * b4 + k < avail) {
+        sel[4 * b4 + k] = v[k] * scale;
+        if (scores_out != nullptr) scores_out[4 * b4 + k] = sel[4 * b4 + k];
+      }
   }
   __syncthreads();
   tstamp(tr, 6);
