@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-decode-baseline", action="store_true")
     return ap.parse_args()
 
 
@@ -286,10 +287,15 @@ def run_ours(a):
                              int(roles[j]))
 
     n_refresh = int((roles == V.ROLE_REFRESH).sum())
-    launches_per_step = R * (n_refresh * 4 + (L - n_refresh) * 1)
+    launches_per_step = R * (n_refresh * 2 + (L - n_refresh) * 1)  # route + attend, attend
+    def progress(msg):
+        if os.environ.get("SPECSV_BENCH_PROGRESS"):
+            print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
     for _ in range(2):
         step()
     torch.cuda.synchronize()
+    progress("eager steps done")
     graph = None
     if not a.no_graph:
         graph = torch.cuda.CUDAGraph()
@@ -300,6 +306,7 @@ def run_ours(a):
                 step()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
+    progress("step graph captured")
 
     def run_step():
         if graph is not None:
@@ -318,6 +325,7 @@ def run_ours(a):
     for _ in range(a.warmup):
         run_step()
     barrier()
+    progress("warmup done")
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -358,7 +366,11 @@ def run_ours(a):
             if roles[j] == V.ROLE_REFRESH:
                 V.route(cfg, caches[0][j], batches[0][j], sets[0][j], outs[0][j], ws, a.group, mode)
 
-    g_att, g_rt = capture(attend_all), capture(route_all)
+    progress("timed steps done")
+    g_att = capture(attend_all)
+    progress("attend graph captured")
+    g_rt = capture(route_all)
+    progress("route graph captured")
     att_ms, rt_ms = [], []
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     for rep in range(6):
@@ -371,6 +383,7 @@ def run_ours(a):
         if rep > 0:
             att_ms.append(e[0].elapsed_time(e[1]) / L)
             rt_ms.append(e[1].elapsed_time(e[2]) / max(1, n_refresh))
+    progress("kernel timings done")
     attend_ms = float(np.median(att_ms))
     route_ms = float(np.median(rt_ms))
     alg_att, alg_route, uniq = [], [], []
@@ -429,6 +442,43 @@ def run_ours(a):
     e2e_ms = max_over_ranks(max(ev0.elapsed_time(ev1) / a.steps, wall_ms))
     e2e_value = world * R * nq / (e2e_ms * 1e-3)
 
+    # ---- per-query NSA decode on the same GPU and caches (north star: verify
+    # >= 3x faster): the 1 + gamma queries as sequential single-query decodes,
+    # every layer refreshing its own indices (C = 1, gamma = 0 per call)
+    decode = None
+    if not a.skip_decode_baseline:
+        ws1 = V.Workspace(cfg, 1, a.ctx, device=dev)
+        pos1 = np.array([a.ctx - 1], np.int64)
+        from paper_2605_19893_b200.workload import chain_tree_mask as _ctm
+        dq = []
+        for j in range(L):
+            for i in range(nq):
+                b1 = V.DraftBatch(pos=pos1, tree_mask=_ctm(0), q=batches[0][j].q[i:i + 1],
+                                  gates=batches[0][j].gates[i:i + 1], tree_k=None, tree_v=None)
+                dq.append((j, b1, V.IndexSets.empty(1, cfg.n, dev),
+                           torch.zeros(1, Hq, dh, device=dev)))
+
+        def decode_all():
+            for j, b1, s1, o1 in dq:
+                V.nsa_verify(cfg, caches[0][j], b1, s1, o1, ws1, 1, V.MODE_EXACT, V.ROLE_REFRESH)
+
+        g_dec = capture(decode_all)
+        dsteps = max(2, a.steps // 4)
+        for _ in range(2):
+            g_dec.replay()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(dsteps):
+            g_dec.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dms = max_over_ranks(ev0.elapsed_time(ev1) / dsteps)
+        dval = world * nq / (dms * 1e-3)  # one request's 1 + gamma queries per decode step
+        decode = {"value": dval, "unit": UNIT, "ms_per_step": dms,
+                  "what": f"{nq} sequential single-query NSA decodes per layer (C=1, gamma=0, "
+                          f"refresh every layer), {L} layers, same GPU and caches",
+                  "verify_speedup": (value / (world * R)) / dval}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -454,6 +504,7 @@ def run_ours(a):
                      "alg_bytes_per_launch": bytes_att, "launch_ms": attend_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
         "cpu_baseline": cpu,
+        "decode_baseline": decode,
         "clocks": clocks,
         "gpu_launches": launches_per_step * a.steps,
         "detail": {
