@@ -6,9 +6,9 @@
 
 constexpr int kLd = 132;
 template <int MT, int NT>
-__global__ void probe(double* out, int reps) {
+__global__ void probe(double* out, int reps, int full_mantissa) {
   extern __shared__ double sm[];
-  for (int i = threadIdx.x; i < 64 * kLd; i += blockDim.x) sm[i] = 1e-3 * (i % 17);
+  for (int i = threadIdx.x; i < 64 * kLd; i += blockDim.x) sm[i] = full_mantissa ? (double)__sinf(0.37f * i + 0.11f) : 1e-3 * (i % 17);
   __syncthreads();
   const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
   double acc[MT][NT][2];
@@ -44,22 +44,23 @@ __global__ void probe(double* out, int reps) {
 }
 
 template <int MT, int NT>
-void run(double* d, int sms, int warps) {
+void run(double* d, int sms, int warps, int fm) {
   cudaFuncSetAttribute(probe<MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kLd * 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int reps = 64;
-  probe<MT, NT><<<sms, 32 * warps, 64 * kLd * 8>>>(d, 2);
+  probe<MT, NT><<<sms, 32 * warps, 64 * kLd * 8>>>(d, 2, fm);
   cudaEventRecord(e0);
-  probe<MT, NT><<<sms, 32 * warps, 64 * kLd * 8>>>(d, reps);
+  probe<MT, NT><<<sms, 32 * warps, 64 * kLd * 8>>>(d, reps, fm);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   const double dmmas = (double)sms * warps * reps * 32 * MT * NT;
-  printf("MT=%d NT=%d warps/SM=%2d: %.2f TFLOP/s, %.2f SM-cycles per DMMA (1.9 GHz)\n", MT, NT, warps,
-         dmmas * 512 / (ms * 1e-3) / 1e12, 1.9e9 * (ms * 1e-3) / (dmmas / sms));
+  printf("%s MT=%d NT=%d warps/SM=%2d: %.2f TFLOP/s, %.2f SM-cycles per DMMA (1.9 GHz)\n",
+         fm ? "random-data" : "simple-data", MT, NT, warps, dmmas * 512 / (ms * 1e-3) / 1e12,
+         1.9e9 * (ms * 1e-3) / (dmmas / sms));
 }
 
 int main() {
@@ -67,9 +68,8 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* d;
   cudaMalloc(&d, 1 << 24);
-  for (int w : {4, 8, 16}) run<5, 2>(d, sms, w);
-  for (int w : {4, 8}) run<5, 4>(d, sms, w);
-  for (int w : {8}) run<1, 8>(d, sms, w);
+  for (int fm : {0, 1})
+    for (int w : {8, 16}) run<5, 2>(d, sms, w, fm);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
