@@ -16,7 +16,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libspecsv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["attend.cu", "route.cu", "compress.cu", "abi.cpp", "policy.cpp"]
+SOURCES = ["attend.cu", "route.cu", "compress.cu", "abi.cpp", "policy.cpp", "planner.cpp"]
 HEADERS = ["attend.h", "sm100.cuh", "policy.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -33,7 +33,8 @@ def _stale(target: str, deps: list[str]) -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [
-        os.path.join(ROOT, "include", "specsv_b200", "nsa_verify.h")]
+        os.path.join(ROOT, "include", "specsv_b200", "nsa_verify.h"),
+        os.path.join(ROOT, "include", "specsv_b200", "planner.h")]
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)

@@ -26,23 +26,7 @@
 namespace specsv_b200 {
 namespace {
 
-thread_local std::string g_last_error;
 thread_local unsigned long long* g_trace = nullptr;
-
-template <class F>
-specsv_status guarded(F&& f) {
-  try {
-    f();
-    g_last_error.clear();
-    return SPECSV_OK;
-  } catch (const Error& e) {
-    g_last_error = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return SPECSV_EINVAL;
-  }
-}
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -328,7 +312,7 @@ specsv_status specsv_debug_attend_trace(unsigned long long* buf) {
   return SPECSV_OK;
 }
 
-const char* specsv_last_error(void) { return g_last_error.c_str(); }
+const char* specsv_last_error(void) { return last_error().c_str(); }
 
 specsv_status specsv_validate_config(const specsv_nsa_config* cfg) {
   return guarded([&] {

@@ -17,6 +17,11 @@
 
 namespace specsv_b200 {
 
+std::string& last_error() {
+  thread_local std::string msg;
+  return msg;
+}
+
 void validate_config(const specsv_nsa_config& c) {
   auto fail = [](const std::string& m) { throw Error(SPECSV_EINVAL, "NsaConfig: " + m); };
   if (c.l <= 0) fail("l must be positive");

@@ -14,6 +14,25 @@ struct Error : std::runtime_error {
   Error(specsv_status c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
+// thread-local message behind specsv_last_error()
+std::string& last_error();
+
+// runs a C-ABI body: exceptions become a status code plus the thread-local message
+template <class F>
+specsv_status guarded(F&& f) {
+  try {
+    f();
+    last_error().clear();
+    return SPECSV_OK;
+  } catch (const Error& e) {
+    last_error() = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    last_error() = e.what();
+    return SPECSV_EINVAL;
+  }
+}
+
 void validate_config(const specsv_nsa_config& c);
 void check_build_limits(const specsv_nsa_config& c);
 int64_t routing_visible_len(const specsv_nsa_config& c, int64_t pos);
