@@ -225,3 +225,56 @@ def test_extreme_logit_ranges(oracle_lib, scale):
     assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
     per, l2 = rel_errors(out, ref["out"])
     assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+TREE32 = [-1] * 4 + [i // 4 - 1 for i in range(4, 32)]
+
+
+@pytest.mark.parametrize("mode", [O.MODE_EXACT, O.MODE_APPROX])
+def test_verify_c3_tree32_64k_refresh_then_reuse(oracle_lib, mode):
+    """Config C3: 32-node draft tree at 64K context, a refresh layer and a
+    reuse layer inheriting its index sets."""
+    cfg = O.llama_config(32)
+    x = LayerInputs(cfg, 65536, 32, 3232, parent_slot=TREE32)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(4, mode, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 4, mode, O.ROLE_REFRESH)
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+    y = LayerInputs(cfg, 65536, 32, 3233, parent_slot=TREE32)
+    case2 = DeviceCase(cfg, y)
+    out2, _ = case2.run(4, mode, V.ROLE_REUSE, sets=sets)
+    ref2 = case2.oracle(oracle_lib, 4, mode, O.ROLE_REUSE, idx=ref["idx"],
+                        idx_count=ref["idx_count"], idx_forced=ref["idx_forced"])
+    per, l2 = rel_errors(out2, ref2["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_verify_c4_context_128k_chain8(oracle_lib):
+    """Config C4's context length (131072 committed rows), one request, one layer."""
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 131072, 8, 12812)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+@pytest.mark.parametrize("gamma,mode,C", [(16, O.MODE_EXACT, 4), (16, O.MODE_APPROX, 4),
+                                          (2, O.MODE_EXACT, 1)])
+def test_verify_c5_draft_lengths(oracle_lib, gamma, mode, C):
+    """Config C5's draft-length extremes (gamma 2 and 16 = routing lag) at 16K."""
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 16384, gamma, 1600 + gamma)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(C, mode, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, C, mode, O.ROLE_REFRESH)
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
