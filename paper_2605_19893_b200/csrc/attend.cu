@@ -49,6 +49,7 @@ constexpr int kTile = 128;
 constexpr int kCols = kAttendCols;  // query columns (queries x heads) per CTA
 constexpr int kSoftWarps = 12;      // 4 lane quadrants x 3 column chunks
 constexpr int kSoftThreads = kSoftWarps * 32;
+static_assert(kSoftThreads == 2 * 3 * 64, "merge: 64 threads per (column, branch), two columns per round");
 constexpr int kMaxSplits = 18;
 constexpr int kWarpTma = 12;
 constexpr int kWarpQk = 13;
@@ -927,16 +928,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   }
   if (warp < kSoftWarps) {
+    // 384 threads = 2 columns x 3 branches x 64 threads of 2 d_head lanes each:
+    // every load of a column pair is in flight at once (one round trip); the
+    // branch contributions meet in shared memory and are summed in branch
+    // order (gated_combine, nsa_attention.cpp:239-251)
     const int64_t unit0 = ((int64_t)chunk * p.Hkv + kvh) * S;
-    const int dh = tid & (kDh - 1);
-    for (int c = split + (tid >> 7) * S; c < ncols; c += (kSoftThreads / kDh) * S) {
-      const int qg = q0 + (c >> gshift);
-      const int h = kvh * p.G + (c & (p.G - 1));
-      const float* gate = p.gates + ((int64_t)qg * p.Hq + h) * 3;
-      float res = 0.f;
-#pragma unroll 1
-      for (int br = 0; br < 3; ++br) {
-        float mv[kMaxSplits], lv[kMaxSplits], ov[kMaxSplits];
+    const int task = tid >> 6, l64 = tid & 63;
+    const int cpair = task / 3, br = task % 3;
+    float2* contrib = reinterpret_cast<float2*>(smem + kOffK);  // [2][3][64]: the K stages are idle now
+    for (int c0m = split; c0m < ncols; c0m += 2 * S) {
+      const int c = c0m + cpair * S;
+      const bool live = c < ncols;
+      float2 res = make_float2(0.f, 0.f);
+      if (live) {
+        const int qg = q0 + (c >> gshift);
+        const int h = kvh * p.G + (c & (p.G - 1));
+        const float g = p.gates[((int64_t)qg * p.Hq + h) * 3 + br];
+        float mv[kMaxSplits], lv[kMaxSplits];
+        float2 ov[kMaxSplits];
 #pragma unroll
         for (int s2 = 0; s2 < kMaxSplits; ++s2) {  // all loads in flight at once
           if (s2 < S) {
@@ -944,29 +953,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p.ws + (unit0 + s2) * (3 * kCols * 2) + 2 * (br * kCols + c));
             mv[s2] = ml.x;
             lv[s2] = ml.y;
-            ov[s2] = p.ws[p.ws_o_offset + (unit0 + s2) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + dh];
+            ov[s2] = *reinterpret_cast<const float2*>(
+                p.ws + p.ws_o_offset + (unit0 + s2) * (3 * kCols * kDh) + ((int64_t)br * kCols + c) * kDh + 2 * l64);
           } else {
             mv[s2] = -INFINITY;
             lv[s2] = 0.f;
-            ov[s2] = 0.f;
+            ov[s2] = make_float2(0.f, 0.f);
           }
         }
-        const float g = gate[br];
         float M = -INFINITY;
 #pragma unroll
         for (int s2 = 0; s2 < kMaxSplits; ++s2)
           if (lv[s2] > 0.f) M = fmaxf(M, mv[s2]);
-        if (M == -INFINITY) continue;  // empty branch contributes 0 (nsa_attention.cpp:244)
-        float L = 0.f, O = 0.f;
+        if (M != -INFINITY) {  // an empty branch contributes 0 (nsa_attention.cpp:244)
+          float L = 0.f;
+          float2 O = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int s2 = 0; s2 < kMaxSplits; ++s2) {
-          const float f = lv[s2] > 0.f ? fast_exp2(mv[s2] - M) : 0.f;
-          L += lv[s2] * f;
-          O += ov[s2] * f;
+          for (int s2 = 0; s2 < kMaxSplits; ++s2) {
+            const float f = lv[s2] > 0.f ? fast_exp2(mv[s2] - M) : 0.f;
+            L += lv[s2] * f;
+            O.x += ov[s2].x * f;
+            O.y += ov[s2].y * f;
+          }
+          if (L > 0.f) res = make_float2(g * (O.x / L), g * (O.y / L));
         }
-        if (L > 0.f) res += g * (O / L);
       }
-      p.out[((int64_t)qg * p.Hq + h) * kDh + dh] = res;
+      named_bar_sync(kBarSoft, kSoftThreads);  // the previous pair's contributions are consumed
+      contrib[(cpair * 3 + br) * 64 + l64] = res;
+      named_bar_sync(kBarSoft, kSoftThreads);
+      if (live && br == 0) {
+        const float2 a0 = contrib[(cpair * 3 + 0) * 64 + l64], a1 = contrib[(cpair * 3 + 1) * 64 + l64],
+                     a2 = contrib[(cpair * 3 + 2) * 64 + l64];
+        const int qg = q0 + (c >> gshift);
+        const int h = kvh * p.G + (c & (p.G - 1));
+        *reinterpret_cast<float2*>(p.out + ((int64_t)qg * p.Hq + h) * kDh + 2 * l64) =
+            make_float2((a0.x + a1.x) + a2.x, (a0.y + a1.y) + a2.y);
+      }
     }
     if (trace && tid == 0) p.trace[cta_id * 64 + 4] = globaltimer();
   }
