@@ -421,7 +421,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     tmem_alloc<kTmemCols>(&m.tmem_base);
   } else if (warp < kSoftWarps) {
+#ifdef ATTEND_NO_KREF  // timing experiment only: breaks the fast-pass reference
+    kr = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+#else
     kr = reinterpret_cast<const uint4*>(p.k_raw + ((int64_t)(p.rows - 1) * p.Hkv + kvh) * kDh)[tid & 15];
+#endif
 #pragma unroll
     for (int it = 0; it < 2; ++it) {  // 48 columns x 16 units of 8 elements, 2 units per thread
       const int unit = tid + it * kSoftThreads;

@@ -4,10 +4,10 @@
 // Replaces nsa::selection_scores + nsa::select_blocks
 // (src/nsa_attention.cpp:38-136) for every query that constructs indices.
 //
-// One cooperative persistent kernel (one 320-thread CTA per SM), two phases
+// One cooperative persistent kernel (one 224-thread CTA per SM), two phases
 // and a single grid-wide arrival barrier:
-//  1. tiles (all CTAs).  Work item = (KV head, <= 40 (query, head) rows, 2
-//     key tiles of 64 compressed blocks).  Warp (m, t) owns 8 rows x tile t:
+//  1. tiles (all CTAs).  Work item = (KV head, <= 40 (query, head) rows, 7
+//     statistics tiles of 16 compressed blocks).  Warp (m, t) owns 8 rows x tile t:
 //     logit = dot(q_h, ck_i) / sqrt(dh) in fp64 on the FP64 tensor pipe (DMMA
 //     m8n8k4; fp32 x fp32 products are exact in fp64).  The key rows are
 //     permuted in shared memory so that lane column c of the MMA fragment
@@ -38,11 +38,15 @@ namespace {
 
 constexpr int kMT = 5;                    // 8-row m-tiles per row chunk (40 rows)
 constexpr int kTB = kRouteTile;           // compressed blocks per statistics tile (16)
-constexpr int kSuper = 128;               // compressed blocks per work item (staged at once)
-constexpr int kTilesPerItem = kSuper / kTB;
-constexpr int kRouteThreads = 32 * kTilesPerItem;  // one warp per 16-block tile, all 40 rows
+constexpr int kTilesPerItem = 7;          // statistics tiles per work item: at 64K, 8 heads x
+                                          // 37 items fill 148 SMs twice exactly
+constexpr int kSuper = kTB * kTilesPerItem;  // compressed blocks per work item
+constexpr int kItemsPerRound = 2;         // items multiplied concurrently by one CTA: a warp's
+                                          // DMMA chain is latency-bound, so more warps per SM
+constexpr int kRouteThreads = 32 * kTilesPerItem * kItemsPerRound;  // warp = (item, tile)
 constexpr int kDhRoute = 128;             // d_head of this build (host-checked)
-constexpr int kLd = kDhRoute + 4;         // fp64 row stride (== 4 mod 16: conflict-free fragment loads)
+constexpr int kLd = kDhRoute + 4;         // fp64 q row stride (== 4 mod 16: conflict-free fragments)
+constexpr int kCkLd = kDhRoute + 4;       // fp32 key row stride (== 4 mod 32: conflict-free fragments)
 constexpr int kWLd = 12;                  // overlap-matrix row stride, doubles (== 4 mod 8)
 constexpr int kWCols = 8;                 // overlap matrix columns: g_stride + the ones column <= 8
 constexpr size_t kTopnSmem = (size_t)kMaxAvail * 8 + (size_t)kMaxAvail * 4;
@@ -51,14 +55,14 @@ constexpr size_t kTailSmem = kTopnSmem;
 static_assert(kTB == 16, "lane column c of the MMA fragment owns blocks 4c .. 4c + 3");
 
 #ifndef ROUTE_UNROLL
-#define ROUTE_UNROLL 4
+#define ROUTE_UNROLL 2
 #endif
-constexpr int kRouteUnroll = ROUTE_UNROLL;  // k steps of the logit loop unrolled (A/B builds)
+constexpr int kRouteUnroll = ROUTE_UNROLL;  // k steps of the logit loop unrolled
 
 struct TileSmem {
-  static constexpr size_t q = 0;                                  // [40][kLd] f64
-  static constexpr size_t ck = q + (size_t)8 * kMT * kLd * 8;     // [kSuper][kLd] f64 (permuted rows)
-  static constexpr size_t w = ck + (size_t)kSuper * kLd * 8;      // [16][kWLd] f64 (K-chunk-major)
+  static constexpr size_t q = 0;                                           // [2][40][kLd] f64
+  static constexpr size_t ck = q + (size_t)kItemsPerRound * 8 * kMT * kLd * 8;  // [2][kSuper][kCkLd] f32
+  static constexpr size_t w = ck + (size_t)kItemsPerRound * kSuper * kCkLd * 4;  // [16][kWLd] f64
   static constexpr size_t bytes = w + (size_t)kTB * kWLd * 8;
   static_assert(bytes <= 227 * 1024, "tile-phase shared memory");
 };
@@ -116,90 +120,86 @@ __device__ __forceinline__ int perm_row(int i) {
   return 8 * ((i >> 1) & 1) + 2 * (i >> 2) + (i & 1);
 }
 
-// Phase 1.  A work item is rows [r0, r0 + nrows) of KV head kvh x the 128
-// compressed blocks of super tile st (8 statistics tiles of 16 blocks; warp w
-// owns tile 8 st + w for all 40 rows: per k step 5 A + 2 B fragment loads
-// feed 10 DMMAs).  Keys and q are converted to fp64 once, while staging (a
-// conversion per fragment load would share the FP64 pipe with the DMMAs).
-// The next item's global loads are issued into registers before the current
-// item is multiplied, so they land meanwhile.
-constexpr int kStageUnits = kSuper * (kDhRoute / 4) + 8 * kMT * (kDhRoute / 4);  // float4s
-constexpr int kStagePer = (kStageUnits + kRouteThreads - 1) / kRouteThreads;
-
+// Phase 1.  A work item is rows [r0, r0 + nrows) of KV head kvh x the 112
+// compressed blocks of super tile st (7 statistics tiles of 16 blocks); a
+// CTA multiplies two items at once, warp (item, w) owning tile w of its item
+// for all 40 rows: per k step 5 A + 2 B fragment loads feed 10 DMMAs.  q is
+// staged in fp64 (converted once); the keys are staged in fp32 by
+// fire-and-forget cp.async and converted per B fragment (2 per 10 DMMAs).
 struct Item {
   int kvh, r0, nrows, st;
+  bool live;
 };
 
-__device__ __forceinline__ Item item_of(const RouteParams& p, int it) {
+__device__ __forceinline__ Item item_of(const RouteParams& p, int it, int items) {
   const int rows_total = p.nr * p.G;
   const int nst = (p.ntiles + kTilesPerItem - 1) / kTilesPerItem;
   const int rest = it / nst;
   Item I;
+  I.live = it < items;
   I.st = it % nst;
   I.kvh = rest % p.Hkv;
   I.r0 = (rest / p.Hkv) * p.chunk_rows;
-  I.nrows = min(p.chunk_rows, rows_total - I.r0);
+  I.nrows = I.live ? min(p.chunk_rows, rows_total - I.r0) : 0;
   return I;
 }
 
-// this thread's staging units of an item -> registers (zero past the cache / rows)
-__device__ __forceinline__ void load_item(const RouteParams& p, const Item& I, float4 (&v)[kStagePer]) {
+// key rows (permuted within each tile, see perm_row) and q rows of the
+// round's items -> shared memory
+__device__ void stage_items(const RouteParams& p, uint8_t* smem, const Item (&I)[kItemsPerRound]) {
   constexpr int dh = kDhRoute;
+  double* qs = reinterpret_cast<double*>(smem + TileSmem::q);
+  float* cks = reinterpret_cast<float*>(smem + TileSmem::ck);
+  for (int e = threadIdx.x; e < kItemsPerRound * kSuper * (dh / 4); e += kRouteThreads) {
+    const int k = e / (kSuper * (dh / 4)), rem = e % (kSuper * (dh / 4));
+    const int b = rem / (dh / 4), x4 = rem % (dh / 4);
+    const int i = I[k].st * kSuper + b;
+    const bool ok = I[k].live && i < p.blocks;
+    sm100::cp_async16_zfill(
+        cks + ((size_t)k * kSuper + (b & ~(kTB - 1)) + perm_row(b & (kTB - 1))) * kCkLd + x4 * 4,
+        p.ck + ((int64_t)(ok ? i : 0) * p.Hkv + I[k].kvh) * dh + x4 * 4, ok ? 16u : 0u);
+  }
+  constexpr int kQUnits = kItemsPerRound * 8 * kMT * (dh / 4);
+  constexpr int kQPer = (kQUnits + kRouteThreads - 1) / kRouteThreads;
+  float4 v[kQPer];
 #pragma unroll
-  for (int k = 0; k < kStagePer; ++k) {
-    const int e = threadIdx.x + k * kRouteThreads;
-    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e < kSuper * (dh / 4)) {
-      const int i = I.st * kSuper + e / (dh / 4), x4 = e % (dh / 4);
-      if (i < p.blocks)
-        v[k] = __ldg(reinterpret_cast<const float4*>(p.ck + ((int64_t)i * p.Hkv + I.kvh) * dh) + x4);
-    } else if (e < kStageUnits) {
-      const int e2 = e - kSuper * (dh / 4);
-      const int r = e2 / (dh / 4), x4 = e2 % (dh / 4);
-      if (r < I.nrows) {
-        const int rr = I.r0 + r;
-        const int h = I.kvh * p.G + (rr & (p.G - 1));
-        v[k] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[rr / p.G] * p.Hq + h) * dh) + x4);
+  for (int u = 0; u < kQPer; ++u) {  // all q loads in flight, then fp64 stores
+    const int e = threadIdx.x + u * kRouteThreads;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e < kQUnits) {
+      const int k = e / (8 * kMT * (dh / 4)), rem = e % (8 * kMT * (dh / 4));
+      const int r = rem / (dh / 4), x4 = rem % (dh / 4);
+      if (r < I[k].nrows) {
+        const int rr = I[k].r0 + r;
+        const int h = I[k].kvh * p.G + (rr & (p.G - 1));
+        v[u] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[rr / p.G] * p.Hq + h) * dh) + x4);
       }
     }
   }
-}
-
-// registers -> fp64 shared memory (key rows permuted within each tile, see perm_row)
-__device__ __forceinline__ void store_item(uint8_t* smem, const float4 (&v)[kStagePer]) {
-  constexpr int dh = kDhRoute;
-  double* qs = reinterpret_cast<double*>(smem + TileSmem::q);
-  double* cks = reinterpret_cast<double*>(smem + TileSmem::ck);
 #pragma unroll
-  for (int k = 0; k < kStagePer; ++k) {
-    const int e = threadIdx.x + k * kRouteThreads;
-    double* dst;
-    if (e < kSuper * (dh / 4)) {
-      const int b = e / (dh / 4), x4 = e % (dh / 4);
-      dst = cks + (size_t)((b & ~(kTB - 1)) + perm_row(b & (kTB - 1))) * kLd + x4 * 4;
-    } else if (e < kStageUnits) {
-      const int e2 = e - kSuper * (dh / 4);
-      dst = qs + (e2 / (dh / 4)) * kLd + (e2 % (dh / 4)) * 4;
-    } else {
-      continue;
+  for (int u = 0; u < kQPer; ++u) {
+    const int e = threadIdx.x + u * kRouteThreads;
+    if (e < kQUnits) {
+      const int k = e / (8 * kMT * (dh / 4)), rem = e % (8 * kMT * (dh / 4));
+      double* dst = qs + ((size_t)k * 8 * kMT + rem / (dh / 4)) * kLd + (rem % (dh / 4)) * 4;
+      reinterpret_cast<double2*>(dst)[0] = make_double2(v[u].x, v[u].y);
+      reinterpret_cast<double2*>(dst)[1] = make_double2(v[u].z, v[u].w);
     }
-    reinterpret_cast<double2*>(dst)[0] = make_double2(v[k].x, v[k].y);
-    reinterpret_cast<double2*>(dst)[1] = make_double2(v[k].z, v[k].w);
   }
+  sm100::cp_async_wait_all();
 }
 
 // one warp's statistics tile of a staged item: logits for all rows, TM, TD, G
-__device__ void tile_compute(const RouteParams& p, const uint8_t* smem, const Item& I,
-                             unsigned long long* tr) {
+__device__ void tile_compute(const RouteParams& p, const uint8_t* smem, const Item& I, int k) {
   constexpr int dh = kDhRoute;
-  const double* qs = reinterpret_cast<const double*>(smem + TileSmem::q);
-  const double* cks = reinterpret_cast<const double*>(smem + TileSmem::ck);
+  const double* qs = reinterpret_cast<const double*>(smem + TileSmem::q) + (size_t)k * 8 * kMT * kLd;
+  const float* cks = reinterpret_cast<const float*>(smem + TileSmem::ck) + (size_t)k * kSuper * kCkLd;
   const double* W = reinterpret_cast<const double*>(smem + TileSmem::w);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wt = (threadIdx.x >> 5) % kTilesPerItem, lane = threadIdx.x & 31;
   const int lr = lane >> 2, lc = lane & 3;
-  const int t = I.st * kTilesPerItem + warp;  // statistics tile
+  const int t = I.st * kTilesPerItem + wt;  // statistics tile
   const int nrows = I.nrows;
-  if (t >= p.ntiles) return;
+  if (!I.live || t >= p.ntiles) return;
   // ---- logits: 40 rows x 16 blocks, fp64 DMMA ----
   double acc[kMT][2][2];
 #pragma unroll
@@ -207,20 +207,19 @@ __device__ void tile_compute(const RouteParams& p, const uint8_t* smem, const It
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   const double* qa = qs + lr * kLd + lc;
-  const double* kb = cks + (size_t)(warp * kTB + lr) * kLd + lc;
+  const float* kb = cks + (size_t)(wt * kTB + lr) * kCkLd + lc;
 #pragma unroll kRouteUnroll
   for (int s = 0; s < dh / 4; ++s) {
     double a[kMT], b[2];
 #pragma unroll
     for (int mt = 0; mt < kMT; ++mt) a[mt] = qa[mt * 8 * kLd + 4 * s];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) b[nt] = kb[nt * 8 * kLd + 4 * s];
+    for (int nt = 0; nt < 2; ++nt) b[nt] = kb[nt * 8 * kCkLd + 4 * s];  // fp32 -> fp64, exact
 #pragma unroll
     for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt], a[mt], b[nt]);
   }
-  tstamp(tr, 0);
   // ---- per row: max over the tile (lane column c holds blocks 4 c .. 4 c + 3),
   // e = exp(logit - max), then TD and G through e x W ----
   const int ib = t * kTB + 4 * lc;  // first block of this lane column
@@ -514,23 +513,23 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   const double* parts = p.part + (int64_t)slot * p.Hkv * p.sel_pad;
   for (int b4 = tid; 4 * b4 < avail; b4 += nthr) {  // 4 blocks per thread; sel_pad % 4 == 0
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    double2 pk[16][2];
+    double2 pk[8][2];
 #pragma unroll
-    for (int kv = 0; kv < 16; ++kv)  // every head's loads in flight (other CTAs' data: L2)
+    for (int kv = 0; kv < 8; ++kv)  // every head's loads in flight (other CTAs' data: L2)
       if (kv < p.Hkv) {
         const double2* src = reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + 2 * b4;
         pk[kv][0] = __ldcg(src);
         pk[kv][1] = __ldcg(src + 1);
       }
 #pragma unroll
-    for (int kv = 0; kv < 16; ++kv)
+    for (int kv = 0; kv < 8; ++kv)
       if (kv < p.Hkv) {
         v[0] += pk[kv][0].x;
         v[1] += pk[kv][0].y;
         v[2] += pk[kv][1].x;
         v[3] += pk[kv][1].y;
       }
-    for (int kv = 16; kv < p.Hkv; ++kv) {
+    for (int kv = 8; kv < p.Hkv; ++kv) {
       const double2* src = reinterpret_cast<const double2*>(parts + (int64_t)kv * p.sel_pad) + 2 * b4;
       const double2 w0 = __ldcg(src), w1 = __ldcg(src + 1);
       v[0] += w0.x;
@@ -585,22 +584,19 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     const int rows_total = p.nr * p.G;
     const int rchunks = (rows_total + p.chunk_rows - 1) / p.chunk_rows;
     const int items = p.Hkv * rchunks * ((p.ntiles + kTilesPerItem - 1) / kTilesPerItem);
-    float4 stage[kStagePer];
-    if (cta < items) load_item(p, item_of(p, cta), stage);
-    int round = 0;
-    for (int it = cta; it < items; it += nctas, ++round) {
-      __syncthreads();  // every warp is done with the previous item's tiles
-      if (round < 4) tstamp(tr, 32 + 3 * round);
-      store_item(smem, stage);
+    // rounds of kItemsPerRound items: item cta + (kItemsPerRound r + k) nctas
+    for (int r = 0; cta + kItemsPerRound * r * nctas < items; ++r) {
+      Item I[kItemsPerRound];
+#pragma unroll
+      for (int k = 0; k < kItemsPerRound; ++k) I[k] = item_of(p, cta + (kItemsPerRound * r + k) * nctas, items);
+      __syncthreads();  // every warp is done with the previous round's tiles
+      if (r < 4) tstamp(tr, 32 + 3 * r);
+      stage_items(p, smem, I);
       __syncthreads();
-      if (round < 4) tstamp(tr, 33 + 3 * round);
-#ifndef ROUTE_PREFETCH
-#define ROUTE_PREFETCH 1
-#endif
-      if (ROUTE_PREFETCH && it + nctas < items) load_item(p, item_of(p, it + nctas), stage);  // lands during the MMAs
-      tile_compute(p, smem, item_of(p, it), round < 4 && tr != nullptr ? tr + 48 + round : nullptr);
-      if (!ROUTE_PREFETCH && it + nctas < items) load_item(p, item_of(p, it + nctas), stage);
-      if (round < 4) tstamp(tr, 34 + 3 * round);
+      if (r < 4) tstamp(tr, 33 + 3 * r);
+      const int k = (threadIdx.x >> 5) / kTilesPerItem;
+      tile_compute(p, smem, I[k], k);
+      if (r < 4) tstamp(tr, 34 + 3 * r);
     }
     tstamp(tr, 1);
   }
