@@ -144,49 +144,54 @@ __device__ __forceinline__ Item item_of(const RouteParams& p, int it, int items)
   return I;
 }
 
-// key rows (permuted within each tile, see perm_row) and q rows of the
-// round's items -> shared memory
-__device__ void stage_items(const RouteParams& p, uint8_t* smem, const Item (&I)[kItemsPerRound]) {
+// Staging of one round, per warp: the warp copies its own tile's 16 key rows
+// (permuted, see perm_row) by fire-and-forget cp.async, the item's 7 warps
+// convert its q rows to fp64 and meet at the item's named barrier, then each
+// warp waits only for its own copies -- a warp starts as soon as its tile
+// has landed.
+__device__ void stage_tile(const RouteParams& p, uint8_t* smem, const Item& I, int k) {
   constexpr int dh = kDhRoute;
-  double* qs = reinterpret_cast<double*>(smem + TileSmem::q);
-  float* cks = reinterpret_cast<float*>(smem + TileSmem::ck);
-  for (int e = threadIdx.x; e < kItemsPerRound * kSuper * (dh / 4); e += kRouteThreads) {
-    const int k = e / (kSuper * (dh / 4)), rem = e % (kSuper * (dh / 4));
-    const int b = rem / (dh / 4), x4 = rem % (dh / 4);
-    const int i = I[k].st * kSuper + b;
-    const bool ok = I[k].live && i < p.blocks;
-    sm100::cp_async16_zfill(
-        cks + ((size_t)k * kSuper + (b & ~(kTB - 1)) + perm_row(b & (kTB - 1))) * kCkLd + x4 * 4,
-        p.ck + ((int64_t)(ok ? i : 0) * p.Hkv + I[k].kvh) * dh + x4 * 4, ok ? 16u : 0u);
+  double* qs = reinterpret_cast<double*>(smem + TileSmem::q) + (size_t)k * 8 * kMT * kLd;
+  float* cks = reinterpret_cast<float*>(smem + TileSmem::ck) + (size_t)k * kSuper * kCkLd;
+  const int wt = (threadIdx.x >> 5) % kTilesPerItem, lane = threadIdx.x & 31;
+  const int it_tid = threadIdx.x % (32 * kTilesPerItem);
+#pragma unroll 4
+  for (int e = lane; e < kTB * (dh / 4); e += 32) {  // this warp's 16 key rows
+    const int b = wt * kTB + e / (dh / 4), x4 = e % (dh / 4);
+    const int i = I.st * kSuper + b;
+    const bool ok = I.live && i < p.blocks;
+    sm100::cp_async16_zfill(cks + (size_t)(wt * kTB + perm_row(b & (kTB - 1))) * kCkLd + x4 * 4,
+                            p.ck + ((int64_t)(ok ? i : 0) * p.Hkv + I.kvh) * dh + x4 * 4, ok ? 16u : 0u);
   }
-  constexpr int kQUnits = kItemsPerRound * 8 * kMT * (dh / 4);
-  constexpr int kQPer = (kQUnits + kRouteThreads - 1) / kRouteThreads;
+  sm100::cp_async_commit();
+  constexpr int kQUnits = 8 * kMT * (dh / 4);
+  constexpr int kQPer = (kQUnits + 32 * kTilesPerItem - 1) / (32 * kTilesPerItem);
   float4 v[kQPer];
 #pragma unroll
-  for (int u = 0; u < kQPer; ++u) {  // all q loads in flight, then fp64 stores
-    const int e = threadIdx.x + u * kRouteThreads;
+  for (int u = 0; u < kQPer; ++u) {  // the item's q rows: all loads in flight, then fp64 stores
+    const int e = it_tid + u * 32 * kTilesPerItem;
     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (e < kQUnits) {
-      const int k = e / (8 * kMT * (dh / 4)), rem = e % (8 * kMT * (dh / 4));
-      const int r = rem / (dh / 4), x4 = rem % (dh / 4);
-      if (r < I[k].nrows) {
-        const int rr = I[k].r0 + r;
-        const int h = I[k].kvh * p.G + (rr & (p.G - 1));
+      const int r = e / (dh / 4), x4 = e % (dh / 4);
+      if (r < I.nrows) {
+        const int rr = I.r0 + r;
+        const int h = I.kvh * p.G + (rr & (p.G - 1));
         v[u] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[rr / p.G] * p.Hq + h) * dh) + x4);
       }
     }
   }
 #pragma unroll
   for (int u = 0; u < kQPer; ++u) {
-    const int e = threadIdx.x + u * kRouteThreads;
+    const int e = it_tid + u * 32 * kTilesPerItem;
     if (e < kQUnits) {
-      const int k = e / (8 * kMT * (dh / 4)), rem = e % (8 * kMT * (dh / 4));
-      double* dst = qs + ((size_t)k * 8 * kMT + rem / (dh / 4)) * kLd + (rem % (dh / 4)) * 4;
+      double* dst = qs + (e / (dh / 4)) * kLd + (e % (dh / 4)) * 4;
       reinterpret_cast<double2*>(dst)[0] = make_double2(v[u].x, v[u].y);
       reinterpret_cast<double2*>(dst)[1] = make_double2(v[u].z, v[u].w);
     }
   }
-  sm100::cp_async_wait_all();
+  sm100::named_bar_sync(1 + k, 32 * kTilesPerItem);  // the item's q rows are in place
+  sm100::cp_async_wait<0>();
+  __syncwarp();  // this warp's key rows are in place
 }
 
 // one warp's statistics tile of a staged item: logits for all rows, TM, TD, G
@@ -591,10 +596,9 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
       for (int k = 0; k < kItemsPerRound; ++k) I[k] = item_of(p, cta + (kItemsPerRound * r + k) * nctas, items);
       __syncthreads();  // every warp is done with the previous round's tiles
       if (r < 4) tstamp(tr, 32 + 3 * r);
-      stage_items(p, smem, I);
-      __syncthreads();
-      if (r < 4) tstamp(tr, 33 + 3 * r);
       const int k = (threadIdx.x >> 5) / kTilesPerItem;
+      stage_tile(p, smem, I[k], k);
+      if (r < 4) tstamp(tr, 33 + 3 * r);
       tile_compute(p, smem, I[k], k);
       if (r < 4) tstamp(tr, 34 + 3 * r);
     }
