@@ -374,8 +374,10 @@ specsv_status specsv_nsa_verify_batched(const specsv_nsa_config* cfg, const spec
     validate_config(*cfg);
     check_build_limits(*cfg);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // validate the whole batch before the first launch: a bad request must not
+    // leave the ones before it half-verified
+    for (int32_t b = 0; b < batch; ++b) validate_args(*cfg, kvs[b], args[b]);
     for (int32_t b = 0; b < batch; ++b) {
-      validate_args(*cfg, kvs[b], args[b]);
       if (args[b].role == SPECSV_ROLE_REFRESH) run_route(*cfg, kvs[b], args[b], ws, ws_bytes, s);
       run_attend(*cfg, kvs[b], args[b], ws, ws_bytes, s);
     }

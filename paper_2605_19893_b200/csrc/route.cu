@@ -4,14 +4,15 @@
 // Replaces nsa::selection_scores + nsa::select_blocks
 // (src/nsa_attention.cpp:38-136) for every query that constructs indices.
 //
-// One cooperative persistent kernel (one 224-thread CTA per SM), two phases
-// and a single grid-wide arrival barrier:
+// One cooperative persistent kernel (one 448-thread CTA per SM, two work
+// items in flight), two phases and a single grid-wide arrival barrier:
 //  1. tiles (all CTAs).  Work item = (KV head, <= 40 (query, head) rows, 7
-//     statistics tiles of 16 compressed blocks).  Warp (m, t) owns 8 rows x tile t:
+//     statistics tiles of 16 compressed blocks).  Warp (item, t) owns all 40
+//     rows x tile t and stages its own 16 key rows (cp.async):
 //     logit = dot(q_h, ck_i) / sqrt(dh) in fp64 on the FP64 tensor pipe (DMMA
 //     m8n8k4; fp32 x fp32 products are exact in fp64).  The key rows are
 //     permuted in shared memory so that lane column c of the MMA fragment
-//     holds the 16 consecutive blocks [16c, 16c + 16): the whole per-row
+//     holds the consecutive blocks 4c .. 4c + 3 of the tile: the whole per-row
 //     epilogue stays inside the warp (no cross-warp reductions).  Per row and
 //     tile it writes TM = max logit and, through a second small DMMA against
 //     the tile-invariant overlap matrix W[block][selection block] (plus a

@@ -189,6 +189,24 @@ def nsa_verify(cfg, cache, batch, sets, out, ws, group_size=4, mode=MODE_EXACT,
     _call(lib().specsv_nsa_verify, cfg, cache, batch, sets, out, ws, group_size, mode, role, stream)
 
 
+def nsa_verify_batched(cfg, caches, batches, sets, outs, ws, group_size=4, mode=MODE_EXACT,
+                       roles=None, stream=None):
+    """`len(caches)` independent requests, one layer each, in one call
+    (specsv_nsa_verify_batched).  The whole batch is validated before the
+    first launch; `ws` must be sized for the largest request."""
+    n = len(caches)
+    if not (len(batches) == len(sets) == len(outs) == n):
+        raise ValueError("caches, batches, sets and outs must have the same length")
+    roles = [ROLE_REFRESH] * n if roles is None else list(roles)
+    kvs = (abi.LayerKvC * max(n, 1))(*[c.c() for c in caches])
+    args = (abi.VerifyArgsC * max(n, 1))(*[_args(b, s, o, group_size, mode, r)
+                                           for b, s, o, r in zip(batches, sets, outs, roles)])
+    c = cfg.c()
+    check(lib().specsv_nsa_verify_batched(C.byref(c), kvs, args, n,
+                                          C.c_void_p(ws.buf.data_ptr()), ws.nbytes,
+                                          _stream(stream)))
+
+
 def route(cfg, cache, batch, sets, out, ws, group_size=4, mode=MODE_EXACT, stream=None):
     _call(lib().specsv_nsa_route, cfg, cache, batch, sets, out, ws, group_size, mode,
           ROLE_REFRESH, stream)

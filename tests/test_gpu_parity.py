@@ -278,3 +278,51 @@ def test_verify_c5_draft_lengths(oracle_lib, gamma, mode, C):
     assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
     per, l2 = rel_errors(out, ref["out"])
     assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_verify_batched_matches_per_request(oracle_lib):
+    """specsv_nsa_verify_batched over three independent requests (different
+    contexts, draft shapes and roles) sharing one workspace: every request's
+    sets and outputs equal the per-request oracle's."""
+    cfg = O.llama_config(4)
+    specs = [(1000, 4, None, V.ROLE_REFRESH), (4096, 8, TREE8, V.ROLE_REFRESH),
+             (3001, 2, None, V.ROLE_REUSE)]
+    cases = [DeviceCase(cfg, LayerInputs(cfg, r, g, 500 + r, parent_slot=p)) for r, g, p, _ in specs]
+    # the reuse request inherits sets built by a standalone refresh of the same request
+    _, src_sets = cases[2].run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    src = sets_to_numpy(src_sets)
+    sets = [V.IndexSets.empty(c.nq, cfg.n) for c in cases[:2]] + [src_sets]
+    outs = [torch.zeros(c.nq, cfg.n_q_heads, cfg.d_head, device="cuda") for c in cases]
+    ws = V.Workspace(cases[0].vcfg, max(c.nq for c in cases), max(c.x.k.shape[0] for c in cases))
+    V.nsa_verify_batched(cases[0].vcfg, [c.cache for c in cases], [c.batch for c in cases], sets,
+                         outs, ws, 4, V.MODE_EXACT, [s[3] for s in specs])
+    torch.cuda.synchronize()
+    for b, case in enumerate(cases):
+        if specs[b][3] == V.ROLE_REFRESH:
+            ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+            gi, gc, gf = sets_to_numpy(sets[b])
+            assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+        else:
+            ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REUSE, idx=src[0],
+                              idx_count=src[1], idx_forced=forced_matrix(src[2], cfg.n))
+        assert ref["rc"] == 0
+        per, l2 = rel_errors(outs[b].cpu().numpy().astype(np.float64), ref["out"])
+        assert per <= TOL and l2 <= TOL, (b, per, l2)
+
+
+def test_verify_batched_validates_before_launch():
+    """A bad request anywhere in the batch fails the call before any request's
+    outputs are written."""
+    cfg = O.llama_config(4)
+    good = DeviceCase(cfg, LayerInputs(cfg, 2000, 2, 8))
+    bad = DeviceCase(cfg, LayerInputs(cfg, 2000, 2, 9))
+    bad.batch.pos = bad.batch.pos.copy()
+    bad.batch.pos[2] = bad.batch.pos[0] + cfg.routing_lag + 1
+    outs = [torch.full((3, cfg.n_q_heads, cfg.d_head), 7.0, device="cuda") for _ in range(2)]
+    sets = [V.IndexSets.empty(3, cfg.n) for _ in range(2)]
+    with pytest.raises(V.SpecsvError) as e:
+        V.nsa_verify_batched(good.vcfg, [good.cache, bad.cache], [good.batch, bad.batch], sets,
+                             outs, good.ws, 1, V.MODE_EXACT)
+    assert e.value.code == 1
+    torch.cuda.synchronize()
+    assert bool((outs[0] == 7.0).all())
