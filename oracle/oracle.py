@@ -308,3 +308,66 @@ def load(which: str = "oracle") -> Oracle:
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+class RefTree:
+    """The reference's own draft-tree utilities (proj/src/draft_tree.cpp) via
+    oracle/ref_tree_shim.cpp in oracle/_ref -- the checker for
+    include/specsv_b200/draft_tree.h.  Trees are flat arrays (node 0 root)."""
+
+    PROPOSE = C.CFUNCTYPE(C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_double,
+                          C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_double))
+
+    def __init__(self, path: str = REF_SO):
+        self.L = C.CDLL(path)
+
+    def expand(self, root_token, propose, D, k, budget=None, capacity=4096):
+        """propose(node_id, token, depth, cum_score, k) -> [(token, score), ...]"""
+        arrs = (np.zeros(capacity, np.int64), np.zeros(capacity, np.int32),
+                np.zeros(capacity, np.int32), np.zeros(capacity, np.float64),
+                np.zeros(capacity, np.float64))
+
+        def cb(_ctx, node, tok, dep, cs, kk, tout, sout):
+            top = list(propose(int(node), int(tok), int(dep), float(cs), int(kk)))
+            for i, (t, s) in enumerate(top):
+                tout[i] = int(t)
+                sout[i] = float(s)
+            return len(top)
+
+        n = C.c_int64(0)
+        rc = self.L.or_ref_tree_expand(C.c_int32(root_token), self.PROPOSE(cb), None, C.c_int64(D),
+                                       C.c_int64(k), C.c_int64(-1 if budget is None else budget),
+                                       C.c_int64(capacity), _p(arrs[0], C.c_int64),
+                                       _p(arrs[1], C.c_int32), _p(arrs[2], C.c_int32),
+                                       _p(arrs[3], C.c_double), _p(arrs[4], C.c_double),
+                                       C.byref(n))
+        m = n.value
+        return rc, tuple(a[:m].copy() for a in arrs)
+
+    def flatten(self, parent, token, depth, score, traversal, committed_len):
+        n = len(parent)
+        g = n - 1
+        arrs = [np.ascontiguousarray(parent, np.int64), np.ascontiguousarray(token, np.int32),
+                np.ascontiguousarray(depth, np.int32), np.ascontiguousarray(score, np.float64)]
+        order = np.zeros(max(g, 1), np.int64)
+        pos = np.zeros(max(g, 1), np.int64)
+        mask = np.zeros((max(g, 1), max(g, 1)), np.uint8)
+        self.L.or_ref_tree_flatten(C.c_int64(n), _p(arrs[0], C.c_int64), _p(arrs[1], C.c_int32),
+                                   _p(arrs[2], C.c_int32), _p(arrs[3], C.c_double),
+                                   C.c_int32(traversal), C.c_int64(committed_len),
+                                   _p(order, C.c_int64), _p(pos, C.c_int64), _p(mask, C.c_uint8))
+        return order[:g], pos[:g], mask[:g, :g].astype(bool)
+
+    def greedy(self, parent, token, depth, score, argmax):
+        n = len(parent)
+        arrs = [np.ascontiguousarray(parent, np.int64), np.ascontiguousarray(token, np.int32),
+                np.ascontiguousarray(depth, np.int32), np.ascontiguousarray(score, np.float64),
+                np.ascontiguousarray(argmax, np.int32)]
+        nodes = np.zeros(max(n, 1), np.int64)
+        toks = np.zeros(max(n, 1), np.int32)
+        na, bonus = C.c_int64(0), C.c_int32(0)
+        rc = self.L.or_ref_tree_greedy(C.c_int64(n), _p(arrs[0], C.c_int64), _p(arrs[1], C.c_int32),
+                                       _p(arrs[2], C.c_int32), _p(arrs[3], C.c_double),
+                                       _p(arrs[4], C.c_int32), _p(nodes, C.c_int64),
+                                       _p(toks, C.c_int32), C.byref(na), C.byref(bonus))
+        return rc, nodes[:na.value].tolist(), toks[:na.value].tolist(), int(bonus.value)

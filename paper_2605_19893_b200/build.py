@@ -16,7 +16,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libspecsv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["attend.cu", "route.cu", "compress.cu", "abi.cpp", "policy.cpp", "planner.cpp"]
+SOURCES = ["attend.cu", "route.cu", "compress.cu", "draft_tree.cu", "abi.cpp", "policy.cpp", "planner.cpp"]
 HEADERS = ["attend.h", "sm100.cuh", "policy.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -34,7 +34,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(ROOT, "include", "specsv_b200", "nsa_verify.h"),
-        os.path.join(ROOT, "include", "specsv_b200", "planner.h")]
+        os.path.join(ROOT, "include", "specsv_b200", "planner.h"),
+        os.path.join(ROOT, "include", "specsv_b200", "draft_tree.h")]
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)

@@ -17,7 +17,7 @@ from paper_2605_19893_b200 import verify as V  # noqa: E402
 
 BASE = 196608
 NAMES = {32: "item0 stage", 33: "item0 staged", 48: "item0 mma done", 49: "item1 mma done", 34: "item0 computed", 35: "item1 stage",
-         36: "item1 staged", 37: "item1 computed", 0: "start", 1: "tiles done", 4: "barrier passed", 7: "F written", 8: "scores",
+         36: "item1 staged", 37: "item1 computed", 0: "start", 1: "tiles done", 4: "barrier passed", 13: "unit staged", 7: "F written", 14: "part written", 8: "slot atomic", 15: "sel summed",
          9: "topn warp-best", 10: "topn bound", 11: "topn survivors", 12: "topn rank", 5: "tail done"}
 
 
