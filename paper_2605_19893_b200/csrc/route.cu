@@ -349,7 +349,6 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
       const double ms = gbest_s[tid];
       const int mi = gbest_i[tid];
       int rank = 0;
-#pragma unroll 8
       for (int o = 0; o < ngroups; ++o) rank += ranks_before(gbest_s[o], gbest_i[o], ms, mi) ? 1 : 0;
       if (want <= ngroups && rank == want - 1 && ms != -INFINITY) { lb_s = ms; lb_i = mi; }
     }
@@ -373,7 +372,6 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
       const int b = surv[k];
       const double sb = sel[b];
       int rank = 0;
-#pragma unroll 4
       for (int o = 0; o < ns; ++o) {
         const int c = surv[o];
         rank += ranks_before(sel[c], c, sb, b) ? 1 : 0;
@@ -457,44 +455,22 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   sm100::cp_async_wait_all();
   __syncthreads();
   tstamp(tr, 13);
-  {  // wph warps per head (every warp busy): partial max / DEN per warp, combined in smem
-    __shared__ double red_m[32], red_d[32];
-    const int wph = max(1, nwarps / G), hpr = nwarps / wph;
-    for (int g0 = 0; g0 < G; g0 += hpr) {
-      const int g = g0 + warp / wph, k = warp % wph, w0 = warp - k;
-      const bool on = warp < hpr * wph && g < G;
-      double mx = -INFINITY;
-      if (on)
-#pragma unroll 4
-        for (int t = k * 32 + lane; t < nt; t += 32 * wph) mx = fmax(mx, sTM[g * nt + t]);
+  for (int g = warp; g < G; g += nwarps) {
+    double mx = -INFINITY;
+    for (int t = lane; t < nt; t += 32) mx = fmax(mx, sTM[g * nt + t]);
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      if (lane == 0) red_m[warp] = mx;
-      __syncthreads();
-      double den = 0.0;
-      if (on) {
-        for (int j = 0; j < wph; ++j) mx = fmax(mx, red_m[w0 + j]);
-#pragma unroll 4
-        for (int t = k * 32 + lane; t < nt; t += 32 * wph) {
-          const double tm = sTM[g * nt + t];
-          const double e = tm == -INFINITY ? 0.0 : exp_nonpos(tm - mx);
-          sF[g * nt + t] = e;
-          den += sTD[g * nt + t] * e;
-        }
-      }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
-      if (lane == 0) red_d[warp] = den;
-      __syncthreads();
-      if (on) {
-        den = 0.0;
-        for (int j = 0; j < wph; ++j) den += red_d[w0 + j];  // ascending warp order
-        const double inv = den > 0.0 ? 1.0 / den : 0.0;
-#pragma unroll 4
-        for (int t = k * 32 + lane; t < nt; t += 32 * wph) sF[g * nt + t] *= inv;
-      }
-      __syncthreads();  // red_m / red_d reuse
+    for (int off = 16; off >= 1; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    double den = 0.0;
+    for (int t = lane; t < nt; t += 32) {
+      const double tm = sTM[g * nt + t];
+      const double e = tm == -INFINITY ? 0.0 : exp_nonpos(tm - mx);
+      sF[g * nt + t] = e;
+      den += sTD[g * nt + t] * e;
     }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) den += __shfl_xor_sync(0xffffffffu, den, off);
+    const double inv = den > 0.0 ? 1.0 / den : 0.0;
+    for (int t = lane; t < nt; t += 32) sF[g * nt + t] *= inv;
   }
   tstamp(tr, 7);
   // part[b] over rounds of staged tiles: round [T0, T1) computes the blocks
