@@ -75,13 +75,15 @@ def llama_cfg(L):
 
 
 def workload_config(a, extra=None):
-    cfg = {"workload": f"C2: Llama-3.1-8B-shaped NSA verify, {a.ctx // 1024}K ctx, "
-                       f"{a.gamma}-token chain draft, bf16 KV, {a.layers} layers",
+    name = "C4" if a.requests > 1 else "C2"  # C4: many requests per GPU, batched calls
+    cfg = {"workload": f"{name}: Llama-3.1-8B-shaped NSA verify, {a.ctx // 1024}K ctx, "
+                       f"{a.gamma}-token chain draft, bf16 KV, {a.layers} layers"
+                       + (f", {a.requests} requests per GPU" if a.requests > 1 else ""),
            "ctx": a.ctx, "draft": "chain", "gamma": a.gamma, "layers": a.layers,
            "requests_per_gpu": a.requests, "mode": a.mode, "group_size": a.group,
            "schedule": a.schedule, "heads": "32q/8kv", "d_head": 128,
            "nsa": "l=32 d=16 l_sel=64 n=16 w=512 lag=16",
-           "l2": "inputs larger than L2 (each step streams >= 9 GB of distinct layer caches)"}
+           "l2": "inputs larger than L2 (each step streams every request-layer cache once: GBs, L2 is 126 MB)"}
     if extra:
         cfg.update(extra)
     return cfg
@@ -280,11 +282,18 @@ def run_ours(a):
     torch.cuda.synchronize()
 
     def step():
-        for r in range(R):
+        if R == 1:
             for j in range(L):
-                s = sets[r][j] if roles[j] == V.ROLE_REFRESH else sets[r][int(source[j])]
-                V.nsa_verify(cfg, caches[r][j], batches[r][j], s, outs[r][j], ws, a.group, mode,
+                s = sets[0][j] if roles[j] == V.ROLE_REFRESH else sets[0][int(source[j])]
+                V.nsa_verify(cfg, caches[0][j], batches[0][j], s, outs[0][j], ws, a.group, mode,
                              int(roles[j]))
+            return
+        for j in range(L):  # C4: one batched call per layer over this GPU's requests
+            src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
+            V.nsa_verify_batched(cfg, [caches[r][j] for r in range(R)],
+                                 [batches[r][j] for r in range(R)], [sets[r][src] for r in range(R)],
+                                 [outs[r][j] for r in range(R)], ws, a.group, mode,
+                                 [int(roles[j])] * R)
 
     n_refresh = int((roles == V.ROLE_REFRESH).sum())
     launches_per_step = R * (n_refresh * 2 + (L - n_refresh) * 1)  # route + attend, attend
