@@ -214,13 +214,24 @@ __device__ void tile_compute(const RouteParams& p, const uint8_t* smem, const It
     for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   const double* qa = qs + lr * kLd + lc;
   const float* kb = cks + (size_t)(wt * kTB + lr) * kCkLd + lc;
+#ifdef ROUTE_DIAG_KSTEPS  // timing diagnostics only: fewer k steps
+#define ROUTE_KS ROUTE_DIAG_KSTEPS
+#else
+#define ROUTE_KS (dh / 4)
+#endif
 #pragma unroll kRouteUnroll
-  for (int s = 0; s < dh / 4; ++s) {
+  for (int s = 0; s < ROUTE_KS; ++s) {
     double a[kMT], b[2];
 #pragma unroll
     for (int mt = 0; mt < kMT; ++mt) a[mt] = qa[mt * 8 * kLd + 4 * s];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) b[nt] = kb[nt * 8 * kCkLd + 4 * s];  // fp32 -> fp64, exact
+    for (int nt = 0; nt < 2; ++nt) {
+#ifdef ROUTE_DIAG_B_CONST  // timing diagnostics only (tools/route_variants.sh): no key loads
+      b[nt] = 1.0 + 1e-3 * (nt + s);
+#else
+      b[nt] = kb[nt * 8 * kCkLd + 4 * s];  // fp32 -> fp64, exact
+#endif
+    }
 #pragma unroll
     for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
@@ -259,7 +270,11 @@ __device__ void tile_compute(const RouteParams& p, const uint8_t* smem, const It
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
+#ifdef ROUTE_DIAG_NO_EXP  // timing diagnostics only
+        acc[mt][nt][c] = ib + 2 * nt + c < mvis[mt] ? acc[mt][nt][c] - mx[mt] : 0.0;
+#else
         acc[mt][nt][c] = ib + 2 * nt + c < mvis[mt] ? exp_nonpos(acc[mt][nt][c] - mx[mt]) : 0.0;
+#endif
   // K chunk (nt, c) = blocks {4 k + 2 nt + c : k < 4}: exactly the value lane
   // column k holds, so the A fragment is the exp as it stands; W is stored
   // K-chunk-major (row 4 (2 nt + c) + k) for conflict-free B fragments
@@ -345,12 +360,16 @@ __device__ void topn_write(const double* sel, int* surv, int avail, int n, int32
     if ((lane & 3) == 0) { gbest_s[tid >> 2] = bs; gbest_i[tid >> 2] = bi; }
     __syncthreads();
     tstamp(tr, 9);
-    if (tid < ngroups) {  // the group maximum of rank K-1 (rank counting among the groups)
-      const double ms = gbest_s[tid];
-      const int mi = gbest_i[tid];
+    {  // the group maximum of rank K-1: group tid/4's rank among the groups,
+       // counted by its 4 lanes (a quarter of the groups each) and combined
+      const int g = tid >> 2, part = tid & 3;
+      const double ms = gbest_s[g];
+      const int mi = gbest_i[g];
       int rank = 0;
-      for (int o = 0; o < ngroups; ++o) rank += ranks_before(gbest_s[o], gbest_i[o], ms, mi) ? 1 : 0;
-      if (want <= ngroups && rank == want - 1 && ms != -INFINITY) { lb_s = ms; lb_i = mi; }
+      for (int o = part; o < ngroups; o += 4) rank += ranks_before(gbest_s[o], gbest_i[o], ms, mi) ? 1 : 0;
+      rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+      rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+      if (part == 0 && want <= ngroups && rank == want - 1 && ms != -INFINITY) { lb_s = ms; lb_i = mi; }
     }
     __syncthreads();
     tstamp(tr, 10);
