@@ -281,19 +281,20 @@ def run_ours(a):
     ws = V.Workspace(cfg, nq, a.ctx, device=dev)
     torch.cuda.synchronize()
 
-    def step():
+    def layer(j):
+        src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
         if R == 1:
-            for j in range(L):
-                s = sets[0][j] if roles[j] == V.ROLE_REFRESH else sets[0][int(source[j])]
-                V.nsa_verify(cfg, caches[0][j], batches[0][j], s, outs[0][j], ws, a.group, mode,
-                             int(roles[j]))
+            V.nsa_verify(cfg, caches[0][j], batches[0][j], sets[0][src], outs[0][j], ws, a.group,
+                         mode, int(roles[j]))
             return
-        for j in range(L):  # C4: one batched call per layer over this GPU's requests
-            src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
-            V.nsa_verify_batched(cfg, [caches[r][j] for r in range(R)],
-                                 [batches[r][j] for r in range(R)], [sets[r][src] for r in range(R)],
-                                 [outs[r][j] for r in range(R)], ws, a.group, mode,
-                                 [int(roles[j])] * R)
+        # C4: one batched call per layer over this GPU's requests
+        V.nsa_verify_batched(cfg, [caches[r][j] for r in range(R)], [batches[r][j] for r in range(R)],
+                             [sets[r][src] for r in range(R)], [outs[r][j] for r in range(R)], ws,
+                             a.group, mode, [int(roles[j])] * R)
+
+    def step():
+        for j in range(L):
+            layer(j)
 
     n_refresh = int((roles == V.ROLE_REFRESH).sum())
     launches_per_step = R * (n_refresh * 2 + (L - n_refresh) * 1)  # route + attend, attend
@@ -430,13 +431,46 @@ def run_ours(a):
     h2d = sum(t.numel() * t.element_size() for bufs in hin for t in bufs)
     d2h = sum(t.numel() * t.element_size() for t in hout)
 
-    def e2e_step():
-        for r in range(R):
-            for dst, src in zip(inbufs[r], hin[r]):
-                dst.copy_(src, non_blocking=True)
-        run_step()
+    copy_stream = torch.cuda.Stream(device=dev)
+
+    def e2e_body():
+        # layer j's inputs go up on a copy stream and only layer j waits for
+        # them, so the copies of later layers overlap the kernels of earlier ones
+        cur = torch.cuda.current_stream()
+        copy_stream.wait_stream(cur)
+        ready = []
+        with torch.cuda.stream(copy_stream):
+            for j in range(L):
+                for r in range(R):
+                    for dst, src in zip(inbufs[r], hin[r]):
+                        dst[j].copy_(src[j], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(copy_stream)
+                ready.append(e)
+        for j in range(L):
+            cur.wait_event(ready[j])
+            layer(j)
         for r in range(R):
             hout[r].copy_(outs[r][L - 1], non_blocking=True)
+
+    e2e_graph = None
+    if not a.no_graph:
+        e2e_body()
+        torch.cuda.synchronize()
+        e2e_graph = torch.cuda.CUDAGraph()
+        s_cap = torch.cuda.Stream(device=dev)
+        s_cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_cap):
+            with torch.cuda.graph(e2e_graph, stream=s_cap):
+                e2e_body()
+        torch.cuda.current_stream().wait_stream(s_cap)
+        torch.cuda.synchronize()
+
+    def e2e_step():
+        if e2e_graph is not None:
+            e2e_graph.replay()
+        else:
+            e2e_body()
 
     for _ in range(max(1, a.warmup)):
         e2e_step()

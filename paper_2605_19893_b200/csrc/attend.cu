@@ -81,7 +81,12 @@ enum TileKind { kTileCmp = 0, kTileTok = 1, kTileTree = 2 };
 
 struct Misc {
   uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], pv_done[2];
-  uint64_t p_full, q_ready, union_ready;
+  // p_full is double-buffered by tile parity like s_full: a softmax warp may
+  // finish tile j + 1 before a slower warp arrives for tile j (tile j + 1 only
+  // needs PV(j - 1)), and a single barrier would then complete tile j's phase
+  // with that warp's P still unwritten (it cannot get two tiles ahead: tile
+  // j + 2 needs PV(j), which needs every tile-j arrival)
+  uint64_t p_full[2], q_ready, union_ready;
   uint32_t tmem_base;
   int32_t n_union, n_tok_tiles;
   int32_t flag;                   // end-of-pass check failed: redo the tiles in the robust pass
@@ -411,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&m.s_free[i], 4 * nch);  // the warps of the active column chunks
         mbar_init(&m.pv_done[i], 1);
       }
-      mbar_init(&m.p_full, 4 * nch);
+      mbar_init(&m.p_full[0], 4 * nch);
+      mbar_init(&m.p_full[1], 4 * nch);
       mbar_init(&m.q_ready, kSoftWarps);
       mbar_init(&m.union_ready, 32);
       m.flag = (p.debug_flags & 1) ? 1 : 0;  // bit 0: force the robust redo (tests)
@@ -716,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&m.p_full);
+        if (lane == 0) mbar_arrive(&m.p_full[J & 1]);
         if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 32 + j] = globaltimer();
       }
       if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 2] = globaltimer();
@@ -844,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; tiles(j); ++j) {
         const int J = J0 + j;
         const int st = J & 1;
-        mbar_sleep_wait(&m.p_full, J & 1);
+        mbar_sleep_wait(&m.p_full[J & 1], (J >> 1) & 1);
         const TileInfo ti = tile_info(m, n_cmp, split + j * S, cwlo, cwhi, p.l_sel);
         mbar_sleep_wait(&m.v_full[st], (J >> 1) & 1);
         if (trace && J < 8) p.trace[cta_id * 64 + 40 + J] = globaltimer();

@@ -326,3 +326,24 @@ def test_verify_batched_validates_before_launch():
     assert e.value.code == 1
     torch.cuda.synchronize()
     assert bool((outs[0] == 7.0).all())
+
+
+def test_c3_compressed_branch_repeated_fresh_caches(oracle_lib):
+    """Regression: the attend kernel's per-tile P hand-off (p_full) once let a
+    softmax warp running a tile ahead complete the previous tile's phase, so
+    the PV MMA read another warp's P before it was written -- intermittently,
+    mostly in the compressed branch of multi-chunk launches (33 queries = 3
+    column chunks).  Repeated fresh runs with compressed-only gates; before
+    the fix ~8% of runs failed (tools/stress_c3.py)."""
+    cfg = O.llama_config(32)
+    x = LayerInputs(cfg, 65536, 32, 3232, parent_slot=TREE32)
+    x.gates = np.zeros_like(x.gates)
+    x.gates[:, :, 0] = 1.0
+    ref = None
+    for _ in range(12):
+        case = DeviceCase(cfg, x)
+        out, _ = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+        if ref is None:
+            ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)["out"]
+        per, l2 = rel_errors(out, ref)
+        assert per <= TOL and l2 <= TOL, (per, l2)
