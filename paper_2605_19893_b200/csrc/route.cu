@@ -177,7 +177,11 @@ __device__ void stage_tile(const RouteParams& p, uint8_t* smem, const Item& I, i
       if (r < I.nrows) {
         const int rr = I.r0 + r;
         const int h = I.kvh * p.G + (rr & (p.G - 1));
+#ifdef ROUTE_DIAG_NO_Q  // timing diagnostics only: no q loads
+        v[u] = make_float4(1e-3f * x4, 1.f, 0.5f, -0.25f + h);
+#else
         v[u] = __ldg(reinterpret_cast<const float4*>(p.q + ((int64_t)p.slot_q[rr / p.G] * p.Hq + h) * dh) + x4);
+#endif
       }
     }
   }

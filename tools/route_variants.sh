@@ -14,14 +14,19 @@ build() {  # name, extra nvcc flags
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $d/libspecsv_b200.so $d/obj/*.o
 }
 if [ "$1" = "build" ]; then
-  build base ""
-  build bconst "-DROUTE_DIAG_B_CONST"
-  build noexp "-DROUTE_DIAG_NO_EXP"
-  build ks16 "-DROUTE_DIAG_KSTEPS=16"
-  build ks0 "-DROUTE_DIAG_KSTEPS=0"
+  for v in ${VARIANTS:-base bconst noexp ks16 ks0 noq}; do
+    case $v in
+      base) build base "";;
+      bconst) build bconst "-DROUTE_DIAG_B_CONST";;
+      noexp) build noexp "-DROUTE_DIAG_NO_EXP";;
+      ks16) build ks16 "-DROUTE_DIAG_KSTEPS=16";;
+      ks0) build ks0 "-DROUTE_DIAG_KSTEPS=0";;
+      noq) build noq "-DROUTE_DIAG_NO_Q";;
+    esac
+  done
   exit 0
 fi
-for v in base bconst noexp ks16 ks0; do
+for v in ${VARIANTS:-base bconst noexp ks16 ks0 noq}; do
   echo "== $v"
   SPECSV_LIB=$OUT/$v/libspecsv_b200.so python tools/trace_route.py 2>&1 | grep -E "staged|computed|tiles done|barrier"
   SPECSV_LIB=$OUT/$v/libspecsv_b200.so python tools/time_route.py 2>&1 | tail -1
