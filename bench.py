@@ -543,6 +543,7 @@ def run_ours(a):
                 "d2h_bytes_per_step": int(d2h)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "frac_vs_spec_8000": achieved / 8000.0,
                      "kernel": "nsa_attend_kernel (fused cmp+slc+win+gate, one launch per layer)",
                      "alg_bytes_per_launch": bytes_att, "launch_ms": attend_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},

@@ -646,6 +646,14 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
       for (int a = 0; a < p.n; ++a) p.idx[(int64_t)q * p.n + a] = -1;
     }
   }
+#ifdef ROUTE_DIAG_TAIL_TWICE  // timing diagnostics only: the trace then shows a warm second pass
+  for (int u = cta; u < units; u += nctas)
+    slot_unit(p, scores_out != nullptr ? scores_slot : u / p.Hkv, u % p.Hkv, smem, scores_out, nullptr);
+  __syncthreads();
+  arrive(bar + 1);
+  wait_all(bar + 1, min(units, nctas));
+  tstamp(tr, 4);
+#endif
   for (int u = cta; u < units; u += nctas)
     slot_unit(p, scores_out != nullptr ? scores_slot : u / p.Hkv, u % p.Hkv, smem, scores_out, tr);
   tstamp(tr, 5);
@@ -655,6 +663,9 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     if (sm100::atom_add_acq_rel_gpu(bar + 2, 1) == unit_ctas - 1) {
       atomicExch(bar, 0);
       atomicExch(bar + 2, 0);
+#ifdef ROUTE_DIAG_TAIL_TWICE
+      atomicExch(bar + 1, 0);
+#endif
     }
   }
 }

@@ -22,6 +22,7 @@ if [ "$1" = "build" ]; then
       ks16) build ks16 "-DROUTE_DIAG_KSTEPS=16";;
       ks0) build ks0 "-DROUTE_DIAG_KSTEPS=0";;
       noq) build noq "-DROUTE_DIAG_NO_Q";;
+      twice) build twice "-DROUTE_DIAG_TAIL_TWICE";;
     esac
   done
   exit 0
