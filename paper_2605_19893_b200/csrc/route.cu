@@ -473,9 +473,11 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
       sm100::cp_async16_zfill(sTM + 2 * e, tm + 2 * e, 16u);
       sm100::cp_async16_zfill(sTD + 2 * e, td + 2 * e, 16u);
     }
+    sm100::cp_async_commit();  // group 1: TM, TD (the F pass below needs only these)
     stage_g(0, min(nt, tc - 1));
+    sm100::cp_async_commit();  // group 2: the first round of G, landing under the F pass
   }
-  sm100::cp_async_wait_all();
+  sm100::cp_async_wait<1>();
   __syncthreads();
   tstamp(tr, 13);
   for (int g = warp; g < G; g += nwarps) {
@@ -496,6 +498,7 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
     for (int t = lane; t < nt; t += 32) sF[g * nt + t] *= inv;
   }
   tstamp(tr, 7);
+  sm100::cp_async_wait<0>();  // this thread's G copies; the round's barrier publishes them all
   // part[b] over rounds of staged tiles: round [T0, T1) computes the blocks
   // [T0 step, T1 step) (the last round: up to avail), from tiles T0 - 1 .. T1 - 1
   // (tile T0 - 1 overhangs into block T0 step)
@@ -527,13 +530,12 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   tstamp(tr, 14);
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
-    const int done = atomicAdd(p.slot_done + slot, 1);
+    // acq_rel: releases this CTA's part writes (ordered before thread 0 by the
+    // barrier above, release is cumulative) and, in the last unit, acquires
+    // every other unit's
+    const int done = sm100::atom_add_acq_rel_gpu(p.slot_done + slot, 1);
     last = done == p.Hkv - 1;
-    if (last) {
-      p.slot_done[slot] = 0;  // self-resetting for the next launch
-      __threadfence();
-    }
+    if (last) p.slot_done[slot] = 0;  // self-resetting; the kernel boundary publishes it
   }
   __syncthreads();
   tstamp(tr, 8);
