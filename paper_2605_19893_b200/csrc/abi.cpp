@@ -90,6 +90,8 @@ int splits_for(const specsv_nsa_config& c, int32_t nq) {
 }
 
 struct Layout {
+  size_t sync_off = 0, sync_bytes = 0;  // attend barrier words: fixed position per config
+  int max_chunks = 1;                   // query chunks of the widest call (kMaxQueries)
   size_t attend_off = 0, attend_bytes = 0;
   size_t E_off = 0, TM_off = 0, TD_off = 0, F_off = 0, sel_off = 0, cnt_off = 0;
   int64_t sel_pad = 0;
@@ -108,14 +110,23 @@ int qc_size_for(const specsv_nsa_config& c) {
 }
 
 Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
-  const int splits = 18;  // upper bound of splits_for()
+  const int splits = 18;  // upper bound of splits_for(); a batched launch keeps R x S <= 18
   Layout L;
   const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
+  L.max_chunks = (kMaxQueries + qc_size_for(c) - 1) / qc_size_for(c);
+  // every self-resetting word (attend barrier sets, routing grid barrier and
+  // per-slot counters) first, at offsets that depend on the config only: a
+  // workspace shared by calls of different query counts or context lengths
+  // must never read one call's data as another call's counter
+  L.sync_off = 0;
+  L.sync_bytes = (size_t)kSyncSets * L.max_chunks * c.n_kv_heads * 2 * sizeof(int32_t);
+  L.cnt_off = align_up(L.sync_off + L.sync_bytes, 256);
+  L.attend_off = align_up(L.cnt_off + (4 + kMaxQueries) * sizeof(int32_t), 256);
   L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
   const int64_t maxblk = max_rows >= c.l ? (max_rows - c.l) / c.d + 1 : 0;
   const int64_t m_pad = align_up(std::max<int64_t>(maxblk, 1), kRouteTile);
   const int64_t ntiles = m_pad / kRouteTile;
-  size_t off = align_up(L.attend_bytes, 256);
+  size_t off = align_up(L.attend_off + L.attend_bytes, 256);
   const int64_t gs = ((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 1;  // = g_stride
   L.E_off = off;  // per-tile selection-block shares [nq][ntiles][Hq][gs]
   off = align_up(off + (size_t)nq * ntiles * c.n_q_heads * gs * 8, 256);
@@ -126,8 +137,6 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
   L.F_off = off;  // per-KV-head score shares [nq][Hkv][sel_pad]
   off = align_up(off + (size_t)nq * c.n_kv_heads * L.sel_pad * 8, 256);
-  L.cnt_off = off;  // routing barrier words + per-slot unit counters, zero-filled, self-resetting
-  off = align_up(off + (4 + kMaxQueries) * sizeof(int32_t), 256);
   L.total = off;
   return L;
 }
@@ -226,12 +235,9 @@ void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spec
   cuda_check(launch_route(p, stream, true), "route launch");
 }
 
-void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
-                void* ws, size_t ws_bytes, cudaStream_t stream) {
-  const int S = splits_for(c, a.n_queries);
-  const Layout L = layout_for(c, a.n_queries, kv.rows);
-  if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
-  AttendParams p;
+// everything of one request's attend launch but its workspace slices
+void fill_attend_params(AttendParams& p, const specsv_nsa_config& c, const specsv_layer_kv& kv,
+                        const specsv_verify_args& a, int S) {
   std::memset(&p, 0, sizeof(p));
   const int64_t H = c.n_kv_heads, dh = c.d_head;
   const int32_t gamma = a.n_queries - 1;
@@ -250,13 +256,10 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
   p.out = a.out;
   p.idx = a.idx;
   p.idx_count = a.idx_count;
-  p.ws = static_cast<float*>(ws);
   p.trace = g_trace;
   p.debug_flags = std::getenv("SPECSV_ATTEND_FORCE_ROBUST") != nullptr ? 1 : 0;
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
-  p.ws_o_offset = (int64_t)nchunks * H * S * (3 * kAttendCols * 2);
-  p.ws_sync_offset = (int64_t)(L.attend_bytes / sizeof(float)) - (int64_t)nchunks * H * 2;
   p.nq = a.n_queries;
   p.gamma = gamma;
   p.Hq = (int32_t)c.n_q_heads;
@@ -295,7 +298,62 @@ void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spe
     p.ch_wlo[ch] = wlo;
     p.ch_whi[ch] = whi;
   }
+}
+
+// request r's partial slice (units of the widest request in the launch) and
+// barrier-word set r
+void set_attend_ws(AttendParams& p, const Layout& L, char* ws, int r, int chunks, int S, int64_t H) {
+  const int64_t units = (int64_t)chunks * H * S;
+  float* base = reinterpret_cast<float*>(ws + L.attend_off);
+  p.ws = base + r * units * (3 * kAttendCols * 2 + 3 * kAttendCols * kAttendDh);
+  p.ws_o_offset = units * (3 * kAttendCols * 2);
+  int32_t* sync = reinterpret_cast<int32_t*>(ws + L.sync_off) + (int64_t)r * L.max_chunks * H * 2;
+  p.ws_sync_offset = reinterpret_cast<float*>(sync) - p.ws;
+}
+
+void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+                void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const int S = splits_for(c, a.n_queries);
+  const Layout L = layout_for(c, a.n_queries, kv.rows);
+  if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
+  AttendParams p;
+  fill_attend_params(p, c, kv, a, S);
+  const int nchunks = (a.n_queries + p.qc_size - 1) / p.qc_size;
+  set_attend_ws(p, L, static_cast<char*>(ws), 0, nchunks, S, c.n_kv_heads);
   cuda_check(launch_attend(p, nchunks, stream), "attend launch");
+}
+
+// One attend launch per kAttendBatch requests: S splits per head with
+// R x S <= 18 (the workspace's partial region) and, when S > 1, the grid
+// co-resident (cooperative); S = 1 needs no cross-CTA merge and may span waves.
+void run_attend_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
+                        const specsv_verify_args* args, int32_t batch, void* ws, size_t ws_bytes,
+                        cudaStream_t stream) {
+  const int qc = qc_size_for(c);
+  const int64_t H = c.n_kv_heads;
+  thread_local AttendBatch b;  // ~31 KB host staging of the launch parameters (copied at launch)
+  for (int32_t b0 = 0; b0 < batch; b0 += kAttendBatch) {
+    const int R = std::min<int32_t>(kAttendBatch, batch - b0);
+    int32_t max_nq = 1;
+    int64_t max_rows = 0;
+    for (int r = 0; r < R; ++r) {
+      max_nq = std::max(max_nq, args[b0 + r].n_queries);
+      max_rows = std::max(max_rows, kvs[b0 + r].rows);
+    }
+    const int chunks = (max_nq + qc - 1) / qc;
+    const Layout L = layout_for(c, max_nq, max_rows);
+    if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
+    const int groups = (int)H * chunks * R;
+    const int S = std::max(1, std::min({18 / R, coresident_for_device() / groups, 18}));
+    std::memset(&b, 0, sizeof(b));
+    b.n_req = R;
+    b.n_chunks = chunks;
+    for (int r = 0; r < R; ++r) {
+      fill_attend_params(b.req[r], c, kvs[b0 + r], args[b0 + r], S);
+      set_attend_ws(b.req[r], L, static_cast<char*>(ws), r, chunks, S, H);
+    }
+    cuda_check(launch_attend_batch(b, S, S > 1, stream), "batched attend launch");
+  }
 }
 
 }  // namespace
@@ -377,10 +435,9 @@ specsv_status specsv_nsa_verify_batched(const specsv_nsa_config* cfg, const spec
     // validate the whole batch before the first launch: a bad request must not
     // leave the ones before it half-verified
     for (int32_t b = 0; b < batch; ++b) validate_args(*cfg, kvs[b], args[b]);
-    for (int32_t b = 0; b < batch; ++b) {
+    for (int32_t b = 0; b < batch; ++b)  // routing launches (stream order: each reuses the region)
       if (args[b].role == SPECSV_ROLE_REFRESH) run_route(*cfg, kvs[b], args[b], ws, ws_bytes, s);
-      run_attend(*cfg, kvs[b], args[b], ws, ws_bytes, s);
-    }
+    run_attend_batched(*cfg, kvs, args, batch, ws, ws_bytes, s);
   });
 }
 

@@ -330,8 +330,10 @@ __device__ __forceinline__ void write_p(uint8_t* pdst, int row, int c0, int nqk,
 // in pass 1 (robust) with the classic lazily-raised running max.
 constexpr float kFastHi = 48.0f;
 
-__global__ void __launch_bounds__(kThreads, 1)
-    nsa_attend_kernel(const __grid_constant__ AttendParams p) {
+// One CTA: split `split` of KV head `kvh` for query chunk `chunk` of the
+// request `p` (the single-request and the batched kernels below).
+__device__ __forceinline__ void attend_cta(const AttendParams& p, const int split, const int kvh,
+                                           const int chunk, const int cta_id) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the shared window without leaving the shared address space
   // (a uintptr_t round trip would turn every Misc access into a generic load)
@@ -341,11 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int split = blockIdx.x;
-  const int kvh = blockIdx.y;
-  const int chunk = blockIdx.z;
   const int S = p.n_splits;
-  const int cta_id = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   const int q0 = chunk * p.qc_size;
   const int nqc = min(p.qc_size, p.nq - q0);
   const int ncols = nqc * p.G;
@@ -1010,13 +1008,51 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+__global__ void __launch_bounds__(kThreads, 1)
+    nsa_attend_kernel(const __grid_constant__ AttendParams p) {
+  attend_cta(p, blockIdx.x, blockIdx.y, blockIdx.z,
+             (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+}
+
+// Many requests of one layer in one launch (specsv_nsa_verify_batched): grid
+// (splits, Hkv, requests x chunks).  With fewer splits per head the fixed
+// per-launch costs (prologue, split merge) amortise over the requests; at one
+// split per head there is no cross-CTA merge and the grid may span waves.
+__global__ void __launch_bounds__(kThreads, 1)
+    nsa_attend_batch_kernel(const __grid_constant__ AttendBatch b) {
+  const int r = blockIdx.z / b.n_chunks, chunk = blockIdx.z % b.n_chunks;
+  if (r >= b.n_req) return;
+  const AttendParams& p = b.req[r];
+  if (chunk * p.qc_size >= p.nq) return;  // this request has fewer query chunks
+  attend_cta(p, blockIdx.x, blockIdx.y, chunk,
+             (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+}
+
 }  // namespace
 
 size_t attend_smem_bytes() { return kOffMisc + sizeof(Misc) + 1024; }
 
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits) {
   const size_t units = (size_t)n_chunks * hkv * n_splits;
-  return units * (3 * kCols * 2) + units * (3 * kCols * kDh) + (size_t)n_chunks * hkv * 2;
+  return units * (3 * kCols * 2) + units * (3 * kCols * kDh);  // split partials (m, l), O
+}
+
+cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, bool cooperative,
+                                cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(nsa_attend_batch_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem_bytes());
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_splits, b.req[0].Hkv, b.n_req * b.n_chunks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = attend_smem_bytes();
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // split CTAs of a head meet at a barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = cooperative ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, nsa_attend_batch_kernel, b);
 }
 
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream) {

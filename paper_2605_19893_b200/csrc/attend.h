@@ -9,6 +9,7 @@
 namespace specsv_b200 {
 
 constexpr int kAttendCols = 48;     // query columns (queries x GQA heads) per attend CTA
+constexpr int kAttendDh = 128;      // d_head of this build (host-checked)
 constexpr int kMaxQueries = 65;      // 1 + gamma, gamma <= 64 (one mask word per row)
 constexpr int kMaxChunkQ = 32;       // queries per CTA column chunk (64 cols / G, G >= 2)
 constexpr int kMaxUnion = 1280;      // union blocks per chunk
@@ -50,9 +51,23 @@ struct AttendParams {
   int32_t ch_whi[kMaxQueries];
 };
 
+// Requests per batched attend launch: 8 x sizeof(AttendParams) (~3.8 KB)
+// fits the 32 KB kernel-parameter space (tensor maps must stay in param space).
+constexpr int kAttendBatch = 8;
+// Barrier-word sets in the workspace (request r of a batched launch uses set
+// r, a single-request call set 0); the region sits at a fixed workspace offset
+// for a given config, so calls with different query counts can share it.
+constexpr int kSyncSets = 18;
+struct AttendBatch {
+  AttendParams req[kAttendBatch];
+  int32_t n_req, n_chunks;  // grid z = n_req x n_chunks (the widest request's chunks)
+};
+
 size_t attend_smem_bytes();
-size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits);
+size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits);  // split partials only
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream);
+cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, bool cooperative,
+                                cudaStream_t stream);
 int attend_max_coresident();
 
 // ---- routing (route.cu) -------------------------------------------------------

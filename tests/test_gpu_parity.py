@@ -347,3 +347,46 @@ def test_c3_compressed_branch_repeated_fresh_caches(oracle_lib):
             ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)["out"]
         per, l2 = rel_errors(out, ref)
         assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_verify_batched_many_requests_one_launch(oracle_lib):
+    """10 requests (batched attend launches of 8 + 2, fewer splits per head)
+    against the same requests through single calls, and 3 against the oracle."""
+    cfg = O.llama_config(4)
+    specs = [(1000 + 350 * r, 4 if r % 2 else 8) for r in range(10)]
+    cases = [DeviceCase(cfg, LayerInputs(cfg, rows, g, 700 + r)) for r, (rows, g) in enumerate(specs)]
+    singles = [c.run(4, V.MODE_EXACT, V.ROLE_REFRESH) for c in cases]
+    sets = [V.IndexSets.empty(c.nq, cfg.n) for c in cases]
+    outs = [torch.zeros(c.nq, cfg.n_q_heads, cfg.d_head, device="cuda") for c in cases]
+    ws = V.Workspace(cases[0].vcfg, max(c.nq for c in cases), max(c.x.k.shape[0] for c in cases))
+    V.nsa_verify_batched(cases[0].vcfg, [c.cache for c in cases], [c.batch for c in cases], sets,
+                         outs, ws, 4, V.MODE_EXACT)
+    torch.cuda.synchronize()
+    for r, case in enumerate(cases):
+        s_out, s_sets = singles[r]
+        gi, gc, gf = sets_to_numpy(sets[r])
+        si, sc, sf = sets_to_numpy(s_sets)
+        assert np.array_equal(gi, si) and np.array_equal(gc, sc) and np.array_equal(gf, sf)
+        got = outs[r].cpu().numpy().astype(np.float64)
+        assert np.abs(got - s_out).max() <= 1e-4 * max(np.abs(s_out).max(), 1e-6), r
+        if r in (0, 5, 9):
+            ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+            per, l2 = rel_errors(got, ref["out"])
+            assert per <= TOL and l2 <= TOL, (r, per, l2)
+
+
+def test_workspace_shared_across_query_counts(oracle_lib):
+    """One workspace for calls with 33, 9 and 1 queries and a batched call:
+    the attend barrier words sit at a fixed workspace offset, so a call never
+    reads another call's partials as barrier words."""
+    cfg = O.llama_config(4)
+    vcfg = V.NsaConfig(**cfg.__dict__)
+    ws = V.Workspace(vcfg, 65, 9000)
+    for rows, g, parents in ((8192, 32, TREE32), (3000, 8, None), (2000, 0, None), (8192, 32, TREE32)):
+        x = LayerInputs(cfg, rows, g, 60 + g + rows, parent_slot=parents)
+        case = DeviceCase(cfg, x)
+        case.ws = ws
+        out, sets = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+        ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+        per, l2 = rel_errors(out, ref["out"])
+        assert per <= TOL and l2 <= TOL, (rows, g, per, l2)
