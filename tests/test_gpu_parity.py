@@ -390,3 +390,53 @@ def test_workspace_shared_across_query_counts(oracle_lib):
         ref = case.oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
         per, l2 = rel_errors(out, ref["out"])
         assert per <= TOL and l2 <= TOL, (rows, g, per, l2)
+
+
+OTHER_CONFIGS = [
+    # GQA group 2, wider window, more selected blocks, shorter lag
+    dict(l=32, d=16, l_sel=64, n=24, w=1024, n_q_heads=8, n_kv_heads=4, d_head=128, routing_lag=8),
+    # GQA group 8, fewer selected blocks, narrow window
+    dict(l=32, d=16, l_sel=64, n=8, w=256, n_q_heads=16, n_kv_heads=2, d_head=128, routing_lag=16),
+    # GQA group 16, longer compression blocks
+    dict(l=64, d=16, l_sel=64, n=16, w=512, n_q_heads=16, n_kv_heads=1, d_head=128, routing_lag=16),
+    # GQA group 32 (one query per column chunk)
+    dict(l=32, d=16, l_sel=64, n=16, w=512, n_q_heads=32, n_kv_heads=1, d_head=128, routing_lag=16),
+]
+
+
+@pytest.mark.parametrize("ci", range(len(OTHER_CONFIGS)))
+@pytest.mark.parametrize("mode", [O.MODE_EXACT, O.MODE_APPROX])
+def test_verify_other_nsa_configs(oracle_lib, ci, mode):
+    """Configs beyond the Llama shape that this build accepts (GQA groups 2 to
+    32, n, w, lag, l/d): indices and outputs against the oracle, refresh then
+    reuse, on a tree draft."""
+    cfg = O.NsaConfig(n_layers=4, **OTHER_CONFIGS[ci])
+    x = LayerInputs(cfg, 5000, 8, 900 + ci, parent_slot=TREE8)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(2, mode, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 2, mode, O.ROLE_REFRESH)
+    assert ref["rc"] == 0
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+    y = LayerInputs(cfg, 5000, 8, 950 + ci, parent_slot=TREE8)
+    case2 = DeviceCase(cfg, y)
+    out2, _ = case2.run(2, mode, V.ROLE_REUSE, sets=sets)
+    ref2 = case2.oracle(oracle_lib, 2, mode, O.ROLE_REUSE, idx=ref["idx"],
+                        idx_count=ref["idx_count"], idx_forced=ref["idx_forced"])
+    per, l2 = rel_errors(out2, ref2["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_config_beyond_build_limits_is_rejected():
+    """A valid reference config this build does not cover (l=64, d=32: one
+    16-block routing tile would touch more than 8 selection blocks) fails
+    with EUNSUPPORTED before any launch, not with wrong results."""
+    cfg = O.NsaConfig(n_layers=2, l=64, d=32, l_sel=64, n=16, w=512, n_q_heads=16, n_kv_heads=1,
+                      d_head=128, routing_lag=16)
+    x = LayerInputs(cfg, 3000, 2, 5)
+    case = DeviceCase(cfg, x)
+    with pytest.raises(V.SpecsvError) as e:
+        case.run(1, V.MODE_EXACT, V.ROLE_REFRESH)
+    assert e.value.code == 3
