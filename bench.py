@@ -278,7 +278,7 @@ def run_ours(a):
         batches.append(br)
         sets.append(sr)
         outs.append(orr)
-    ws = V.Workspace(cfg, nq, a.ctx, device=dev)
+    ws = V.Workspace(cfg, nq, a.ctx, device=dev, batch=min(R, 16))  # C4: batched routing
     torch.cuda.synchronize()
 
     def layer(j):

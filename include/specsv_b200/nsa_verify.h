@@ -134,6 +134,13 @@ specsv_status specsv_validate_config(const specsv_nsa_config* cfg);
 size_t specsv_verify_workspace_size(const specsv_nsa_config* cfg, int32_t n_queries,
                                     int64_t max_rows);
 
+/* Workspace for specsv_nsa_verify_batched that routes up to `batch` (<= 16)
+ * REFRESH requests in one launch (each needs its own routing regions).  Any
+ * workspace of at least specsv_verify_workspace_size works; a larger one lets
+ * more requests share a routing launch. */
+size_t specsv_verify_workspace_size_batched(const specsv_nsa_config* cfg, int32_t n_queries,
+                                            int64_t max_rows, int32_t batch);
+
 /* ---- the hot path ------------------------------------------------------ */
 /* Full per-layer verify: REFRESH = routing launch(es) + fused downstream
  * launch; REUSE = one fully fused launch. */

@@ -21,7 +21,8 @@ MAX_PAIRS = 128
 
 EXPORTED = (
     "specsv_abi_version", "specsv_last_error", "specsv_validate_config",
-    "specsv_verify_workspace_size", "specsv_nsa_verify", "specsv_nsa_verify_batched",
+    "specsv_verify_workspace_size", "specsv_verify_workspace_size_batched", "specsv_nsa_verify",
+    "specsv_nsa_verify_batched",
     "specsv_nsa_route", "specsv_nsa_attend_fused", "specsv_nsa_scores", "specsv_select_blocks",
     "specsv_compress_append", "specsv_resolve_layer_roles", "specsv_clamp_inherited",
     "specsv_load_stats", "specsv_algorithmic_bytes", "specsv_debug_attend_trace",
@@ -95,6 +96,7 @@ def lib() -> C.CDLL:
         "specsv_last_error": ([], C.c_char_p),
         "specsv_validate_config": ([cfgp], C.c_int),
         "specsv_verify_workspace_size": ([cfgp, i32, i64], sz),
+        "specsv_verify_workspace_size_batched": ([cfgp, i32, i64, i32], sz),
         "specsv_nsa_verify": ([cfgp, kvp, argp, vp, sz, vp], C.c_int),
         "specsv_nsa_verify_batched": ([cfgp, kvp, argp, i32, vp, sz, vp], C.c_int),
         "specsv_nsa_route": ([cfgp, kvp, argp, vp, sz, vp], C.c_int),

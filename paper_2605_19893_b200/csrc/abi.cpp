@@ -89,6 +89,9 @@ int splits_for(const specsv_nsa_config& c, int32_t nq) {
   return std::max(1, std::min(18, coresident_for_device() / groups));
 }
 
+// routing counter set: [0] tiles done, [2] tail CTAs done, [4..] per-slot units
+constexpr int kCntSetInts = 4 + kMaxQueries;
+
 struct Layout {
   size_t sync_off = 0, sync_bytes = 0;  // attend barrier words: fixed position per config
   int max_chunks = 1;                   // query chunks of the widest call (kMaxQueries)
@@ -121,7 +124,7 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   L.sync_off = 0;
   L.sync_bytes = (size_t)kSyncSets * L.max_chunks * c.n_kv_heads * 2 * sizeof(int32_t);
   L.cnt_off = align_up(L.sync_off + L.sync_bytes, 256);
-  L.attend_off = align_up(L.cnt_off + (4 + kMaxQueries) * sizeof(int32_t), 256);
+  L.attend_off = align_up(L.cnt_off + (size_t)kSyncSets * kCntSetInts * sizeof(int32_t), 256);
   L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
   const int64_t maxblk = max_rows >= c.l ? (max_rows - c.l) / c.d + 1 : 0;
   const int64_t m_pad = align_up(std::max<int64_t>(maxblk, 1), kRouteTile);
@@ -224,6 +227,55 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
   p.counters = reinterpret_cast<int32_t*>(ws + L.cnt_off);
   p.slot_done = p.counters + 4;
   return p;
+}
+
+void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+               void* ws, size_t ws_bytes, cudaStream_t stream);
+
+// bytes of one request's routing regions (E, TM, TD, F); a batched routing
+// launch places request q's at E_off + q x route_bytes
+size_t route_bytes(const Layout& L) { return L.total - L.E_off; }
+
+// routing of the REFRESH requests of a batch: one cooperative launch per
+// group of up to kRouteBatch requests whose regions fit the workspace
+// (specsv_verify_workspace_size_batched); a group of one is the single path
+void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
+                       const specsv_verify_args* args, int32_t batch, void* ws, size_t ws_bytes,
+                       cudaStream_t stream) {
+  std::vector<int32_t> refresh;
+  int32_t max_nq = 1;
+  int64_t max_rows = 0;
+  for (int32_t b = 0; b < batch; ++b)
+    if (args[b].role == SPECSV_ROLE_REFRESH) {
+      refresh.push_back(b);
+      max_nq = std::max(max_nq, args[b].n_queries);
+      max_rows = std::max(max_rows, kvs[b].rows);
+    }
+  if (refresh.empty()) return;
+  const Layout L = layout_for(c, max_nq, max_rows);
+  if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
+  const size_t cap = 1 + (ws_bytes - L.total) / std::max<size_t>(route_bytes(L), 1);
+  const int group = (int)std::min<size_t>({(size_t)kRouteBatch, (size_t)kSyncSets, cap});
+  char* w = static_cast<char*>(ws);
+  thread_local RouteBatch rb;  // ~20 KB host staging of the launch parameters
+  for (size_t g0 = 0; g0 < refresh.size(); g0 += group) {
+    const int n = (int)std::min<size_t>(group, refresh.size() - g0);
+    if (n == 1) {
+      run_route(c, kvs[refresh[g0]], args[refresh[g0]], ws, ws_bytes, stream);
+      continue;
+    }
+    std::memset(&rb, 0, sizeof(rb));
+    rb.n_req = n;
+    for (int q = 0; q < n; ++q) {
+      const int32_t b = refresh[g0 + q];
+      const auto routed = routed_queries(args[b].n_queries, args[b].pos, args[b].group_size, args[b].mode);
+      rb.req[q] = make_route_params(c, kvs[b], args[b], L, w + (size_t)q * route_bytes(L), routed);
+      rb.req[q].counters = reinterpret_cast<int32_t*>(w + L.cnt_off) + (size_t)q * kCntSetInts;
+      rb.req[q].slot_done = rb.req[q].counters + 4;
+      rb.req[q].trace = nullptr;
+    }
+    cuda_check(launch_route_batch(rb, stream), "batched route launch");
+  }
 }
 
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
@@ -386,6 +438,14 @@ size_t specsv_verify_workspace_size(const specsv_nsa_config* cfg, int32_t n_quer
   return layout_for(*cfg, n_queries, max_rows).total;
 }
 
+size_t specsv_verify_workspace_size_batched(const specsv_nsa_config* cfg, int32_t n_queries,
+                                            int64_t max_rows, int32_t batch) {
+  if (cfg == nullptr || n_queries < 1 || batch < 1) return 0;
+  const Layout L = layout_for(*cfg, n_queries, max_rows);
+  const int32_t r = std::min<int32_t>(batch, std::min(kRouteBatch, kSyncSets));
+  return L.total + (size_t)(r - 1) * route_bytes(L);
+}
+
 specsv_status specsv_nsa_route(const specsv_nsa_config* cfg, const specsv_layer_kv* kv,
                                const specsv_verify_args* args, void* ws, size_t ws_bytes,
                                specsv_stream_t stream) {
@@ -435,8 +495,7 @@ specsv_status specsv_nsa_verify_batched(const specsv_nsa_config* cfg, const spec
     // validate the whole batch before the first launch: a bad request must not
     // leave the ones before it half-verified
     for (int32_t b = 0; b < batch; ++b) validate_args(*cfg, kvs[b], args[b]);
-    for (int32_t b = 0; b < batch; ++b)  // routing launches (stream order: each reuses the region)
-      if (args[b].role == SPECSV_ROLE_REFRESH) run_route(*cfg, kvs[b], args[b], ws, ws_bytes, s);
+    run_route_batched(*cfg, kvs, args, batch, ws, ws_bytes, s);
     run_attend_batched(*cfg, kvs, args, batch, ws, ws_bytes, s);
   });
 }

@@ -103,7 +103,18 @@ struct RouteParams {
 };
 constexpr int kRouteTraceBase = 196608;  // route stamps: trace[kRouteTraceBase + cta * 16 + k]
 
+// Requests per batched routing launch (kernel-parameter space); request q
+// uses its own workspace regions and counter set q (< kSyncSets).
+constexpr int kRouteBatch = 16;
+struct RouteBatch {
+  RouteParams req[kRouteBatch];
+  int32_t n_req;
+  int32_t item_start[kRouteBatch + 1];  // tile work items of requests < q (set at launch)
+  int32_t unit_start[kRouteBatch + 1];  // (slot, KV head) units of requests < q
+};
+
 cudaError_t launch_route(const RouteParams& p, cudaStream_t stream, bool write_idx);
+cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t stream);
 cudaError_t launch_scores_only(const RouteParams& p, double* scores, int slot, cudaStream_t stream);
 cudaError_t launch_select(const double* scores, int avail, int n, int32_t* idx, int32_t* count,
                           uint32_t* forced, cudaStream_t stream);

@@ -672,6 +672,79 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   }
 }
 
+// Many requests' routing in one cooperative launch (specsv_nsa_verify_batched):
+// the tile items of every request share the grid, then ONE grid barrier, then
+// every request's (slot, KV head) units -- the per-launch tail and barrier are
+// paid once per batch instead of once per request.  Request q uses its own
+// workspace regions and counter set (RouteBatch built on the host).
+__device__ __forceinline__ int batch_owner(const int32_t* start, int n_req, int i) {
+  int q = 0;
+  while (q + 1 < n_req && i >= start[q + 1]) ++q;
+  return q;
+}
+
+__global__ void __launch_bounds__(kRouteThreads, 1)
+    route_batch_kernel(const __grid_constant__ RouteBatch b) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int cta = blockIdx.x, nctas = gridDim.x;
+  int* bar = b.req[0].counters;  // [0] tiles done, [2] tail CTAs done; both return to 0
+  const int items = b.item_start[b.n_req];
+  if (items > 0) {
+    const RouteParams& p0 = b.req[0];  // the overlap matrix is a function of the config only
+    double* W = reinterpret_cast<double*>(smem + TileSmem::w);
+    for (int e = threadIdx.x; e < kTB * kWCols; e += kRouteThreads) {
+      const int i = e / kWCols, j = e % kWCols;
+      const int wr = 4 * (i & 3) + (i >> 2);
+      W[wr * kWLd + j] = j < p0.g_stride ? (double)overlap(i, j, p0.d, p0.l, p0.l_sel)
+                                         : (j == p0.g_stride ? 1.0 : 0.0);
+    }
+    for (int r = 0; cta + kItemsPerRound * r * nctas < items; ++r) {
+      Item I[kItemsPerRound];
+      int rq[kItemsPerRound];
+#pragma unroll
+      for (int k = 0; k < kItemsPerRound; ++k) {
+        const int it = cta + (kItemsPerRound * r + k) * nctas;
+        rq[k] = it < items ? batch_owner(b.item_start, b.n_req, it) : 0;
+        const int n_it = b.item_start[rq[k] + 1] - b.item_start[rq[k]];
+        I[k] = item_of(b.req[rq[k]], it < items ? it - b.item_start[rq[k]] : n_it, n_it);
+      }
+      __syncthreads();  // every warp is done with the previous round's tiles
+      const int k = (threadIdx.x >> 5) / kTilesPerItem;
+      stage_tile(b.req[rq[k]], smem, I[k], k);
+      tile_compute(b.req[rq[k]], smem, I[k], k);
+    }
+  }
+  const int units = b.unit_start[b.n_req];
+  arrive(bar);
+  if (cta >= units) return;  // no unit: leave without waiting
+  wait_all(bar, nctas);
+  if (cta == 0) {
+    for (int q = 0; q < b.n_req; ++q) {
+      const RouteParams& p = b.req[q];
+      for (int u = threadIdx.x; u < p.n_unrouted; u += blockDim.x) {
+        const int qq = p.unrouted[u];
+        p.idx_count[qq] = -1;
+        p.idx_forced[qq] = 0u;
+        for (int a = 0; a < p.n; ++a) p.idx[(int64_t)qq * p.n + a] = -1;
+      }
+    }
+  }
+  for (int u = cta; u < units; u += nctas) {
+    const int q = batch_owner(b.unit_start, b.n_req, u);
+    const RouteParams& p = b.req[q];
+    const int lu = u - b.unit_start[q];
+    slot_unit(p, lu / p.Hkv, lu % p.Hkv, smem, nullptr, nullptr);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // the last unit CTA resets the barrier words for the next launch
+    const int unit_ctas = min(units, nctas);
+    if (sm100::atom_add_acq_rel_gpu(bar + 2, 1) == unit_ctas - 1) {
+      atomicExch(bar, 0);
+      atomicExch(bar + 2, 0);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024)
     select_only_kernel(const double* scores, int avail, int n, int32_t* idx, int32_t* count,
                        uint32_t* forced) {
@@ -707,6 +780,32 @@ cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_sl
 }
 
 }  // namespace
+
+cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t s) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  b.item_start[0] = 0;
+  b.unit_start[0] = 0;
+  for (int q = 0; q < b.n_req; ++q) {
+    RouteParams& p = b.req[q];
+    p.chunk_rows = (8 * kMT / p.G) * p.G;
+    if (p.chunk_rows < 1) return cudaErrorInvalidValue;
+    const int rchunks = (p.nr * p.G + p.chunk_rows - 1) / p.chunk_rows;
+    b.item_start[q + 1] = b.item_start[q] + p.Hkv * rchunks * ((p.ntiles + kTilesPerItem - 1) / kTilesPerItem);
+    b.unit_start[q + 1] = b.unit_start[q] + p.nr * p.Hkv;
+  }
+  const int ctas = std::max(1, std::min(sms, std::max(b.item_start[b.n_req], b.unit_start[b.n_req])));
+  const size_t smem = std::max({TileSmem::bytes, kUnitSmem, kTailSmem});
+  cudaError_t e = cudaFuncSetAttribute(route_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  void* args[] = {&b};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(route_batch_kernel), dim3(ctas),
+                                     dim3(kRouteThreads), args, smem, s);
+}
 
 cudaError_t launch_route(const RouteParams& p, cudaStream_t s, bool write_idx) {
   (void)write_idx;

@@ -144,9 +144,15 @@ class DraftBatch:
 
 
 class Workspace:
-    def __init__(self, cfg: NsaConfig, n_queries: int, max_rows: int, device="cuda"):
+    def __init__(self, cfg: NsaConfig, n_queries: int, max_rows: int, device="cuda", batch: int = 1):
+        """batch > 1: room for that many REFRESH requests of nsa_verify_batched
+        to share one routing launch (specsv_verify_workspace_size_batched)."""
         c = cfg.c()
-        self.nbytes = int(lib().specsv_verify_workspace_size(C.byref(c), n_queries, max_rows))
+        if batch > 1:
+            self.nbytes = int(lib().specsv_verify_workspace_size_batched(C.byref(c), n_queries,
+                                                                          max_rows, batch))
+        else:
+            self.nbytes = int(lib().specsv_verify_workspace_size(C.byref(c), n_queries, max_rows))
         # zero-filled once: the library keeps its barrier words consistent afterwards
         self.buf = torch.zeros(max(self.nbytes, 256), dtype=torch.uint8, device=device)
 

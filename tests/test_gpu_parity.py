@@ -350,15 +350,18 @@ def test_c3_compressed_branch_repeated_fresh_caches(oracle_lib):
 
 
 def test_verify_batched_many_requests_one_launch(oracle_lib):
-    """10 requests (batched attend launches of 8 + 2, fewer splits per head)
-    against the same requests through single calls, and 3 against the oracle."""
+    """10 requests (batched routing launches of 6 + 4, batched attend launches
+    of 8 + 2 with fewer splits per head) against the same requests through
+    single calls, and 3 against the oracle."""
     cfg = O.llama_config(4)
     specs = [(1000 + 350 * r, 4 if r % 2 else 8) for r in range(10)]
     cases = [DeviceCase(cfg, LayerInputs(cfg, rows, g, 700 + r)) for r, (rows, g) in enumerate(specs)]
     singles = [c.run(4, V.MODE_EXACT, V.ROLE_REFRESH) for c in cases]
     sets = [V.IndexSets.empty(c.nq, cfg.n) for c in cases]
     outs = [torch.zeros(c.nq, cfg.n_q_heads, cfg.d_head, device="cuda") for c in cases]
-    ws = V.Workspace(cases[0].vcfg, max(c.nq for c in cases), max(c.x.k.shape[0] for c in cases))
+    # a workspace for 6 requests per routing launch: routing groups of 6 + 4
+    ws = V.Workspace(cases[0].vcfg, max(c.nq for c in cases), max(c.x.k.shape[0] for c in cases),
+                     batch=6)
     V.nsa_verify_batched(cases[0].vcfg, [c.cache for c in cases], [c.batch for c in cases], sets,
                          outs, ws, 4, V.MODE_EXACT)
     torch.cuda.synchronize()
