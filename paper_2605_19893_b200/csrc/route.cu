@@ -618,17 +618,21 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
     const int rows_total = p.nr * p.G;
     const int rchunks = (rows_total + p.chunk_rows - 1) / p.chunk_rows;
     const int items = p.Hkv * rchunks * ((p.ntiles + kTilesPerItem - 1) / kTilesPerItem);
-    // rounds of kItemsPerRound items: item cta + (kItemsPerRound r + k) nctas
-    for (int r = 0; cta + kItemsPerRound * r * nctas < items; ++r) {
-      Item I[kItemsPerRound];
-#pragma unroll
-      for (int k = 0; k < kItemsPerRound; ++k) I[k] = item_of(p, cta + (kItemsPerRound * r + k) * nctas, items);
-      __syncthreads();  // every warp is done with the previous round's tiles
+    // item slot k (7 warps) runs items cta + (kItemsPerRound r + k) nctas on its
+    // own barrier; with several rounds, slot 1 starts once slot 0's first
+    // tiles are staged, so one slot's staging overlaps the other's DMMAs
+    const int k = (threadIdx.x >> 5) / kTilesPerItem;
+    const bool offset = cta + kItemsPerRound * nctas < items;  // slot 0 has a second round
+    __syncthreads();  // the overlap matrix is in place
+    if (offset && k == 1) sm100::named_bar_sync(5, kRouteThreads);
+    for (int r = 0; cta + (kItemsPerRound * r + k) * nctas < items; ++r) {
+      const Item I = item_of(p, cta + (kItemsPerRound * r + k) * nctas, items);
+      if (r > 0) sm100::named_bar_sync(3 + k, 32 * kTilesPerItem);  // the slot's previous tiles are done
       if (r < 4) tstamp(tr, 32 + 3 * r);
-      const int k = (threadIdx.x >> 5) / kTilesPerItem;
-      stage_tile(p, smem, I[k], k);
+      stage_tile(p, smem, I, k);
+      if (offset && k == 0 && r == 0) sm100::named_bar_arrive(5, kRouteThreads);
       if (r < 4) tstamp(tr, 33 + 3 * r);
-      tile_compute(p, smem, I[k], k);
+      tile_compute(p, smem, I, k);
       if (r < 4) tstamp(tr, 34 + 3 * r);
     }
     tstamp(tr, 1);
@@ -698,20 +702,18 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
       W[wr * kWLd + j] = j < p0.g_stride ? (double)overlap(i, j, p0.d, p0.l, p0.l_sel)
                                          : (j == p0.g_stride ? 1.0 : 0.0);
     }
-    for (int r = 0; cta + kItemsPerRound * r * nctas < items; ++r) {
-      Item I[kItemsPerRound];
-      int rq[kItemsPerRound];
-#pragma unroll
-      for (int k = 0; k < kItemsPerRound; ++k) {
-        const int it = cta + (kItemsPerRound * r + k) * nctas;
-        rq[k] = it < items ? batch_owner(b.item_start, b.n_req, it) : 0;
-        const int n_it = b.item_start[rq[k] + 1] - b.item_start[rq[k]];
-        I[k] = item_of(b.req[rq[k]], it < items ? it - b.item_start[rq[k]] : n_it, n_it);
-      }
-      __syncthreads();  // every warp is done with the previous round's tiles
-      const int k = (threadIdx.x >> 5) / kTilesPerItem;
-      stage_tile(b.req[rq[k]], smem, I[k], k);
-      tile_compute(b.req[rq[k]], smem, I[k], k);
+    const int k = (threadIdx.x >> 5) / kTilesPerItem;  // item slot, as in route_fused_kernel
+    const bool offset = cta + kItemsPerRound * nctas < items;
+    __syncthreads();  // the overlap matrix is in place
+    if (offset && k == 1) sm100::named_bar_sync(5, kRouteThreads);
+    for (int r = 0; cta + (kItemsPerRound * r + k) * nctas < items; ++r) {
+      const int it = cta + (kItemsPerRound * r + k) * nctas;
+      const int q = batch_owner(b.item_start, b.n_req, it);
+      const Item I = item_of(b.req[q], it - b.item_start[q], b.item_start[q + 1] - b.item_start[q]);
+      if (r > 0) sm100::named_bar_sync(3 + k, 32 * kTilesPerItem);
+      stage_tile(b.req[q], smem, I, k);
+      if (offset && k == 0 && r == 0) sm100::named_bar_arrive(5, kRouteThreads);
+      tile_compute(b.req[q], smem, I, k);
     }
   }
   const int units = b.unit_start[b.n_req];
