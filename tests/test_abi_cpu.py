@@ -95,3 +95,24 @@ def test_algorithmic_bytes_counts_union_once():
     tokens = 14 * 64 + 512  # 14 distinct non-window blocks + the window (covers 1022, 1023)
     expect = m * 8 * 128 * 4 + tokens * 8 * 128 * 4 + 8 * 8 * 128 * 4 + 9 * 32 * 128 * 8 + 9 * 32 * 12
     assert b == expect
+
+
+def test_workspace_sizes():
+    """The single-request workspace covers every query count up to 65 at its
+    row bound; the batched size adds one routing region per extra REFRESH
+    request up to the 16 a routing launch takes, and no more."""
+    import ctypes as C
+    L = abi.lib()
+    c = V.NsaConfig(l=32, d=16, l_sel=64, n=16, w=512, n_q_heads=32, n_kv_heads=8, d_head=128,
+                    n_layers=32, routing_lag=16).c()
+    one = L.specsv_verify_workspace_size(C.byref(c), 9, 65536)
+    assert one > 0
+    assert L.specsv_verify_workspace_size(C.byref(c), 65, 65536) >= one
+    assert L.specsv_verify_workspace_size(C.byref(c), 9, 131072) > one
+    assert L.specsv_verify_workspace_size_batched(C.byref(c), 9, 65536, 1) == one
+    sizes = [L.specsv_verify_workspace_size_batched(C.byref(c), 9, 65536, b) for b in (2, 8, 16, 17, 64)]
+    step = sizes[0] - one
+    assert step > 0
+    assert sizes[1] == one + 7 * step and sizes[2] == one + 15 * step
+    assert sizes[3] == sizes[2] and sizes[4] == sizes[2]  # a routing launch takes at most 16
+    assert L.specsv_verify_workspace_size_batched(C.byref(c), 9, 65536, 0) == 0
