@@ -293,7 +293,9 @@ def test_verify_batched_matches_per_request(oracle_lib):
     src = sets_to_numpy(src_sets)
     sets = [V.IndexSets.empty(c.nq, cfg.n) for c in cases[:2]] + [src_sets]
     outs = [torch.zeros(c.nq, cfg.n_q_heads, cfg.d_head, device="cuda") for c in cases]
-    ws = V.Workspace(cases[0].vcfg, max(c.nq for c in cases), max(c.x.k.shape[0] for c in cases))
+    # room for both REFRESH requests in one routing launch (the REUSE one routes nothing)
+    ws = V.Workspace(cases[0].vcfg, max(c.nq for c in cases), max(c.x.k.shape[0] for c in cases),
+                     batch=3)
     V.nsa_verify_batched(cases[0].vcfg, [c.cache for c in cases], [c.batch for c in cases], sets,
                          outs, ws, 4, V.MODE_EXACT, [s[3] for s in specs])
     torch.cuda.synchronize()
