@@ -445,3 +445,29 @@ def test_config_beyond_build_limits_is_rejected():
     with pytest.raises(V.SpecsvError) as e:
         case.run(1, V.MODE_EXACT, V.ROLE_REFRESH)
     assert e.value.code == 3
+
+
+TREE64 = [-1] * 4 + [i // 4 - 1 for i in range(4, 64)]  # 64 nodes, depth <= 3
+
+
+@pytest.mark.parametrize("mode", [O.MODE_EXACT, O.MODE_APPROX])
+def test_verify_max_queries_tree64(oracle_lib, mode):
+    """The largest call this build takes: 1 + 64 queries (six column chunks, a
+    full 64-bit tree-mask word), refresh then reuse, against the oracle."""
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 8192, 64, 6464, parent_slot=TREE64)
+    case = DeviceCase(cfg, x)
+    out, sets = case.run(4, mode, V.ROLE_REFRESH)
+    ref = case.oracle(oracle_lib, 4, mode, O.ROLE_REFRESH)
+    assert ref["rc"] == 0
+    gi, gc, gf = sets_to_numpy(sets)
+    assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0
+    per, l2 = rel_errors(out, ref["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
+    y = LayerInputs(cfg, 8192, 64, 6465, parent_slot=TREE64)
+    case2 = DeviceCase(cfg, y)
+    out2, _ = case2.run(4, mode, V.ROLE_REUSE, sets=sets)
+    ref2 = case2.oracle(oracle_lib, 4, mode, O.ROLE_REUSE, idx=ref["idx"],
+                        idx_count=ref["idx_count"], idx_forced=ref["idx_forced"])
+    per, l2 = rel_errors(out2, ref2["out"])
+    assert per <= TOL and l2 <= TOL, (per, l2)
