@@ -442,7 +442,14 @@ def run_ours(a):
     d2h = sum(t.numel() * t.element_size() for t in hout)
 
     copy_stream = torch.cuda.Stream(device=dev)
-    E2E_GROUP = int(os.environ.get("SPECSV_E2E_GROUP", "4"))  # layers per host->device copy (measured best)
+    # layers per host->device copy: fixed groups (SPECSV_E2E_GROUP=k) or, by
+    # default, geometric 1, 1, 2, 4, ... so layer 0 waits for one small copy
+    e2e_groups, j0 = [], 0
+    fixed = int(os.environ.get("SPECSV_E2E_GROUP", "0"))
+    while j0 < L:
+        size = fixed if fixed > 0 else max(1, j0)
+        e2e_groups.append((j0, min(L, j0 + size)))
+        j0 = min(L, j0 + size)
 
     def e2e_body():
         # layer j's inputs go up on a copy stream and only layer j waits for
@@ -451,16 +458,18 @@ def run_ours(a):
         copy_stream.wait_stream(cur)
         ready = []
         with torch.cuda.stream(copy_stream):
-            for j0 in range(0, L, E2E_GROUP):  # one copy per E2E_GROUP layers' packed rows
+            for j0, j1 in e2e_groups:  # one copy per group of layers' packed rows
                 for r in range(R):
                     for dst, src in zip(inbufs[r], hin[r]):
-                        dst[j0:j0 + E2E_GROUP].copy_(src[j0:j0 + E2E_GROUP], non_blocking=True)
+                        dst[j0:j1].copy_(src[j0:j1], non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(copy_stream)
                 ready.append(e)
+        g = 0
         for j in range(L):
-            if j % E2E_GROUP == 0:
-                cur.wait_event(ready[j // E2E_GROUP])
+            if j == e2e_groups[g][0]:
+                cur.wait_event(ready[g])
+                g = min(g + 1, len(e2e_groups) - 1)
             layer(j)
         for r in range(R):
             hout[r].copy_(outs[r][L - 1], non_blocking=True)
