@@ -471,3 +471,20 @@ def test_verify_max_queries_tree64(oracle_lib, mode):
                         idx_count=ref["idx_count"], idx_forced=ref["idx_forced"])
     per, l2 = rel_errors(out2, ref2["out"])
     assert per <= TOL and l2 <= TOL, (per, l2)
+
+
+def test_exact_grouping_equals_independent_queries():
+    """Exact coarsening is lossless (test_grouped_verifier.cpp:162-182): group
+    sizes C = 2, 4, 8 give the same index sets as C = 1 and outputs equal up to
+    fp32 rounding of the different launch configurations."""
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 6000, 8, 4321, parent_slot=TREE8)
+    case = DeviceCase(cfg, x)
+    base, base_sets = case.run(1, V.MODE_EXACT, V.ROLE_REFRESH)
+    bi, bc, bf = sets_to_numpy(base_sets)
+    scale = max(np.abs(base).max(), 1e-6)
+    for C in (2, 4, 8):
+        out, sets = case.run(C, V.MODE_EXACT, V.ROLE_REFRESH)
+        gi, gc, gf = sets_to_numpy(sets)
+        assert np.array_equal(gi, bi) and np.array_equal(gc, bc) and np.array_equal(gf, bf), C
+        assert np.abs(out - base).max() <= 1e-5 * scale, C
