@@ -1,30 +1,51 @@
 #!/usr/bin/env python3
 """Benchmark of the sparse speculative-verification hot path on B200.
 
-Workload (BASELINE.json configs[1]): Llama-3.1-8B-shaped NSA
+Workloads (BASELINE.json configs), Llama-3.1-8B-shaped NSA
 (32 q / 8 KV heads, d_head 128, l=32, d=16, l_sel=64, n=16, w=512, lag 16),
-64K committed context, 8-token chain draft, bf16 KV, one request per GPU,
-one verify pass over L=32 DISTINCT layer caches per step (the layers run in
-sequence, one C-ABI verify call each, like run_target_pass).  Strategy:
-EXACT grouping (C=4) with the reference's "alt" refresh/reuse schedule
-(layers 1,3,..,31 reuse the preceding layer's index sets).
+8-token chain draft, bf16 KV, EXACT grouping (C=4) with the reference's "alt"
+refresh/reuse schedule (layers 1,3,.. reuse the preceding layer's sets):
 
-A step touches ~10 GB of KV (> 126 MB L2), so successive steps never hit L2
+  C2 (default at 1 GPU; configs[1], the metric's config): 64K committed
+     context, one request per GPU, one verify pass over L=32 DISTINCT layer
+     caches per step (one C-ABI verify call per layer, like run_target_pass).
+     At N GPUs (--workload c2) every rank runs its own request: weak scaling.
+  C4 (default at N>1 GPUs; configs[3]): 128K context, 64 requests in total,
+     4 layer caches per request, sharded over the ranks by request (64/N each,
+     one batched verify call per layer over a rank's requests); with fewer
+     requests than ranks (--total-requests) a request is split by KV-head
+     group (routing replicated, sharding.shard_plan).  Strong scaling: the
+     total work is fixed.
+
+A step touches GBs of KV (>> the 126 MB L2), so successive steps never hit L2
 on the same layer.  The step is captured once in a CUDA graph and replayed.
 
-metric: verified query-tokens/s = requests * (1 + gamma) / seconds per step
-(whole job over all GPUs).  `e2e` runs the same step through the public API
-with the step's inputs copied host->device (pinned) and the last layer's
-output copied back inside the timed region.
+metric: verified query-tokens/s = (requests x (1 + gamma)) / seconds per step
+(whole job over all GPUs, max over ranks of the device time).  `e2e` runs
+real steps through the public API: every step copies its inputs host->device
+(pinned), re-issues every layer's C-ABI verify call with the positions and
+committed rows of THAT step (eager: the host work of each call is inside the
+timed region), commits the accepted draft rows (specsv_commit_rows +
+compressed-block append) so the context grows, and reads the last layer's
+output back.
+
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, NCCL; only timing gathers and barriers cross ranks).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
-reference compiled from its sources) on this host's cores, same workload.
+reference compiled from its sources) on this host's cores, same workload,
+rank 0 only.
+--dry-run: the multi-rank orchestration (launch, process group, shard plan,
+barrier, max-over-ranks timing, JSON line) with the GPU step replaced by a
+CPU stand-in -- the gloo CPU test drives this path.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
@@ -35,29 +56,60 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "verified query-tokens/s at 64K ctx, 8-tok draft; achieved HBM GB/s vs peak"
 UNIT = "query-tokens/s"
 
 
-def parse():
+def metric_for(ctx: int, gamma: int) -> str:
+    # the C2 default reproduces BASELINE.json's metric string exactly
+    return (f"verified query-tokens/s at {ctx // 1024}K ctx, {gamma}-tok draft; "
+            "achieved HBM GB/s vs peak")
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ctx", type=int, default=65536)
+    ap.add_argument("--workload", default="auto", choices=["auto", "c2", "c4"],
+                    help="auto: C2 at 1 GPU, C4 at N > 1")
+    ap.add_argument("--ctx", type=int, default=0, help="override the workload's context")
     ap.add_argument("--gamma", type=int, default=8)
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=0, help="override the workload's layer caches")
     ap.add_argument("--mode", default="exact", choices=["exact", "approx"])
     ap.add_argument("--group", type=int, default=4)
     ap.add_argument("--schedule", default="alt")
-    ap.add_argument("--requests", type=int, default=1, help="requests per GPU")
+    ap.add_argument("--requests", type=int, default=0,
+                    help="C2: requests per GPU (default 1)")
+    ap.add_argument("--total-requests", type=int, default=0,
+                    help="C4: requests over all GPUs (default 64)")
+    ap.add_argument("--accept", type=int, default=4,
+                    help="e2e: draft rows accepted (and committed) per step")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-decode-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true")
+    return ap.parse_args(argv)
+
+
+def resolve_workload(a, world: int):
+    """Fill the workload's shape into `a` (explicit flags win)."""
+    w = a.workload if a.workload != "auto" else ("c2" if world == 1 else "c4")
+    a.workload = w
+    if w == "c2":
+        a.ctx = a.ctx or 65536
+        a.layers = a.layers or 32
+        per_gpu = a.requests or 1
+        a.total_requests = a.total_requests or per_gpu * world  # weak: fixed per-GPU work
+        a.scaling = "weak"
+    else:
+        a.ctx = a.ctx or 131072
+        a.layers = a.layers or 4
+        a.total_requests = a.total_requests or 64  # strong: fixed total work
+        a.scaling = "strong"
+    return a
 
 
 def reuse_set(schedule: str, L: int):
@@ -74,19 +126,53 @@ def llama_cfg(L):
                      n_layers=L, routing_lag=16)
 
 
-def workload_config(a, extra=None):
-    name = "C4" if a.requests > 1 else "C2"  # C4: many requests per GPU, batched calls
-    cfg = {"workload": f"{name}: Llama-3.1-8B-shaped NSA verify, {a.ctx // 1024}K ctx, "
-                       f"{a.gamma}-token chain draft, bf16 KV, {a.layers} layers"
-                       + (f", {a.requests} requests per GPU" if a.requests > 1 else ""),
-           "ctx": a.ctx, "draft": "chain", "gamma": a.gamma, "layers": a.layers,
-           "requests_per_gpu": a.requests, "mode": a.mode, "group_size": a.group,
-           "schedule": a.schedule, "heads": "32q/8kv", "d_head": 128,
-           "nsa": "l=32 d=16 l_sel=64 n=16 w=512 lag=16",
-           "l2": "inputs larger than L2 (each step streams every request-layer cache once: GBs, L2 is 126 MB)"}
-    if extra:
-        cfg.update(extra)
-    return cfg
+def parallelism(a, world: int) -> str:
+    if world == 1:
+        return "single GPU"
+    if a.total_requests >= world:
+        return f"request sharding x{world} (no collective on the data path)"
+    return (f"request + KV-head-group sharding x{world} ({a.total_requests} requests, routing "
+            "replicated per head group, no collective on the data path)")
+
+
+def workload_config(a, world: int):
+    """Identical for both arms (the driver compares the dicts)."""
+    name = a.workload.upper()
+    per = a.total_requests / world
+    return {"workload": f"{name}: Llama-3.1-8B-shaped NSA verify, {a.ctx // 1024}K ctx, "
+                        f"{a.gamma}-token chain draft, bf16 KV, {a.layers} layer caches, "
+                        f"{a.total_requests} request(s) over {world} GPU(s)",
+            "ctx": a.ctx, "draft": "chain", "gamma": a.gamma, "layers": a.layers,
+            "total_requests": a.total_requests, "requests_per_gpu": per, "mode": a.mode,
+            "group_size": a.group, "schedule": a.schedule, "heads": "32q/8kv", "d_head": 128,
+            "nsa": "l=32 d=16 l_sel=64 n=16 w=512 lag=16", "parallelism": parallelism(a, world),
+            "l2": "inputs larger than L2 (each step streams every request-layer cache once: GBs, "
+                  "L2 is 126 MB)"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(a, argv) -> int:
+    """--gpus N outside torchrun: one process per GPU under torch.distributed.run
+    (rendezvous on 127.0.0.1); rank 0's JSON line reaches our stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd).returncode
 
 
 # --------------------------------------------------------------------------- CPU
@@ -113,6 +199,14 @@ class CpuReference:
             self.cfg, x0.k, x0.v, ck0, cv0, x0.q, x0.pos, x0.gates.astype(np.float64), x0.tree_k,
             x0.tree_v, x0.tree_mask, a.group, self.mode, O.ROLE_REFRESH)
         self.n_reuse = len(reuse_set(a.schedule, a.layers))
+
+    def describe(self):
+        try:
+            dispatch = self.lib.name
+        except Exception:  # noqa: BLE001 -- the port has no dispatch slot
+            dispatch = "n/a"
+        return {"cpu_model": cpu_model(), "kernel_dispatch": dispatch,
+                "SPECSV_KERNEL": os.environ.get("SPECSV_KERNEL", "(unset: avx2 when available)")}
 
     def measure(self, seconds: float):
         """query-tokens/s for full L-layer steps (schedule's refresh/reuse mix),
@@ -154,12 +248,11 @@ class CpuReference:
                   f"gamma={a.gamma}, {a.mode} C={a.group}; mean refresh {tr * 1e3:.0f} ms, reuse "
                   f"{tu * 1e3:.0f} ms per call per thread) on {self.threads} threads in {el:.1f} s, "
                   f"scaled to {a.layers}-layer steps ({a.layers - self.n_reuse} refresh + "
-                  f"{self.n_reuse} reuse layers)")
+                  f"{self.n_reuse} reuse layers) of one request")
         return rate, sample
 
 
-def run_reference_arm(a):
-    rank = int(os.environ.get("RANK", "0"))
+def run_reference_arm(a, world: int, rank: int):
     if rank != 0:
         return
     threads = a.cpu_threads or os.cpu_count() or 1
@@ -172,13 +265,14 @@ def run_reference_arm(a):
             vals.append(rate)
             sample = sample or smp
     v = float(np.median(vals))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * (1 + a.gamma) / v,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+    line = {"impl": "reference", "metric": metric_for(a.ctx, a.gamma), "value": v, "unit": UNIT,
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * a.total_requests * (1 + a.gamma) / v,
+            "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 U[-1,1] KV/q, bf16-rounded)",
-            "config": workload_config(a),
+            "config": workload_config(a, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": ref.kind,
-                             "sample": sample},
+                             "sample": sample, **ref.describe()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -225,38 +319,84 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def run_ours(a):
+def ncu_traffic(workload: str, n_req_launch: int):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture of the SAME workload (profiles/), or None."""
+    name = "attend_ncu_summary.json" if n_req_launch == 1 else "attend_batch_c4_ncu_summary.json"
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", name)))
+    except (OSError, ValueError):
+        return None, None
+    if prof.get("workload", workload.upper()) != workload.upper():
+        return None, name
+    if int(prof.get("requests_per_launch", 1 if n_req_launch == 1 else 8)) != n_req_launch:
+        return None, name
+    return prof.get("dram_bytes_per_launch"), name
+
+
+def run_dry(a, world: int, rank: int):
+    """The orchestration of run_ours with a CPU stand-in for the GPU step."""
+    import torch.distributed as dist
+
+    from paper_2605_19893_b200 import sharding
+    if world > 1:
+        dist.init_process_group("gloo")
+    shards = sharding.shard_plan(a.total_requests, world, rank, 8)
+    nq = 1 + a.gamma
+    units = sum(s.fraction for s in shards) * nq
+    ms = 1.0 + 0.25 * rank  # stand-in device time: the slowest rank sets the step
+    value, ms_max = sharding.job_throughput(units, ms)
+    plan = [[(s.request, s.head_begin, s.head_count) for s in shards]]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, plan[0])
+        plan = gathered
+    if rank == 0:
+        line = {"metric": metric_for(a.ctx, a.gamma), "value": value, "unit": UNIT,
+                "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max,
+                "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
+                "dtype": "bf16", "data": "dry run (no GPU): CPU stand-in step",
+                "config": workload_config(a, world), "dry_run": True, "shard_plan": plan}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_ours(a, world: int, rank: int, local: int):
     import torch
     import torch.distributed as dist
 
+    from paper_2605_19893_b200 import sharding
+    from paper_2605_19893_b200 import tree as TR
     from paper_2605_19893_b200 import verify as V
+    from paper_2605_19893_b200.workload import chain_tree_mask
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = llama_cfg(a.layers)
     L, g, nq = a.layers, a.gamma, 1 + a.gamma
-    R = a.requests
     mode = V.MODE_EXACT if a.mode == "exact" else V.MODE_APPROX
     roles, source = V.resolve_layer_roles(reuse_set(a.schedule, L), L)
     H, dh, Hq = cfg.n_kv_heads, cfg.d_head, cfg.n_q_heads
-    from paper_2605_19893_b200 import sharding
-    my_requests = sharding.request_shard(world * R, world, rank)  # global ids of this rank
+    shards = sharding.shard_plan(a.total_requests, world, rank, H)
+    R = len(shards)
+    heads = [s.kv_heads() for s in shards]
+    units_this_rank = sum(s.fraction for s in shards) * nq  # query-tokens completed per step
+    extra_rows = (a.warmup + a.steps + 4) * (a.accept + 1)  # e2e steps grow the context
+    cap = a.ctx + extra_rows
     gen = torch.Generator(device=dev)
 
     def urand(*shape, dtype=torch.float32):
         return (torch.rand(*shape, generator=gen, device=dev) * 2 - 1).to(dtype)
 
     pos = np.array([a.ctx - 1 + i for i in range(nq)], np.int64)
-    from paper_2605_19893_b200.workload import chain_tree_mask
     tmask = chain_tree_mask(g)
-    caches, batches, sets, outs, inbufs = [], [], [], [], []
+    caches, batches, sets, outs, inbufs, pes = [], [], [], [], [], []
     for r in range(R):
-        gen.manual_seed(sharding.request_seed(my_requests[r]))
+        gen.manual_seed(sharding.request_seed(shards[r].request))
         # one packed row per layer -- q | gates | draft K | draft V -- so the
         # e2e path moves a layer's inputs with ONE host->device copy
         parts = [((nq, Hq, dh), torch.float32), ((nq, Hq, 3), torch.float32),
@@ -271,16 +411,18 @@ def run_ours(a):
         ga.copy_(torch.rand(L, nq, Hq, 3, generator=gen, device=dev) * 0.6 + 0.2)
         tka.copy_(urand(L, max(g, 1), H, dh, dtype=torch.bfloat16))
         tva.copy_(urand(L, max(g, 1), H, dh, dtype=torch.bfloat16))
-        inbufs.append((packed,))
+        inbufs.append(packed)
+        pe = urand(cfg.l, dh) * 0.1
+        pes.append(pe)
         cr, br, sr, orr = [], [], [], []
         for j in range(L):
-            c = V.LayerCache(cfg, a.ctx, device=dev)
-            c.k.copy_(urand(a.ctx, H, dh, dtype=torch.bfloat16))
-            c.v.copy_(urand(a.ctx, H, dh, dtype=torch.bfloat16))
+            c = V.LayerCache(cfg, cap, device=dev)
+            c.k[:a.ctx].copy_(urand(a.ctx, H, dh, dtype=torch.bfloat16))
+            c.v[:a.ctx].copy_(urand(a.ctx, H, dh, dtype=torch.bfloat16))
             c.rows = a.ctx
-            c.extend_compressed(urand(cfg.l, dh) * 0.1)
+            c.extend_compressed(pe)
             cr.append(c)
-            br.append(V.DraftBatch(pos=pos, tree_mask=tmask, q=qa[j], gates=ga[j],
+            br.append(V.DraftBatch(pos=pos.copy(), tree_mask=tmask, q=qa[j], gates=ga[j],
                                    tree_k=tka[j], tree_v=tva[j]))
             sr.append(V.IndexSets.empty(nq, cfg.n, dev))
             orr.append(torch.zeros(nq, Hq, dh, device=dev))
@@ -288,44 +430,53 @@ def run_ours(a):
         batches.append(br)
         sets.append(sr)
         outs.append(orr)
-    ws = V.Workspace(cfg, nq, a.ctx, device=dev, batch=min(R, 16))  # C4: batched routing
+    ws = V.Workspace(cfg, nq, cap, device=dev, batch=min(R, 16))  # C4: batched routing
     torch.cuda.synchronize()
 
-    def layer(j):
+    def layer(j, role=None):
+        rj = int(roles[j]) if role is None else role
+        # index sets: a refresh layer's own, a reuse layer's source layer's
         src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
         if R == 1:
             V.nsa_verify(cfg, caches[0][j], batches[0][j], sets[0][src], outs[0][j], ws, a.group,
-                         mode, int(roles[j]))
+                         mode, rj, kv_heads=heads[0])
             return
         # C4: one batched call per layer over this GPU's requests
         V.nsa_verify_batched(cfg, [caches[r][j] for r in range(R)], [batches[r][j] for r in range(R)],
                              [sets[r][src] for r in range(R)], [outs[r][j] for r in range(R)], ws,
-                             a.group, mode, [int(roles[j])] * R)
+                             a.group, mode, [rj] * R, kv_heads=heads)
 
     def step():
         for j in range(L):
             layer(j)
 
     n_refresh = int((roles == V.ROLE_REFRESH).sum())
-    launches_per_step = R * (n_refresh * 2 + (L - n_refresh) * 1)  # route + attend, attend
+    att_launches_per_layer = (R + 7) // 8 if R > 1 else 1        # batched attend: 8 requests each
+    route_launches_per_layer = (R + 15) // 16 if R > 1 else 1    # batched routing: 16 each
+    launches_per_step = n_refresh * route_launches_per_layer + L * att_launches_per_layer
+
     def progress(msg):
         if os.environ.get("SPECSV_BENCH_PROGRESS"):
-            print(f"[bench] {msg}", file=sys.stderr, flush=True)
+            print(f"[bench r{rank}] {msg}", file=sys.stderr, flush=True)
+
+    def capture(fn):
+        gph = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            fn()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gph, stream=cs):
+                fn()
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        return gph
 
     for _ in range(2):
         step()
     torch.cuda.synchronize()
     progress("eager steps done")
-    graph = None
-    if not a.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream(device=dev)
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(graph, stream=s):
-                step()
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
+    graph = None if a.no_graph else capture(step)
     progress("step graph captured")
 
     def run_step():
@@ -338,9 +489,6 @@ def run_ours(a):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        return sharding.max_over_ranks(x, dev)
 
     for _ in range(a.warmup):
         run_step()
@@ -355,176 +503,103 @@ def run_ours(a):
             run_step()
         ev1.record(stream)
         barrier()
-    ms = ev0.elapsed_time(ev1) / a.steps
-    ms = max_over_ranks(ms)
-    value = world * R * nq / (ms * 1e-3)
+    ms_rank = ev0.elapsed_time(ev1) / a.steps
+    value, ms = sharding.job_throughput(units_this_rank, ms_rank, dev)
+    progress("timed steps done")
 
-    # ---- kernel-level roofline: the fused attend kernel and the routing
-    # launches, each captured alone over all L layers (same stream, graphs so
-    # host launch overhead does not leak into the device timing)
-    def capture(fn):
-        gph = torch.cuda.CUDAGraph()
-        cs = torch.cuda.Stream(device=dev)
-        cs.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cs):
-            fn()
-            torch.cuda.synchronize()
-            with torch.cuda.graph(gph, stream=cs):
-                fn()
-        torch.cuda.current_stream().wait_stream(cs)
-        torch.cuda.synchronize()
-        return gph
-
+    # ---- kernel-level roofline of the dominant kernel (the fused attend) and
+    # the routing launches, each captured alone over all L layers (graphs on
+    # the launching stream, CUDA events around the replay)
     def attend_all():
         for j in range(L):
-            src = sets[0][j] if roles[j] == V.ROLE_REFRESH else sets[0][int(source[j])]
-            V.attend_fused(cfg, caches[0][j], batches[0][j], src, outs[0][j], ws, a.group, mode,
-                           V.ROLE_REUSE)
+            layer(j, V.ROLE_REUSE)  # reuse = the fused attend launch(es) only
 
-    def route_all():
+    def route_refresh_all():
         for j in range(L):
             if roles[j] == V.ROLE_REFRESH:
-                V.route(cfg, caches[0][j], batches[0][j], sets[0][j], outs[0][j], ws, a.group, mode)
+                layer(j, V.ROLE_REFRESH)
 
-    progress("timed steps done")
     g_att = capture(attend_all)
-    progress("attend graph captured")
-    g_rt = capture(route_all)
-    progress("route graph captured")
-    att_ms, rt_ms = [], []
+    g_rf = capture(route_refresh_all)
+    att_ms, rf_ms = [], []
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     for rep in range(6):
         e[0].record(stream)
         g_att.replay()
         e[1].record(stream)
-        g_rt.replay()
+        g_rf.replay()
         e[2].record(stream)
         torch.cuda.synchronize()
         if rep > 0:
-            att_ms.append(e[0].elapsed_time(e[1]) / L)
-            rt_ms.append(e[1].elapsed_time(e[2]) / max(1, n_refresh))
+            att_ms.append(e[0].elapsed_time(e[1]) / (L * att_launches_per_layer))
+            rf_ms.append(e[1].elapsed_time(e[2]) / max(1, n_refresh))
+    attend_ms = float(np.median(att_ms))                      # per attend launch
+    refresh_layer_ms = float(np.median(rf_ms))                # route + attend of a refresh layer
+    route_ms = (refresh_layer_ms - attend_ms * att_launches_per_layer) / route_launches_per_layer
     progress("kernel timings done")
-    attend_ms = float(np.median(att_ms))
-    route_ms = float(np.median(rt_ms))
-    alg_att, alg_route, uniq = [], [], []
+
+    # ---- algorithmic bytes from the actual index sets, summed over
+    # this rank's requests; KV bytes per verified query vs the no-reuse
+    # per-query decode of the same queries (the north star's counter)
+    alg_att, alg_route, uniq, noreuse = [], [], [], []
     for j in range(L):
-        src = sets[0][j] if roles[j] == V.ROLE_REFRESH else sets[0][int(source[j])]
-        idx = src.idx.cpu().numpy()
-        cnt = src.count.cpu().numpy()
-        b_att = V.algorithmic_bytes(cfg, a.ctx, pos, V.ROLE_REUSE, idx, cnt, mode, a.group)
-        b_ref = V.algorithmic_bytes(cfg, a.ctx, pos, V.ROLE_REFRESH, idx, cnt, mode, a.group)
+        src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
+        b_att = b_route = b_nr = 0
+        for r in range(R):
+            idx = sets[r][src].idx.cpu().numpy()
+            cnt = sets[r][src].count.cpu().numpy()
+            frac = shards[r].fraction
+            ba = V.algorithmic_bytes(cfg, a.ctx, pos, V.ROLE_REUSE, idx, cnt, mode, a.group)
+            bf = V.algorithmic_bytes(cfg, a.ctx, pos, V.ROLE_REFRESH, idx, cnt, mode, a.group)
+            b_att += ba * frac
+            b_route += bf - ba  # routing is replicated on head-group shards
+            for q in range(nq):  # one single-query decode per query, its own set, refresh
+                b_nr += frac * V.algorithmic_bytes(cfg, a.ctx, pos[q:q + 1], V.ROLE_REFRESH,
+                                                   idx[q:q + 1], np.maximum(cnt[q:q + 1], 0),
+                                                   V.MODE_EXACT, 1)
+            if r == 0:
+                uniq.append(len(set(idx[cnt > 0].ravel().tolist()) - {-1}))
         alg_att.append(b_att)
-        alg_route.append(b_ref - b_att)
-        uniq.append(len(set(idx[cnt > 0].ravel().tolist()) - {-1}))
-    bytes_att = float(np.mean(alg_att))
+        alg_route.append(b_route)
+        noreuse.append(b_nr)
+    bytes_att_launch = float(np.mean(alg_att)) / att_launches_per_layer
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bytes_att / (attend_ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "attend_ncu_summary.json")))
-        traffic = prof.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
-    # step-level algorithmic bytes / time
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = ("MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
+                else "B200_PROFILING.md fallback")
+    achieved = bytes_att_launch / (attend_ms * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(a.workload, min(R, 8) if R > 1 else 1)
     step_bytes = sum(alg_att) + sum(alg_route[j] for j in range(L) if roles[j] == V.ROLE_REFRESH)
-
-    # ---- e2e through the public API with host buffers: the step's inputs
-    # (q, gates, draft K/V of every layer) arrive from pinned host memory and
-    # the last layer's output goes back, inside the timed region
-    hin = [tuple(t.cpu().pin_memory() for t in bufs) for bufs in inbufs]
-    hout = [torch.empty(nq, Hq, dh, pin_memory=True) for _ in range(R)]
-    h2d = sum(t.numel() * t.element_size() for bufs in hin for t in bufs)
-    d2h = sum(t.numel() * t.element_size() for t in hout)
-
-    copy_stream = torch.cuda.Stream(device=dev)
-    # layers per host->device copy: fixed groups (SPECSV_E2E_GROUP=k) or, by
-    # default, geometric 1, 1, 2, 4, ... so layer 0 waits for one small copy
-    e2e_groups, j0 = [], 0
-    fixed = int(os.environ.get("SPECSV_E2E_GROUP", "0"))
-    while j0 < L:
-        size = fixed if fixed > 0 else max(1, j0)
-        e2e_groups.append((j0, min(L, j0 + size)))
-        j0 = min(L, j0 + size)
-
-    def e2e_body():
-        # layer j's inputs go up on a copy stream and only layer j waits for
-        # them, so the copies of later layers overlap the kernels of earlier ones
-        cur = torch.cuda.current_stream()
-        copy_stream.wait_stream(cur)
-        ready = []
-        with torch.cuda.stream(copy_stream):
-            for j0, j1 in e2e_groups:  # one copy per group of layers' packed rows
-                for r in range(R):
-                    for dst, src in zip(inbufs[r], hin[r]):
-                        dst[j0:j1].copy_(src[j0:j1], non_blocking=True)
-                e = torch.cuda.Event()
-                e.record(copy_stream)
-                ready.append(e)
-        g = 0
-        for j in range(L):
-            if j == e2e_groups[g][0]:
-                cur.wait_event(ready[g])
-                g = min(g + 1, len(e2e_groups) - 1)
-            layer(j)
-        for r in range(R):
-            hout[r].copy_(outs[r][L - 1], non_blocking=True)
-
-    e2e_graph = None
-    if not a.no_graph:
-        e2e_body()
-        torch.cuda.synchronize()
-        e2e_graph = torch.cuda.CUDAGraph()
-        s_cap = torch.cuda.Stream(device=dev)
-        s_cap.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s_cap):
-            with torch.cuda.graph(e2e_graph, stream=s_cap):
-                e2e_body()
-        torch.cuda.current_stream().wait_stream(s_cap)
-        torch.cuda.synchronize()
-
-    def e2e_step():
-        if e2e_graph is not None:
-            e2e_graph.replay()
-        else:
-            e2e_body()
-
-    for _ in range(max(1, a.warmup)):
-        e2e_step()
-    barrier()
-    t0w = time.perf_counter()
-    ev0.record(stream)
-    for _ in range(a.steps):
-        e2e_step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    wall_ms = (time.perf_counter() - t0w) * 1e3 / a.steps
-    e2e_ms = max_over_ranks(max(ev0.elapsed_time(ev1) / a.steps, wall_ms))
-    e2e_value = world * R * nq / (e2e_ms * 1e-3)
+    step_noreuse = sum(noreuse)
+    q_done = units_this_rank  # query-tokens this rank completes per step
+    kv_per_query = {"verify": step_bytes / q_done, "no_reuse_decode": step_noreuse / q_done,
+                    "ratio": step_noreuse / max(step_bytes, 1.0),
+                    "what": "algorithmic HBM bytes per verified query-token over one step (all "
+                            "layers, routing included): this verify vs 1+gamma independent "
+                            "single-query NSA decodes (own index sets, no cross-query reuse)"}
 
     # ---- per-query NSA decode on the same GPU and caches (north star: verify
-    # >= 3x faster): the 1 + gamma queries as sequential single-query decodes,
-    # every layer refreshing its own indices (C = 1, gamma = 0 per call)
+    # >= 3x faster), request 0: the 1 + gamma queries as sequential
+    # single-query decodes, every layer refreshing its own indices
     decode = None
     if not a.skip_decode_baseline:
-        ws1 = V.Workspace(cfg, 1, a.ctx, device=dev)
+        ws1 = V.Workspace(cfg, 1, cap, device=dev)
         pos1 = np.array([a.ctx - 1], np.int64)
-        from paper_2605_19893_b200.workload import chain_tree_mask as _ctm
         dq = []
         for j in range(L):
             for i in range(nq):
-                b1 = V.DraftBatch(pos=pos1, tree_mask=_ctm(0), q=batches[0][j].q[i:i + 1],
+                b1 = V.DraftBatch(pos=pos1, tree_mask=chain_tree_mask(0), q=batches[0][j].q[i:i + 1],
                                   gates=batches[0][j].gates[i:i + 1], tree_k=None, tree_v=None)
-                dq.append((j, b1, V.IndexSets.empty(1, cfg.n, dev),
-                           torch.zeros(1, Hq, dh, device=dev)))
+                dq.append((j, b1, V.IndexSets.empty(1, cfg.n, dev), torch.zeros(1, Hq, dh, device=dev)))
 
         def decode_all():
             for j, b1, s1, o1 in dq:
-                V.nsa_verify(cfg, caches[0][j], b1, s1, o1, ws1, 1, V.MODE_EXACT, V.ROLE_REFRESH)
+                V.nsa_verify(cfg, caches[0][j], b1, s1, o1, ws1, 1, V.MODE_EXACT, V.ROLE_REFRESH,
+                             kv_heads=heads[0])
 
         g_dec = capture(decode_all)
         dsteps = max(2, a.steps // 4)
@@ -536,15 +611,92 @@ def run_ours(a):
             g_dec.replay()
         ev1.record(stream)
         torch.cuda.synchronize()
-        dms = max_over_ranks(ev0.elapsed_time(ev1) / dsteps)
-        dval = world * nq / (dms * 1e-3)  # one request's 1 + gamma queries per decode step
-        decode = {"value": dval, "unit": UNIT, "ms_per_step": dms,
+        dms = ev0.elapsed_time(ev1) / dsteps
+        dbytes = 0
+        for j, b1, s1, o1 in dq:
+            dbytes += shards[0].fraction * V.algorithmic_bytes(
+                cfg, a.ctx, pos1, V.ROLE_REFRESH, s1.idx.cpu().numpy(),
+                np.maximum(s1.count.cpu().numpy(), 0), V.MODE_EXACT, 1)
+        dgbs = dbytes / (dms * 1e-3) / 1e9
+        verify_ms_one_request = ms_rank / R
+        decode = {"value": nq * shards[0].fraction / (dms * 1e-3), "unit": UNIT, "ms_per_step": dms,
                   "what": f"{nq} sequential single-query NSA decodes per layer (C=1, gamma=0, "
-                          f"refresh every layer), {L} layers, same GPU and caches",
-                  "verify_speedup": (value / (world * R)) / dval}
+                          f"refresh every layer), {L} layers, request 0 of rank 0, same GPU and caches",
+                  "verify_speedup": dms / verify_ms_one_request,
+                  "roofline": {"achieved": dgbs, "peak": peak, "unit": "GB/s", "frac": dgbs / peak,
+                               "alg_bytes_per_step": dbytes}}
+        progress("decode baseline done")
+
+    # ---- e2e through the public API on REAL steps: each step copies its inputs
+    # from pinned host memory, re-issues every layer's verify call with this
+    # step's positions and rows (eager: host work in the timed region), commits
+    # `accept` draft rows + the next root into every layer (the context grows)
+    # and reads the last layer's output back
+    hin = [t.cpu().pin_memory() for t in inbufs]
+    hout = [torch.empty(nq, Hq, dh, pin_memory=True) for _ in range(R)]
+    h2d = sum(t.numel() * t.element_size() for t in hin)
+    d2h = sum(t.numel() * t.element_size() for t in hout)
+    acc = max(0, min(a.accept, g))
+    slots = list(range(acc)) + ([acc] if acc < g else [])  # accepted drafts, then the bonus root's row
+    host_s = [0.0]
+    n_calls = [0]
+    copy_stream = torch.cuda.Stream(device=dev)
+    # layers per host->device copy: geometric 1, 1, 2, 4, ... so layer 0 waits
+    # for one small copy and later copies overlap earlier layers' kernels
+    groups, j0 = [], 0
+    while j0 < L:
+        groups.append((j0, min(L, j0 + max(1, j0))))
+        j0 = groups[-1][1]
+
+    def e2e_step():
+        cur = torch.cuda.current_stream()
+        copy_stream.wait_stream(cur)  # the previous step's readers of the inputs are done
+        ready = []
+        with torch.cuda.stream(copy_stream):
+            for g0, g1 in groups:
+                for r in range(R):
+                    inbufs[r][g0:g1].copy_(hin[r][g0:g1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                ready.append(ev)
+        gi = 0
+        for j in range(L):
+            if gi < len(groups) and j == groups[gi][0]:
+                cur.wait_event(ready[gi])
+                gi += 1
+            t0 = time.perf_counter()
+            layer(j)
+            host_s[0] += time.perf_counter() - t0
+            n_calls[0] += 1
+        for r in range(R):
+            hout[r].copy_(outs[r][L - 1], non_blocking=True)
+        if slots:  # commit: rows + positions advance for the next step
+            for r in range(R):
+                TR.commit_accepted(cfg, caches[r], [batches[r][j].tree_k for j in range(L)],
+                                   [batches[r][j].tree_v for j in range(L)], slots, pes[r], cur)
+                new_pos = np.array([caches[r][0].rows - 1 + i for i in range(nq)], np.int64)
+                for j in range(L):
+                    batches[r][j].pos = new_pos
+
+    for _ in range(max(3, a.warmup)):
+        e2e_step()
+    barrier()
+    host_s[0], n_calls[0] = 0.0, 0
+    t0w = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(a.steps):
+        e2e_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t0w) * 1e3 / a.steps
+    e2e_rank_ms = max(ev0.elapsed_time(ev1) / a.steps, wall_ms)
+    e2e_value, e2e_ms = sharding.job_throughput(units_this_rank, e2e_rank_ms, dev)
+    host_us = host_s[0] / max(1, n_calls[0]) * 1e6
+    progress("e2e done")
 
     if rank != 0:
         if world > 1:
+            dist.barrier()
             dist.destroy_process_group()
         return
     cpu = None
@@ -552,48 +704,72 @@ def run_ours(a):
         threads = a.cpu_threads or os.cpu_count() or 1
         ref = CpuReference(a, threads)
         rate, sample = ref.measure(a.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": ref.kind, "sample": sample}
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": ref.kind, "sample": sample,
+               **ref.describe()}
     clocks = clk.summary()
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16",
+        "metric": metric_for(a.ctx, a.gamma), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (U[-1,1] KV and queries, random-init; no checkpoint)",
-        "config": workload_config(a, {"parallelism": f"replicas x{world} (request sharding)"}),
+        "config": workload_config(a, world),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+                "d2h_bytes_per_step": int(d2h), "advancing": True, "ms_per_step": e2e_ms,
+                "host_us_per_call": host_us, "accepted_rows_per_step": len(slots),
+                "what": "eager C-ABI calls per layer with each step's positions/rows, pinned "
+                        "host->device inputs, accepted-row commit + compressed append, "
+                        "last layer's output device->host"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": f"profiles/{traffic_src}" if traffic_src else None,
                      "frac_vs_spec_8000": achieved / 8000.0,
-                     "kernel": "nsa_attend_kernel (fused cmp+slc+win+gate, one launch per layer)",
-                     "alg_bytes_per_launch": bytes_att, "launch_ms": attend_ms,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
+                     "kernel": ("nsa_attend_kernel" if R == 1 else "nsa_attend_batch_kernel")
+                               + " (fused cmp+slc+win+gate, one launch per layer"
+                               + ("" if R == 1 else ", up to 8 requests") + ")",
+                     "alg_bytes_per_launch": bytes_att_launch, "launch_ms": attend_ms,
+                     "peak_source": peak_src},
+        "kv_bytes_per_query": kv_per_query,
         "cpu_baseline": cpu,
         "decode_baseline": decode,
         "clocks": clocks,
         "gpu_launches": launches_per_step * a.steps,
         "detail": {
             "per_layer_us_step_avg": ms * 1e3 / L,
-            "attend_us": attend_ms * 1e3, "route_us": route_ms * 1e3,
-            "route_alg_bytes": float(np.mean(alg_route)),
-            "step_alg_GBps": step_bytes / (ms * 1e-3) / 1e9,
-            "step_frac_of_peak": step_bytes / (ms * 1e-3) / 1e9 / peak,
+            "attend_us_per_launch": attend_ms * 1e3, "route_us_per_launch": route_ms * 1e3,
+            "route_alg_bytes_per_layer": float(np.mean(alg_route)),
+            "step_alg_bytes_this_rank": step_bytes,
+            "step_alg_GBps": step_bytes / (ms_rank * 1e-3) / 1e9,
+            "step_frac_of_peak": step_bytes / (ms_rank * 1e-3) / 1e9 / peak,
             "unique_selected_blocks_per_layer": float(np.mean(uniq)),
             "refresh_layers": n_refresh, "reuse_layers": L - n_refresh,
-            "graph": graph is not None,
+            "requests_this_rank": R, "graph": graph is not None,
+            "shards_rank0": [(s.request, s.head_begin, s.head_count) for s in shards],
         },
     }
     print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
-def main():
-    a = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    a = parse(argv)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(a, argv))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus and rank == 0:
+        print(f"[bench] note: --gpus {a.gpus} but WORLD_SIZE={world}; using {world}",
+              file=sys.stderr)
+    resolve_workload(a, world)
     if a.impl == "reference":
-        run_reference_arm(a)
+        run_reference_arm(a, world, rank)
+    elif a.dry_run:
+        run_dry(a, world, rank)
     else:
-        run_ours(a)
+        run_ours(a, world, rank, local)
 
 
 if __name__ == "__main__":

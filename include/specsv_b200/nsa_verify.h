@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SPECSV_ABI_VERSION 1
+#define SPECSV_ABI_VERSION 2  /* 2: specsv_layer_kv.capacity, verify-args KV-head range */
 
 typedef struct CUstream_st* specsv_stream_t; /* == cudaStream_t */
 
@@ -83,6 +83,10 @@ typedef struct specsv_layer_kv {
   void* ck16;           /* device bf16 [>= blocks][Hkv][dh]  (bf16 copy for the compressed branch) */
   void* cv;             /* device bf16 [>= blocks][Hkv][dh]  (pooled values) */
   int64_t blocks;       /* compressed blocks built over `rows`: (rows - l) / d + 1 */
+  int64_t capacity;     /* rows the k / v buffers hold (>= rows); ck / ck16 / cv hold
+                           (capacity - l) / d + 1 blocks.  Appends and commits are
+                           bounds-checked against it (the reference asserts on the
+                           same invariant, cache.hpp:26-30) */
 } specsv_layer_kv;
 
 /* One verify call: one layer x one request, root + gamma draft queries in
@@ -105,6 +109,13 @@ typedef struct specsv_verify_args {
   int32_t* idx_count;         /* device [nq]; -1 = no set (approx non-representatives) */
   uint32_t* idx_forced;       /* device [nq]; bit i = idx[q][i] is a forced block */
   float* out;                 /* device fp32 [nq][Hq][dh] gated-combine output */
+  int32_t kv_head_begin;      /* KV-head group sharding: attend only KV heads
+                                 [kv_head_begin, kv_head_begin + kv_head_count) and write
+                                 only their q heads' rows of `out`; routing (REFRESH) still
+                                 scores every head (the reference sums the selection mass
+                                 over all Hq heads, nsa_attention.cpp:51-63), so q and gates
+                                 stay full-size.  kv_head_count = 0: all heads */
+  int32_t kv_head_count;
 } specsv_verify_args;
 
 /* LoadStats (grouping.hpp:33-52), group-summed over the draft queries of one

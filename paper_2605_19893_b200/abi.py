@@ -44,7 +44,7 @@ class NsaConfigC(C.Structure):
 class LayerKvC(C.Structure):
     _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("rows", C.c_int64),
                 ("ck", C.c_void_p), ("ck16", C.c_void_p), ("cv", C.c_void_p),
-                ("blocks", C.c_int64)]
+                ("blocks", C.c_int64), ("capacity", C.c_int64)]
 
 
 class VerifyArgsC(C.Structure):
@@ -53,7 +53,8 @@ class VerifyArgsC(C.Structure):
                 ("tree_mask", C.POINTER(C.c_uint64)), ("mask_words", C.c_int32),
                 ("q", C.c_void_p), ("gates", C.c_void_p), ("tree_k", C.c_void_p),
                 ("tree_v", C.c_void_p), ("idx", C.c_void_p), ("idx_count", C.c_void_p),
-                ("idx_forced", C.c_void_p), ("out", C.c_void_p)]
+                ("idx_forced", C.c_void_p), ("out", C.c_void_p),
+                ("kv_head_begin", C.c_int32), ("kv_head_count", C.c_int32)]
 
 
 class LoadStatsC(C.Structure):

@@ -83,10 +83,25 @@ int coresident_for_device() {
 int qc_size_for(const specsv_nsa_config& c);
 
 // split CTAs per (KV head, query chunk): all of them must be co-resident
-int splits_for(const specsv_nsa_config& c, int32_t nq) {
+int splits_for(const specsv_nsa_config& c, int32_t nq, int n_heads) {
   const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
-  const int groups = (int)c.n_kv_heads * nchunks;
+  const int groups = n_heads * nchunks;
   return std::max(1, std::min(18, coresident_for_device() / groups));
+}
+
+// KV heads of a call: [begin, begin + count), count 0 = all
+int head_count(const specsv_nsa_config& c, const specsv_verify_args& a) {
+  return a.kv_head_count > 0 ? a.kv_head_count : (int)c.n_kv_heads;
+}
+
+// a cooperative grid larger than the device's co-resident CTAs would be
+// rejected by the driver (or, without the attribute, deadlock at the split
+// barrier): refuse it with a message before launching
+void check_coresident(int ctas, const char* what) {
+  const int cap = coresident_for_device();
+  if (ctas > cap)
+    throw Error(SPECSV_ECUDA, std::string(what) + ": cooperative grid of " + std::to_string(ctas) +
+                                  " CTAs exceeds the " + std::to_string(cap) + " co-resident CTAs");
 }
 
 // routing counter set: [0] tiles done, [2] tail CTAs done, [4..] per-slot units
@@ -160,6 +175,11 @@ void validate_args(const specsv_nsa_config& c, const specsv_layer_kv& kv,
       kv.cv == nullptr)
     throw Error(SPECSV_EINVAL, "null cache pointer");
   if (kv.rows < 1) throw Error(SPECSV_EINVAL, "rows must be >= 1 (the pending root is committed)");
+  if (kv.capacity < kv.rows) throw Error(SPECSV_EINVAL, "rows exceed the cache capacity");
+  if (a.kv_head_count < 0 || a.kv_head_begin < 0 ||
+      (int64_t)a.kv_head_begin + a.kv_head_count > c.n_kv_heads ||
+      (a.kv_head_count == 0 && a.kv_head_begin != 0))
+    throw Error(SPECSV_EINVAL, "KV-head range outside [0, n_kv_heads)");
   if (kv.rows > (int64_t)kMaxUnionWords * 32 * c.l_sel)
     throw Error(SPECSV_EUNSUPPORTED, "context exceeds this build's selection-block bitmap");
   const int64_t want_blocks = kv.rows >= c.l ? (kv.rows - c.l) / c.d + 1 : 0;
@@ -176,7 +196,11 @@ void validate_args(const specsv_nsa_config& c, const specsv_layer_kv& kv,
     if (a.pos[q] - a.pos[0] > c.routing_lag)  // engine.cpp:479-480
       throw Error(SPECSV_EINVAL, "step: draft depth exceeds routing lag");
   }
-  if (selection_block_count(c, routing_visible_len(c, a.pos[a.n_queries - 1])) > kMaxAvail)
+  // the deepest query sees the most selection blocks; in DFS flat order that
+  // need not be the last one, so bound every query
+  int64_t max_pos = a.pos[0];
+  for (int32_t q = 1; q < a.n_queries; ++q) max_pos = std::max(max_pos, a.pos[q]);
+  if (selection_block_count(c, routing_visible_len(c, max_pos)) > kMaxAvail)
     throw Error(SPECSV_EUNSUPPORTED, "too many selection blocks for the Top-n kernel");
 }
 
@@ -327,6 +351,8 @@ void fill_attend_params(AttendParams& p, const specsv_nsa_config& c, const specs
   p.lag = (int32_t)c.routing_lag;
   p.qc_size = qc;
   p.n_splits = S;
+  p.kvh0 = a.kv_head_count > 0 ? a.kv_head_begin : 0;
+  p.nkvh = head_count(c, a);
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)dh));
   const auto src = source_rows(c, a.n_queries, a.pos, a.group_size, a.mode);
   for (int32_t q = 0; q < a.n_queries; ++q) {
@@ -365,12 +391,13 @@ void set_attend_ws(AttendParams& p, const Layout& L, char* ws, int r, int chunks
 
 void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                 void* ws, size_t ws_bytes, cudaStream_t stream) {
-  const int S = splits_for(c, a.n_queries);
+  const int S = splits_for(c, a.n_queries, head_count(c, a));
   const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   AttendParams p;
   fill_attend_params(p, c, kv, a, S);
   const int nchunks = (a.n_queries + p.qc_size - 1) / p.qc_size;
+  if (S > 1) check_coresident(S * p.nkvh * nchunks, "attend launch");
   set_attend_ws(p, L, static_cast<char*>(ws), 0, nchunks, S, c.n_kv_heads);
   cuda_check(launch_attend(p, nchunks, stream), "attend launch");
 }
@@ -392,10 +419,12 @@ void run_attend_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
       max_nq = std::max(max_nq, args[b0 + r].n_queries);
       max_rows = std::max(max_rows, kvs[b0 + r].rows);
     }
+    int heads = 1;
+    for (int r = 0; r < R; ++r) heads = std::max(heads, head_count(c, args[b0 + r]));
     const int chunks = (max_nq + qc - 1) / qc;
     const Layout L = layout_for(c, max_nq, max_rows);
     if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
-    const int groups = (int)H * chunks * R;
+    const int groups = heads * chunks * R;
     const int S = std::max(1, std::min({18 / R, coresident_for_device() / groups, 18}));
     std::memset(&b, 0, sizeof(b));
     b.n_req = R;
@@ -404,7 +433,8 @@ void run_attend_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
       fill_attend_params(b.req[r], c, kvs[b0 + r], args[b0 + r], S);
       set_attend_ws(b.req[r], L, static_cast<char*>(ws), r, chunks, S, H);
     }
-    cuda_check(launch_attend_batch(b, S, S > 1, stream), "batched attend launch");
+    if (S > 1) check_coresident(S * groups, "batched attend launch");
+    cuda_check(launch_attend_batch(b, S, heads, S > 1, stream), "batched attend launch");
   }
 }
 
@@ -540,6 +570,8 @@ specsv_status specsv_compress_append(const specsv_nsa_config* cfg, const specsv_
     if (!cfg || !kv) throw Error(SPECSV_EINVAL, "null argument");
     validate_config(*cfg);
     if (cfg->d_head > 1024) throw Error(SPECSV_EUNSUPPORTED, "d_head too large");
+    if (kv->rows < 0 || kv->rows > kv->capacity)
+      throw Error(SPECSV_EINVAL, "rows exceed the cache capacity");
     const int64_t want = kv->rows >= cfg->l ? (kv->rows - cfg->l) / cfg->d + 1 : 0;
     if (first_block < 0 || last_block > want || first_block > last_block)
       throw Error(SPECSV_EINVAL, "block range outside the committed rows");

@@ -1010,7 +1010,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
 
 __global__ void __launch_bounds__(kThreads, 1)
     nsa_attend_kernel(const __grid_constant__ AttendParams p) {
-  attend_cta(p, blockIdx.x, blockIdx.y, blockIdx.z,
+  attend_cta(p, blockIdx.x, p.kvh0 + blockIdx.y, blockIdx.z,
              (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
 }
 
@@ -1024,7 +1024,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (r >= b.n_req) return;
   const AttendParams& p = b.req[r];
   if (chunk * p.qc_size >= p.nq) return;  // this request has fewer query chunks
-  attend_cta(p, blockIdx.x, blockIdx.y, chunk,
+  if ((int)blockIdx.y >= p.nkvh) return;   // this request attends fewer KV heads
+  attend_cta(p, blockIdx.x, p.kvh0 + blockIdx.y, chunk,
              (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
 }
 
@@ -1037,13 +1038,13 @@ size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits) {
   return units * (3 * kCols * 2) + units * (3 * kCols * kDh);  // split partials (m, l), O
 }
 
-cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, bool cooperative,
+cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, int n_heads, bool cooperative,
                                 cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(nsa_attend_batch_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem_bytes());
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_splits, b.req[0].Hkv, b.n_req * b.n_chunks);
+  cfg.gridDim = dim3(n_splits, n_heads, b.n_req * b.n_chunks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = attend_smem_bytes();
   cfg.stream = stream;
@@ -1061,7 +1062,7 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
                                        (int)attend_smem_bytes());
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.n_splits, p.Hkv, n_chunks);
+  cfg.gridDim = dim3(p.n_splits, p.nkvh, n_chunks);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = attend_smem_bytes();
   cfg.stream = stream;
@@ -1069,7 +1070,8 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
   attr[0].id = cudaLaunchAttributeCooperative;  // split CTAs of a head meet at a barrier
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  // one split per head: no cross-CTA barrier, so the grid may span waves
+  cfg.numAttrs = p.n_splits > 1 ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, nsa_attend_kernel, p);
 }
 

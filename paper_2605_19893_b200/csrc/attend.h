@@ -36,6 +36,7 @@ struct AttendParams {
   int32_t nq, gamma, Hq, Hkv, G, n_sel;
   int32_t rows, blocks, l, d, l_sel, w, lag;
   int32_t qc_size, n_splits;
+  int32_t kvh0, nkvh;            // KV heads [kvh0, kvh0 + nkvh) of this call (head-group shard)
   float scale_log2;
   int32_t pos[kMaxQueries];
   int32_t src_row[kMaxQueries];  // index-set row each query attends with
@@ -66,7 +67,7 @@ struct AttendBatch {
 size_t attend_smem_bytes();
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits);  // split partials only
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream);
-cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, bool cooperative,
+cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, int n_heads, bool cooperative,
                                 cudaStream_t stream);
 int attend_max_coresident();
 

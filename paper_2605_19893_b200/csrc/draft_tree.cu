@@ -266,6 +266,8 @@ specsv_status specsv_commit_rows(const specsv_nsa_config* cfg, const specsv_laye
         if (kv.k == nullptr || kv.v == nullptr || tree_k[j0 + jj] == nullptr || tree_v[j0 + jj] == nullptr)
           throw Error(SPECSV_EINVAL, "null cache or draft-row pointer");
         if (kv.rows < 0) throw Error(SPECSV_EINVAL, "negative rows");
+        if (kv.rows + n_accepted > kv.capacity)  // LayerKv::append's assert (cache.hpp:26-30)
+          throw Error(SPECSV_EINVAL, "commit exceeds the cache capacity");
         p.rows[jj] = kv.rows;
         p.k[jj] = reinterpret_cast<uint4*>(const_cast<void*>(kv.k));
         p.v[jj] = reinterpret_cast<uint4*>(const_cast<void*>(kv.v));

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "attend.h"
@@ -758,18 +759,29 @@ __global__ void __launch_bounds__(1024)
   topn_write(sel, surv, avail, n, idx, count, forced);
 }
 
+// SM count of the current device, cached per device (a device constant; the
+// cache is a per-device atomic, so concurrent callers on different devices or
+// threads never see another device's value)
+int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& slot = cache[dev < 64 ? dev : 63];
+  int sms = slot.load(std::memory_order_relaxed);
+  if (sms == 0) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev < 64) slot.store(sms, std::memory_order_relaxed);
+  }
+  return sms;
+}
+
 cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_slot, cudaStream_t s) {
   RouteParams pc = p;
   pc.chunk_rows = (8 * kMT / p.G) * p.G;  // whole slots per row chunk (G <= 32 <= 40)
   if (pc.chunk_rows < 1) return cudaErrorInvalidValue;
   const int rows_total = p.nr * p.G;
   const int rchunks = (rows_total + pc.chunk_rows - 1) / pc.chunk_rows;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = sm_count();
   const int items = p.Hkv * rchunks * ((p.ntiles + kTilesPerItem - 1) / kTilesPerItem);
   const int units = (scores_out != nullptr ? 1 : p.nr) * p.Hkv;
   const int ctas = std::min(sms, std::max(items, units));  // one CTA per SM: co-resident
@@ -784,12 +796,7 @@ cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_sl
 }  // namespace
 
 cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t s) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = sm_count();
   b.item_start[0] = 0;
   b.unit_start[0] = 0;
   for (int q = 0; q < b.n_req; ++q) {

@@ -99,7 +99,7 @@ class LayerCache:
 
     def c(self) -> abi.LayerKvC:
         return abi.LayerKvC(self.k.data_ptr(), self.v.data_ptr(), self.rows, self.ck.data_ptr(),
-                            self.ck16.data_ptr(), self.cv.data_ptr(), self.blocks)
+                            self.ck16.data_ptr(), self.cv.data_ptr(), self.blocks, self.capacity)
 
     def extend_compressed(self, pos_embed: torch.Tensor | None = None, stream=None) -> None:
         """extend_compressed_layer: pool the blocks the new rows complete."""
@@ -158,7 +158,7 @@ class Workspace:
 
 
 def _args(batch: DraftBatch, sets: IndexSets, out: torch.Tensor, group_size: int, mode: int,
-          role: int) -> abi.VerifyArgsC:
+          role: int, kv_heads: tuple[int, int] | None = None) -> abi.VerifyArgsC:
     pos = np.ascontiguousarray(batch.pos, np.int64)
     mask = np.ascontiguousarray(batch.tree_mask, np.uint64)
     batch._keep[:] = [pos, mask]
@@ -178,25 +178,30 @@ def _args(batch: DraftBatch, sets: IndexSets, out: torch.Tensor, group_size: int
     a.idx_count = sets.count.data_ptr()
     a.idx_forced = sets.forced.data_ptr()
     a.out = out.data_ptr()
+    if kv_heads is not None:  # KV-head group shard: attend heads [begin, begin + count)
+        a.kv_head_begin, a.kv_head_count = int(kv_heads[0]), int(kv_heads[1])
     return a
 
 
-def _call(fn, cfg, cache, batch, sets, out, ws, group_size, mode, role, stream):
+def _call(fn, cfg, cache, batch, sets, out, ws, group_size, mode, role, stream, kv_heads=None):
     c, kv = cfg.c(), cache.c()
-    a = _args(batch, sets, out, group_size, mode, role)
+    a = _args(batch, sets, out, group_size, mode, role, kv_heads)
     check(fn(C.byref(c), C.byref(kv), C.byref(a), C.c_void_p(ws.buf.data_ptr()), ws.nbytes,
              _stream(stream)))
 
 
 def nsa_verify(cfg, cache, batch, sets, out, ws, group_size=4, mode=MODE_EXACT,
-               role=ROLE_REFRESH, stream=None):
+               role=ROLE_REFRESH, stream=None, kv_heads=None):
     """One layer of the verify pass (engine.cpp:175-278). REFRESH writes `sets`;
-    REUSE reads the source layer's `sets`."""
-    _call(lib().specsv_nsa_verify, cfg, cache, batch, sets, out, ws, group_size, mode, role, stream)
+    REUSE reads the source layer's `sets`.  kv_heads=(begin, count): KV-head
+    group shard -- routing still scores every head, attention (and `out`) covers
+    only that group's heads."""
+    _call(lib().specsv_nsa_verify, cfg, cache, batch, sets, out, ws, group_size, mode, role, stream,
+          kv_heads)
 
 
 def nsa_verify_batched(cfg, caches, batches, sets, outs, ws, group_size=4, mode=MODE_EXACT,
-                       roles=None, stream=None):
+                       roles=None, stream=None, kv_heads=None):
     """`len(caches)` independent requests, one layer each, in one call
     (specsv_nsa_verify_batched).  The whole batch is validated before the
     first launch; `ws` must be sized for the largest request."""
@@ -205,8 +210,18 @@ def nsa_verify_batched(cfg, caches, batches, sets, outs, ws, group_size=4, mode=
         raise ValueError("caches, batches, sets and outs must have the same length")
     roles = [ROLE_REFRESH] * n if roles is None else list(roles)
     kvs = (abi.LayerKvC * max(n, 1))(*[c.c() for c in caches])
-    args = (abi.VerifyArgsC * max(n, 1))(*[_args(b, s, o, group_size, mode, r)
-                                           for b, s, o, r in zip(batches, sets, outs, roles)])
+    # kv_heads: None (all heads), one (begin, count) for every request, or a
+    # per-request list of (begin, count) / None
+    if kv_heads is None:
+        heads = [None] * n
+    elif len(kv_heads) == 2 and all(isinstance(v, int) for v in kv_heads):
+        heads = [tuple(kv_heads)] * n
+    else:
+        heads = list(kv_heads)
+        if len(heads) != n:
+            raise ValueError("kv_heads: one entry per request")
+    args = (abi.VerifyArgsC * max(n, 1))(*[_args(b, s, o, group_size, mode, r, hh)
+                                           for b, s, o, r, hh in zip(batches, sets, outs, roles, heads)])
     c = cfg.c()
     check(lib().specsv_nsa_verify_batched(C.byref(c), kvs, args, n,
                                           C.c_void_p(ws.buf.data_ptr()), ws.nbytes,
@@ -219,9 +234,9 @@ def route(cfg, cache, batch, sets, out, ws, group_size=4, mode=MODE_EXACT, strea
 
 
 def attend_fused(cfg, cache, batch, sets, out, ws, group_size=4, mode=MODE_EXACT,
-                 role=ROLE_REUSE, stream=None):
+                 role=ROLE_REUSE, stream=None, kv_heads=None):
     _call(lib().specsv_nsa_attend_fused, cfg, cache, batch, sets, out, ws, group_size, mode,
-          role, stream)
+          role, stream, kv_heads)
 
 
 def selection_scores(cfg, cache, batch, query: int, ws, stream=None) -> torch.Tensor:

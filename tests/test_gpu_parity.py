@@ -473,18 +473,40 @@ def test_verify_max_queries_tree64(oracle_lib, mode):
     assert per <= TOL and l2 <= TOL, (per, l2)
 
 
-def test_exact_grouping_equals_independent_queries():
-    """Exact coarsening is lossless (test_grouped_verifier.cpp:162-182): group
-    sizes C = 2, 4, 8 give the same index sets as C = 1 and outputs equal up to
-    fp32 rounding of the different launch configurations."""
+def test_exact_grouping_equals_independent_queries(oracle_lib):
+    """Exact coarsening is lossless (test_grouped_verifier.cpp:162-182): every
+    draft query of a grouped call gets the indices and output it gets when it
+    runs on its own.  On a chain, query i's independent execution is the call
+    over the root and drafts 1..i (its ancestors; EXACT ownership keeps the
+    other members out of its selected branch), a different launch (fewer
+    columns, a smaller union, other tile-to-split assignment), so outputs agree
+    up to fp32 summation order.  Query 0 (the root) also runs alone as a
+    one-query call, and the grouped call matches the oracle at every C."""
     cfg = O.llama_config(4)
-    x = LayerInputs(cfg, 6000, 8, 4321, parent_slot=TREE8)
+    x = LayerInputs(cfg, 6000, 8, 4321)
     case = DeviceCase(cfg, x)
-    base, base_sets = case.run(1, V.MODE_EXACT, V.ROLE_REFRESH)
-    bi, bc, bf = sets_to_numpy(base_sets)
-    scale = max(np.abs(base).max(), 1e-6)
-    for C in (2, 4, 8):
+    full, full_sets = case.run(4, V.MODE_EXACT, V.ROLE_REFRESH)
+    fi, fc, ff = sets_to_numpy(full_sets)
+    scale = max(np.abs(full).max(), 1e-6)
+    b = case.batch
+    for i in range(case.nq):
+        sub = V.DraftBatch(pos=b.pos[:i + 1].copy(), tree_mask=x.tree_mask[:max(i, 1)].copy(),
+                           q=b.q[:i + 1].contiguous(), gates=b.gates[:i + 1].contiguous(),
+                           tree_k=b.tree_k[:i].contiguous() if i else None,
+                           tree_v=b.tree_v[:i].contiguous() if i else None)
+        sets = V.IndexSets.empty(i + 1, cfg.n)
+        out = torch.zeros(i + 1, cfg.n_q_heads, cfg.d_head, device="cuda")
+        V.nsa_verify(case.vcfg, case.cache, sub, sets, out, case.ws, 1, V.MODE_EXACT,
+                     V.ROLE_REFRESH)
+        torch.cuda.synchronize()
+        si, sc, sf = sets_to_numpy(sets)
+        assert sc[i] == fc[i] and np.array_equal(si[i], fi[i]) and sf[i] == ff[i], i
+        got = out[i].cpu().numpy().astype(np.float64)
+        assert np.abs(got - full[i]).max() <= 1e-5 * scale, i
+    for C in (1, 2, 8):
+        ref = case.oracle(oracle_lib, C, O.MODE_EXACT, O.ROLE_REFRESH)
         out, sets = case.run(C, V.MODE_EXACT, V.ROLE_REFRESH)
         gi, gc, gf = sets_to_numpy(sets)
-        assert np.array_equal(gi, bi) and np.array_equal(gc, bc) and np.array_equal(gf, bf), C
-        assert np.abs(out - base).max() <= 1e-5 * scale, C
+        assert np.array_equal(gi, fi) and np.array_equal(gc, fc), C
+        per, l2 = rel_errors(out, ref["out"])
+        assert per <= TOL and l2 <= TOL, (C, per, l2)

@@ -63,3 +63,68 @@ def test_gloo_world2_sharding_and_timing():
         assert ms_max == 3.0                       # max over ranks, not rank-local
         assert value == pytest.approx(64 * 9 / 3e-3)  # all units / slowest rank
         assert mx == 20.0
+
+
+def test_shard_plan_requests_and_head_groups():
+    """total >= world: whole requests (request_shard); total < world: each
+    request's rank group splits its KV heads into contiguous balanced ranges."""
+    for total, world in ((64, 8), (64, 2), (8, 8), (4, 8), (1, 8), (3, 8), (1, 2), (5, 4)):
+        got = [S.shard_plan(total, world, r, 8) for r in range(world)]
+        cover = {}
+        for r, shards in enumerate(got):
+            assert shards, (total, world, r)
+            for s in shards:
+                cover.setdefault(s.request, []).append((s.head_begin, s.head_count))
+        assert sorted(cover) == list(range(total))
+        for req, ranges in cover.items():
+            heads = sorted(h for b, n in ranges for h in range(b, b + n))
+            assert heads == list(range(8)), (total, world, req, ranges)
+        units = sum(s.fraction for shards in got for s in shards)
+        assert units == pytest.approx(total)
+    with pytest.raises(ValueError):
+        S.shard_plan(1, 16, 0, 8)  # 16 ranks cannot split 8 KV heads
+
+
+def _bench_dry(*args):
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", *args],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_bench_gpus2_spawns_two_ranks_over_gloo():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as two ranks
+    (torch.distributed.run, 127.0.0.1 rendezvous), each rank takes its shard of
+    the C4 requests, and rank 0 prints one line with n_gpus 2 and the
+    whole-job throughput over the slowest rank's time."""
+    d = _bench_dry("--gpus", "2")
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["ctx"] == 131072 and d["config"]["total_requests"] == 64
+    plan = d["shard_plan"]
+    assert len(plan) == 2
+    reqs = [s[0] for rank in plan for s in rank]
+    assert sorted(reqs) == list(range(64)) and len(set(reqs)) == 64
+    assert d["ms_per_step"] == 1.25  # max over ranks of the stand-in times (1.0, 1.25)
+    assert d["value"] == pytest.approx(64 * 9 / 1.25e-3)
+
+
+def test_bench_head_group_sharding_dry_run():
+    """Fewer requests than ranks: the request's KV heads are split across its ranks."""
+    d = _bench_dry("--gpus", "2", "--total-requests", "1")
+    assert d["shard_plan"] == [[[0, 0, 4]], [[0, 4, 4]]]
+    assert "KV-head-group" in d["config"]["parallelism"]
+    assert d["value"] == pytest.approx(9 / 1.25e-3)
+
+
+def test_bench_single_gpu_default_is_c2():
+    d = _bench_dry()
+    assert d["n_gpus"] == 1 and d["config"]["ctx"] == 65536 and d["config"]["layers"] == 32
+    assert d["metric"] == ("verified query-tokens/s at 64K ctx, 8-tok draft; achieved HBM GB/s "
+                           "vs peak")

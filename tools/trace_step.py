@@ -1,0 +1,120 @@
+"""Diagnostics (not a test): per-kernel phase timeline of the bench step in
+its real setting -- distinct 64K layer caches (cold L2), one CUDA graph of
+`L` verify calls ("alt" refresh/reuse) -- from the kernels' globaltimer
+stamps (specsv_debug_attend_trace; one trace buffer per layer).
+
+    python tools/trace_step.py [layers] [ctx] [gamma]
+
+Prints, per layer, the attend kernel's first-CTA start, the median/max CTA
+phase times (union built, tile loop done, partials written, barrier passed,
+merge done, relative to the first CTA start) and the gap to the previous
+kernel's last CTA end; refresh layers also show the routing kernel.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2605_19893_b200 import abi  # noqa: E402
+from paper_2605_19893_b200 import verify as V  # noqa: E402
+from paper_2605_19893_b200.workload import chain_tree_mask  # noqa: E402
+
+RBASE = 196608
+
+
+def main():
+    L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+    ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
+    g = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+    dev = torch.device("cuda", 0)
+    cfg = V.NsaConfig(n_layers=L)
+    nq = g + 1
+    torch.manual_seed(0)
+    pos = np.array([ctx - 1 + i for i in range(nq)], np.int64)
+    layers = []
+    for j in range(L):
+        c = V.LayerCache(cfg, ctx, device=dev)
+        c.k.copy_((torch.rand(ctx, 8, 128, device=dev) * 2 - 1).bfloat16())
+        c.v.copy_((torch.rand(ctx, 8, 128, device=dev) * 2 - 1).bfloat16())
+        c.rows = ctx
+        c.extend_compressed((torch.rand(cfg.l, 128, device=dev) * 2 - 1) * 0.1)
+        b = V.DraftBatch(pos=pos, tree_mask=chain_tree_mask(g),
+                         q=torch.rand(nq, 32, 128, device=dev) * 2 - 1,
+                         gates=torch.rand(nq, 32, 3, device=dev) * 0.6 + 0.2,
+                         tree_k=(torch.rand(g, 8, 128, device=dev) * 2 - 1).bfloat16(),
+                         tree_v=(torch.rand(g, 8, 128, device=dev) * 2 - 1).bfloat16())
+        layers.append((c, b, V.IndexSets.empty(nq, cfg.n, dev), torch.zeros(nq, 32, 128, device=dev)))
+    ws = V.Workspace(cfg, nq, ctx, device=dev)
+    bufs = [torch.zeros(4096 * 64, dtype=torch.int64, device=dev) for _ in range(L)]
+
+    def step(trace):
+        for j in range(L):
+            if trace:
+                abi.lib().specsv_debug_attend_trace(bufs[j].data_ptr())
+            c, b, s, o = layers[j]
+            refresh = j % 2 == 0
+            src = s if refresh else layers[j - 1][2]
+            V.nsa_verify(cfg, c, b, src, o, ws, 4, V.MODE_EXACT,
+                         V.ROLE_REFRESH if refresh else V.ROLE_REUSE)
+        abi.lib().specsv_debug_attend_trace(None)
+
+    step(False)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            step(True)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    for bb in bufs:
+        bb.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"step of {L} layers: {e0.elapsed_time(e1) * 1e3:.1f} us (traced)")
+    t_first = None
+    prev_end = None
+    for j in range(L):
+        t = bufs[j][:RBASE].view(-1, 64).cpu().numpy()
+        t = t[t[:, 0] > 0]
+        r = bufs[j][RBASE:RBASE + 1024 * 64].view(-1, 64).cpu().numpy()
+        r = r[r[:, 0] > 0]
+        if t_first is None:
+            t_first = (r[:, 0].min() if len(r) else t[:, 0].min())
+        line = f"layer {j:2d} {'R' if j % 2 == 0 else 'U'}"
+        if len(r):
+            r0 = r[:, 0].min()
+            rend = r[:, 5][r[:, 5] > 0].max() if (r[:, 5] > 0).any() else r[:, 1].max()
+            gap = (r0 - prev_end) / 1e3 if prev_end is not None else 0.0
+            tiles = (np.median(r[:, 1]) - r0) / 1e3
+            bar = (np.median(r[:, 4][r[:, 4] > 0]) - r0) / 1e3 if (r[:, 4] > 0).any() else -1
+            line += (f" | route start {(r0 - t_first) / 1e3:8.2f} gap {gap:5.2f} tiles(med) {tiles:5.2f}"
+                     f" barrier {bar:5.2f} end {(rend - r0) / 1e3:5.2f}")
+            prev_end = rend
+        t0 = t[:, 0].min()
+        gap = (t0 - prev_end) / 1e3 if prev_end is not None else 0.0
+
+        def ph(col):
+            d = t[:, col]
+            d = d[d > 0]
+            return ((np.median(d) - t0) / 1e3, (d.max() - t0) / 1e3) if len(d) else (-1, -1)
+
+        end = t[:, 4].max()
+        line += (f" | attend start {(t0 - t_first) / 1e3:8.2f} gap {gap:5.2f} spread {(t[:, 0].max() - t0) / 1e3:4.2f}"
+                 f" union {ph(1)[0]:5.2f} loop {ph(2)[0]:5.2f}/{ph(2)[1]:5.2f} part {ph(3)[0]:5.2f}/{ph(3)[1]:5.2f}"
+                 f" bar {ph(6)[0]:5.2f} merge {ph(4)[0]:5.2f}/{ph(4)[1]:5.2f} ctas {len(t)}")
+        prev_end = end
+        print(line)
+
+
+if __name__ == "__main__":
+    main()
