@@ -65,6 +65,21 @@ void encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int64_t hkv
   if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
+// fp32 [blocks][hkv][dh] as a 3-D map (dh, hkv, blocks) with 32x1x16 SWIZZLE_128B
+// boxes (route2's key tiles; rows past `blocks` read as zeros)
+void encode_ck_map(CUtensorMap* m, const float* base, int64_t blocks, int64_t hkv, int64_t dh) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)hkv, (cuuint64_t)std::max<int64_t>(blocks, 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)(dh * 4), (cuuint64_t)(hkv * dh * 4)};
+  const cuuint32_t box[3] = {32, 1, 16};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled (ck) failed");
+}
+
 // co-resident CTAs of the attend kernel on this device (a device constant,
 // computed once per device)
 int coresident_for_device() {
@@ -110,6 +125,8 @@ constexpr int kCntSetInts = 4 + kMaxQueries;
 struct Layout {
   size_t sync_off = 0, sync_bytes = 0;  // attend barrier words: fixed position per config
   int max_chunks = 1;                   // query chunks of the widest call (kMaxQueries)
+  size_t r2cnt_off = 0;                 // route2 barrier words: fixed position per config
+  size_t r2_off = 0;                    // route2 regions (dm, part, ovh, candidates)
   size_t attend_off = 0, attend_bytes = 0;
   size_t E_off = 0, TM_off = 0, TD_off = 0, F_off = 0, sel_off = 0, cnt_off = 0;
   int64_t sel_pad = 0;
@@ -139,12 +156,15 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   L.sync_off = 0;
   L.sync_bytes = (size_t)kSyncSets * L.max_chunks * c.n_kv_heads * 2 * sizeof(int32_t);
   L.cnt_off = align_up(L.sync_off + L.sync_bytes, 256);
-  L.attend_off = align_up(L.cnt_off + (size_t)kSyncSets * kCntSetInts * sizeof(int32_t), 256);
+  L.r2cnt_off = align_up(L.cnt_off + (size_t)kSyncSets * kCntSetInts * sizeof(int32_t), 256);
+  L.attend_off = align_up(L.r2cnt_off + (size_t)kR2CntInts * sizeof(int32_t), 256);
   L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
   const int64_t maxblk = max_rows >= c.l ? (max_rows - c.l) / c.d + 1 : 0;
   const int64_t m_pad = align_up(std::max<int64_t>(maxblk, 1), kRouteTile);
   const int64_t ntiles = m_pad / kRouteTile;
-  size_t off = align_up(L.attend_off + L.attend_bytes, 256);
+  L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
+  L.r2_off = align_up(L.attend_off + L.attend_bytes, 256);
+  size_t off = align_up(L.r2_off + route2_ws_bytes(nq, (int)c.n_kv_heads, (int)L.sel_pad), 256);
   const int64_t gs = ((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 1;  // = g_stride
   L.E_off = off;  // per-tile selection-block shares [nq][ntiles][Hq][gs]
   off = align_up(off + (size_t)nq * ntiles * c.n_q_heads * gs * 8, 256);
@@ -152,7 +172,6 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
   L.TD_off = off;
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
-  L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
   L.F_off = off;  // per-KV-head score shares [nq][Hkv][sel_pad]
   off = align_up(off + (size_t)nq * c.n_kv_heads * L.sel_pad * 8, 256);
   L.total = off;
@@ -302,11 +321,90 @@ void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
   }
 }
 
+// the per-range routing variant (route2.cu) when SPECSV_ROUTE2=1 and its range
+// decomposition fits; false = route_fused_kernel (the default: measured faster
+// at the bench shape, 40.8 vs 49.9 us -- DESIGN.md "Routing").  Tests cover both.
+bool make_route2(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+                 const Layout& L, char* ws, const std::vector<int32_t>& routed, double* scores_out,
+                 Route2Params& p) {
+  const char* want = std::getenv("SPECSV_ROUTE2");
+  if (want == nullptr || want[0] != '1') return false;
+  std::memset(&p, 0, sizeof(p));
+  const int nr = static_cast<int>(routed.size());
+  int64_t mmax = 0, smax = 0;
+  std::vector<bool> is_routed(a.n_queries, false);
+  for (int s = 0; s < nr; ++s) {
+    const int32_t q = routed[s];
+    is_routed[q] = true;
+    const int64_t vis = routing_visible_len(c, a.pos[q]);
+    p.slot_q[s] = q;
+    p.slot_mvis[s] = (int32_t)visible_blocks(c, kv.blocks, vis);
+    p.slot_avail[s] = (int32_t)selection_block_count(c, vis);
+    mmax = std::max<int64_t>(mmax, p.slot_mvis[s]);
+    smax = std::max<int64_t>(smax, p.slot_avail[s]);
+  }
+  for (int32_t q = 0; q < a.n_queries; ++q)
+    if (!is_routed[q]) p.unrouted[p.n_unrouted++] = q;
+  const int ntiles = (int)((mmax + kRouteTile - 1) / kRouteTile);
+  const int gs = (int)(((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 1);
+  const int spt = (int)(kRouteTile * c.d / c.l_sel);
+  const int G = (int)(c.n_q_heads / c.n_kv_heads);
+  if (!route2_plan(nr, G, (int)c.n_kv_heads, ntiles, gs, spt, (int)c.n, p)) return false;
+  if (c.d_head != 128) return false;
+  encode_ck_map(&p.tm_ck, kv.ck, kv.blocks, c.n_kv_heads, c.d_head);
+  p.q = a.q;
+  p.ck = kv.ck;
+  p.idx = a.idx;
+  p.idx_count = a.idx_count;
+  p.idx_forced = a.idx_forced;
+  p.scores_out = scores_out;
+  p.trace = g_trace;
+  if (const char* e = std::getenv("SPECSV_ROUTE2_DEBUG_EXIT")) p.debug_exit = std::atoi(e);  // timing only
+  p.nr = nr;
+  p.Hq = (int32_t)c.n_q_heads;
+  p.Hkv = (int32_t)c.n_kv_heads;
+  p.G = G;
+  p.n = (int32_t)c.n;
+  p.l = (int32_t)c.l;
+  p.d = (int32_t)c.d;
+  p.l_sel = (int32_t)c.l_sel;
+  p.blocks = (int32_t)kv.blocks;
+  p.spt = spt;
+  p.gs = gs;
+  p.sel_pad = (int32_t)L.sel_pad;
+  p.s_total = (int32_t)smax;
+  p.scale = 1.0 / std::sqrt(static_cast<double>(c.d_head));
+  // regions: dm [kR2MaxRanges][40] (m, den) | part [nr][Hkv][sel_pad] | ovh | cand_s | cand_i | cand_n
+  char* r = ws + L.r2_off;
+  const size_t items = kR2MaxRanges;
+  p.dm = reinterpret_cast<double*>(r);
+  r += align_up(items * kR2Rows * 16, 256);
+  p.part = reinterpret_cast<double*>(r);
+  r += align_up((size_t)nr * c.n_kv_heads * L.sel_pad * 8, 256);
+  p.ovh = reinterpret_cast<double*>(r);
+  r += align_up((size_t)nr * c.n_kv_heads * kR2MaxRanges * 8 * 8, 256);
+  p.cand_s = reinterpret_cast<double*>(r);
+  r += align_up((size_t)nr * kR2MaxRanges * 64 * 8, 256);
+  p.cand_i = reinterpret_cast<int32_t*>(r);
+  r += align_up((size_t)nr * kR2MaxRanges * 64 * 4, 256);
+  p.cand_n = reinterpret_cast<int32_t*>(r);
+  int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.r2cnt_off);
+  p.bar = cnt;
+  p.rcnt = cnt + 2 * kR2MaxRanges;
+  p.fcnt = cnt + 3 * kR2MaxRanges;
+  return true;
+}
+
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                void* ws, size_t ws_bytes, cudaStream_t stream) {
   const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   const auto routed = routed_queries(a.n_queries, a.pos, a.group_size, a.mode);
+  Route2Params p2;
+  if (make_route2(c, kv, a, L, static_cast<char*>(ws), routed, nullptr, p2)) {
+    cuda_check(launch_route2(p2, stream), "route launch");
+    return;
+  }
   RouteParams p = make_route_params(c, kv, a, L, static_cast<char*>(ws), routed);
   cuda_check(launch_route(p, stream, true), "route launch");
 }
@@ -542,6 +640,11 @@ specsv_status specsv_nsa_scores(const specsv_nsa_config* cfg, const specsv_layer
     const Layout L = layout_for(*cfg, args->n_queries, kv->rows);
     if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
     std::vector<int32_t> routed{query};
+    Route2Params p2;
+    if (make_route2(*cfg, *kv, *args, L, static_cast<char*>(ws), routed, scores, p2)) {
+      cuda_check(launch_route2(p2, reinterpret_cast<cudaStream_t>(stream)), "scores launch");
+      return;
+    }
     RouteParams p = make_route_params(*cfg, *kv, *args, L, static_cast<char*>(ws), routed);
     cuda_check(launch_scores_only(p, scores, 0, reinterpret_cast<cudaStream_t>(stream)),
                "scores launch");

@@ -114,6 +114,47 @@ struct RouteBatch {
   int32_t unit_start[kRouteBatch + 1];  // (slot, KV head) units of requests < q
 };
 
+// ---- routing, single-request fast path (route2.cu) ---------------------------
+// One CTA per (KV head, row chunk, block range): the range's 16-block tiles
+// stay in shared memory, the softmax statistics are combined per range, and a
+// short tail (one barrier among a head's ranges, per-range score sums, per-range
+// Top-n candidates, one final merge) replaces the grid-wide unit phase.
+constexpr int kR2MaxTiles = 16;   // tiles (16 blocks) per range CTA (one warp each)
+constexpr int kR2Rows = 40;       // (slot, head) rows per CTA
+constexpr int kR2MaxRanges = 160; // >= SM count
+struct Route2Params {
+  CUtensorMap tm_ck;       // fp32 compressed K, dims (dh, Hkv, blocks), box 32 x 1 x 16, 128B swizzle
+  const float* q;          // [nq][Hq][dh]
+  const float* ck;         // fp32 [blocks][Hkv][dh]
+  int32_t* idx;            // [nq][n]
+  int32_t* idx_count;      // [nq]
+  uint32_t* idx_forced;    // [nq]
+  double* scores_out;      // diagnostics: dense scores of slot 0, no Top-n (NULL: Top-n)
+  double* dm;              // [items][kR2Rows] (range max, range denominator)
+  double* part;            // [nr][Hkv][sel_pad] per-KV-head score shares
+  double* ovh;             // [nr][Hkv][NR][8] shares a range's last tile overhangs into the next
+  double* cand_s;          // [nr][NR][64] Top-n candidates per range (score)
+  int32_t* cand_i;         // [nr][NR][64] (block id)
+  int32_t* cand_n;         // [nr][NR]
+  int32_t* bar;            // [2 * Hkv * rc] range barrier (count, generation) per (KV head, row chunk)
+  int32_t* rcnt;           // [NR] arrivals per range
+  int32_t* fcnt;           // [1] finished ranges
+  int32_t nr, Hq, Hkv, G, n, l, d, l_sel, blocks;
+  int32_t rc, chunk_rows, NR, T, ntiles, spt, gs, sel_pad, s_total;
+  double scale;            // 1 / sqrt(dh)
+  int32_t slot_q[kMaxQueries], slot_mvis[kMaxQueries], slot_avail[kMaxQueries];
+  int32_t unrouted[kMaxQueries];
+  int32_t n_unrouted;
+  unsigned long long* trace;  // diagnostics only: per-CTA phase stamps at kRouteTraceBase
+  int32_t debug_exit;         // diagnostics only (timing): 0 = full kernel, k = return after phase k
+};
+// workspace words of route2's barriers (fixed offset per config; self-resetting)
+constexpr int kR2CntInts = 2 * kR2MaxRanges + kR2MaxRanges + 8;
+// shape of the range decomposition for one call; false = use route_fused_kernel
+bool route2_plan(int nr, int G, int Hkv, int ntiles, int gs, int spt, int n, Route2Params& p);
+size_t route2_ws_bytes(int nr, int Hkv, int sel_pad);  // dm/part/ovh/cand regions
+cudaError_t launch_route2(const Route2Params& p, cudaStream_t stream);
+
 cudaError_t launch_route(const RouteParams& p, cudaStream_t stream, bool write_idx);
 cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t stream);
 cudaError_t launch_scores_only(const RouteParams& p, double* scores, int slot, cudaStream_t stream);

@@ -89,6 +89,16 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
+// bulk (non-tensor) global -> shared copy completing on an mbarrier's tx count
+// (bytes and both addresses multiples of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- gpu-scope sync
 // acq_rel atomic add: releases this thread's (and, cumulatively, its CTA's
 // barrier-ordered) prior writes and acquires the writes released by earlier
