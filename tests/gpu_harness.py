@@ -92,3 +92,21 @@ def boundary_gap(lib, cfg, q, ck, pos):
     if k <= 0 or k >= rest.size:
         return np.inf
     return float((rest[k - 1] - rest[k]) / max(rest[k - 1], 1e-300))
+
+
+def diff_within_near_tie(lib, cfg, q, ck, pos, got, want, near_tie):
+    """True when every block in the symmetric difference of two index sets
+    has a reference score within `near_tie` (relative) of the Top-n boundary
+    score (the n-th best non-forced score): the sets differ only by a flip at
+    a near-tie, nothing else (contract P2)."""
+    vis = cfg.routing_visible_len(int(pos))
+    s = lib.selection_scores(cfg, q, ck, vis)
+    avail = s.size
+    forced = {0, avail - 2, avail - 1} if avail > 2 else set(range(avail))
+    rest = np.sort(np.array([s[b] for b in range(avail) if b not in forced]))[::-1]
+    k = cfg.n - len(forced)
+    if k <= 0 or k >= rest.size:
+        return False
+    sb = rest[k - 1]
+    diff = set(int(b) for b in got) ^ set(int(b) for b in want)
+    return all(b < avail and abs(s[b] - sb) <= near_tie * max(abs(sb), 1e-300) for b in diff)

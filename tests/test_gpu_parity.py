@@ -17,8 +17,8 @@ pytestmark = pytest.mark.gpu
 from oracle import oracle as O  # noqa: E402
 from paper_2605_19893_b200 import verify as V  # noqa: E402
 from paper_2605_19893_b200.workload import LayerInputs, bf16_round  # noqa: E402
-from tests.gpu_harness import (TOL, DeviceCase, boundary_gap, forced_matrix,  # noqa: E402
-                               rel_errors, sets_to_numpy)
+from tests.gpu_harness import (TOL, DeviceCase, boundary_gap, diff_within_near_tie,  # noqa: E402
+                               forced_matrix, rel_errors, sets_to_numpy)
 
 NEAR_TIE = 1e-12
 TREE8 = [-1, -1, 0, 0, 1, 2, 2, 4]
@@ -45,6 +45,11 @@ def _check_indices(oracle_lib, case, got_idx, got_cnt, got_forced, ref, routed_o
         if not same:
             gap = boundary_gap(oracle_lib, cfg, case.x.q[q], ck, case.x.pos[q])
             assert gap <= NEAR_TIE, f"query {q}: indices differ with gap {gap}"
+            # and only by blocks at that near-tie
+            assert diff_within_near_tie(oracle_lib, cfg, case.x.q[q], ck, case.x.pos[q],
+                                        got_idx[q, :max(got_cnt[q], 0)],
+                                        ref["idx"][q, :ref["idx_count"][q]], NEAR_TIE), \
+                f"query {q}: indices differ beyond the near-tie"
             near += 1
     return near
 
