@@ -90,6 +90,15 @@ specsv_status specsv_commit_rows(const specsv_nsa_config* cfg, const specsv_laye
                                  int32_t n_layers, const int32_t* slots, int32_t n_accepted,
                                  specsv_stream_t stream);
 
+/* The commit plus extend_compressed_layer of the blocks it completes
+ * (nsa_cache.cpp:45-66), for every layer in two launches: kvs[j].rows and
+ * .blocks are the values BEFORE the commit (the caller advances them after);
+ * pos_embed: per-layer device fp32 [l][dh] pointers, or NULL. */
+specsv_status specsv_commit_rows_compress(const specsv_nsa_config* cfg, const specsv_layer_kv* kvs,
+                                          const void* const* tree_k, const void* const* tree_v,
+                                          int32_t n_layers, const int32_t* slots, int32_t n_accepted,
+                                          const float* const* pos_embed, specsv_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

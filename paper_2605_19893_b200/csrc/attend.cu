@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "attend.h"
 #include "sm100.cuh"
@@ -445,8 +446,6 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         xb[it] = xa[it];
       }
     }
-  } else if (warp == kWarpUnion) {
-    stage_index_rows(p, m, q0, nqc, lane);
   } else if (warp == kWarpQk && lane == 0) {
     tma_prefetch(&p.tm_k);
     tma_prefetch(&p.tm_v);
@@ -910,6 +909,11 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       }
     };
     for (int j = 2; split + j * S < n_cmp; ++j) prefetch_tile(split + j * S);
+    // the index rows may come from the routing launch just before this one
+    // (programmatic dependent launch: the rest of this CTA -- q, the
+    // compressed tiles -- does not wait for it)
+    griddep_wait();
+    stage_index_rows(p, m, q0, nqc, lane);
     if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
     build_union_warp(p, m, q0, nqc, lane, cwlo, cwhi, trace ? p.trace + cta_id * 64 : nullptr);
     mbar_arrive(&m.union_ready);  // every lane: releases its own union writes
@@ -1002,6 +1006,9 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
   }
   tc_fence_before();
   __syncthreads();
+  // every read of this launch's workspace partials is done: the next launch
+  // (which may reuse them) can start placing CTAs
+  griddep_launch();
   if (warp == kWarpTma) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -1033,6 +1040,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t attend_smem_bytes() { return kOffMisc + sizeof(Misc) + 1024; }
 
+bool pdl_enabled() {
+  const char* e = std::getenv("SPECSV_NO_PDL");
+  return e == nullptr || e[0] != '1';
+}
+
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits) {
   const size_t units = (size_t)n_chunks * hkv * n_splits;
   return units * (3 * kCols * 2) + units * (3 * kCols * kDh);  // split partials (m, l), O
@@ -1048,11 +1060,18 @@ cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, int n_heads,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = attend_smem_bytes();
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // split CTAs of a head meet at a barrier
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cooperative) {  // split CTAs of a head meet at a barrier
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = cooperative ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, nsa_attend_batch_kernel, b);
 }
 
@@ -1066,12 +1085,18 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = attend_smem_bytes();
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // split CTAs of a head meet at a barrier
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (p.n_splits > 1) {  // split CTAs of a head meet at a barrier (one split: may span waves)
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
+  if (pdl_enabled()) {  // starts while the previous launch's last CTAs finish
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
-  // one split per head: no cross-CTA barrier, so the grid may span waves
-  cfg.numAttrs = p.n_splits > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, nsa_attend_kernel, p);
 }
 

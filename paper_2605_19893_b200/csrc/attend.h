@@ -64,6 +64,9 @@ struct AttendBatch {
   int32_t n_req, n_chunks;  // grid z = n_req x n_chunks (the widest request's chunks)
 };
 
+// programmatic dependent launch between this library's launches (default on;
+// SPECSV_NO_PDL=1 turns it off for A/B timing)
+bool pdl_enabled();
 size_t attend_smem_bytes();
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits);  // split partials only
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream);
@@ -162,6 +165,20 @@ cudaError_t launch_select(const double* scores, int avail, int n, int32_t* idx, 
                           uint32_t* forced, cudaStream_t stream);
 
 // ---- compression (compress.cu) ------------------------------------------------
+constexpr int kCompressLayers = 32;  // layers per batched compress launch
+struct CompressLayers {
+  const void* k[kCompressLayers];
+  const void* v[kCompressLayers];
+  const float* pe[kCompressLayers];
+  float* ck[kCompressLayers];
+  void* ck16[kCompressLayers];
+  void* cv[kCompressLayers];
+  int64_t first[kCompressLayers];
+  int64_t count[kCompressLayers];
+  int32_t hkv, dh, l, d;
+};
+cudaError_t launch_compress_layers(const CompressLayers& c, int n_layers, int64_t max_count,
+                                   cudaStream_t stream);
 cudaError_t launch_compress(const void* k, const void* v, const float* pe, float* ck, void* ck16,
                             void* cv, int64_t first, int64_t last, int hkv, int dh, int l, int d,
                             cudaStream_t stream);

@@ -41,7 +41,45 @@ __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,
   }
 }
 
+// the blocks a commit completed, in every layer at once: grid (block, head,
+// layer); the same pooling as compress_kernel
+__global__ void compress_layers_kernel(const __grid_constant__ CompressLayers c) {
+  const int j = blockIdx.z;
+  if ((int64_t)blockIdx.x >= c.count[j]) return;
+  const int64_t b = c.first[j] + blockIdx.x;
+  const int h = blockIdx.y;
+  const int hkv = c.hkv, dh = c.dh, l = c.l, d = c.d;
+  const __nv_bfloat16* k = static_cast<const __nv_bfloat16*>(c.k[j]);
+  const __nv_bfloat16* v = static_cast<const __nv_bfloat16*>(c.v[j]);
+  const float* pe = c.pe[j];
+  const double inv_l = 1.0 / (double)l;
+  for (int x = threadIdx.x; x < dh; x += blockDim.x) {
+    double acc_k = 0.0, acc_v = 0.0;
+    for (int o = 0; o < l; ++o) {
+      const int64_t off = ((b * d + o) * hkv + h) * dh + x;
+      acc_k = __dadd_rn(acc_k, (double)__bfloat162float(k[off]));
+      if (pe != nullptr) acc_k = __dadd_rn(acc_k, (double)pe[o * dh + x]);
+      acc_v = __dadd_rn(acc_v, (double)__bfloat162float(v[off]));
+    }
+    const float fk = (float)__dmul_rn(acc_k, inv_l);
+    const float fv = (float)__dmul_rn(acc_v, inv_l);
+    const int64_t o = (b * hkv + h) * dh + x;
+    c.ck[j][o] = fk;
+    static_cast<__nv_bfloat16*>(c.ck16[j])[o] = __float2bfloat16_rn(fk);
+    static_cast<__nv_bfloat16*>(c.cv[j])[o] = __float2bfloat16_rn(fv);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_compress_layers(const CompressLayers& c, int n_layers, int64_t max_count,
+                                   cudaStream_t stream) {
+  if (n_layers <= 0 || max_count <= 0) return cudaSuccess;
+  if (max_count > 65535) return cudaErrorInvalidValue;
+  compress_layers_kernel<<<dim3((unsigned)max_count, c.hkv, n_layers), c.dh < 256 ? c.dh : 256, 0,
+                           stream>>>(c);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_compress(const void* k, const void* v, const float* pe, float* ck, void* ck16,
                             void* cv, int64_t first, int64_t last, int hkv, int dh, int l, int d,

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "attend.h"
 #include "policy.h"
 #include "specsv_b200/draft_tree.h"
 
@@ -277,6 +278,46 @@ specsv_status specsv_commit_rows(const specsv_nsa_config* cfg, const specsv_laye
       commit_rows_kernel<<<dim3(n_accepted, p.n_layers), 128, 0, st>>>(p);
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) throw Error(SPECSV_ECUDA, std::string("commit launch: ") + cudaGetErrorString(e));
+    }
+  });
+}
+
+specsv_status specsv_commit_rows_compress(const specsv_nsa_config* cfg, const specsv_layer_kv* kvs,
+                                          const void* const* tree_k, const void* const* tree_v,
+                                          int32_t n_layers, const int32_t* slots, int32_t n_accepted,
+                                          const float* const* pos_embed, specsv_stream_t stream) {
+  return guarded([&] {
+    const specsv_status st = specsv_commit_rows(cfg, kvs, tree_k, tree_v, n_layers, slots, n_accepted, stream);
+    if (st != SPECSV_OK) throw Error(st, last_error());
+    if (n_accepted == 0 || n_layers == 0) return;
+    if (cfg->d_head > 1024) throw Error(SPECSV_EUNSUPPORTED, "d_head too large");
+    cudaStream_t sm = reinterpret_cast<cudaStream_t>(stream);
+    CompressLayers c{};
+    c.hkv = (int32_t)cfg->n_kv_heads;
+    c.dh = (int32_t)cfg->d_head;
+    c.l = (int32_t)cfg->l;
+    c.d = (int32_t)cfg->d;
+    for (int32_t j0 = 0; j0 < n_layers; j0 += kCompressLayers) {
+      const int nl = std::min(kCompressLayers, n_layers - j0);
+      int64_t max_count = 0;
+      for (int jj = 0; jj < nl; ++jj) {
+        const specsv_layer_kv& kv = kvs[j0 + jj];
+        if (!kv.ck || !kv.ck16 || !kv.cv) throw Error(SPECSV_EINVAL, "null cache pointer");
+        const int64_t rows = kv.rows + n_accepted;
+        const int64_t want = rows >= cfg->l ? (rows - cfg->l) / cfg->d + 1 : 0;
+        if (kv.blocks < 0 || kv.blocks > want) throw Error(SPECSV_EINVAL, "compressed block count exceeds the rows");
+        c.k[jj] = kv.k;
+        c.v[jj] = kv.v;
+        c.pe[jj] = pos_embed != nullptr ? pos_embed[j0 + jj] : nullptr;
+        c.ck[jj] = kv.ck;
+        c.ck16[jj] = kv.ck16;
+        c.cv[jj] = kv.cv;
+        c.first[jj] = kv.blocks;
+        c.count[jj] = want - kv.blocks;
+        max_count = std::max(max_count, want - kv.blocks);
+      }
+      const cudaError_t e = launch_compress_layers(c, nl, max_count, sm);
+      if (e != cudaSuccess) throw Error(SPECSV_ECUDA, std::string("compress launch: ") + cudaGetErrorString(e));
     }
   });
 }

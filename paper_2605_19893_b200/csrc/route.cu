@@ -30,6 +30,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 #include <cstdint>
 
 #include "attend.h"
@@ -586,6 +588,9 @@ __device__ __noinline__ void slot_unit(const RouteParams& p, int slot, int kvh, 
   topn_write(sel, surv, avail, p.n, p.idx + (int64_t)q * p.n, p.idx_count + q, p.idx_forced + q, tr);
 }
 
+__device__ __forceinline__ void griddep_wait_r() { sm100::griddep_wait(); }
+__device__ __forceinline__ void griddep_launch_r() { sm100::griddep_launch(); }
+
 __device__ __forceinline__ void arrive(int* w) {
   __syncthreads();
   if (threadIdx.x == 0) sm100::red_add_release_gpu(w, 1);
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   int* bar = p.counters;  // [0] tiles done, [2] tail CTAs done; both return to 0
   unsigned long long* tr =
       p.trace != nullptr && threadIdx.x == 0 ? p.trace + kRouteTraceBase + cta * 16 * 4 : nullptr;
+  griddep_wait_r();  // the inputs may come from the launch just before (PDL)
   tstamp(tr, 0);
   // ---- phase 1: work items (KV head, row chunk, tile set) over the grid ----
   if (p.ntiles > 0) {
@@ -644,6 +650,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   arrive(bar);
   if (cta >= units) return;  // no unit: leave without waiting
   wait_all(bar, nctas);
+  griddep_launch_r();  // no more waiting on other CTAs: the next launch may start placing CTAs
   tstamp(tr, 4);
   if (cta == 0 && scores_out == nullptr) {
     for (int u = threadIdx.x; u < p.n_unrouted; u += blockDim.x) {
@@ -694,6 +701,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   const int cta = blockIdx.x, nctas = gridDim.x;
   int* bar = b.req[0].counters;  // [0] tiles done, [2] tail CTAs done; both return to 0
   const int items = b.item_start[b.n_req];
+  griddep_wait_r();
   if (items > 0) {
     const RouteParams& p0 = b.req[0];  // the overlap matrix is a function of the config only
     double* W = reinterpret_cast<double*>(smem + TileSmem::w);
@@ -721,6 +729,7 @@ __global__ void __launch_bounds__(kRouteThreads, 1)
   arrive(bar);
   if (cta >= units) return;  // no unit: leave without waiting
   wait_all(bar, nctas);
+  griddep_launch_r();
   if (cta == 0) {
     for (int q = 0; q < b.n_req; ++q) {
       const RouteParams& p = b.req[q];
@@ -775,6 +784,29 @@ int sm_count() {
   return sms;
 }
 
+// a cooperative launch (every CTA co-resident: grid barrier) that may also
+// start early behind the previous launch (programmatic dependent launch)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop_pdl(void (*kernel)(KArgs...), int ctas, int threads, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeCooperative;
+  attr[na++].val.cooperative = 1;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_slot, cudaStream_t s) {
   RouteParams pc = p;
   pc.chunk_rows = (8 * kMT / p.G) * p.G;  // whole slots per row chunk (G <= 32 <= 40)
@@ -788,9 +820,7 @@ cudaError_t launch_chain(const RouteParams& p, double* scores_out, int scores_sl
   const size_t smem = std::max({TileSmem::bytes, kUnitSmem, kTailSmem});
   cudaError_t e = cudaFuncSetAttribute(route_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  void* args[] = {&pc, &scores_out, &scores_slot};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(route_fused_kernel), dim3(ctas),
-                                     dim3(kRouteThreads), args, smem, s);
+  return launch_coop_pdl(route_fused_kernel, ctas, kRouteThreads, smem, s, pc, scores_out, scores_slot);
 }
 
 }  // namespace
@@ -811,9 +841,7 @@ cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t s) {
   const size_t smem = std::max({TileSmem::bytes, kUnitSmem, kTailSmem});
   cudaError_t e = cudaFuncSetAttribute(route_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  void* args[] = {&b};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(route_batch_kernel), dim3(ctas),
-                                     dim3(kRouteThreads), args, smem, s);
+  return launch_coop_pdl(route_batch_kernel, ctas, kRouteThreads, smem, s, b);
 }
 
 cudaError_t launch_route(const RouteParams& p, cudaStream_t s, bool write_idx) {

@@ -99,6 +99,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// wait: the preceding grid in the stream has completed and its writes are
+// visible (a no-op when this grid was launched without the PDL attribute);
+// launch_dependents: this CTA needs nothing more from co-resident CTAs, so the
+// next grid may start placing CTAs as SMs free up
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // ---------------------------------------------------------------- gpu-scope sync
 // acq_rel atomic add: releases this thread's (and, cumulatively, its CTA's
 // barrier-ordered) prior writes and acquires the writes released by earlier

@@ -30,7 +30,7 @@ BFS, DFS = 0, 1
 NO_PARENT = -1
 
 EXPORTED = ("specsv_tree_expand", "specsv_tree_flatten", "specsv_tree_mask",
-            "specsv_tree_greedy_accept", "specsv_commit_rows")
+            "specsv_tree_greedy_accept", "specsv_commit_rows", "specsv_commit_rows_compress")
 
 
 class DraftTreeC(C.Structure):
@@ -62,6 +62,9 @@ def _lib() -> C.CDLL:
         "specsv_tree_greedy_accept": ([tp, i32p, i64p, i32p, i64p, i32p], C.c_int),
         "specsv_commit_rows": ([C.POINTER(abi.NsaConfigC), C.POINTER(abi.LayerKvC),
                                 C.POINTER(vp), C.POINTER(vp), i32, i32p, i32, vp], C.c_int),
+        "specsv_commit_rows_compress": ([C.POINTER(abi.NsaConfigC), C.POINTER(abi.LayerKvC),
+                                         C.POINTER(vp), C.POINTER(vp), i32, i32p, i32, C.POINTER(vp),
+                                         vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -278,10 +281,12 @@ def commit_accepted(cfg, caches, tree_ks, tree_vs, slots: Sequence[int], pos_emb
     kvs = (abi.LayerKvC * max(n, 1))(*[c.c() for c in caches])
     tk = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in tree_ks])
     tv = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in tree_vs])
-    c = cfg.c()
-    check(_lib().specsv_commit_rows(C.byref(c), kvs, tk, tv, n, _p(s, C.c_int32), int(s.shape[0]),
-                                    _stream(stream)))
     pes = list(pos_embed) if isinstance(pos_embed, (list, tuple)) else [pos_embed] * n
-    for cache, pe in zip(caches, pes):
+    pe = (C.c_void_p * max(n, 1))(*[None if x is None else x.data_ptr() for x in pes])
+    c = cfg.c()
+    # the commit and the compressed blocks it completes, every layer, two launches
+    check(_lib().specsv_commit_rows_compress(C.byref(c), kvs, tk, tv, n, _p(s, C.c_int32),
+                                             int(s.shape[0]), pe, _stream(stream)))
+    for cache in caches:
         cache.rows += int(s.shape[0])
-        cache.extend_compressed(pe, stream)
+        cache.blocks = cfg.compressed_block_count(cache.rows)

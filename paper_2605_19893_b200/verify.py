@@ -26,6 +26,7 @@ from . import abi
 from .abi import MODE_APPROX, MODE_EXACT, ROLE_REFRESH, ROLE_REUSE, SpecsvError, check, lib
 
 __all__ = ["NsaConfig", "LayerCache", "IndexSets", "DraftBatch", "Workspace", "nsa_verify",
+           "nsa_verify_batched", "PreparedVerify",
            "route", "attend_fused", "selection_scores", "select_blocks", "resolve_layer_roles",
            "clamp_inherited_indices", "load_stats", "algorithmic_bytes", "MODE_EXACT",
            "MODE_APPROX", "ROLE_REFRESH", "ROLE_REUSE", "SpecsvError"]
@@ -226,6 +227,56 @@ def nsa_verify_batched(cfg, caches, batches, sets, outs, ws, group_size=4, mode=
     check(lib().specsv_nsa_verify_batched(C.byref(c), kvs, args, n,
                                           C.c_void_p(ws.buf.data_ptr()), ws.nbytes,
                                           _stream(stream)))
+
+
+class PreparedVerify:
+    """nsa_verify / nsa_verify_batched for a fixed set of buffers with the
+    ctypes arguments built once: run() refreshes only what changes from step
+    to step (committed rows and blocks, positions, tree mask) and calls the
+    C-ABI -- the low-overhead form an engine issues every step (same entry
+    points, same semantics as nsa_verify)."""
+
+    def __init__(self, cfg, caches, batches, sets, outs, ws, group_size=4, mode=MODE_EXACT,
+                 role=ROLE_REFRESH, kv_heads=None):
+        one = isinstance(caches, LayerCache)
+        self.caches = [caches] if one else list(caches)
+        self.batches = [batches] if one else list(batches)
+        sets = [sets] if one else list(sets)
+        outs = [outs] if one else list(outs)
+        heads = [kv_heads] if one or kv_heads is None or isinstance(kv_heads[0], int) \
+            else list(kv_heads)
+        if len(heads) == 1:
+            heads = heads * len(self.caches)
+        n = len(self.caches)
+        self.cfgc = cfg.c()
+        self.kvs = (abi.LayerKvC * n)(*[c.c() for c in self.caches])
+        self.args = (abi.VerifyArgsC * n)(*[_args(b, s, o, group_size, mode, role, h)
+                                           for b, s, o, h in zip(self.batches, sets, outs, heads)])
+        self._keep = [b._keep[:] for b in self.batches]
+        self.ws = C.c_void_p(ws.buf.data_ptr())
+        self.wsn = ws.nbytes
+        self.n = n
+        self.fn = lib().specsv_nsa_verify if n == 1 else lib().specsv_nsa_verify_batched
+
+    def run(self, stream=None):
+        for i in range(self.n):
+            c, b, kv, a = self.caches[i], self.batches[i], self.kvs[i], self.args[i]
+            kv.rows = c.rows
+            kv.blocks = c.blocks
+            if self._keep[i][0] is not b.pos:  # positions / mask replaced since the last step
+                pos = np.ascontiguousarray(b.pos, np.int64)
+                mask = np.ascontiguousarray(b.tree_mask, np.uint64)
+                a.pos = pos.ctypes.data_as(C.POINTER(C.c_int64))
+                a.tree_mask = mask.ctypes.data_as(C.POINTER(C.c_uint64))
+                a.mask_words = mask.shape[1] if mask.ndim == 2 else 1
+                b.pos = pos
+                self._keep[i] = [pos, mask]
+        st = _stream(stream)
+        if self.n == 1:
+            check(self.fn(C.byref(self.cfgc), C.byref(self.kvs[0]), C.byref(self.args[0]), self.ws,
+                          self.wsn, st))
+        else:
+            check(self.fn(C.byref(self.cfgc), self.kvs, self.args, self.n, self.ws, self.wsn, st))
 
 
 def route(cfg, cache, batch, sets, out, ws, group_size=4, mode=MODE_EXACT, stream=None):
