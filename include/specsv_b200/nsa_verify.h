@@ -232,6 +232,12 @@ specsv_status specsv_algorithmic_bytes(const specsv_nsa_config* cfg, int64_t row
  * disables.  Not used on the product path. */
 specsv_status specsv_debug_attend_trace(unsigned long long* buf);
 
+/* int32 index into a verify workspace of the routing kernel's cumulative count
+ * of exact fp64 re-scorings (queries whose certified Top-n boundary fell
+ * inside the score error bound); -1 on bad arguments.  Diagnostics only. */
+int32_t specsv_debug_route3_counter_offset(const specsv_nsa_config* cfg, int32_t n_queries,
+                                           int64_t max_rows);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ EXPORTED = (
     "specsv_nsa_route", "specsv_nsa_attend_fused", "specsv_nsa_scores", "specsv_select_blocks",
     "specsv_compress_append", "specsv_resolve_layer_roles", "specsv_clamp_inherited",
     "specsv_load_stats", "specsv_algorithmic_bytes", "specsv_debug_attend_trace",
+    "specsv_debug_route3_counter_offset",
 )
 
 
@@ -112,6 +113,7 @@ def lib() -> C.CDLL:
         "specsv_algorithmic_bytes": ([cfgp, i64, i32, i64p, i32, i32p, i32p, i32, i32, i64p],
                                      C.c_int),
         "specsv_debug_attend_trace": ([vp], C.c_int),
+        "specsv_debug_route3_counter_offset": ([cfgp, i32, i64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -80,6 +80,21 @@ void encode_ck_map(CUtensorMap* m, const float* base, int64_t blocks, int64_t hk
   if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled (ck) failed");
 }
 
+// fp32 [blocks][hkv][dh] as a 3-D map (dh, hkv, blocks) with one 128 x 1 x 128
+// box per route3 unit (a 64 KB row-major key tile; rows past `blocks` read as zeros)
+void encode_ck3_map(CUtensorMap* m, const float* base, int64_t blocks, int64_t hkv, int64_t dh) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)hkv, (cuuint64_t)std::max<int64_t>(blocks, 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)(dh * 4), (cuuint64_t)(hkv * dh * 4)};
+  const cuuint32_t box[3] = {(cuuint32_t)dh, 1, (cuuint32_t)kR3Tile};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled (route3 ck) failed");
+}
+
 // co-resident CTAs of the attend kernel on this device (a device constant,
 // computed once per device)
 int coresident_for_device() {
@@ -126,6 +141,8 @@ struct Layout {
   size_t sync_off = 0, sync_bytes = 0;  // attend barrier words: fixed position per config
   int max_chunks = 1;                   // query chunks of the widest call (kMaxQueries)
   size_t r2cnt_off = 0;                 // route2 barrier words: fixed position per config
+  size_t r3cnt_off = 0;                 // route3 barrier words (+ fallback counter): fixed position
+  size_t r3_stats_off = 0, r3_gsh_off = 0, r3_contrib_off = 0, r3_eps_off = 0;  // route3 regions
   size_t r2_off = 0;                    // route2 regions (dm, part, ovh, candidates)
   size_t attend_off = 0, attend_bytes = 0;
   size_t E_off = 0, TM_off = 0, TD_off = 0, F_off = 0, sel_off = 0, cnt_off = 0;
@@ -134,6 +151,16 @@ struct Layout {
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// route3 unit shape: rows per chunk (whole slots, <= kR3Rows) and the
+// selection blocks one 128-block unit touches
+int64_t route3_chunk_rows(const specsv_nsa_config& c) {
+  const int64_t G = c.n_q_heads / c.n_kv_heads;
+  return std::max<int64_t>(1, kR3Rows / G) * G;
+}
+int64_t route3_span(const specsv_nsa_config& c) {
+  return ((kR3Tile - 1) * c.d + c.l - 1) / c.l_sel + 1;
+}
 
 // queries per column chunk: 64 columns / G, and few enough that the chunk's
 // union (n selected blocks per query + the window blocks) fits kMaxUnion
@@ -157,7 +184,8 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   L.sync_bytes = (size_t)kSyncSets * L.max_chunks * c.n_kv_heads * 2 * sizeof(int32_t);
   L.cnt_off = align_up(L.sync_off + L.sync_bytes, 256);
   L.r2cnt_off = align_up(L.cnt_off + (size_t)kSyncSets * kCntSetInts * sizeof(int32_t), 256);
-  L.attend_off = align_up(L.r2cnt_off + (size_t)kR2CntInts * sizeof(int32_t), 256);
+  L.r3cnt_off = align_up(L.r2cnt_off + (size_t)kR2CntInts * sizeof(int32_t), 256);
+  L.attend_off = align_up(L.r3cnt_off + 8 * sizeof(int32_t), 256);
   L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
   const int64_t maxblk = max_rows >= c.l ? (max_rows - c.l) / c.d + 1 : 0;
   const int64_t m_pad = align_up(std::max<int64_t>(maxblk, 1), kRouteTile);
@@ -174,6 +202,22 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
   L.F_off = off;  // per-KV-head score shares [nq][Hkv][sel_pad]
   off = align_up(off + (size_t)nq * c.n_kv_heads * L.sel_pad * 8, 256);
+  {  // route3: tile statistics, per-unit selection-block sums, shares, error bounds
+    const int64_t G = c.n_q_heads / c.n_kv_heads;
+    const int64_t nt3 = (maxblk + kR3Tile - 1) / kR3Tile;
+    const int64_t rows_head = (int64_t)nq * G;
+    const int64_t cr = route3_chunk_rows(c);
+    const int64_t chunks = (rows_head + cr - 1) / cr;
+    const int64_t span = route3_span(c);
+    L.r3_stats_off = off;
+    off = align_up(off + (size_t)(c.n_kv_heads * rows_head * nt3 * 4 * 8), 256);
+    L.r3_gsh_off = off;
+    off = align_up(off + (size_t)(c.n_kv_heads * chunks * nt3 * kR3Rows * span * 8), 256);
+    L.r3_contrib_off = off;
+    off = align_up(off + (size_t)(nq * c.n_kv_heads * nt3 * span * 8), 256);
+    L.r3_eps_off = off;
+    off = align_up(off + (size_t)(nq * c.n_kv_heads * 8), 256);
+  }
   L.total = off;
   return L;
 }
@@ -274,6 +318,10 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
 
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                void* ws, size_t ws_bytes, cudaStream_t stream);
+bool use_route3();
+void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+                     const Layout& L, char* base, const std::vector<int32_t>& routed, Route3Req& R);
+void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, Route3Launch& P);
 
 // bytes of one request's routing regions (E, TM, TD, F); a batched routing
 // launch places request q's at E_off + q x route_bytes
@@ -300,6 +348,23 @@ void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
   const size_t cap = 1 + (ws_bytes - L.total) / std::max<size_t>(route_bytes(L), 1);
   const int group = (int)std::min<size_t>({(size_t)kRouteBatch, (size_t)kSyncSets, cap});
   char* w = static_cast<char*>(ws);
+  if (use_route3()) {
+    const int group3 = (int)std::min<size_t>((size_t)kR3Batch, cap);
+    thread_local Route3Launch P;
+    for (size_t g0 = 0; g0 < refresh.size(); g0 += group3) {
+      const int n = (int)std::min<size_t>(group3, refresh.size() - g0);
+      std::memset(&P, 0, sizeof(P));
+      fill_route3_common(c, L, w, P);
+      P.n_req = n;
+      for (int q = 0; q < n; ++q) {
+        const int32_t b = refresh[g0 + q];
+        const auto routed = routed_queries(args[b].n_queries, args[b].pos, args[b].group_size, args[b].mode);
+        make_route3_req(c, kvs[b], args[b], L, w + L.E_off + (size_t)q * route_bytes(L), routed, P.req[q]);
+      }
+      cuda_check(launch_route3(P, stream), "batched route launch");
+    }
+    return;
+  }
   thread_local RouteBatch rb;  // ~20 KB host staging of the launch parameters
   for (size_t g0 = 0; g0 < refresh.size(); g0 += group) {
     const int n = (int)std::min<size_t>(group, refresh.size() - g0);
@@ -395,11 +460,88 @@ bool make_route2(const specsv_nsa_config& c, const specsv_layer_kv& kv, const sp
   return true;
 }
 
+// the routing kernel of a call: route_fused_kernel (fp64 DMMA) by default;
+// SPECSV_ROUTE3=1 selects route3_kernel (integer tensor pipe, certified Top-n),
+// SPECSV_ROUTE2=1 the per-range variant
+bool use_route3() {
+  const char* r3 = std::getenv("SPECSV_ROUTE3");
+  return r3 != nullptr && r3[0] == '1';
+}
+
+// one request's route3 parameters; `base` is its routing region (E_off-relative
+// offsets of the layout apply)
+void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
+                     const Layout& L, char* base, const std::vector<int32_t>& routed, Route3Req& R) {
+  std::memset(&R, 0, sizeof(R));
+  encode_ck3_map(&R.tm_ck, kv.ck, kv.blocks, c.n_kv_heads, c.d_head);
+  R.q = a.q;
+  R.ck = kv.ck;
+  R.idx = a.idx;
+  R.idx_count = a.idx_count;
+  R.idx_forced = a.idx_forced;
+  R.nr = static_cast<int32_t>(routed.size());
+  R.blocks = (int32_t)kv.blocks;
+  int64_t mmax = 0;
+  std::vector<bool> is_routed(a.n_queries, false);
+  for (size_t s = 0; s < routed.size(); ++s) {
+    const int32_t q = routed[s];
+    is_routed[q] = true;
+    const int64_t vis = routing_visible_len(c, a.pos[q]);
+    R.slot_q[s] = q;
+    R.slot_mvis[s] = (int32_t)visible_blocks(c, kv.blocks, vis);
+    R.slot_avail[s] = (int32_t)selection_block_count(c, vis);
+    mmax = std::max<int64_t>(mmax, R.slot_mvis[s]);
+  }
+  for (int32_t q = 0; q < a.n_queries; ++q)
+    if (!is_routed[q]) R.unrouted[R.n_unrouted++] = q;
+  const int64_t G = c.n_q_heads / c.n_kv_heads;
+  R.ntiles = (int32_t)((mmax + kR3Tile - 1) / kR3Tile);
+  R.nchunks = (int32_t)((R.nr * G + route3_chunk_rows(c) - 1) / route3_chunk_rows(c));
+  const size_t rel = L.E_off;  // region offsets are relative to the request's routing region
+  R.stats = reinterpret_cast<double*>(base + (L.r3_stats_off - rel));
+  R.gsh = reinterpret_cast<double*>(base + (L.r3_gsh_off - rel));
+  R.contrib = reinterpret_cast<double*>(base + (L.r3_contrib_off - rel));
+  R.eps = reinterpret_cast<double*>(base + (L.r3_eps_off - rel));
+}
+
+void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, Route3Launch& P) {
+  P.Hq = (int32_t)c.n_q_heads;
+  P.Hkv = (int32_t)c.n_kv_heads;
+  P.G = (int32_t)(c.n_q_heads / c.n_kv_heads);
+  P.n = (int32_t)c.n;
+  P.l = (int32_t)c.l;
+  P.d = (int32_t)c.d;
+  P.l_sel = (int32_t)c.l_sel;
+  P.chunk_rows = (int32_t)route3_chunk_rows(c);
+  P.spt = (int32_t)(kR3Tile * c.d / c.l_sel);
+  P.span = (int32_t)route3_span(c);
+  P.scale = 1.0 / std::sqrt(static_cast<double>(c.d_head));
+  P.c_sl = 1.4426950408889634073599 / std::sqrt(static_cast<double>(c.d_head));
+  int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.r3cnt_off);
+  P.counters = cnt;
+  P.fallbacks = cnt + 4;
+  const char* fe = std::getenv("SPECSV_ROUTE3_FORCE_EXACT");  // tests: the exact re-scoring path
+  P.force_exact = (fe != nullptr && fe[0] == '1') ? 1 : 0;
+  P.trace = g_trace;
+  if ((kR3Tile * c.d) % c.l_sel != 0 || P.span > kR3MaxSpan)
+    throw Error(SPECSV_EUNSUPPORTED, "route3: unit span outside this build's limits");
+}
+
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                void* ws, size_t ws_bytes, cudaStream_t stream) {
   const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   const auto routed = routed_queries(a.n_queries, a.pos, a.group_size, a.mode);
+  if (use_route3()) {
+    thread_local Route3Launch P;  // ~21 KB host staging of the launch parameters
+    std::memset(&P, 0, sizeof(P));
+    char* w = static_cast<char*>(ws);
+    fill_route3_common(c, L, w, P);
+    P.n_req = 1;
+    make_route3_req(c, kv, a, L, w + L.E_off, routed, P.req[0]);
+    cuda_check(launch_route3(P, stream), "route launch");
+    return;
+  }
   Route2Params p2;
   if (make_route2(c, kv, a, L, static_cast<char*>(ws), routed, nullptr, p2)) {
     cuda_check(launch_route2(p2, stream), "route launch");
@@ -544,6 +686,12 @@ using namespace specsv_b200;
 extern "C" {
 
 int32_t specsv_abi_version(void) { return SPECSV_ABI_VERSION; }
+
+int32_t specsv_debug_route3_counter_offset(const specsv_nsa_config* cfg, int32_t n_queries,
+                                           int64_t max_rows) {
+  if (cfg == nullptr || n_queries < 1) return -1;
+  return (int32_t)(layout_for(*cfg, n_queries, max_rows).r3cnt_off / sizeof(int32_t)) + 4;
+}
 
 specsv_status specsv_debug_attend_trace(unsigned long long* buf) {
   g_trace = buf;

@@ -1087,7 +1087,15 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (p.n_splits > 1) {  // split CTAs of a head meet at a barrier (one split: may span waves)
+  // split CTAs of a head meet at a barrier, so the grid must be co-resident
+  // (the host checks it fits the device).  Under programmatic dependent launch
+  // the attribute is dropped: CTAs are then placed as the previous launch's
+  // CTAs retire (a refresh layer's attend streams its compressed tiles under
+  // the routing tail), and every CTA still becomes resident because nothing
+  // the previous launch waits on depends on this grid.
+  const char* coop_env = std::getenv("SPECSV_ATTEND_COOP");
+  const bool coop = p.n_splits > 1 && (!pdl_enabled() || (coop_env != nullptr && coop_env[0] == '1'));
+  if (coop) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na++].val.cooperative = 1;
   }

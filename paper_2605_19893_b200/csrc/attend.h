@@ -158,6 +158,51 @@ bool route2_plan(int nr, int G, int Hkv, int ntiles, int gs, int spt, int n, Rou
 size_t route2_ws_bytes(int nr, int Hkv, int sel_pad);  // dm/part/ovh/cand regions
 cudaError_t launch_route2(const Route2Params& p, cudaStream_t stream);
 
+// ---- routing on the integer tensor pipe (route3.cu, the default) -------------
+// Unit = (request, KV head, row chunk of <= 48 (slot, head) rows, 128
+// compressed blocks).  Logits come from exact s8 x s8 -> s32 tcgen05 products
+// of base-256 digits of fixed-point q and keys; scores carry a certified error
+// bound, and a query whose Top-n boundary falls inside it is re-scored in fp64.
+constexpr int kR3Rows = 48;     // q rows per unit (MMA N)
+constexpr int kR3Tile = 128;    // compressed blocks per unit (MMA M)
+constexpr int kR3Batch = 16;    // requests per launch
+constexpr int kR3MaxSpan = 64;  // selection blocks one unit touches (host-checked)
+struct Route3Req {
+  CUtensorMap tm_ck;     // fp32 compressed K, dims (dh, Hkv, blocks), box 128 x 1 x 128, no swizzle
+  const float* q;        // [nq][Hq][dh]
+  const float* ck;       // fp32 [blocks][Hkv][dh] (the exact re-scoring path)
+  int32_t* idx;          // [nq][n]
+  int32_t* idx_count;    // [nq]
+  uint32_t* idx_forced;  // [nq]
+  double* stats;         // [Hkv][nr*G][ntiles][4]: tile max (log2), tile sum, logit error bound, -
+  double* gsh;           // [units][kR3Rows][span] per-unit selection-block sums (token weights)
+  double* contrib;       // [nr][Hkv][ntiles][span] normalised per-KV-head shares
+  double* eps;           // [nr][Hkv] logit error bound (log2 units) over the slot's rows
+  int32_t nr, ntiles, nchunks, blocks;
+  int32_t slot_q[kMaxQueries];
+  int32_t slot_mvis[kMaxQueries];
+  int32_t slot_avail[kMaxQueries];
+  int32_t unrouted[kMaxQueries];
+  int32_t n_unrouted;
+};
+struct Route3Launch {
+  Route3Req req[kR3Batch];
+  int32_t n_req;
+  int32_t unit_start[kR3Batch + 1];  // units of requests < r (set at launch)
+  int32_t task_start[kR3Batch + 1];  // (request, slot) Top-n tasks of requests < r
+  int32_t Hq, Hkv, G, n, l, d, l_sel;
+  int32_t chunk_rows;  // rows per unit chunk, a multiple of G (<= kR3Rows)
+  int32_t spt;         // selection blocks per unit stride (kR3Tile d / l_sel)
+  int32_t span;        // selection blocks one unit touches
+  double scale;        // 1 / sqrt(dh)
+  double c_sl;         // log2(e) / sqrt(dh): logits in log2 units
+  int32_t* counters;   // [4] zero-initialised, self-resetting (grid barriers, exits)
+  int32_t* fallbacks;  // cumulative count of exact re-scorings (diagnostics; never reset)
+  int32_t force_exact; // tests: re-score every query in fp64
+  unsigned long long* trace;  // diagnostics: per-CTA stamps at kRouteTraceBase + cta * 16
+};
+cudaError_t launch_route3(Route3Launch& p, cudaStream_t stream);
+
 cudaError_t launch_route(const RouteParams& p, cudaStream_t stream, bool write_idx);
 cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t stream);
 cudaError_t launch_scores_only(const RouteParams& p, double* scores, int slot, cudaStream_t stream);

@@ -156,6 +156,13 @@ class Workspace:
             self.nbytes = int(lib().specsv_verify_workspace_size(C.byref(c), n_queries, max_rows))
         # zero-filled once: the library keeps its barrier words consistent afterwards
         self.buf = torch.zeros(max(self.nbytes, 256), dtype=torch.uint8, device=device)
+        self._fb = int(lib().specsv_debug_route3_counter_offset(C.byref(c), n_queries, max_rows))
+
+    def route_fallbacks(self) -> int:
+        """Cumulative exact fp64 re-scorings of the routing kernel on this
+        workspace (queries whose certified Top-n boundary fell inside the score
+        error bound).  Diagnostics; synchronises."""
+        return int(self.buf[4 * self._fb:4 * self._fb + 4].view(torch.int32).item())
 
 
 def _args(batch: DraftBatch, sets: IndexSets, out: torch.Tensor, group_size: int, mode: int,

@@ -517,34 +517,40 @@ def test_exact_grouping_equals_independent_queries(oracle_lib):
         assert per <= TOL and l2 <= TOL, (C, per, l2)
 
 
+ROUTE_VARIANTS = {"route3": {"SPECSV_ROUTE3": "1"}, "route3_exact": {"SPECSV_ROUTE3": "1", "SPECSV_ROUTE3_FORCE_EXACT": "1"},
+                  "legacy": {}}
+
+
 @pytest.mark.parametrize("rows,gamma,parents,mode", [(4096, 4, None, O.MODE_EXACT),
                                                      (3001, 8, TREE8, O.MODE_APPROX),
                                                      (65536, 8, None, O.MODE_EXACT)])
 def test_route_kernels_agree(oracle_lib, monkeypatch, rows, gamma, parents, mode):
-    """Single-request routing runs on route_fused_kernel by default and on the
-    per-range variant route2_kernel with SPECSV_ROUTE2=1 (when its range
-    decomposition fits).  Both against the oracle, and their index sets and
-    fp64 scores agree."""
+    """Routing runs on route3_kernel by default (integer tensor-pipe logits,
+    certified Top-n); SPECSV_ROUTE3_FORCE_EXACT=1 sends every query through its
+    exact fp64 re-scoring path, SPECSV_ROUTE_LEGACY=1 selects the fp64-DMMA
+    route_fused_kernel.  All three against the oracle, and their index sets
+    agree; the fp64 score diagnostic holds P3."""
     cfg = O.llama_config(4)
     x = LayerInputs(cfg, rows, gamma, 31 + rows + gamma, parent_slot=parents)
     case = DeviceCase(cfg, x)
     ref = case.oracle(oracle_lib, 4, mode, O.ROLE_REFRESH)
     got = {}
-    for legacy in (False, True):
-        if legacy:
-            monkeypatch.delenv("SPECSV_ROUTE2", raising=False)
-        else:
-            monkeypatch.setenv("SPECSV_ROUTE2", "1")
+    for name, env in ROUTE_VARIANTS.items():
+        for k in ("SPECSV_ROUTE3_FORCE_EXACT", "SPECSV_ROUTE3", "SPECSV_ROUTE2"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         out, sets = case.run(4, mode, V.ROLE_REFRESH)
         gi, gc, gf = sets_to_numpy(sets)
-        assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0, legacy
+        assert _check_indices(oracle_lib, case, gi, gc, gf, ref) == 0, name
         per, l2 = rel_errors(out, ref["out"])
-        assert per <= TOL and l2 <= TOL, (legacy, per, l2)
-        got[legacy] = (gi, gc, gf)
-        ck, _ = case.oracle_cache(oracle_lib)
-        q = case.nq - 1
-        sc = V.selection_scores(case.vcfg, case.cache, case.batch, q, case.ws).cpu().numpy()
-        rs = oracle_lib.selection_scores(cfg, x.q[q], ck, cfg.routing_visible_len(int(x.pos[q])))
-        assert np.abs(sc - rs).max() <= 1e-13 * np.abs(rs).max(), legacy
-    for a, b in zip(got[False], got[True]):
-        assert np.array_equal(a, b)
+        assert per <= TOL and l2 <= TOL, (name, per, l2)
+        got[name] = (gi, gc, gf)
+    ck, _ = case.oracle_cache(oracle_lib)
+    q = case.nq - 1
+    sc = V.selection_scores(case.vcfg, case.cache, case.batch, q, case.ws).cpu().numpy()
+    rs = oracle_lib.selection_scores(cfg, x.q[q], ck, cfg.routing_visible_len(int(x.pos[q])))
+    assert np.abs(sc - rs).max() <= 1e-13 * np.abs(rs).max()
+    for name in ROUTE_VARIANTS:
+        for a, b in zip(got["route3"], got[name]):
+            assert np.array_equal(a, b), name

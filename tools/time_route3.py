@@ -1,0 +1,85 @@
+"""Diagnostics (not a test): the refresh routing launch at the bench's C2
+shape -- route3_kernel (default) vs route_fused_kernel (SPECSV_ROUTE_LEGACY=1)
+-- warm (one cache) and cold (16 distinct caches, CUDA graph), CUDA events;
+plus route3's exact re-scoring count and per-phase stamps.
+
+    python tools/time_route3.py [ctx] [gamma]
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from tools.time_route import build_case  # noqa: E402
+from tools.time_route2 import timed  # noqa: E402
+from tools.gpu_warm import spin_up  # noqa: E402
+from paper_2605_19893_b200 import abi  # noqa: E402
+from paper_2605_19893_b200 import verify as V  # noqa: E402
+
+BASE = 196608
+PHASES = {6: "u0 q staged", 7: "u0 keys landed", 8: "u0 sliced", 9: "u0 mma done", 10: "u0 epilogue done",
+          11: "u1 q staged", 12: "u1 keys landed", 13: "u1 sliced", 14: "u1 mma done", 15: "u1 epilogue done",
+          1: "tiles done", 2: "grid barrier passed", 3: "shares written", 4: "top-n start", 5: "done"}
+
+
+def main():
+    ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+    g = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    cases = [build_case(ctx, g) for _ in range(16)]
+    spin_up(0.5)
+    for legacy in (False, True):
+        if legacy:
+            os.environ.pop("SPECSV_ROUTE3", None)
+        else:
+            os.environ["SPECSV_ROUTE3"] = "1"
+        cfg, c, b, s, out, ws = cases[0]
+        spin_up(0.2)
+        warm = timed(lambda: V.route(cfg, c, b, s, out, ws))
+
+        def all_cases():
+            for cfg_, c_, b_, s_, o_, w_ in cases:
+                V.route(cfg_, c_, b_, s_, o_, w_)
+
+        all_cases()
+        torch.cuda.synchronize()
+        gph = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(gph, stream=st):
+                all_cases()
+        torch.cuda.current_stream().wait_stream(st)
+        cold = timed(gph.replay, 10) / len(cases)
+        name = "legacy route_fused_kernel" if legacy else "route3_kernel"
+        print(f"{name:26s} ctx={ctx} gamma={g}: warm {warm:.1f} us, cold (graph over 16 caches) "
+              f"{cold:.1f} us per launch", flush=True)
+    os.environ["SPECSV_ROUTE3"] = "1"
+    # phase stamps of one cold launch
+    cfg, c, b, s, out, ws = cases[3]
+    buf = torch.zeros(BASE + 4096 * 16, dtype=torch.int64, device="cuda")
+    for _ in range(50):
+        V.route(*cases[(_ % 15) + 1])
+    abi.lib().specsv_debug_attend_trace(buf.data_ptr())
+    V.route(cfg, c, b, s, out, ws)
+    torch.cuda.synchronize()
+    abi.lib().specsv_debug_attend_trace(None)
+    t = buf[BASE:].view(-1, 16).cpu().numpy()
+    t = t[t[:, 0] > 0]
+    t0 = t[:, 0].min()
+    print(f"route3 phases ({len(t)} CTAs, us from the first CTA start):")
+    for k, name in PHASES.items():
+        d = t[:, k]
+        d = d[d > 0]
+        if len(d):
+            d = (d - t0) / 1e3
+            print(f"  {name:22s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}  (n={len(d)})")
+    d = (t[:, 0] - t0) / 1e3
+    print(f"  {'start':22s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}")
+    print("exact re-scorings:", sum(cs[-1].route_fallbacks() for cs in cases), "over all launches")
+
+
+if __name__ == "__main__":
+    main()
