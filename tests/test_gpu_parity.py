@@ -518,18 +518,18 @@ def test_exact_grouping_equals_independent_queries(oracle_lib):
 
 
 ROUTE_VARIANTS = {"route3": {"SPECSV_ROUTE3": "1"}, "route3_exact": {"SPECSV_ROUTE3": "1", "SPECSV_ROUTE3_FORCE_EXACT": "1"},
-                  "legacy": {}}
+                  "default": {}}
 
 
 @pytest.mark.parametrize("rows,gamma,parents,mode", [(4096, 4, None, O.MODE_EXACT),
                                                      (3001, 8, TREE8, O.MODE_APPROX),
                                                      (65536, 8, None, O.MODE_EXACT)])
 def test_route_kernels_agree(oracle_lib, monkeypatch, rows, gamma, parents, mode):
-    """Routing runs on route3_kernel by default (integer tensor-pipe logits,
-    certified Top-n); SPECSV_ROUTE3_FORCE_EXACT=1 sends every query through its
-    exact fp64 re-scoring path, SPECSV_ROUTE_LEGACY=1 selects the fp64-DMMA
-    route_fused_kernel.  All three against the oracle, and their index sets
-    agree; the fp64 score diagnostic holds P3."""
+    """Routing runs on the fp64-DMMA route_fused_kernel by default;
+    SPECSV_ROUTE3=1 selects route3_kernel (integer tensor-pipe logits,
+    certified Top-n) and SPECSV_ROUTE3_FORCE_EXACT=1 sends every query through
+    its exact fp64 re-scoring path.  All three against the oracle, and their
+    index sets agree; the fp64 score diagnostic holds P3."""
     cfg = O.llama_config(4)
     x = LayerInputs(cfg, rows, gamma, 31 + rows + gamma, parent_slot=parents)
     case = DeviceCase(cfg, x)
@@ -554,3 +554,67 @@ def test_route_kernels_agree(oracle_lib, monkeypatch, rows, gamma, parents, mode
     for name in ROUTE_VARIANTS:
         for a, b in zip(got["route3"], got[name]):
             assert np.array_equal(a, b), name
+
+
+def test_verify_batched_c4_shape(oracle_lib):
+    """Config C4's own shape through the batched entry point: 16 requests at
+    128K committed rows (gamma = 8 chain), ONE routing launch over all 16
+    refresh requests and two attend launches of 8 (the per-GPU share of 64
+    requests on 4 GPUs, what bench.py runs).  Every request's sets and outputs
+    equal its single call; two requests are checked against the oracle; then a
+    batched REUSE pass over the same sets equals the refresh outputs."""
+    cfg = O.llama_config(4)
+    vcfg = V.NsaConfig(**cfg.__dict__)
+    R, rows, g = 16, 131072, 8
+    nq = 1 + g
+    oracle_reqs = {0: 31001, 11: 31011}
+    cases = {r: DeviceCase(cfg, LayerInputs(cfg, rows, g, seed)) for r, seed in oracle_reqs.items()}
+    gen = torch.Generator(device="cuda")
+    caches, batches = [], []
+    pos = np.array([rows - 1 + i for i in range(nq)], np.int64)
+    from paper_2605_19893_b200.workload import chain_tree_mask
+    for r in range(R):
+        if r in cases:
+            caches.append(cases[r].cache)
+            batches.append(cases[r].batch)
+            continue
+        gen.manual_seed(7000 + r)
+        c = V.LayerCache(vcfg, rows)
+        u = lambda *s: torch.rand(*s, generator=gen, device="cuda") * 2 - 1  # noqa: E731
+        c.append(u(rows, cfg.n_kv_heads, cfg.d_head).bfloat16(), u(rows, cfg.n_kv_heads, cfg.d_head).bfloat16())
+        c.extend_compressed(u(cfg.l, cfg.d_head) * 0.1)
+        caches.append(c)
+        batches.append(V.DraftBatch(pos=pos.copy(), tree_mask=chain_tree_mask(g),
+                                    q=u(nq, cfg.n_q_heads, cfg.d_head),
+                                    gates=torch.rand(nq, cfg.n_q_heads, 3, generator=gen, device="cuda") * 0.6 + 0.2,
+                                    tree_k=u(g, cfg.n_kv_heads, cfg.d_head).bfloat16(),
+                                    tree_v=u(g, cfg.n_kv_heads, cfg.d_head).bfloat16()))
+    ws1 = V.Workspace(vcfg, nq, rows)
+    singles = []
+    for r in range(R):
+        s = V.IndexSets.empty(nq, cfg.n)
+        o = torch.zeros(nq, cfg.n_q_heads, cfg.d_head, device="cuda")
+        V.nsa_verify(vcfg, caches[r], batches[r], s, o, ws1, 4, V.MODE_EXACT, V.ROLE_REFRESH)
+        singles.append((o, s))
+    ws = V.Workspace(vcfg, nq, rows, batch=R)
+    sets = [V.IndexSets.empty(nq, cfg.n) for _ in range(R)]
+    outs = [torch.zeros(nq, cfg.n_q_heads, cfg.d_head, device="cuda") for _ in range(R)]
+    V.nsa_verify_batched(vcfg, caches, batches, sets, outs, ws, 4, V.MODE_EXACT)
+    outs2 = [torch.zeros_like(o) for o in outs]
+    V.nsa_verify_batched(vcfg, caches, batches, sets, outs2, ws, 4, V.MODE_EXACT,
+                         [V.ROLE_REUSE] * R)
+    torch.cuda.synchronize()
+    for r in range(R):
+        so, ss = singles[r]
+        gi, gc, gf = sets_to_numpy(sets[r])
+        si, sc, sf = sets_to_numpy(ss)
+        assert np.array_equal(gi, si) and np.array_equal(gc, sc) and np.array_equal(gf, sf), r
+        got = outs[r].cpu().numpy().astype(np.float64)
+        ref1 = so.cpu().numpy().astype(np.float64)
+        assert np.abs(got - ref1).max() <= 1e-4 * max(np.abs(ref1).max(), 1e-6), r
+        assert np.abs(outs2[r].cpu().numpy() - got).max() <= 1e-5 * max(np.abs(got).max(), 1e-6), r
+        if r in cases:
+            ref = cases[r].oracle(oracle_lib, 4, O.MODE_EXACT, O.ROLE_REFRESH)
+            assert _check_indices(oracle_lib, cases[r], gi, gc, gf, ref) == 0, r
+            per, l2 = rel_errors(got, ref["out"])
+            assert per <= TOL and l2 <= TOL, (r, per, l2)
