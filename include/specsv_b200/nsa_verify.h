@@ -39,7 +39,8 @@
 extern "C" {
 #endif
 
-#define SPECSV_ABI_VERSION 2  /* 2: specsv_layer_kv.capacity, verify-args KV-head range */
+#define SPECSV_ABI_VERSION 3  /* 2: specsv_layer_kv.capacity, verify-args KV-head range;
+                                 3: specsv_layer_kv.ckd / ckexp (routing digit planes) */
 
 typedef struct CUstream_st* specsv_stream_t; /* == cudaStream_t */
 
@@ -87,6 +88,14 @@ typedef struct specsv_layer_kv {
                            (capacity - l) / d + 1 blocks.  Appends and commits are
                            bounds-checked against it (the reference asserts on the
                            same invariant, cache.hpp:26-30) */
+  void* ckd;            /* device int8 [>= blocks][Hkv][4][dh], or NULL: the routing keys as
+                           fixed-point digits -- byte s of element x is the base-256 digit
+                           of weight 256^s of round(ck[x] * 2^(30 - e)), e = ckexp, digits
+                           in [-128, 127].  Written by specsv_compress_append next to ck;
+                           the integer tensor-pipe routing kernel streams these planes
+                           (NULL selects the fp64 routing kernel over ck) */
+  int32_t* ckexp;       /* device [>= blocks][Hkv]: e with max_x |ck[x]| < 2^e (0 for an
+                           all-zero row); NULL iff ckd is NULL */
 } specsv_layer_kv;
 
 /* One verify call: one layer x one request, root + gamma draft queries in

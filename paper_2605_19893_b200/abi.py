@@ -45,7 +45,8 @@ class NsaConfigC(C.Structure):
 class LayerKvC(C.Structure):
     _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("rows", C.c_int64),
                 ("ck", C.c_void_p), ("ck16", C.c_void_p), ("cv", C.c_void_p),
-                ("blocks", C.c_int64), ("capacity", C.c_int64)]
+                ("blocks", C.c_int64), ("capacity", C.c_int64),
+                ("ckd", C.c_void_p), ("ckexp", C.c_void_p)]
 
 
 class VerifyArgsC(C.Structure):

@@ -16,7 +16,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libspecsv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["attend.cu", "route.cu", "route2.cu", "route3.cu", "compress.cu", "draft_tree.cu", "abi.cpp", "policy.cpp", "planner.cpp"]
+SOURCES = ["attend.cu", "route.cu", "route3.cu", "compress.cu", "draft_tree.cu", "abi.cpp", "policy.cpp", "planner.cpp"]
 HEADERS = ["attend.h", "sm100.cuh", "policy.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

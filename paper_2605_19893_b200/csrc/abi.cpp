@@ -65,34 +65,21 @@ void encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int64_t hkv
   if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
-// fp32 [blocks][hkv][dh] as a 3-D map (dh, hkv, blocks) with 32x1x16 SWIZZLE_128B
-// boxes (route2's key tiles; rows past `blocks` read as zeros)
-void encode_ck_map(CUtensorMap* m, const float* base, int64_t blocks, int64_t hkv, int64_t dh) {
+// int8 digit planes [blocks][hkv][4][dh] as a 4-D map (dh, plane, hkv, blocks)
+// with 128 x 1 x 1 x 128 SWIZZLE_128B boxes: one box is one digit plane of a
+// 128-block routing tile, already in the K-major SW128 layout of the MMA's A
+// operand (rows past `blocks` read as zeros)
+void encode_ckd_map(CUtensorMap* m, const void* base, int64_t blocks, int64_t hkv, int64_t dh) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)hkv, (cuuint64_t)std::max<int64_t>(blocks, 1)};
-  const cuuint64_t strides[2] = {(cuuint64_t)(dh * 4), (cuuint64_t)(hkv * dh * 4)};
-  const cuuint32_t box[3] = {32, 1, 16};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const cuuint64_t dims[4] = {(cuuint64_t)dh, 4, (cuuint64_t)hkv, (cuuint64_t)std::max<int64_t>(blocks, 1)};
+  const cuuint64_t strides[3] = {(cuuint64_t)dh, (cuuint64_t)(4 * dh), (cuuint64_t)(hkv * 4 * dh)};
+  const cuuint32_t box[4] = {(cuuint32_t)dh, 1, 1, (cuuint32_t)kR3Tile};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled (ck) failed");
-}
-
-// fp32 [blocks][hkv][dh] as a 3-D map (dh, hkv, blocks) with one 128 x 1 x 128
-// box per route3 unit (a 64 KB row-major key tile; rows past `blocks` read as zeros)
-void encode_ck3_map(CUtensorMap* m, const float* base, int64_t blocks, int64_t hkv, int64_t dh) {
-  EncodeTiledFn fn = encode_fn();
-  if (fn == nullptr) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {(cuuint64_t)dh, (cuuint64_t)hkv, (cuuint64_t)std::max<int64_t>(blocks, 1)};
-  const cuuint64_t strides[2] = {(cuuint64_t)(dh * 4), (cuuint64_t)(hkv * dh * 4)};
-  const cuuint32_t box[3] = {(cuuint32_t)dh, 1, (cuuint32_t)kR3Tile};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled (route3 ck) failed");
+  if (r != CUDA_SUCCESS) throw Error(SPECSV_ECUDA, "cuTensorMapEncodeTiled (digit planes) failed");
 }
 
 // co-resident CTAs of the attend kernel on this device (a device constant,
@@ -140,10 +127,9 @@ constexpr int kCntSetInts = 4 + kMaxQueries;
 struct Layout {
   size_t sync_off = 0, sync_bytes = 0;  // attend barrier words: fixed position per config
   int max_chunks = 1;                   // query chunks of the widest call (kMaxQueries)
-  size_t r2cnt_off = 0;                 // route2 barrier words: fixed position per config
-  size_t r3cnt_off = 0;                 // route3 barrier words (+ fallback counter): fixed position
-  size_t r3_stats_off = 0, r3_gsh_off = 0, r3_contrib_off = 0, r3_eps_off = 0;  // route3 regions
-  size_t r2_off = 0;                    // route2 regions (dm, part, ovh, candidates)
+  size_t r3cnt_off = 0;                 // route3 words: [0] exit count, [4] fallbacks, then one
+                                        // counter set per request of a launch (fixed position)
+  size_t r3_den_off = 0, r3_spill_off = 0, r3_contrib_off = 0;  // route3 regions (per request)
   size_t attend_off = 0, attend_bytes = 0;
   size_t E_off = 0, TM_off = 0, TD_off = 0, F_off = 0, sel_off = 0, cnt_off = 0;
   int64_t sel_pad = 0;
@@ -152,14 +138,33 @@ struct Layout {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// route3 unit shape: rows per chunk (whole slots, <= kR3Rows) and the
-// selection blocks one 128-block unit touches
-int64_t route3_chunk_rows(const specsv_nsa_config& c) {
-  const int64_t G = c.n_q_heads / c.n_kv_heads;
-  return std::max<int64_t>(1, kR3Rows / G) * G;
+// route3 unit shape: slots per row chunk (whole slots, <= kR3Rows rows), the
+// widest selection-block range whose compressed blocks fit one unit
+// (kR3MaxBlk), and a bound on the ranges per (chunk, KV head)
+int64_t route3_spc(const specsv_nsa_config& c) {
+  return std::max<int64_t>(1, kR3Rows / (c.n_q_heads / c.n_kv_heads));
 }
-int64_t route3_span(const specsv_nsa_config& c) {
-  return ((kR3Tile - 1) * c.d + c.l - 1) / c.l_sel + 1;
+int64_t route3_spr_max(const specsv_nsa_config& c) {
+  for (int64_t spr = kR3MaxSpr; spr > 1; --spr) {
+    bool ok = true;
+    for (int64_t b0 = 0; b0 < 64 && ok; ++b0) {  // the pattern repeats with period d / gcd
+      const int64_t num = b0 * c.l_sel - c.l;
+      const int64_t lo = num >= 0 ? num / c.d + 1 : 0;
+      const int64_t hi = ((b0 + spr) * c.l_sel - 1) / c.d;
+      ok = hi - lo + 1 <= kR3MaxBlk;
+    }
+    if (ok) return spr;
+  }
+  return 1;
+}
+int64_t route3_nchunks(const specsv_nsa_config& c, int32_t nr) {
+  const int64_t spc = route3_spc(c);
+  return (nr + spc - 1) / spc;
+}
+constexpr int64_t kR3SmBound = 160;  // >= SM count: the ranges a single request spreads over
+int64_t route3_nranges_bound(const specsv_nsa_config& c, int64_t sel_pad) {
+  const int64_t per = std::max<int64_t>(1, c.n_kv_heads);  // one row chunk (the fewest units)
+  return std::max<int64_t>((sel_pad + route3_spr_max(c) - 1) / route3_spr_max(c), (kR3SmBound + per - 1) / per);
 }
 
 // queries per column chunk: 64 columns / G, and few enough that the chunk's
@@ -183,16 +188,14 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   L.sync_off = 0;
   L.sync_bytes = (size_t)kSyncSets * L.max_chunks * c.n_kv_heads * 2 * sizeof(int32_t);
   L.cnt_off = align_up(L.sync_off + L.sync_bytes, 256);
-  L.r2cnt_off = align_up(L.cnt_off + (size_t)kSyncSets * kCntSetInts * sizeof(int32_t), 256);
-  L.r3cnt_off = align_up(L.r2cnt_off + (size_t)kR2CntInts * sizeof(int32_t), 256);
-  L.attend_off = align_up(L.r3cnt_off + 8 * sizeof(int32_t), 256);
+  L.r3cnt_off = align_up(L.cnt_off + (size_t)kSyncSets * kCntSetInts * sizeof(int32_t), 256);
+  L.attend_off = align_up(L.r3cnt_off + (8 + (size_t)kR3Batch * kR3CntPerReq) * sizeof(int32_t), 256);
   L.attend_bytes = attend_workspace_floats(nchunks, (int)c.n_kv_heads, splits) * sizeof(float);
   const int64_t maxblk = max_rows >= c.l ? (max_rows - c.l) / c.d + 1 : 0;
   const int64_t m_pad = align_up(std::max<int64_t>(maxblk, 1), kRouteTile);
   const int64_t ntiles = m_pad / kRouteTile;
   L.sel_pad = (int64_t)align_up((size_t)((max_rows + c.l_sel - 1) / c.l_sel + 1), 32);
-  L.r2_off = align_up(L.attend_off + L.attend_bytes, 256);
-  size_t off = align_up(L.r2_off + route2_ws_bytes(nq, (int)c.n_kv_heads, (int)L.sel_pad), 256);
+  size_t off = align_up(L.attend_off + L.attend_bytes, 256);
   const int64_t gs = ((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 1;  // = g_stride
   L.E_off = off;  // per-tile selection-block shares [nq][ntiles][Hq][gs]
   off = align_up(off + (size_t)nq * ntiles * c.n_q_heads * gs * 8, 256);
@@ -202,21 +205,15 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
   off = align_up(off + (size_t)nq * c.n_q_heads * ntiles * 8, 256);
   L.F_off = off;  // per-KV-head score shares [nq][Hkv][sel_pad]
   off = align_up(off + (size_t)nq * c.n_kv_heads * L.sel_pad * 8, 256);
-  {  // route3: tile statistics, per-unit selection-block sums, shares, error bounds
-    const int64_t G = c.n_q_heads / c.n_kv_heads;
-    const int64_t nt3 = (maxblk + kR3Tile - 1) / kR3Tile;
-    const int64_t rows_head = (int64_t)nq * G;
-    const int64_t cr = route3_chunk_rows(c);
-    const int64_t chunks = (rows_head + cr - 1) / cr;
-    const int64_t span = route3_span(c);
-    L.r3_stats_off = off;
-    off = align_up(off + (size_t)(c.n_kv_heads * rows_head * nt3 * 4 * 8), 256);
-    L.r3_gsh_off = off;
-    off = align_up(off + (size_t)(c.n_kv_heads * chunks * nt3 * kR3Rows * span * 8), 256);
+  {  // route3: per-range den rows, spilled selection-block sums, per-KV-head shares
+    const int64_t chunks = route3_nchunks(c, nq);
+    const int64_t nranges = route3_nranges_bound(c, L.sel_pad);
+    L.r3_den_off = off;
+    off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * kR3Rows * 8), 256);
+    L.r3_spill_off = off;
+    off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * kR3Rows * kR3MaxSpr * 8), 256);
     L.r3_contrib_off = off;
-    off = align_up(off + (size_t)(nq * c.n_kv_heads * nt3 * span * 8), 256);
-    L.r3_eps_off = off;
-    off = align_up(off + (size_t)(nq * c.n_kv_heads * 8), 256);
+    off = align_up(off + (size_t)(nq * c.n_kv_heads * L.sel_pad * 8), 256);
   }
   L.total = off;
   return L;
@@ -238,6 +235,8 @@ void validate_args(const specsv_nsa_config& c, const specsv_layer_kv& kv,
       kv.cv == nullptr)
     throw Error(SPECSV_EINVAL, "null cache pointer");
   if (kv.rows < 1) throw Error(SPECSV_EINVAL, "rows must be >= 1 (the pending root is committed)");
+  if ((kv.ckd == nullptr) != (kv.ckexp == nullptr))
+    throw Error(SPECSV_EINVAL, "ckd and ckexp must both be set or both be NULL");
   if (kv.capacity < kv.rows) throw Error(SPECSV_EINVAL, "rows exceed the cache capacity");
   if (a.kv_head_count < 0 || a.kv_head_begin < 0 ||
       (int64_t)a.kv_head_begin + a.kv_head_count > c.n_kv_heads ||
@@ -318,10 +317,12 @@ RouteParams make_route_params(const specsv_nsa_config& c, const specsv_layer_kv&
 
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
                void* ws, size_t ws_bytes, cudaStream_t stream);
-bool use_route3();
+bool use_route3(const specsv_layer_kv& kv);
 void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
-                     const Layout& L, char* base, const std::vector<int32_t>& routed, Route3Req& R);
+                     const Layout& L, char* base, const std::vector<int32_t>& routed, int32_t* cnt,
+                     bool spread, Route3Req& R);
 void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, Route3Launch& P);
+int32_t* route3_cnt(const Layout& L, char* ws, int r);
 
 // bytes of one request's routing regions (E, TM, TD, F); a batched routing
 // launch places request q's at E_off + q x route_bytes
@@ -348,7 +349,9 @@ void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
   const size_t cap = 1 + (ws_bytes - L.total) / std::max<size_t>(route_bytes(L), 1);
   const int group = (int)std::min<size_t>({(size_t)kRouteBatch, (size_t)kSyncSets, cap});
   char* w = static_cast<char*>(ws);
-  if (use_route3()) {
+  bool all3 = true;
+  for (int32_t b : refresh) all3 = all3 && use_route3(kvs[b]);
+  if (all3) {
     const int group3 = (int)std::min<size_t>((size_t)kR3Batch, cap);
     thread_local Route3Launch P;
     for (size_t g0 = 0; g0 < refresh.size(); g0 += group3) {
@@ -359,7 +362,8 @@ void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
       for (int q = 0; q < n; ++q) {
         const int32_t b = refresh[g0 + q];
         const auto routed = routed_queries(args[b].n_queries, args[b].pos, args[b].group_size, args[b].mode);
-        make_route3_req(c, kvs[b], args[b], L, w + L.E_off + (size_t)q * route_bytes(L), routed, P.req[q]);
+        make_route3_req(c, kvs[b], args[b], L, w + L.E_off + (size_t)q * route_bytes(L), routed,
+                        route3_cnt(L, w, q), n == 1, P.req[q]);
       }
       cuda_check(launch_route3(P, stream), "batched route launch");
     }
@@ -386,94 +390,23 @@ void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
   }
 }
 
-// the per-range routing variant (route2.cu) when SPECSV_ROUTE2=1 and its range
-// decomposition fits; false = route_fused_kernel (the default: measured faster
-// at the bench shape, 40.8 vs 49.9 us -- DESIGN.md "Routing").  Tests cover both.
-bool make_route2(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
-                 const Layout& L, char* ws, const std::vector<int32_t>& routed, double* scores_out,
-                 Route2Params& p) {
-  const char* want = std::getenv("SPECSV_ROUTE2");
-  if (want == nullptr || want[0] != '1') return false;
-  std::memset(&p, 0, sizeof(p));
-  const int nr = static_cast<int>(routed.size());
-  int64_t mmax = 0, smax = 0;
-  std::vector<bool> is_routed(a.n_queries, false);
-  for (int s = 0; s < nr; ++s) {
-    const int32_t q = routed[s];
-    is_routed[q] = true;
-    const int64_t vis = routing_visible_len(c, a.pos[q]);
-    p.slot_q[s] = q;
-    p.slot_mvis[s] = (int32_t)visible_blocks(c, kv.blocks, vis);
-    p.slot_avail[s] = (int32_t)selection_block_count(c, vis);
-    mmax = std::max<int64_t>(mmax, p.slot_mvis[s]);
-    smax = std::max<int64_t>(smax, p.slot_avail[s]);
-  }
-  for (int32_t q = 0; q < a.n_queries; ++q)
-    if (!is_routed[q]) p.unrouted[p.n_unrouted++] = q;
-  const int ntiles = (int)((mmax + kRouteTile - 1) / kRouteTile);
-  const int gs = (int)(((kRouteTile - 1) * c.d + c.l - 1) / c.l_sel + 1);
-  const int spt = (int)(kRouteTile * c.d / c.l_sel);
-  const int G = (int)(c.n_q_heads / c.n_kv_heads);
-  if (!route2_plan(nr, G, (int)c.n_kv_heads, ntiles, gs, spt, (int)c.n, p)) return false;
-  if (c.d_head != 128) return false;
-  encode_ck_map(&p.tm_ck, kv.ck, kv.blocks, c.n_kv_heads, c.d_head);
-  p.q = a.q;
-  p.ck = kv.ck;
-  p.idx = a.idx;
-  p.idx_count = a.idx_count;
-  p.idx_forced = a.idx_forced;
-  p.scores_out = scores_out;
-  p.trace = g_trace;
-  if (const char* e = std::getenv("SPECSV_ROUTE2_DEBUG_EXIT")) p.debug_exit = std::atoi(e);  // timing only
-  p.nr = nr;
-  p.Hq = (int32_t)c.n_q_heads;
-  p.Hkv = (int32_t)c.n_kv_heads;
-  p.G = G;
-  p.n = (int32_t)c.n;
-  p.l = (int32_t)c.l;
-  p.d = (int32_t)c.d;
-  p.l_sel = (int32_t)c.l_sel;
-  p.blocks = (int32_t)kv.blocks;
-  p.spt = spt;
-  p.gs = gs;
-  p.sel_pad = (int32_t)L.sel_pad;
-  p.s_total = (int32_t)smax;
-  p.scale = 1.0 / std::sqrt(static_cast<double>(c.d_head));
-  // regions: dm [kR2MaxRanges][40] (m, den) | part [nr][Hkv][sel_pad] | ovh | cand_s | cand_i | cand_n
-  char* r = ws + L.r2_off;
-  const size_t items = kR2MaxRanges;
-  p.dm = reinterpret_cast<double*>(r);
-  r += align_up(items * kR2Rows * 16, 256);
-  p.part = reinterpret_cast<double*>(r);
-  r += align_up((size_t)nr * c.n_kv_heads * L.sel_pad * 8, 256);
-  p.ovh = reinterpret_cast<double*>(r);
-  r += align_up((size_t)nr * c.n_kv_heads * kR2MaxRanges * 8 * 8, 256);
-  p.cand_s = reinterpret_cast<double*>(r);
-  r += align_up((size_t)nr * kR2MaxRanges * 64 * 8, 256);
-  p.cand_i = reinterpret_cast<int32_t*>(r);
-  r += align_up((size_t)nr * kR2MaxRanges * 64 * 4, 256);
-  p.cand_n = reinterpret_cast<int32_t*>(r);
-  int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.r2cnt_off);
-  p.bar = cnt;
-  p.rcnt = cnt + 2 * kR2MaxRanges;
-  p.fcnt = cnt + 3 * kR2MaxRanges;
-  return true;
-}
-
-// the routing kernel of a call: route_fused_kernel (fp64 DMMA) by default;
-// SPECSV_ROUTE3=1 selects route3_kernel (integer tensor pipe, certified Top-n),
-// SPECSV_ROUTE2=1 the per-range variant
-bool use_route3() {
-  const char* r3 = std::getenv("SPECSV_ROUTE3");
-  return r3 != nullptr && r3[0] == '1';
+// the routing kernel of a call: route3_kernel (integer tensor pipe, certified
+// Top-n) whenever the cache carries digit planes; route_fused_kernel (fp64
+// DMMA over ck) otherwise or with SPECSV_ROUTE_LEGACY=1
+bool use_route3(const specsv_layer_kv& kv) {
+  const char* e = std::getenv("SPECSV_ROUTE_LEGACY");
+  return kv.ckd != nullptr && (e == nullptr || e[0] != '1');
 }
 
 // one request's route3 parameters; `base` is its routing region (E_off-relative
-// offsets of the layout apply)
+// offsets of the layout apply); `spread`: ranges per (chunk, KV head) may grow
+// until the units fill the device (a launch of one request)
 void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
-                     const Layout& L, char* base, const std::vector<int32_t>& routed, Route3Req& R) {
+                     const Layout& L, char* base, const std::vector<int32_t>& routed, int32_t* cnt,
+                     bool spread, Route3Req& R) {
   std::memset(&R, 0, sizeof(R));
-  encode_ck3_map(&R.tm_ck, kv.ck, kv.blocks, c.n_kv_heads, c.d_head);
+  encode_ckd_map(&R.tm_ckd, kv.ckd, kv.blocks, c.n_kv_heads, c.d_head);
+  R.ckexp = kv.ckexp;
   R.q = a.q;
   R.ck = kv.ck;
   R.idx = a.idx;
@@ -481,7 +414,9 @@ void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, cons
   R.idx_forced = a.idx_forced;
   R.nr = static_cast<int32_t>(routed.size());
   R.blocks = (int32_t)kv.blocks;
-  int64_t mmax = 0;
+  R.sel_pad = (int32_t)L.sel_pad;
+  R.cnt = cnt;
+  int64_t amax = 0;
   std::vector<bool> is_routed(a.n_queries, false);
   for (size_t s = 0; s < routed.size(); ++s) {
     const int32_t q = routed[s];
@@ -490,18 +425,26 @@ void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, cons
     R.slot_q[s] = q;
     R.slot_mvis[s] = (int32_t)visible_blocks(c, kv.blocks, vis);
     R.slot_avail[s] = (int32_t)selection_block_count(c, vis);
-    mmax = std::max<int64_t>(mmax, R.slot_mvis[s]);
+    amax = std::max<int64_t>(amax, R.slot_avail[s]);
   }
   for (int32_t q = 0; q < a.n_queries; ++q)
     if (!is_routed[q]) R.unrouted[R.n_unrouted++] = q;
-  const int64_t G = c.n_q_heads / c.n_kv_heads;
-  R.ntiles = (int32_t)((mmax + kR3Tile - 1) / kR3Tile);
-  R.nchunks = (int32_t)((R.nr * G + route3_chunk_rows(c) - 1) / route3_chunk_rows(c));
+  R.avail_max = (int32_t)amax;
+  R.nchunks = (int32_t)route3_nchunks(c, R.nr);
+  const int64_t per = R.nchunks * c.n_kv_heads;
+  if (per > kR3CntPerReq - 176) throw Error(SPECSV_EUNSUPPORTED, "route3: too many row chunks x KV heads");
+  int64_t nranges = std::max<int64_t>(1, (amax + route3_spr_max(c) - 1) / route3_spr_max(c));
+  if (spread) nranges = std::max<int64_t>(nranges, route3_grid() / per);
+  const int64_t spr = std::max<int64_t>(1, (amax + nranges - 1) / nranges);
+  nranges = std::max<int64_t>(1, (amax + spr - 1) / spr);
+  if (nranges > route3_nranges_bound(c, L.sel_pad))
+    throw Error(SPECSV_EUNSUPPORTED, "route3: selection-block ranges exceed the workspace bound");
+  R.nranges = (int32_t)nranges;
+  R.spr = (int32_t)spr;
   const size_t rel = L.E_off;  // region offsets are relative to the request's routing region
-  R.stats = reinterpret_cast<double*>(base + (L.r3_stats_off - rel));
-  R.gsh = reinterpret_cast<double*>(base + (L.r3_gsh_off - rel));
+  R.den = reinterpret_cast<double*>(base + (L.r3_den_off - rel));
+  R.gspill = reinterpret_cast<double*>(base + (L.r3_spill_off - rel));
   R.contrib = reinterpret_cast<double*>(base + (L.r3_contrib_off - rel));
-  R.eps = reinterpret_cast<double*>(base + (L.r3_eps_off - rel));
 }
 
 void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, Route3Launch& P) {
@@ -512,19 +455,23 @@ void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, R
   P.l = (int32_t)c.l;
   P.d = (int32_t)c.d;
   P.l_sel = (int32_t)c.l_sel;
-  P.chunk_rows = (int32_t)route3_chunk_rows(c);
-  P.spt = (int32_t)(kR3Tile * c.d / c.l_sel);
-  P.span = (int32_t)route3_span(c);
+  P.spc = (int32_t)route3_spc(c);
+  P.bps = (int32_t)((c.l_sel - 1 + c.l - 1) / c.d + 1);  // blocks_of: hi - lo + 1 at most
+  if (P.bps > kR3MaxBps) throw Error(SPECSV_EUNSUPPORTED, "route3: too many compressed blocks per selection block");
   P.scale = 1.0 / std::sqrt(static_cast<double>(c.d_head));
   P.c_sl = 1.4426950408889634073599 / std::sqrt(static_cast<double>(c.d_head));
   int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.r3cnt_off);
-  P.counters = cnt;
+  P.exit_cnt = cnt;
   P.fallbacks = cnt + 4;
   const char* fe = std::getenv("SPECSV_ROUTE3_FORCE_EXACT");  // tests: the exact re-scoring path
   P.force_exact = (fe != nullptr && fe[0] == '1') ? 1 : 0;
   P.trace = g_trace;
-  if ((kR3Tile * c.d) % c.l_sel != 0 || P.span > kR3MaxSpan)
-    throw Error(SPECSV_EUNSUPPORTED, "route3: unit span outside this build's limits");
+  if (c.d_head != kR3Tile) throw Error(SPECSV_EUNSUPPORTED, "route3: d_head must be 128");
+}
+
+// counter set `r` of a route3 launch
+int32_t* route3_cnt(const Layout& L, char* ws, int r) {
+  return reinterpret_cast<int32_t*>(ws + L.r3cnt_off) + 8 + (size_t)r * kR3CntPerReq;
 }
 
 void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
@@ -532,19 +479,14 @@ void run_route(const specsv_nsa_config& c, const specsv_layer_kv& kv, const spec
   const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   const auto routed = routed_queries(a.n_queries, a.pos, a.group_size, a.mode);
-  if (use_route3()) {
-    thread_local Route3Launch P;  // ~21 KB host staging of the launch parameters
+  if (use_route3(kv)) {
+    thread_local Route3Launch P;  // ~33 KB host staging of the launch parameters
     std::memset(&P, 0, sizeof(P));
     char* w = static_cast<char*>(ws);
     fill_route3_common(c, L, w, P);
     P.n_req = 1;
-    make_route3_req(c, kv, a, L, w + L.E_off, routed, P.req[0]);
+    make_route3_req(c, kv, a, L, w + L.E_off, routed, route3_cnt(L, w, 0), true, P.req[0]);
     cuda_check(launch_route3(P, stream), "route launch");
-    return;
-  }
-  Route2Params p2;
-  if (make_route2(c, kv, a, L, static_cast<char*>(ws), routed, nullptr, p2)) {
-    cuda_check(launch_route2(p2, stream), "route launch");
     return;
   }
   RouteParams p = make_route_params(c, kv, a, L, static_cast<char*>(ws), routed);
@@ -788,11 +730,6 @@ specsv_status specsv_nsa_scores(const specsv_nsa_config* cfg, const specsv_layer
     const Layout L = layout_for(*cfg, args->n_queries, kv->rows);
     if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
     std::vector<int32_t> routed{query};
-    Route2Params p2;
-    if (make_route2(*cfg, *kv, *args, L, static_cast<char*>(ws), routed, scores, p2)) {
-      cuda_check(launch_route2(p2, reinterpret_cast<cudaStream_t>(stream)), "scores launch");
-      return;
-    }
     RouteParams p = make_route_params(*cfg, *kv, *args, L, static_cast<char*>(ws), routed);
     cuda_check(launch_scores_only(p, scores, 0, reinterpret_cast<cudaStream_t>(stream)),
                "scores launch");
@@ -828,8 +765,10 @@ specsv_status specsv_compress_append(const specsv_nsa_config* cfg, const specsv_
       throw Error(SPECSV_EINVAL, "block range outside the committed rows");
     if (!kv->k || !kv->v || !kv->ck || !kv->ck16 || !kv->cv)
       throw Error(SPECSV_EINVAL, "null cache pointer");
-    cuda_check(launch_compress(kv->k, kv->v, pos_embed, kv->ck, kv->ck16, kv->cv, first_block,
-                               last_block, (int)cfg->n_kv_heads, (int)cfg->d_head, (int)cfg->l,
+    if ((kv->ckd == nullptr) != (kv->ckexp == nullptr))
+      throw Error(SPECSV_EINVAL, "ckd and ckexp must both be set or both be NULL");
+    cuda_check(launch_compress(kv->k, kv->v, pos_embed, kv->ck, kv->ck16, kv->cv, kv->ckd, kv->ckexp,
+                               first_block, last_block, (int)cfg->n_kv_heads, (int)cfg->d_head, (int)cfg->l,
                                (int)cfg->d, reinterpret_cast<cudaStream_t>(stream)),
                "compress launch");
   });

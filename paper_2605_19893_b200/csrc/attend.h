@@ -117,68 +117,34 @@ struct RouteBatch {
   int32_t unit_start[kRouteBatch + 1];  // (slot, KV head) units of requests < q
 };
 
-// ---- routing, single-request fast path (route2.cu) ---------------------------
-// One CTA per (KV head, row chunk, block range): the range's 16-block tiles
-// stay in shared memory, the softmax statistics are combined per range, and a
-// short tail (one barrier among a head's ranges, per-range score sums, per-range
-// Top-n candidates, one final merge) replaces the grid-wide unit phase.
-constexpr int kR2MaxTiles = 16;   // tiles (16 blocks) per range CTA (one warp each)
-constexpr int kR2Rows = 40;       // (slot, head) rows per CTA
-constexpr int kR2MaxRanges = 160; // >= SM count
-struct Route2Params {
-  CUtensorMap tm_ck;       // fp32 compressed K, dims (dh, Hkv, blocks), box 32 x 1 x 16, 128B swizzle
-  const float* q;          // [nq][Hq][dh]
-  const float* ck;         // fp32 [blocks][Hkv][dh]
-  int32_t* idx;            // [nq][n]
-  int32_t* idx_count;      // [nq]
-  uint32_t* idx_forced;    // [nq]
-  double* scores_out;      // diagnostics: dense scores of slot 0, no Top-n (NULL: Top-n)
-  double* dm;              // [items][kR2Rows] (range max, range denominator)
-  double* part;            // [nr][Hkv][sel_pad] per-KV-head score shares
-  double* ovh;             // [nr][Hkv][NR][8] shares a range's last tile overhangs into the next
-  double* cand_s;          // [nr][NR][64] Top-n candidates per range (score)
-  int32_t* cand_i;         // [nr][NR][64] (block id)
-  int32_t* cand_n;         // [nr][NR]
-  int32_t* bar;            // [2 * Hkv * rc] range barrier (count, generation) per (KV head, row chunk)
-  int32_t* rcnt;           // [NR] arrivals per range
-  int32_t* fcnt;           // [1] finished ranges
-  int32_t nr, Hq, Hkv, G, n, l, d, l_sel, blocks;
-  int32_t rc, chunk_rows, NR, T, ntiles, spt, gs, sel_pad, s_total;
-  double scale;            // 1 / sqrt(dh)
-  int32_t slot_q[kMaxQueries], slot_mvis[kMaxQueries], slot_avail[kMaxQueries];
-  int32_t unrouted[kMaxQueries];
-  int32_t n_unrouted;
-  unsigned long long* trace;  // diagnostics only: per-CTA phase stamps at kRouteTraceBase
-  int32_t debug_exit;         // diagnostics only (timing): 0 = full kernel, k = return after phase k
-};
-// workspace words of route2's barriers (fixed offset per config; self-resetting)
-constexpr int kR2CntInts = 2 * kR2MaxRanges + kR2MaxRanges + 8;
-// shape of the range decomposition for one call; false = use route_fused_kernel
-bool route2_plan(int nr, int G, int Hkv, int ntiles, int gs, int spt, int n, Route2Params& p);
-size_t route2_ws_bytes(int nr, int Hkv, int sel_pad);  // dm/part/ovh/cand regions
-cudaError_t launch_route2(const Route2Params& p, cudaStream_t stream);
-
-// ---- routing on the integer tensor pipe (route3.cu, the default) -------------
-// Unit = (request, KV head, row chunk of <= 48 (slot, head) rows, 128
-// compressed blocks).  Logits come from exact s8 x s8 -> s32 tcgen05 products
-// of base-256 digits of fixed-point q and keys; scores carry a certified error
-// bound, and a query whose Top-n boundary falls inside it is re-scored in fp64.
-constexpr int kR3Rows = 48;     // q rows per unit (MMA N)
-constexpr int kR3Tile = 128;    // compressed blocks per unit (MMA M)
-constexpr int kR3Batch = 16;    // requests per launch
-constexpr int kR3MaxSpan = 64;  // selection blocks one unit touches (host-checked)
+// ---- routing on the integer tensor pipe (route3.cu) --------------------------
+// Unit = (request, row chunk of <= kR3Rows (slot, head) rows, KV head, range of
+// <= kR3MaxSpr selection blocks); one CTA streams the range's key-digit planes
+// (<= 256 compressed blocks) once.  Logits are exact s8 x s8 -> s32 tcgen05
+// products of base-256 digits of fixed-point q and keys; every probability
+// uses one fixed fp64 reference (no max pass), so per-range partial sums are
+// additive.  Scores carry a certified error bound, and a query whose Top-n
+// boundary falls inside it is re-scored exactly in fp64.
+constexpr int kR3Rows = 48;      // (slot, head) rows per unit (MMA N)
+constexpr int kR3Tile = 128;     // compressed blocks per MMA tile (MMA M)
+constexpr int kR3MaxBlk = 256;   // compressed blocks per unit (two tiles)
+constexpr int kR3MaxSpr = 64;    // selection blocks per unit
+constexpr int kR3MaxBps = 16;    // compressed blocks overlapping one selection block (host-checked)
+constexpr int kR3Batch = 16;     // requests per launch
+constexpr int kR3CntPerReq = 448;  // counter words per request (den arrivals, top arrivals, expo)
 struct Route3Req {
-  CUtensorMap tm_ck;     // fp32 compressed K, dims (dh, Hkv, blocks), box 128 x 1 x 128, no swizzle
+  CUtensorMap tm_ckd;    // int8 digit planes, dims (dh, 4, Hkv, blocks), box 128 x 1 x 1 x 128, SW128
+  const int32_t* ckexp;  // [blocks][Hkv] row exponents of the digit planes
   const float* q;        // [nq][Hq][dh]
   const float* ck;       // fp32 [blocks][Hkv][dh] (the exact re-scoring path)
   int32_t* idx;          // [nq][n]
   int32_t* idx_count;    // [nq]
   uint32_t* idx_forced;  // [nq]
-  double* stats;         // [Hkv][nr*G][ntiles][4]: tile max (log2), tile sum, logit error bound, -
-  double* gsh;           // [units][kR3Rows][span] per-unit selection-block sums (token weights)
-  double* contrib;       // [nr][Hkv][ntiles][span] normalised per-KV-head shares
-  double* eps;           // [nr][Hkv] logit error bound (log2 units) over the slot's rows
-  int32_t nr, ntiles, nchunks, blocks;
+  double* den;           // [nchunks][Hkv][nranges][kR3Rows] per-range denominators (token-weighted)
+  double* gspill;        // [units][kR3Rows][kR3MaxSpr] selection-block sums of a CTA's earlier units
+  double* contrib;       // [nr][Hkv][sel_pad] normalised per-KV-head score shares
+  int32_t* cnt;          // [kR3CntPerReq] this request's counter set (zero-initialised, self-resetting)
+  int32_t nr, nchunks, nranges, spr, blocks, avail_max, sel_pad;
   int32_t slot_q[kMaxQueries];
   int32_t slot_mvis[kMaxQueries];
   int32_t slot_avail[kMaxQueries];
@@ -191,17 +157,17 @@ struct Route3Launch {
   int32_t unit_start[kR3Batch + 1];  // units of requests < r (set at launch)
   int32_t task_start[kR3Batch + 1];  // (request, slot) Top-n tasks of requests < r
   int32_t Hq, Hkv, G, n, l, d, l_sel;
-  int32_t chunk_rows;  // rows per unit chunk, a multiple of G (<= kR3Rows)
-  int32_t spt;         // selection blocks per unit stride (kR3Tile d / l_sel)
-  int32_t span;        // selection blocks one unit touches
+  int32_t spc;         // slots per row chunk (chunk rows = spc x G <= kR3Rows)
+  int32_t bps;         // compressed blocks overlapping one selection block (at most)
   double scale;        // 1 / sqrt(dh)
   double c_sl;         // log2(e) / sqrt(dh): logits in log2 units
-  int32_t* counters;   // [4] zero-initialised, self-resetting (grid barriers, exits)
+  int32_t* exit_cnt;   // [1] CTAs done (the last one resets every request's counter set)
   int32_t* fallbacks;  // cumulative count of exact re-scorings (diagnostics; never reset)
   int32_t force_exact; // tests: re-score every query in fp64
   unsigned long long* trace;  // diagnostics: per-CTA stamps at kRouteTraceBase + cta * 16
 };
 cudaError_t launch_route3(Route3Launch& p, cudaStream_t stream);
+int route3_grid();  // CTAs of a route3 launch on this device (one per SM)
 
 cudaError_t launch_route(const RouteParams& p, cudaStream_t stream, bool write_idx);
 cudaError_t launch_route_batch(RouteBatch& b, cudaStream_t stream);
@@ -218,6 +184,8 @@ struct CompressLayers {
   float* ck[kCompressLayers];
   void* ck16[kCompressLayers];
   void* cv[kCompressLayers];
+  void* ckd[kCompressLayers];       // digit planes (NULL: none)
+  int32_t* ckexp[kCompressLayers];
   int64_t first[kCompressLayers];
   int64_t count[kCompressLayers];
   int32_t hkv, dh, l, d;
@@ -225,7 +193,7 @@ struct CompressLayers {
 cudaError_t launch_compress_layers(const CompressLayers& c, int n_layers, int64_t max_count,
                                    cudaStream_t stream);
 cudaError_t launch_compress(const void* k, const void* v, const float* pe, float* ck, void* ck16,
-                            void* cv, int64_t first, int64_t last, int hkv, int dh, int l, int d,
-                            cudaStream_t stream);
+                            void* cv, void* ckd, int32_t* ckexp, int64_t first, int64_t last, int hkv,
+                            int dh, int l, int d, cudaStream_t stream);
 
 }  // namespace specsv_b200

@@ -6,6 +6,11 @@
 // reference's order (per offset o: += k, += pe, then += v), scaled by 1/l and
 // rounded to fp32, so ck is bit-identical to the reference on the same bf16
 // rows.  ck16 / cv are the bf16 (RNE) copies the attention kernel streams.
+// When the cache carries digit planes (ckd / ckexp), each (block, head) row of
+// ck is also written as a 31-bit fixed-point integer on the row's own
+// power-of-two grid (X = round(ck 2^(30 - e)), max |ck| < 2^e), split into
+// four signed base-256 digits: the routing kernel (route3.cu) feeds them to
+// the integer tensor pipe without converting anything per call.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -16,15 +21,65 @@
 namespace specsv_b200 {
 namespace {
 
+// max |v| over the (block, head) row held by this CTA (blockDim threads)
+__device__ float row_absmax(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float m = 0.f;
+  for (int i = 0; i < nw; ++i) m = fmaxf(m, red[i]);
+  return m;
+}
+
+// four signed base-256 digits of round(x 2^(30 - e)) (|result| <= 2^30):
+// byte s is the digit of weight 256^s, in [-128, 127]
+__device__ __forceinline__ uint32_t digits4(float x, int e) {
+  const int X = __float2int_rn(ldexpf(x, 30 - e));
+  return (static_cast<uint32_t>(X) + 0x80808080u) ^ 0x80808080u;
+}
+
+// the digit planes of one (block, head) row: fk[r] is element threadIdx.x + r blockDim
+template <int kPer>
+__device__ void write_digit_row(const float (&fk)[kPer], int dh, int8_t* ckd, int32_t* ckexp,
+                                int64_t row) {
+  __shared__ float red[32];
+  float a = 0.f;
+#pragma unroll
+  for (int r = 0; r < kPer; ++r)
+    if (threadIdx.x + r * blockDim.x < dh) a = fmaxf(a, fabsf(fk[r]));
+  const float mx = row_absmax(a, red);
+  int e = 0;
+  if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
+  int8_t* dst = ckd + row * 4 * dh;
+#pragma unroll
+  for (int r = 0; r < kPer; ++r) {
+    const int x = threadIdx.x + r * blockDim.x;
+    if (x >= dh) break;
+    const uint32_t w = digits4(fk[r], e);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) dst[s * dh + x] = static_cast<int8_t>((w >> (8 * s)) & 0xFFu);
+  }
+  if (threadIdx.x == 0) ckexp[row] = e;
+}
+
 __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,
                                 const __nv_bfloat16* __restrict__ v, const float* __restrict__ pe,
                                 float* __restrict__ ck, __nv_bfloat16* __restrict__ ck16,
-                                __nv_bfloat16* __restrict__ cv, int64_t first, int hkv, int dh,
-                                int l, int d) {
+                                __nv_bfloat16* __restrict__ cv, int8_t* __restrict__ ckd,
+                                int32_t* __restrict__ ckexp, int64_t first, int hkv, int dh, int l,
+                                int d) {
   const int64_t b = first + blockIdx.x;
   const int h = blockIdx.y;
   const double inv_l = 1.0 / (double)l;
-  for (int x = threadIdx.x; x < dh; x += blockDim.x) {
+  float fkr[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int x = threadIdx.x + r * blockDim.x;
+    fkr[r] = 0.f;
+    if (x >= dh) continue;
     double acc_k = 0.0, acc_v = 0.0;
     for (int o = 0; o < l; ++o) {
       const int64_t off = ((b * d + o) * hkv + h) * dh + x;
@@ -38,7 +93,9 @@ __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,
     ck[o] = fk;
     ck16[o] = __float2bfloat16_rn(fk);
     cv[o] = __float2bfloat16_rn(fv);
+    fkr[r] = fk;
   }
+  if (ckd != nullptr) write_digit_row(fkr, dh, ckd, ckexp, b * hkv + h);
 }
 
 // the blocks a commit completed, in every layer at once: grid (block, head,
@@ -53,7 +110,12 @@ __global__ void compress_layers_kernel(const __grid_constant__ CompressLayers c)
   const __nv_bfloat16* v = static_cast<const __nv_bfloat16*>(c.v[j]);
   const float* pe = c.pe[j];
   const double inv_l = 1.0 / (double)l;
-  for (int x = threadIdx.x; x < dh; x += blockDim.x) {
+  float fkr[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int x = threadIdx.x + r * blockDim.x;
+    fkr[r] = 0.f;
+    if (x >= dh) continue;
     double acc_k = 0.0, acc_v = 0.0;
     for (int o = 0; o < l; ++o) {
       const int64_t off = ((b * d + o) * hkv + h) * dh + x;
@@ -67,7 +129,9 @@ __global__ void compress_layers_kernel(const __grid_constant__ CompressLayers c)
     c.ck[j][o] = fk;
     static_cast<__nv_bfloat16*>(c.ck16[j])[o] = __float2bfloat16_rn(fk);
     static_cast<__nv_bfloat16*>(c.cv[j])[o] = __float2bfloat16_rn(fv);
+    fkr[r] = fk;
   }
+  if (c.ckd[j] != nullptr) write_digit_row(fkr, dh, static_cast<int8_t*>(c.ckd[j]), c.ckexp[j], b * hkv + h);
 }
 
 }  // namespace
@@ -82,16 +146,16 @@ cudaError_t launch_compress_layers(const CompressLayers& c, int n_layers, int64_
 }
 
 cudaError_t launch_compress(const void* k, const void* v, const float* pe, float* ck, void* ck16,
-                            void* cv, int64_t first, int64_t last, int hkv, int dh, int l, int d,
-                            cudaStream_t stream) {
+                            void* cv, void* ckd, int32_t* ckexp, int64_t first, int64_t last, int hkv,
+                            int dh, int l, int d, cudaStream_t stream) {
   if (last <= first) return cudaSuccess;
   const int64_t nb = last - first;
   for (int64_t done = 0; done < nb; done += 65535) {
     const int64_t chunk = nb - done < 65535 ? nb - done : 65535;
     compress_kernel<<<dim3((unsigned)chunk, hkv), dh < 256 ? dh : 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), pe, ck,
-        static_cast<__nv_bfloat16*>(ck16), static_cast<__nv_bfloat16*>(cv), first + done, hkv, dh,
-        l, d);
+        static_cast<__nv_bfloat16*>(ck16), static_cast<__nv_bfloat16*>(cv), static_cast<int8_t*>(ckd),
+        ckexp, first + done, hkv, dh, l, d);
   }
   return cudaGetLastError();
 }

@@ -312,6 +312,8 @@ specsv_status specsv_commit_rows_compress(const specsv_nsa_config* cfg, const sp
         c.ck[jj] = kv.ck;
         c.ck16[jj] = kv.ck16;
         c.cv[jj] = kv.cv;
+        c.ckd[jj] = kv.ckd;
+        c.ckexp[jj] = kv.ckexp;
         c.first[jj] = kv.blocks;
         c.count[jj] = want - kv.blocks;
         max_count = std::max(max_count, want - kv.blocks);

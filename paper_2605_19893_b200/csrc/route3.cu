@@ -5,35 +5,47 @@
 // Replaces nsa::selection_scores + nsa::select_blocks
 // (src/nsa_attention.cpp:38-136) for every query that constructs indices.
 //
+// Work unit = (request, row chunk, KV head, range of <= 64 selection blocks):
+// one CTA, the range's <= 256 compressed blocks streamed ONCE by TMA as key
+// digit planes written at compression time (compress.cu), all of the chunk's
+// (slot, GQA head) rows multiplied against them.  At the bench shape (64K,
+// 9 routed queries, 8 KV heads) that is 8 heads x 18 ranges = 144 units, one
+// per SM.
+//
 // Logits.  The reference forms logit = dot(q_h, ck_i) / sqrt(dh) in double
-// from fp32 operands (nsa_attention.cpp:51-56).  Here every q row and every
-// key row is a 31-bit fixed-point integer on its own power-of-two grid
-// (X = round(x 2^(30 - e)), |x| < 2^e the row maximum), split into four signed
-// base-256 digits.  Digit products are exact s8 x s8 -> s32 tcgen05 MMAs
-// (kind::i8, M = 128 blocks, N = 48 (query, head) rows, K = 128): the 13
-// digit pairs of weight >= 256^2 accumulate exactly into five TMEM columns
-// sets by weight class, which the epilogue recombines in int64.  The result
-// differs from the exact fp32-operand dot by at most 2^-21.9 |q|_max |k|_max
-// (grid rounding plus the three dropped low pairs), a bound carried per row.
+// from fp32 operands (nsa_attention.cpp:51-56).  Here every q row and key row
+// is a 31-bit fixed-point integer on its own power-of-two grid
+// (X = round(x 2^(30 - e)), max |x| < 2^e) split into four signed base-256
+// digits; the 13 digit pairs of weight >= 256^2 are exact s8 x s8 -> s32
+// tcgen05 MMAs (kind::i8, M = 128 blocks, N = 48 rows, K = 128) summed per
+// weight class in TMEM and recombined in int64.  The logit differs from the
+// exact fp32-operand dot by < 2^(eq + ek - 22.98) (grid rounding plus the
+// three dropped low pairs).
 //
-// Scores.  Per unit and row: tile max, e = 2^(logit - max) in fp64, tile sum
-// and the tile's selection-block sums G_b = sum_i overlap(i, b) e_i.  One
-// grid barrier later every unit normalises its rows (max / denominator over
-// all tiles of the row), folds the GQA heads of each slot, and writes the KV
-// head's share per selection block.  A second arrival gates the Top-n tasks
-// (one per (request, slot)): score_b = sum over KV heads and tiles of the
-// shares / (Hq l) -- the reference's sum over heads and blocks of
-// p * overlap / l (nsa_attention.cpp:57-78), regrouped.
+// Scores without a max pass.  p_hi = e_hi / DEN_h with e = 2^(logit log2 e)
+// taken against the fixed reference 0 in fp64 (logits beyond +-960 log2
+// units send the query to the exact path), so a range's sums are additive
+// across ranges: per row j the range computes the selection-block sums
+// g_jb = sum_i overlap(i, b) e_ij and its share of the denominator
+// den_j = sum_b g_jb (every visible block's tokens sum to l over the
+// selection blocks, so summing over all ranges gives l x DEN).  One exchange
+// of the per-range den rows per (chunk, KV head), then every unit writes its
+// KV head's normalised share contrib_b = sum_{g in G} g_(q,g),b / den_(q,g),
+// and the Top-n task of each slot sums the KV heads in ascending order:
+// score_b = sum_h sum_i p_hi overlap(i, b) / (l Hq) -- the reference's sum
+// over heads and blocks of p * overlap / l / Hq (nsa_attention.cpp:57-78),
+// regrouped (P3: <= 1e-13 relative).
 //
-// Certification.  Each logit error bound delta (log2 units) makes every
-// probability exact to a factor 2^(+-2 delta), so every score is within a
-// relative eps = 2 ln2 delta_max of its exact value.  The Top-n (forced
-// {0, avail-2, avail-1} plus the best by (score desc, id asc),
-// nsa_attention.cpp:94-136) is accepted when the last pick and the best
-// non-pick are separated by more than eps; otherwise the task re-scores its
-// query exactly in fp64 (the reference's arithmetic, regrouped) and selects on
-// those scores.  The indices therefore equal the reference's whatever the
-// inputs; the re-scoring path is exercised by tests (force_exact).
+// Certification.  A logit error bound delta (log2 units) makes every e exact
+// to a factor 2^(+-delta), so every score is within a relative
+// eps = 2 ln2 delta_max (x1.5 margin, plus 2e-12 for the fp64 exp and sums)
+// of its exact value.  The Top-n (forced {0, avail-2, avail-1} plus the best
+// by (score desc, id asc), nsa_attention.cpp:94-136) is accepted when the last
+// pick and the best non-pick are separated by more than eps; otherwise the
+// task re-scores its query exactly in fp64 (the reference's arithmetic,
+// regrouped) and selects on those scores.  The indices therefore equal the
+// reference's whatever the inputs; the re-scoring path is exercised by tests
+// (force_exact).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -51,35 +63,49 @@ using namespace sm100;
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTB = kR3Tile;   // compressed blocks per unit
 constexpr int kDh = 128;
-constexpr int kN = kR3Rows;    // q rows per unit
-constexpr int kAcc = 5;        // digit-pair weight classes 256^2 .. 256^6
-constexpr uint32_t kTmemCols = 256;
+constexpr int kN = kR3Rows;   // rows per unit (MMA N)
+constexpr int kTB = kR3Tile;  // compressed blocks per MMA tile
+constexpr int kAcc = 5;       // digit-pair weight classes 256^2 .. 256^6
+constexpr int kWarpMma = 12;
+constexpr uint32_t kTmemCols = 512;  // 2 tiles x 5 classes x 48 columns
 constexpr int kTopnGroups = kThreads / 4;
+static_assert(kN == 4 * 12, "epilogue: 4 TMEM lane quadrants x 4 column groups of 12 (16 warps)");
+static_assert(kR3MaxSpr == 64, "two selection blocks per lane in the row sums");
+
+// counter words of one request (Route3Req::cnt)
+constexpr int kCntDen = 0;     // [nchunks x Hkv] arrivals of a (chunk, KV head)'s ranges
+constexpr int kCntTop = 272;   // [nchunks] arrivals of a chunk's units after their shares
+constexpr int kCntExpo = 352;  // [nr] max (qe + ke) + kExpoBias per slot (kExpoFlag: exact path)
+static_assert(kCntExpo + kMaxQueries <= kR3CntPerReq, "counter set");
+constexpr int kExpoBias = 4096;
+constexpr int kExpoFlag = 1 << 24;
 
 // shared memory map (bytes from the 1024-aligned base)
-constexpr uint32_t kOffStage = 0;                    // 2 x fp32 key tile [128][128] (TMA)
-constexpr uint32_t kStageBytes = kTB * kDh * 4;      // 65536
-constexpr uint32_t kOffKs = 2 * kStageBytes;         // key digits [4][128 rows x 128 B], SW128
-constexpr uint32_t kKsSlice = kTB * 128;             // 16384
-constexpr uint32_t kOffQs = kOffKs + 4 * kKsSlice;   // q digits [4][48 rows x 128 B], SW128
-constexpr uint32_t kQsSlice = kN * 128;              // 6144
-constexpr uint32_t kOffMisc = kOffQs + 4 * kQsSlice;
-static_assert(kN * kTB * 8 <= 4 * kKsSlice, "fp64 logits alias the key digits");
+constexpr uint32_t kPlaneBytes = kTB * 128;                // one digit plane of one tile (SW128)
+constexpr uint32_t kTileBytes = 4 * kPlaneBytes;           // 64 KB; then the tile's e values [48][128] fp64
+constexpr uint32_t kOffQs = 2 * kTileBytes;                // q digits [4][48 rows x 128 B], SW128
+constexpr uint32_t kQsSlice = kN * 128;                    // 6144
+constexpr uint32_t kOffG = kOffQs + 4 * kQsSlice;          // g [48][64] fp64
+constexpr uint32_t kOffMisc = kOffG + kN * kR3MaxSpr * 8;
+static_assert(kN * kTB * 8 <= kTileBytes, "e values alias the tile's planes");
 static_assert(kQsSlice % 1024 == 0, "SW128 atoms");
-static_assert((size_t)kMaxAvail * 12 <= 2 * kStageBytes, "Top-n arrays alias the key stages");
+static_assert((size_t)kMaxAvail * 12 + 4 * kDh * 8 <= 2 * kTileBytes, "Top-n arrays alias the planes");
 
 struct Misc {
-  uint64_t tma_full[2], mma_done;
+  uint64_t tma_full[2], mma_done[2];
   uint32_t tmem_base;
-  int32_t kexp[kTB];
-  float kmax[kTB];
+  int32_t flag, kemax;
   int32_t qexp[kN];
-  float qmax[kN];
-  double F[kN];       // phase C: this unit's tile weight per row
-  double E[kN];       // phase C: row error bound (log2 units)
-  double red_m[kWarps][4], red_s[kWarps][4];  // exact path: per-warp (max, sum)
+  int32_t colmvis[kN];  // visible compressed blocks of the column's slot (0: no column)
+  double qsc[kN];       // c_sl 2^(qe - 44): logit (log2 units) per unit of h 2^ke
+  double invD[kN];
+  double kpow[kR3MaxBlk];
+  double T16[16];       // 2^(k/16)
+  int32_t glo[kR3MaxSpr];                 // first compressed block overlapping each selection block
+  double gw[kR3MaxBps][kR3MaxSpr];        // its blocks' token overlaps (0 past the last one)
+  // Top-n / exact path
+  double red_m[kWarps][4], red_s[kWarps][4];
   double fin_m[4], fin_s[4];
   double gbest_s[kTopnGroups];
   int32_t gbest_i[kTopnGroups];
@@ -201,81 +227,98 @@ __device__ __forceinline__ void write_digit_row(uint8_t* base, uint32_t slice_by
   }
 }
 
-struct UnitInfo {
-  int req, kvh, chunk, tile, r0, nrows;
+
+// 2^L for L in [-1020, 960] in fp64 (relative error < 2e-13): 16 L rounded to
+// an integer k16 by the 1.5 2^52 shifter, 2^(k16 / 16) from the table and the
+// exponent field, 2^r (|r| <= 1/32) by a degree-5 polynomial in r
+__device__ __forceinline__ double exp2_fast(double L, const double* T16) {
+  const double kShift = 6755399441055744.0;  // 1.5 x 2^52
+  const double t = fma(L, 16.0, kShift);
+  const double k16 = t - kShift;
+  const int ki = __double2loint(t);
+  const double r = fma(k16, -0.0625, L);
+  double p = 1.3333558146428443e-03;        // ln2^5 / 5!
+  p = fma(p, r, 9.6181291076284772e-03);    // ln2^4 / 4!
+  p = fma(p, r, 5.5504108664821580e-02);
+  p = fma(p, r, 2.4022650695910071e-01);
+  p = fma(p, r, 6.9314718055994531e-01);
+  p = fma(p, r, 1.0);
+  const double v = p * T16[ki & 15];
+  return __hiloint2double(__double2hiint(v) + ((ki >> 4) << 20), __double2loint(v));
+}
+
+struct Unit {
+  int req, lu, chunk, kvh, range;
+  int s0, nslots, nrows;  // slots [s0, s0 + nslots) of the chunk; rows = nslots x G
+  int b0, b1;             // selection blocks [b0, b1)
+  int row0, nblk;         // compressed blocks [row0, row0 + nblk)
 };
 
-__device__ __forceinline__ UnitInfo unit_info(const Route3Launch& P, int u) {
+__device__ __forceinline__ Unit unit_of(const Route3Launch& P, int u) {
   int r = 0;
   while (r + 1 < P.n_req && u >= P.unit_start[r + 1]) ++r;
   const Route3Req& R = P.req[r];
-  int lu = u - P.unit_start[r];
-  UnitInfo U;
+  Unit U;
   U.req = r;
-  U.tile = lu % R.ntiles;
-  lu /= R.ntiles;
-  U.kvh = lu % P.Hkv;
-  U.chunk = lu / P.Hkv;
-  U.r0 = U.chunk * P.chunk_rows;
-  U.nrows = min(P.chunk_rows, R.nr * P.G - U.r0);
+  U.lu = u - P.unit_start[r];
+  int x = U.lu;
+  U.range = x % R.nranges;
+  x /= R.nranges;
+  U.kvh = x % P.Hkv;
+  U.chunk = x / P.Hkv;
+  U.s0 = U.chunk * P.spc;
+  U.nslots = min(P.spc, R.nr - U.s0);
+  U.nrows = U.nslots * P.G;
+  U.b0 = U.range * R.spr;
+  U.b1 = min(U.b0 + R.spr, R.avail_max);
+  int lo, hi, lo1, hi1;
+  blocks_of(U.b0, P.d, P.l, P.l_sel, lo, hi);
+  blocks_of(max(U.b1 - 1, U.b0), P.d, P.l, P.l_sel, lo1, hi1);
+  U.row0 = lo;
+  U.nblk = U.b1 > U.b0 ? min(hi1, R.blocks - 1) - lo + 1 : 0;
   return U;
 }
 
-__device__ __forceinline__ int64_t unit_gsh_offset(const Route3Launch& P, const UnitInfo& U, int u) {
-  return (int64_t)(u - P.unit_start[U.req]) * kN * P.span;
-}
-
-__device__ __forceinline__ void issue_unit_tma(const Route3Launch& P, int u, uint8_t* dst, uint64_t* bar) {
-  const UnitInfo U = unit_info(P, u);
-  mbar_expect_tx(bar, kStageBytes);
-  tma_load_3d(dst, &P.req[U.req].tm_ck, 0, U.kvh, U.tile * kTB, bar);
-}
-
-// q rows of a unit -> digit slices (all 16 warps, three rows each; every
-// row's load is in flight before the first reduction)
-__device__ void stage_q(const Route3Launch& P, const UnitInfo& U, uint8_t* smem, Misc& m) {
-  const Route3Req& R = P.req[U.req];
+// the unit's q rows (16 warps, three rows each), loaded first so the loads are
+// in flight across the rest of the unit's setup
+__device__ __forceinline__ void load_q(const Route3Launch& P, const Route3Req& R, const Unit& U, float4 (&v)[3]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kPer = (kN + kWarps - 1) / kWarps;
-  float4 v[kPer];
 #pragma unroll
-  for (int z = 0; z < kPer; ++z) {
+  for (int z = 0; z < 3; ++z) {
     const int j = warp + z * kWarps;
     v[z] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (j < U.nrows) {
-      const int row = U.r0 + j, slot = row / P.G, h = U.kvh * P.G + row % P.G;
+      const int slot = U.s0 + j / P.G, h = U.kvh * P.G + j % P.G;
       v[z] = __ldg(reinterpret_cast<const float4*>(R.q + ((int64_t)R.slot_q[slot] * P.Hq + h) * kDh) + lane);
-    }
-  }
-#pragma unroll
-  for (int z = 0; z < kPer; ++z) {
-    const int j = warp + z * kWarps;
-    if (j >= kN) break;
-    const float mx = warp_max_f(fmaxf(fmaxf(fabsf(v[z].x), fabsf(v[z].y)), fmaxf(fabsf(v[z].z), fabsf(v[z].w))));
-    int e = 0;
-    frexpf(mx, &e);  // mx < 2^e
-    write_digit_row(smem + kOffQs, kQsSlice, j, lane, v[z], e);
-    if (lane == 0) {
-      m.qexp[j] = e;
-      m.qmax[j] = mx;
     }
   }
 }
 
-// the staged fp32 key tile -> digit slices (8 rows per warp)
-__device__ void slice_keys(const float* st, uint8_t* smem, Misc& m) {
+// ... -> digit slices, plus per-column tables
+__device__ __forceinline__ void digit_q(const Route3Launch& P, const Route3Req& R, const Unit& U,
+                                        const float4 (&v)[3], uint8_t* smem, Misc& m) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll 2
-  for (int r = warp; r < kTB; r += kWarps) {
-    const float4 v = reinterpret_cast<const float4*>(st + r * kDh)[lane];
-    const float mx = warp_max_f(fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  static_assert(kN == 3 * kWarps, "three q rows per warp");
+#pragma unroll
+  for (int z = 0; z < 3; ++z) {
+    const int j = warp + z * kWarps;
+    const float mx = warp_max_f(fmaxf(fmaxf(fabsf(v[z].x), fabsf(v[z].y)), fmaxf(fabsf(v[z].z), fabsf(v[z].w))));
     int e = 0;
-    frexpf(mx, &e);
-    write_digit_row(smem + kOffKs, kKsSlice, r, lane, v, e);
+    if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
+    write_digit_row(smem + kOffQs, kQsSlice, j, lane, v[z], e);
     if (lane == 0) {
-      m.kexp[r] = e;
-      m.kmax[r] = mx;
+      m.qexp[j] = e;
+      m.qsc[j] = P.c_sl * pow2i(e - 44);
+      m.colmvis[j] = j < U.nrows ? R.slot_mvis[U.s0 + j / P.G] : 0;
     }
+  }
+}
+
+__device__ __forceinline__ void stamp(const Route3Launch& P, int k) {
+  if (P.trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.trace[kRouteTraceBase + blockIdx.x * 16 + k] = t;
   }
 }
 
@@ -530,33 +573,25 @@ __device__ void exact_scores(const Route3Launch& P, const Route3Req& R, int slot
 }
 
 // ------------------------------------------------------------------ kernel
-__device__ __forceinline__ void stamp(const Route3Launch& P, int k) {
-  if (P.trace != nullptr && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    P.trace[kRouteTraceBase + blockIdx.x * 16 + k] = t;
-  }
-}
-
 __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_constant__ Route3Launch P) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   Misc& m = *reinterpret_cast<Misc*>(smem + kOffMisc);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x, nctas = gridDim.x;
-  int* bar = P.counters;
+  double* g = reinterpret_cast<double*>(smem + kOffG);  // [kN][kR3MaxSpr]
   griddep_wait();  // inputs (q) may come from the launch just before (PDL)
   stamp(P, 0);
   const int units = P.unit_start[P.n_req];
   if (tid == 0) {
-    mbar_init(&m.tma_full[0], 1);
-    mbar_init(&m.tma_full[1], 1);
-    mbar_init(&m.mma_done, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&m.tma_full[t], 1);
+      mbar_init(&m.mma_done[t], 1);
+    }
     fence_mbar_init();
-    for (int k = 0; k < 2 && cta + k * nctas < units; ++k)
-      issue_unit_tma(P, cta + k * nctas, smem + kOffStage + k * kStageBytes, &m.tma_full[k]);
   }
+  if (tid < 16) m.T16[tid] = exp2((double)tid * 0.0625);
   if (cta == nctas - 1) {  // queries that reuse a representative's set get count -1
     for (int r = 0; r < P.n_req; ++r) {
       const Route3Req& R = P.req[r];
@@ -572,282 +607,292 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     }
   }
   if (warp == 0 && cta < units) tmem_alloc<kTmemCols>(&m.tmem_base);
+  tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  const uint32_t tmem = m.tmem_base;
 
-  // ================= phase A: units (logits, tile statistics, G) =================
-  int staged = -1;  // (request, KV head, chunk) whose q digits are in shared memory
+  // ================= phase 1: logits, e, selection-block sums, den rows =================
   int k = 0;
   for (int u = cta; u < units; u += nctas, ++k) {
-    const UnitInfo U = unit_info(P, u);
+    const Unit U = unit_of(P, u);
     const Route3Req& R = P.req[U.req];
-    const int qkey = (U.req * 128 + U.chunk) * 128 + U.kvh;
-    if (qkey != staged) {
-      stage_q(P, U, smem, m);
-      staged = qkey;
+    const uint32_t par = k & 1;
+    const int ntile = U.nblk > kTB ? 2 : 1;
+    float4 qv[3];
+    load_q(P, R, U, qv);
+    static_assert(kR3MaxBlk <= kThreads, "one block exponent per thread");
+    const bool has_ke = tid < U.nblk;  // the exponent load is in flight across the setup
+    const int ke = has_ke ? __ldg(R.ckexp + (int64_t)(U.row0 + tid) * P.Hkv + U.kvh) : 0;
+    if (tid == 0) {
+      for (int t = 0; t < 2; ++t) {
+        if (t < ntile) {
+          mbar_expect_tx(&m.tma_full[t], kTileBytes);
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            tma_load_4d(smem + t * kTileBytes + s * kPlaneBytes, &R.tm_ckd, 0, s, U.kvh, U.row0 + t * kTB,
+                        &m.tma_full[t]);
+        } else {
+          mbar_arrive(&m.tma_full[t]);
+        }
+      }
+      m.flag = 0;
+      m.kemax = -100000;
     }
-    if (k < 2) stamp(P, 6 + 5 * k);
-    const int sb = k & 1;
-    mbar_wait(&m.tma_full[sb], (k >> 1) & 1);
-    if (k < 2) stamp(P, 7 + 5 * k);
-    slice_keys(reinterpret_cast<const float*>(smem + kOffStage + sb * kStageBytes), smem, m);
-    fence_proxy_async_smem();
+    {  // compressed blocks overlapping each selection block of the range, and their token overlaps
+      const int bl = tid & (kR3MaxSpr - 1), kg = tid / kR3MaxSpr;
+      const int b = U.b0 + bl;
+      int lo, hi;
+      blocks_of(b, P.d, P.l, P.l_sel, lo, hi);
+      hi = min(hi, U.row0 + U.nblk - 1);
+      if (kg == 0) m.glo[bl] = lo;
+      for (int kq = kg; kq < kR3MaxBps; kq += kThreads / kR3MaxSpr)
+        m.gw[kq][bl] = lo + kq <= hi ? (double)overlap(lo + kq, b, P.d, P.l, P.l_sel) : 0.0;
+    }
+    digit_q(P, R, U, qv, smem, m);
+    __syncthreads();  // flag / kemax reset before the block exponents
+    if (tid < kR3MaxBlk) {
+      m.kpow[tid] = has_ke ? pow2i(ke) : 0.0;
+      if (has_ke) atomicMax(&m.kemax, ke);
+    }
+    for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) g[e] = 0.0;
+    fence_proxy_async_smem();  // q digits: generic-proxy writes read by the MMA
+    tc_fence_before();
     __syncthreads();
-    if (k < 2) stamp(P, 8 + 5 * k);
-    if (tid == 0 && u + 2 * nctas < units)  // the stage is free: prefetch two units ahead
-      issue_unit_tma(P, u + 2 * nctas, smem + kOffStage + sb * kStageBytes, &m.tma_full[sb]);
-    if (warp == 0) {
-      tc_fence_after();
-      constexpr uint32_t idesc = idesc_s8(kTB, kN);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            if (s + t < 2) continue;
-            const int cls = s + t - 2;
-            const bool first = kk == 0 && s == (s + t - 3 > 0 ? s + t - 3 : 0);
-            umma_i8_warp(m.tmem_base + cls * kN,
-                         desc_sw128(sbase + kOffKs + t * kKsSlice + 32 * kk, 16, 1024),
-                         desc_sw128(sbase + kOffQs + s * kQsSlice + 32 * kk, 16, 1024), idesc,
-                         first ? 0u : 1u);
-          }
-      umma_commit_warp(&m.mma_done);
-    }
-    __syncwarp();
-    mbar_wait(&m.mma_done, k & 1);
     tc_fence_after();
-    if (k < 2) stamp(P, 9 + 5 * k);
-    double* L = reinterpret_cast<double*>(smem + kOffKs);  // [kN][kTB] log2-unit logits (aliases the digits)
-    if (warp < 12) {
-      const int qd = warp & 3, cg = warp >> 2;
-      const int i = 32 * qd + lane;
-      uint32_t a[kAcc][16];
+    if (k == 0) stamp(P, 1);
+
+    if (warp == kWarpMma) {  // both tiles' MMAs as their planes land
+      // B = the q digit planes s >= s_lo stacked along N (rows s x 48 + j), so
+      // one MMA multiplies key plane tt by every q plane it needs and writes
+      // class c = s + tt at TMEM column block c - 2 (classes 2..6 = weights
+      // 256^2..256^6; the lower pairs are dropped).  Per K step: (tt 2: s 0-3,
+      // blocks 0-3, initialising), (tt 3, s 3: block 4, initialising), then
+      // (tt 3: s 0-2), (tt 1: s 1-3), (tt 0: s 2-3) accumulate.
+      const uint32_t qb = sbase + kOffQs;
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(&m.tma_full[t], par);
+        if (t < ntile) {
+          tc_fence_after();
+          const uint32_t kb = sbase + t * kTileBytes, d0 = tmem + t * kAcc * kN;
 #pragma unroll
-      for (int c = 0; c < kAcc; ++c)
-        tmem_ld16(m.tmem_base + (static_cast<uint32_t>(32 * qd) << 16) + c * kN + 16 * cg, a[c]);
-      tmem_wait_ld();
-      const int gblk = U.tile * kTB + i;
-      const int ke = m.kexp[i];
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t ko = 32 * kk;
+            umma_i8_warp(d0, desc_sw128(kb + 2 * kPlaneBytes + ko, 16, 1024), desc_sw128(qb + ko, 16, 1024),
+                         idesc_s8(kTB, 4 * kN), kk ? 1u : 0u);
+            umma_i8_warp(d0 + 4 * kN, desc_sw128(kb + 3 * kPlaneBytes + ko, 16, 1024),
+                         desc_sw128(qb + 3 * kQsSlice + ko, 16, 1024), idesc_s8(kTB, kN), kk ? 1u : 0u);
+            umma_i8_warp(d0 + 1 * kN, desc_sw128(kb + 3 * kPlaneBytes + ko, 16, 1024), desc_sw128(qb + ko, 16, 1024),
+                         idesc_s8(kTB, 3 * kN), 1u);
+            umma_i8_warp(d0, desc_sw128(kb + 1 * kPlaneBytes + ko, 16, 1024),
+                         desc_sw128(qb + 1 * kQsSlice + ko, 16, 1024), idesc_s8(kTB, 3 * kN), 1u);
+            umma_i8_warp(d0, desc_sw128(kb + ko, 16, 1024), desc_sw128(qb + 2 * kQsSlice + ko, 16, 1024),
+                         idesc_s8(kTB, 2 * kN), 1u);
+          }
+        }
+        umma_commit_warp(&m.mma_done[t]);  // (no MMAs for a missing tile: arrives at once)
+      }
+    }
+    for (int t = 0; t < ntile; ++t) {
+      const int qd = warp & 3, cg = warp >> 2;  // TMEM lane quadrant, 12-column group
+      if (12 * cg < U.nrows) {
+        // ---- epilogue: recombine the classes, logit, e = 2^logit -> e values [48][128]
+        mbar_wait(&m.mma_done[t], par);
+        tc_fence_after();
+        if (k == 0) stamp(P, 9 + t);
+        uint32_t a[kAcc][12];
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        const int j = 16 * cg + jj;
-        double val = -INFINITY;
-        if (j < U.nrows && gblk < R.slot_mvis[(U.r0 + j) / P.G]) {
+        for (int c = 0; c < kAcc; ++c) {
+          const uint32_t ta = tmem + ((uint32_t)(32 * qd) << 16) + (t * kAcc + c) * kN + 12 * cg;
+          tmem_ld8(ta, a[c]);
+          tmem_ld4(ta + 8, a[c] + 8);
+        }
+        tmem_wait_ld();
+        const int il = 32 * qd + lane, i = t * kTB + il;
+        const int gb = U.row0 + i;
+        const double kp = m.kpow[i];
+        double* E = reinterpret_cast<double*>(smem + t * kTileBytes);
+        bool ovf = false;
+        // branch-free so the 12 independent chains interleave: logits first,
+        // then e = 2^logit (clamped into the exponent range; out-of-range
+        // logits flag the query for the exact path)
+        double Lv[12];
+#pragma unroll
+        for (int jj = 0; jj < 12; ++jj) {
           long long h = (int)a[4][jj];
           h = h * 256 + (int)a[3][jj];
           h = h * 256 + (int)a[2][jj];
           h = h * 256 + (int)a[1][jj];
           h = h * 256 + (int)a[0][jj];
-          val = (double)h * pow2i(m.qexp[j] + ke - 44) * P.c_sl;
+          Lv[jj] = (double)h * m.qsc[12 * cg + jj] * kp;
         }
-        L[j * kTB + i] = val;
+        const bool row_ok = i < U.nblk;
+#pragma unroll
+        for (int jj = 0; jj < 12; ++jj) {
+          const int j = 12 * cg + jj;
+          const bool valid = row_ok && gb < m.colmvis[j];
+          ovf |= valid && Lv[jj] > 960.0;
+          const double e = exp2_fast(fmin(fmax(Lv[jj], -1020.0), 960.0), m.T16);
+          E[j * kTB + il] = valid ? e : 0.0;
+        }
+        if (__any_sync(0xffffffffu, ovf) && lane == 0) m.flag = 1;
+      }
+      tc_fence_before();
+      __syncthreads();
+      if (k == 0) stamp(P, t == 0 ? 2 : 11);
+      // ---- selection-block sums of this tile's blocks (all warps)
+      {
+        const double* E = reinterpret_cast<const double*>(smem + t * kTileBytes);
+        const int nsel = U.b1 - U.b0;
+        const int tlo = U.row0 + t * kTB, thi = min(U.row0 + U.nblk, tlo + kTB) - 1;
+        for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) {
+          const int j = e >> 6, bl = e & 63;
+          if (j >= U.nrows || bl >= nsel) continue;
+          const int r0 = m.glo[bl] - tlo;  // tile row of the selection block's first block
+          const double* Ej = E + j * kTB;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int kq = 0; kq < P.bps; ++kq) {
+            const int r = r0 + kq;
+            const bool in = r >= 0 && r < kTB;
+            acc = fma(m.gw[kq][bl], in ? Ej[in ? r : 0] : 0.0, acc);
+          }
+          g[e] += acc;
+        }
+      }
+      __syncthreads();
+      if (k == 0) stamp(P, 12 + t);
+    }
+    if (12 * (warp >> 2) < U.nrows && ntile < 2) mbar_wait(&m.mma_done[1], par);  // the empty commit's phase
+    if (k == 0) stamp(P, 3);
+    // ---- this range's denominator rows, error exponents, spill, arrival
+    {
+      double* den = R.den + ((int64_t)(U.chunk * P.Hkv + U.kvh) * R.nranges + U.range) * kN;
+#pragma unroll
+      for (int z = 0; z < kN / kWarps; ++z) {
+        const int j = warp + z * kWarps;
+        const double v = warp_sum_d(g[j * kR3MaxSpr + lane] + g[j * kR3MaxSpr + lane + 32]);
+        if (lane == 0) den[j] = v;
+      }
+      if (tid < U.nrows) {
+        const int ex = m.flag ? kExpoFlag : m.qexp[tid] + m.kemax + kExpoBias;
+        atomicMax(&R.cnt[kCntExpo + U.s0 + tid / P.G], ex);
+      }
+      if (u + nctas < units) {  // not this CTA's last unit: phase 2 reloads g from L2
+        double* sp = R.gspill + (int64_t)U.lu * kN * kR3MaxSpr;
+        for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) sp[e] = g[e];
       }
     }
     tc_fence_before();
     __syncthreads();
-    if (k < 2) stamp(P, 10 + 5 * k);
-    // per row: tile max, e = 2^(logit - max), tile sum, selection-block sums
-    {
-      float akm = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) akm = fmaxf(akm, m.kmax[4 * lane + c]);
-      akm = warp_max_f(akm);
-      const int rows_head = R.nr * P.G;
-      double* gsh = R.gsh + unit_gsh_offset(P, U, u);
-      for (int j = warp; j < U.nrows; j += kWarps) {
-        double* Lj = L + j * kTB;
-        double v[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) v[c] = Lj[lane + 32 * c];
-        const double mx = warp_max_d(fmax(fmax(v[0], v[1]), fmax(v[2], v[3])));
-        double td = 0.0;
-        if (mx != -INFINITY) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const double e = v[c] == -INFINITY ? 0.0 : exp2_nonpos(v[c] - mx);
-            Lj[lane + 32 * c] = e;
-            td += e;
-          }
-        }
-        td = warp_sum_d(td);
-        __syncwarp();
-        const int b0 = U.tile * P.spt;
-        for (int bl = lane; bl < P.span; bl += 32) {
-          double g = 0.0;
-          if (mx != -INFINITY) {
-            int lo, hi;
-            blocks_of(b0 + bl, P.d, P.l, P.l_sel, lo, hi);
-            lo = max(lo, U.tile * kTB);
-            hi = min(hi, U.tile * kTB + kTB - 1);
-            for (int i = lo; i <= hi; ++i)
-              g += (double)overlap(i, b0 + bl, P.d, P.l, P.l_sel) * Lj[i - U.tile * kTB];
-          }
-          gsh[j * P.span + bl] = g;
-        }
-        if (lane == 0) {
-          double* st = R.stats + ((int64_t)(U.kvh * rows_head + U.r0 + j) * R.ntiles + U.tile) * 4;
-          st[0] = mx;
-          st[1] = td;
-          // logit error bound (log2 units): grid rounding + dropped digit pairs
-          // <= 2^-21.9 |q|max |k|max, with a factor-2 margin
-          st[2] = P.c_sl * (double)m.qmax[j] * (double)akm * 4.76837158203125e-07;  // 2^-21
-        }
-      }
-    }
-    __syncthreads();  // L / digits / staging reuse by the next unit
-  }
-  if (warp == 0 && cta < units) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(m.tmem_base);
+    if (tid == 0) red_add_release_gpu(&R.cnt[kCntDen + U.chunk * P.Hkv + U.kvh], 1);
   }
-  stamp(P, 1);
+  if (warp == 0 && cta < units) tmem_dealloc<kTmemCols>(tmem);
+  if (k > 0) stamp(P, 4);
 
-  // ================= grid barrier: every tile statistic is out =================
-  __syncthreads();
-  if (tid == 0) {
-    red_add_release_gpu(bar + 0, 1);
-    while (ld_acquire_gpu(bar + 0) < nctas) {
-    }
-  }
-  __syncthreads();
-  stamp(P, 2);
-
-  // ================= phase C: normalise, fold GQA heads, per-KV-head shares =================
+  // ================= phase 2: denominators, per-KV-head shares =================
   for (int u = cta; u < units; u += nctas) {
-    const UnitInfo U = unit_info(P, u);
+    const Unit U = unit_of(P, u);
     const Route3Req& R = P.req[U.req];
-    const int rows_head = R.nr * P.G;
-    for (int j = warp; j < U.nrows; j += kWarps) {
-      // every tile's statistics of the row in registers (one L2 round trip)
-      const double* sj = R.stats + (int64_t)(U.kvh * rows_head + U.r0 + j) * R.ntiles * 4;
-      constexpr int kTpl = 8;  // tiles per lane: ntiles <= 256 (kMaxAvail selection blocks)
-      double m2v[kTpl], tdv[kTpl];
-      double mx = -INFINITY, bmax = 0.0;
-#pragma unroll
-      for (int z = 0; z < kTpl; ++z) {
-        const int t = lane + 32 * z;
-        m2v[z] = -INFINITY;
-        tdv[z] = 0.0;
-        if (t < R.ntiles) {
-          const double2 a = __ldcg(reinterpret_cast<const double2*>(sj) + 2 * t);
-          const double2 c = __ldcg(reinterpret_cast<const double2*>(sj) + 2 * t + 1);
-          m2v[z] = a.x;
-          tdv[z] = a.y;
-          bmax = fmax(bmax, c.x);
-        }
-        mx = fmax(mx, m2v[z]);
-      }
-      mx = warp_max_d(mx);
-      bmax = warp_max_d(bmax);
-      double den = 0.0;
-      if (mx != -INFINITY)
-#pragma unroll
-        for (int z = 0; z < kTpl; ++z)
-          if (m2v[z] != -INFINITY) den += tdv[z] * exp2_nonpos(m2v[z] - mx);
-      den = warp_sum_d(den);
-      if (lane == (U.tile & 31)) {
-        double ownv = -INFINITY;
-#pragma unroll
-        for (int z = 0; z < kTpl; ++z)
-          if (z == (U.tile >> 5)) ownv = m2v[z];
-        m.F[j] = (ownv == -INFINITY || !(den > 0.0)) ? 0.0 : exp2_nonpos(ownv - mx) / den;
-        m.E[j] = bmax;
+    const bool last = u + nctas >= units;
+    if (tid == 0) {
+      const int* c = &R.cnt[kCntDen + U.chunk * P.Hkv + U.kvh];
+      while (ld_acquire_gpu(c) < R.nranges) {
       }
     }
     __syncthreads();
-    const int s0 = U.r0 / P.G, ns = U.nrows / P.G;
-    const double* gsh = R.gsh + unit_gsh_offset(P, U, u);
-    for (int e = tid; e < ns * P.span; e += kThreads) {
-      const int sl = e / P.span, bl = e % P.span;
+    if (u == cta) stamp(P, 5);
+    double* st = reinterpret_cast<double*>(smem);                // [nranges][48] den rows
+    double* gs = last ? g : reinterpret_cast<double*>(smem + kTileBytes);  // this unit's g
+    const double* src = R.den + (int64_t)(U.chunk * P.Hkv + U.kvh) * R.nranges * kN;
+    for (int e = tid; e < R.nranges * kN; e += kThreads) st[e] = __ldcg(src + e);
+    if (!last) {
+      const double* sp = R.gspill + (int64_t)U.lu * kN * kR3MaxSpr;
+      for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) gs[e] = __ldcg(sp + e);
+    }
+    __syncthreads();
+    if (tid < kN) {
+      double D = 0.0;  // ranges in ascending order
+      for (int r = 0; r < R.nranges; ++r) D += st[r * kN + tid];
+      m.invD[tid] = D > 0.0 ? 1.0 / D : 0.0;
+      if (tid < U.nrows && D > 0.0 && D < 0x1p-900)  // e values may have lost bits: exact path
+        atomicMax(&R.cnt[kCntExpo + U.s0 + tid / P.G], kExpoFlag);
+    }
+    __syncthreads();
+    const int nsel = U.b1 - U.b0;
+    for (int e = tid; e < U.nslots * nsel; e += kThreads) {
+      const int sl = e / nsel, bl = e % nsel;
       double c = 0.0;
-      for (int g = 0; g < P.G; ++g) c += m.F[sl * P.G + g] * gsh[(sl * P.G + g) * P.span + bl];
-      R.contrib[(((int64_t)(s0 + sl) * P.Hkv + U.kvh) * R.ntiles + U.tile) * P.span + bl] = c;
+      for (int h = 0; h < P.G; ++h) c = fma(gs[(sl * P.G + h) * kR3MaxSpr + bl], m.invD[sl * P.G + h], c);
+      R.contrib[((int64_t)(U.s0 + sl) * P.Hkv + U.kvh) * R.sel_pad + U.b0 + bl] = c;
     }
-    if (U.tile == 0)
-      for (int sl = tid; sl < ns; sl += kThreads) {
-        double e = 0.0;
-        for (int g = 0; g < P.G; ++g) e = fmax(e, m.E[sl * P.G + g]);
-        R.eps[(int64_t)(s0 + sl) * P.Hkv + U.kvh] = e;
-      }
     __syncthreads();
+    if (tid == 0) red_add_release_gpu(&R.cnt[kCntTop + U.chunk], 1);
   }
-  stamp(P, 3);
+  stamp(P, 6);
 
-  // ================= Top-n tasks after every share is out =================
-  const int tasks = P.task_start[P.n_req];
-  __syncthreads();
-  if (tid == 0) red_add_release_gpu(bar + 1, 1);
+  // ================= phase 3: one Top-n task per routed slot =================
   griddep_launch();  // the next launch may start placing CTAs as this grid drains
-  if (cta < tasks) {
-    if (tid == 0)
-      while (ld_acquire_gpu(bar + 1) < nctas) {
+  const int tasks = P.task_start[P.n_req];
+  double* sel = reinterpret_cast<double*>(smem);                          // [kMaxAvail]
+  int* surv = reinterpret_cast<int*>(smem + 8 * kMaxAvail);                // [kMaxAvail]
+  double* qrows = reinterpret_cast<double*>(smem + 12 * kMaxAvail);        // [4][128]
+  for (int t = nctas - 1 - cta; t < tasks; t += nctas) {
+    int r = 0;
+    while (r + 1 < P.n_req && t >= P.task_start[r + 1]) ++r;
+    const Route3Req& R = P.req[r];
+    const int slot = t - P.task_start[r];
+    const int chunk = slot / P.spc;
+    if (tid == 0) {
+      const int* c = &R.cnt[kCntTop + chunk];
+      while (ld_acquire_gpu(c) < P.Hkv * R.nranges) {
       }
-    __syncthreads();
-    stamp(P, 4);
-    double* sel = reinterpret_cast<double*>(smem + kOffStage);                // [kMaxAvail]
-    int* surv = reinterpret_cast<int*>(smem + kOffStage + 8 * kMaxAvail);    // [kMaxAvail]
-    double* qrows = reinterpret_cast<double*>(smem + kOffStage + 12 * kMaxAvail);  // [4][128]
-    for (int t = cta; t < tasks; t += nctas) {
-      int r = 0;
-      while (r + 1 < P.n_req && t >= P.task_start[r + 1]) ++r;
-      const Route3Req& R = P.req[r];
-      const int slot = t - P.task_start[r];
-      const int avail = R.slot_avail[slot];
-      const double inv = 1.0 / ((double)P.Hq * (double)P.l);
-      const double* cb = R.contrib + (int64_t)slot * P.Hkv * R.ntiles * P.span;
-      for (int b = tid; b < avail; b += kThreads) {
-        const int t_hi = min(R.ntiles - 1, b / P.spt);
-        const int t_lo = max(0, (b - P.span + P.spt) / P.spt);
-        double v[8][2];  // every share of the block in flight at once
-#pragma unroll
-        for (int kvh = 0; kvh < 8; ++kvh)
-#pragma unroll
-          for (int z = 0; z < 2; ++z) {
-            const int tt = t_lo + z;
-            v[kvh][z] = (kvh < P.Hkv && tt <= t_hi)
-                            ? __ldcg(cb + ((int64_t)kvh * R.ntiles + tt) * P.span + (b - tt * P.spt))
-                            : 0.0;
-          }
-        double s = 0.0;  // KV heads ascending, tiles ascending
-#pragma unroll
-        for (int kvh = 0; kvh < 8; ++kvh) {
-          if (kvh >= P.Hkv) break;
-          s += v[kvh][0];
-          s += v[kvh][1];
-          for (int tt = t_lo + 2; tt <= t_hi; ++tt)
-            s += __ldcg(cb + ((int64_t)kvh * R.ntiles + tt) * P.span + (b - tt * P.spt));
-        }
-        for (int kvh = 8; kvh < P.Hkv; ++kvh)
-          for (int tt = t_lo; tt <= t_hi; ++tt)
-            s += __ldcg(cb + ((int64_t)kvh * R.ntiles + tt) * P.span + (b - tt * P.spt));
-        sel[b] = s * inv;
-      }
-      double dl = 0.0;
-      if (tid < P.Hkv && R.ntiles > 0) dl = __ldcg(R.eps + (int64_t)slot * P.Hkv + tid);
-      dl = warp_max_d(dl);
-      if (tid == 0) m.red_w[0] = dl;
-      __syncthreads();
-      // relative score error <= 2 ln2 delta (+ fp64 rounding), with margin
-      const double eps = 1.5 * 2.0 * 0.6931471805599453 * m.red_w[0] + 1e-12;
-      select_topn(sel, surv, avail, P.n, eps, m);
-      if (!m.certified || P.force_exact) {
-        if (tid == 0 && P.fallbacks != nullptr) atomicAdd(P.fallbacks, 1);
-        exact_scores(P, R, slot, sel, qrows, m);
-        select_topn(sel, surv, avail, P.n, 0.0, m);
-      }
-      const int q = R.slot_q[slot];
-      write_row(m, m, avail, P.n, R.idx + (int64_t)q * P.n, R.idx_count + q, R.idx_forced + q);
-      __syncthreads();
     }
+    __syncthreads();
+    stamp(P, 7);
+    const int avail = R.slot_avail[slot];
+    const double inv = 1.0 / (double)P.Hq;
+    const double* cb = R.contrib + (int64_t)slot * P.Hkv * R.sel_pad;
+    for (int b = tid; b < avail; b += kThreads) {
+      double v[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) v[h] = h < P.Hkv ? __ldcg(cb + (int64_t)h * R.sel_pad + b) : 0.0;
+      double s = 0.0;  // KV heads ascending
+#pragma unroll
+      for (int h = 0; h < 8; ++h) s += v[h];
+      for (int h = 8; h < P.Hkv; ++h) s += __ldcg(cb + (int64_t)h * R.sel_pad + b);
+      sel[b] = s * inv;
+    }
+    const int ex = __ldcg(&R.cnt[kCntExpo + slot]);
+    __syncthreads();
+    stamp(P, 14);
+    if (tid == 0) R.cnt[kCntExpo + slot] = 0;  // every atomicMax of this launch is in
+    // relative score error <= 2 ln2 delta (+ fp64 exp / summation rounding), with margin
+    const bool flagged = ex >= kExpoFlag;
+    const double delta = flagged ? 0.0 : P.c_sl * pow2i(max(-1000, min(1000, ex - kExpoBias - 22)));
+    const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-12;
+    select_topn(sel, surv, avail, P.n, eps, m);
+    stamp(P, 15);
+    if (flagged || !m.certified || P.force_exact) {
+      if (tid == 0 && P.fallbacks != nullptr) atomicAdd(P.fallbacks, 1);
+      exact_scores(P, R, slot, sel, qrows, m);
+      select_topn(sel, surv, avail, P.n, 0.0, m);
+    }
+    const int q = R.slot_q[slot];
+    write_row(m, m, avail, P.n, R.idx + (int64_t)q * P.n, R.idx_count + q, R.idx_forced + q);
+    __syncthreads();
   }
-  stamp(P, 5);
+  stamp(P, 8);
   __syncthreads();
-  if (tid == 0 && atom_add_acq_rel_gpu(bar + 2, 1) == nctas - 1) {  // the last CTA out resets
-    atomicExch(bar + 0, 0);
-    atomicExch(bar + 1, 0);
-    atomicExch(bar + 2, 0);
+  if (tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt, 1) == nctas - 1) {  // the last CTA out resets
+    for (int r = 0; r < P.n_req; ++r) {
+      const Route3Req& R = P.req[r];
+      for (int i = 0; i < R.nchunks * P.Hkv; ++i) R.cnt[kCntDen + i] = 0;
+      for (int i = 0; i < R.nchunks; ++i) R.cnt[kCntTop + i] = 0;
+    }
+    __threadfence();
+    atomicExch(P.exit_cnt, 0);
   }
 }
 
@@ -866,12 +911,14 @@ int sm_count3() {
 
 }  // namespace
 
+int route3_grid() { return sm_count3(); }
+
 cudaError_t launch_route3(Route3Launch& p, cudaStream_t s) {
   p.unit_start[0] = 0;
   p.task_start[0] = 0;
   for (int r = 0; r < p.n_req; ++r) {
     const Route3Req& R = p.req[r];
-    p.unit_start[r + 1] = p.unit_start[r] + p.Hkv * R.nchunks * R.ntiles;
+    p.unit_start[r + 1] = p.unit_start[r] + p.Hkv * R.nchunks * R.nranges;
     p.task_start[r + 1] = p.task_start[r] + R.nr;
   }
   const int work = std::max(p.unit_start[p.n_req], p.task_start[p.n_req]);
@@ -885,7 +932,7 @@ cudaError_t launch_route3(Route3Launch& p, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  attr[na].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
+  attr[na].id = cudaLaunchAttributeCooperative;  // arrival waits: every CTA co-resident
   attr[na++].val.cooperative = 1;
   if (pdl_enabled()) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -87,6 +87,10 @@ class LayerCache:
         self.ck = torch.zeros(nb, H, dh, dtype=torch.float32, device=device)
         self.ck16 = torch.zeros(nb, H, dh, dtype=torch.bfloat16, device=device)
         self.cv = torch.zeros_like(self.ck16)
+        # routing keys as fixed-point digit planes (int8 [blocks][Hkv][4][dh])
+        # and their row exponents, written with ck by every compressed append
+        self.ckd = torch.zeros(nb, H, 4, dh, dtype=torch.int8, device=device)
+        self.ckexp = torch.zeros(nb, H, dtype=torch.int32, device=device)
         self.rows = 0
         self.blocks = 0
 
@@ -100,7 +104,8 @@ class LayerCache:
 
     def c(self) -> abi.LayerKvC:
         return abi.LayerKvC(self.k.data_ptr(), self.v.data_ptr(), self.rows, self.ck.data_ptr(),
-                            self.ck16.data_ptr(), self.cv.data_ptr(), self.blocks, self.capacity)
+                            self.ck16.data_ptr(), self.cv.data_ptr(), self.blocks, self.capacity,
+                            self.ckd.data_ptr(), self.ckexp.data_ptr())
 
     def extend_compressed(self, pos_embed: torch.Tensor | None = None, stream=None) -> None:
         """extend_compressed_layer: pool the blocks the new rows complete."""

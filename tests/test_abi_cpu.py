@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     L = abi.lib()
     for name in decl:
         assert hasattr(L, name), name
-    assert L.specsv_abi_version() == 2
+    assert L.specsv_abi_version() == 3
 
 
 def test_validate_config_rules():

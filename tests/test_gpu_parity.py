@@ -69,6 +69,26 @@ def test_compress_append_bit_exact(oracle_lib):
     assert np.array_equal(got_ck16, bf16_round(ck))
 
 
+def test_compress_digit_planes():
+    """The routing keys' digit planes (ABI v3) written by the compressed append:
+    per (block, head) row, e is the smallest power of two above max |ck|, and
+    the four signed base-256 digits recombine to round(ck 2^(30 - e))."""
+    cfg = O.llama_config(4)
+    x = LayerInputs(cfg, 3000, 2, 77)
+    case = DeviceCase(cfg, x)
+    c = case.cache
+    nb = c.blocks
+    ck = c.ck[:nb].cpu().numpy().astype(np.float64)
+    e = c.ckexp[:nb].cpu().numpy().astype(np.int64)
+    dg = c.ckd[:nb].cpu().numpy().astype(np.int64)  # [nb][H][4][dh]
+    X = dg[:, :, 0] + 256 * dg[:, :, 1] + 65536 * dg[:, :, 2] + 16777216 * dg[:, :, 3]
+    mx = np.abs(ck).max(-1)
+    assert (mx < np.ldexp(1.0, e)).all() and (mx >= np.ldexp(1.0, e - 1)).all()
+    want = np.rint(ck * np.ldexp(1.0, 30 - e)[..., None])
+    assert np.array_equal(X, want.astype(np.int64))
+    assert dg.min() >= -128 and dg.max() <= 127
+
+
 def test_compress_append_incremental(oracle_lib):
     cfg = O.llama_config(2)
     x = LayerInputs(cfg, 2000, 0, 6)
@@ -517,26 +537,27 @@ def test_exact_grouping_equals_independent_queries(oracle_lib):
         assert per <= TOL and l2 <= TOL, (C, per, l2)
 
 
-ROUTE_VARIANTS = {"route3": {"SPECSV_ROUTE3": "1"}, "route3_exact": {"SPECSV_ROUTE3": "1", "SPECSV_ROUTE3_FORCE_EXACT": "1"},
-                  "default": {}}
+ROUTE_VARIANTS = {"route3": {}, "route3_exact": {"SPECSV_ROUTE3_FORCE_EXACT": "1"},
+                  "legacy": {"SPECSV_ROUTE_LEGACY": "1"}}
 
 
 @pytest.mark.parametrize("rows,gamma,parents,mode", [(4096, 4, None, O.MODE_EXACT),
                                                      (3001, 8, TREE8, O.MODE_APPROX),
                                                      (65536, 8, None, O.MODE_EXACT)])
 def test_route_kernels_agree(oracle_lib, monkeypatch, rows, gamma, parents, mode):
-    """Routing runs on the fp64-DMMA route_fused_kernel by default;
-    SPECSV_ROUTE3=1 selects route3_kernel (integer tensor-pipe logits,
-    certified Top-n) and SPECSV_ROUTE3_FORCE_EXACT=1 sends every query through
-    its exact fp64 re-scoring path.  All three against the oracle, and their
-    index sets agree; the fp64 score diagnostic holds P3."""
+    """Routing runs on route3_kernel (integer tensor-pipe logits over the
+    cache's digit planes, certified Top-n) by default;
+    SPECSV_ROUTE3_FORCE_EXACT=1 sends every query through its exact fp64
+    re-scoring path and SPECSV_ROUTE_LEGACY=1 selects the fp64-DMMA
+    route_fused_kernel.  All three against the oracle, and their index sets
+    agree; the fp64 score diagnostic holds P3."""
     cfg = O.llama_config(4)
     x = LayerInputs(cfg, rows, gamma, 31 + rows + gamma, parent_slot=parents)
     case = DeviceCase(cfg, x)
     ref = case.oracle(oracle_lib, 4, mode, O.ROLE_REFRESH)
     got = {}
     for name, env in ROUTE_VARIANTS.items():
-        for k in ("SPECSV_ROUTE3_FORCE_EXACT", "SPECSV_ROUTE3", "SPECSV_ROUTE2"):
+        for k in ("SPECSV_ROUTE3_FORCE_EXACT", "SPECSV_ROUTE_LEGACY"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)

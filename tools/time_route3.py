@@ -14,15 +14,28 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from tools.time_route import build_case  # noqa: E402
-from tools.time_route2 import timed  # noqa: E402
 from tools.gpu_warm import spin_up  # noqa: E402
 from paper_2605_19893_b200 import abi  # noqa: E402
 from paper_2605_19893_b200 import verify as V  # noqa: E402
 
 BASE = 196608
-PHASES = {6: "u0 q staged", 7: "u0 keys landed", 8: "u0 sliced", 9: "u0 mma done", 10: "u0 epilogue done",
-          11: "u1 q staged", 12: "u1 keys landed", 13: "u1 sliced", 14: "u1 mma done", 15: "u1 epilogue done",
-          1: "tiles done", 2: "grid barrier passed", 3: "shares written", 4: "top-n start", 5: "done"}
+PHASES = {1: "q digits staged", 9: "tile 0 MMAs done", 2: "tile 0 e values", 12: "tile 0 sums",
+          10: "tile 1 MMAs done", 11: "tile 1 e values", 13: "tile 1 sums", 3: "unit sums done", 4: "phase 1 done",
+          5: "den rows in", 6: "shares written", 7: "top-n start", 14: "top-n scores in", 15: "top-n selected",
+          8: "done"}
+
+
+def timed(fn, n=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n * 1e3
 
 
 def main():
@@ -32,9 +45,9 @@ def main():
     spin_up(0.5)
     for legacy in (False, True):
         if legacy:
-            os.environ.pop("SPECSV_ROUTE3", None)
+            os.environ["SPECSV_ROUTE_LEGACY"] = "1"
         else:
-            os.environ["SPECSV_ROUTE3"] = "1"
+            os.environ.pop("SPECSV_ROUTE_LEGACY", None)
         cfg, c, b, s, out, ws = cases[0]
         spin_up(0.2)
         warm = timed(lambda: V.route(cfg, c, b, s, out, ws))
@@ -56,7 +69,7 @@ def main():
         name = "legacy route_fused_kernel" if legacy else "route3_kernel"
         print(f"{name:26s} ctx={ctx} gamma={g}: warm {warm:.1f} us, cold (graph over 16 caches) "
               f"{cold:.1f} us per launch", flush=True)
-    os.environ["SPECSV_ROUTE3"] = "1"
+    os.environ.pop("SPECSV_ROUTE_LEGACY", None)
     # phase stamps of one cold launch
     cfg, c, b, s, out, ws = cases[3]
     buf = torch.zeros(BASE + 4096 * 16, dtype=torch.int64, device="cuda")
