@@ -211,7 +211,7 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
     L.r3_den_off = off;
     off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * kR3Rows * 8), 256);
     L.r3_spill_off = off;
-    off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * kR3Rows * kR3MaxSpr * 8), 256);
+    off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * (kR3Rows + 1) * kR3MaxSpr * 8), 256);
     L.r3_contrib_off = off;
     off = align_up(off + (size_t)(nq * c.n_kv_heads * L.sel_pad * 8), 256);
   }

@@ -141,7 +141,7 @@ struct Route3Req {
   int32_t* idx_count;    // [nq]
   uint32_t* idx_forced;  // [nq]
   double* den;           // [nchunks][Hkv][nranges][kR3Rows] per-range denominators (token-weighted)
-  double* gspill;        // [units][kR3Rows][kR3MaxSpr] selection-block sums of a CTA's earlier units
+  double* gspill;        // [units][kR3MaxSpr][kR3Rows + 1] selection-block sums of a CTA's earlier units
   double* contrib;       // [nr][Hkv][sel_pad] normalised per-KV-head score shares
   int32_t* cnt;          // [kR3CntPerReq] this request's counter set (zero-initialised, self-resetting)
   int32_t nr, nchunks, nranges, spr, blocks, avail_max, sel_pad;

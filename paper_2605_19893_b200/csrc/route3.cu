@@ -38,7 +38,7 @@
 //
 // Certification.  A logit error bound delta (log2 units) makes every e exact
 // to a factor 2^(+-delta), so every score is within a relative
-// eps = 2 ln2 delta_max (x1.5 margin, plus 2e-12 for the fp64 exp and sums)
+// eps = 2 ln2 delta_max (x1.5 margin, plus 2e-10 for the fp64 exp and sums)
 // of its exact value.  The Top-n (forced {0, avail-2, avail-1} plus the best
 // by (score desc, id asc), nsa_attention.cpp:94-136) is accepted when the last
 // pick and the best non-pick are separated by more than eps; otherwise the
@@ -86,9 +86,12 @@ constexpr uint32_t kPlaneBytes = kTB * 128;                // one digit plane of
 constexpr uint32_t kTileBytes = 4 * kPlaneBytes;           // 64 KB; then the tile's e values [48][128] fp64
 constexpr uint32_t kOffQs = 2 * kTileBytes;                // q digits [4][48 rows x 128 B], SW128
 constexpr uint32_t kQsSlice = kN * 128;                    // 6144
-constexpr uint32_t kOffG = kOffQs + 4 * kQsSlice;          // g [48][64] fp64
-constexpr uint32_t kOffMisc = kOffG + kN * kR3MaxSpr * 8;
-static_assert(kN * kTB * 8 <= kTileBytes, "e values alias the tile's planes");
+constexpr int kES = 64;  // e values: [256 rows][64] fp64 over both tiles' plane regions, column
+                         // j stored at j ^ (row & 15) (conflict-free row stores and column reads)
+constexpr int kGS = kN + 1;                                // selection-block sums: [64][kGS] fp64
+constexpr uint32_t kOffG = kOffQs + 4 * kQsSlice;          // g [kR3MaxSpr][kGS] fp64
+constexpr uint32_t kOffMisc = kOffG + kR3MaxSpr * kGS * 8;
+static_assert(kTB * kES * 8 == kTileBytes, "e values: tile t's rows alias tile t's planes");
 static_assert(kQsSlice % 1024 == 0, "SW128 atoms");
 static_assert((size_t)kMaxAvail * 12 + 4 * kDh * 8 <= 2 * kTileBytes, "Top-n arrays alias the planes");
 
@@ -100,7 +103,7 @@ struct Misc {
   int32_t colmvis[kN];  // visible compressed blocks of the column's slot (0: no column)
   double qsc[kN];       // c_sl 2^(qe - 44): logit (log2 units) per unit of h 2^ke
   double invD[kN];
-  double kpow[kR3MaxBlk];
+  int32_t kexp[kR3MaxBlk];  // row exponents of the unit's blocks
   double T16[16];       // 2^(k/16)
   int32_t glo[kR3MaxSpr];                 // first compressed block overlapping each selection block
   double gw[kR3MaxBps][kR3MaxSpr];        // its blocks' token overlaps (0 past the last one)
@@ -228,23 +231,37 @@ __device__ __forceinline__ void write_digit_row(uint8_t* base, uint32_t slice_by
 }
 
 
-// 2^L for L in [-1020, 960] in fp64 (relative error < 2e-13): 16 L rounded to
-// an integer k16 by the 1.5 2^52 shifter, 2^(k16 / 16) from the table and the
-// exponent field, 2^r (|r| <= 1/32) by a degree-5 polynomial in r
+// 2^L for |L| < 512 in fp64 (relative error < 5e-11, inside the 2e-10 term of
+// the certification bound): 16 L rounded to an integer k16 by the
+// 1.5 2^52 shifter, 2^(k16 / 16) from the table and the exponent field,
+// 2^r (|r| <= 1/32) by a degree-4 polynomial in r
 __device__ __forceinline__ double exp2_fast(double L, const double* T16) {
   const double kShift = 6755399441055744.0;  // 1.5 x 2^52
   const double t = fma(L, 16.0, kShift);
   const double k16 = t - kShift;
   const int ki = __double2loint(t);
   const double r = fma(k16, -0.0625, L);
-  double p = 1.3333558146428443e-03;        // ln2^5 / 5!
-  p = fma(p, r, 9.6181291076284772e-03);    // ln2^4 / 4!
+  double p = 9.6181291076284772e-03;        // ln2^4 / 4!
   p = fma(p, r, 5.5504108664821580e-02);
   p = fma(p, r, 2.4022650695910071e-01);
   p = fma(p, r, 6.9314718055994531e-01);
   p = fma(p, r, 1.0);
   const double v = p * T16[ki & 15];
   return __hiloint2double(__double2hiint(v) + ((ki >> 4) << 20), __double2loint(v));
+}
+
+// int32 -> double on the fp64 pipe (no conversion unit): 2^52 + 2^31 + x, minus the bias
+__device__ __forceinline__ double i2d(int x) {
+  return __hiloint2double(0x43300000, x ^ 0x80000000) - 4503601774854144.0;
+}
+// int64 with |x| < 2^51 -> double: 1.5 2^52 + x, minus the bias
+__device__ __forceinline__ double l2d(long long x) {
+  return __longlong_as_double(x + 0x4338000000000000LL) - 6755399441055744.0;
+}
+// x 2^k for x = 0 or a normal x whose result stays normal (the exponent field)
+__device__ __forceinline__ double scale2(double x, int k) {
+  const int hi = __double2hiint(x);
+  return __hiloint2double((hi & 0x7ff00000) ? hi + (k << 20) : hi, __double2loint(x));
 }
 
 struct Unit {
@@ -580,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
   Misc& m = *reinterpret_cast<Misc*>(smem + kOffMisc);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x, nctas = gridDim.x;
-  double* g = reinterpret_cast<double*>(smem + kOffG);  // [kN][kR3MaxSpr]
+  double* g = reinterpret_cast<double*>(smem + kOffG);  // [kR3MaxSpr][kGS]
   griddep_wait();  // inputs (q) may come from the launch just before (PDL)
   stamp(P, 0);
   const int units = P.unit_start[P.n_req];
@@ -652,10 +669,10 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     digit_q(P, R, U, qv, smem, m);
     __syncthreads();  // flag / kemax reset before the block exponents
     if (tid < kR3MaxBlk) {
-      m.kpow[tid] = has_ke ? pow2i(ke) : 0.0;
+      m.kexp[tid] = has_ke ? ke : 0;
       if (has_ke) atomicMax(&m.kemax, ke);
     }
-    for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) g[e] = 0.0;
+    for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) g[e] = 0.0;  // (selection blocks past nsel stay 0)
     fence_proxy_async_smem();  // q digits: generic-proxy writes read by the MMA
     tc_fence_before();
     __syncthreads();
@@ -693,10 +710,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
         umma_commit_warp(&m.mma_done[t]);  // (no MMAs for a missing tile: arrives at once)
       }
     }
-    for (int t = 0; t < ntile; ++t) {
-      const int qd = warp & 3, cg = warp >> 2;  // TMEM lane quadrant, 12-column group
+    const int qd = warp & 3, cg = warp >> 2;  // TMEM lane quadrant, 12-column group
+    for (int t = 0; t < 2; ++t) {
+      if (t >= ntile) {  // the empty commit's phase
+        if (12 * cg < U.nrows) mbar_wait(&m.mma_done[t], par);
+        continue;
+      }
       if (12 * cg < U.nrows) {
-        // ---- epilogue: recombine the classes, logit, e = 2^logit -> e values [48][128]
+        // ---- epilogue: recombine the classes, logit, e = 2^logit -> e values [256][64]
         mbar_wait(&m.mma_done[t], par);
         tc_fence_after();
         if (k == 0) stamp(P, 9 + t);
@@ -710,8 +731,8 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
         tmem_wait_ld();
         const int il = 32 * qd + lane, i = t * kTB + il;
         const int gb = U.row0 + i;
-        const double kp = m.kpow[i];
-        double* E = reinterpret_cast<double*>(smem + t * kTileBytes);
+        const int ke_row = m.kexp[i];
+        double* E = reinterpret_cast<double*>(smem);
         bool ovf = false;
         // branch-free so the 12 independent chains interleave: logits first,
         // then e = 2^logit (clamped into the exponent range; out-of-range
@@ -719,68 +740,73 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
         double Lv[12];
 #pragma unroll
         for (int jj = 0; jj < 12; ++jj) {
-          long long h = (int)a[4][jj];
-          h = h * 256 + (int)a[3][jj];
-          h = h * 256 + (int)a[2][jj];
-          h = h * 256 + (int)a[1][jj];
-          h = h * 256 + (int)a[0][jj];
-          Lv[jj] = (double)h * m.qsc[12 * cg + jj] * kp;
+          // h = a6 2^32 + a5 2^24 + a4 2^16 + a3 2^8 + a2 (classes 2..6; |a_c|
+          // <= pairs x 2^21): the top two in int32 (< 2^30), the bottom three in
+          // int64 (< 2^40), one fp64 FMA (rounding 2^-53 relative)
+          const double hi = i2d((int)a[3][jj] + ((int)a[4][jj] << 8));
+          const long long lo = (long long)(int)a[2][jj] * 65536 + (long long)(int)a[1][jj] * 256 + (int)a[0][jj];
+          Lv[jj] = scale2(fma(hi, 16777216.0, l2d(lo)) * m.qsc[12 * cg + jj], ke_row);
         }
         const bool row_ok = i < U.nblk;
 #pragma unroll
         for (int jj = 0; jj < 12; ++jj) {
           const int j = 12 * cg + jj;
           const bool valid = row_ok && gb < m.colmvis[j];
-          ovf |= valid && Lv[jj] > 960.0;
-          const double e = exp2_fast(fmin(fmax(Lv[jj], -1020.0), 960.0), m.T16);
-          E[j * kTB + il] = valid ? e : 0.0;
+          // |logit| >= 512 log2 units: outside the fp64 exp's range here -- the
+          // query goes to the exact path
+          ovf |= valid && (__double2hiint(Lv[jj]) & 0x7fffffff) >= 0x40800000;
+          const double e = exp2_fast(Lv[jj], m.T16);
+          E[i * kES + (j ^ (i & 15))] = valid ? e : 0.0;
         }
         if (__any_sync(0xffffffffu, ovf) && lane == 0) m.flag = 1;
       }
-      tc_fence_before();
-      __syncthreads();
-      if (k == 0) stamp(P, t == 0 ? 2 : 11);
-      // ---- selection-block sums of this tile's blocks (all warps)
-      {
-        const double* E = reinterpret_cast<const double*>(smem + t * kTileBytes);
-        const int nsel = U.b1 - U.b0;
-        const int tlo = U.row0 + t * kTB, thi = min(U.row0 + U.nblk, tlo + kTB) - 1;
-        for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) {
-          const int j = e >> 6, bl = e & 63;
-          if (j >= U.nrows || bl >= nsel) continue;
-          const int r0 = m.glo[bl] - tlo;  // tile row of the selection block's first block
-          const double* Ej = E + j * kTB;
-          double acc = 0.0;
-#pragma unroll 8
-          for (int kq = 0; kq < P.bps; ++kq) {
-            const int r = r0 + kq;
-            const bool in = r >= 0 && r < kTB;
-            acc = fma(m.gw[kq][bl], in ? Ej[in ? r : 0] : 0.0, acc);
-          }
-          g[e] += acc;
-        }
-      }
-      __syncthreads();
-      if (k == 0) stamp(P, 12 + t);
     }
-    if (12 * (warp >> 2) < U.nrows && ntile < 2) mbar_wait(&m.mma_done[1], par);  // the empty commit's phase
+    tc_fence_before();
+    __syncthreads();
+    if (k == 0) stamp(P, 2);
+    {  // ---- selection-block sums: thread (row j, eight consecutive selection
+       // blocks), eight independent chains; the rows of one column read along a
+       // warp are consecutive (conflict-free)
+      const double* E = reinterpret_cast<const double*>(smem);
+      const int nsel = U.b1 - U.b0;
+      const int ngrp = (nsel + 7) / 8;
+      for (int item = tid; item < U.nrows * ngrp; item += kThreads) {
+        const int j = item % U.nrows, bl0 = 8 * (item / U.nrows);
+        int rr[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) rr[z] = m.glo[min(bl0 + z, kR3MaxSpr - 1)] - U.row0;
+        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int kq = 0; kq < P.bps; ++kq)
+#pragma unroll
+          for (int z = 0; z < 8; ++z) {
+            const int r = min(rr[z] + kq, U.nblk - 1);  // (weights past a block's last row are 0; rows
+                                                         //  below nblk are written, zero when masked)
+            acc[z] = fma(m.gw[kq][min(bl0 + z, kR3MaxSpr - 1)], E[r * kES + (j ^ (r & 15))], acc[z]);
+          }
+#pragma unroll
+        for (int z = 0; z < 8; ++z)
+          if (bl0 + z < nsel) g[(bl0 + z) * kGS + j] = acc[z];
+      }
+    }
+    __syncthreads();
     if (k == 0) stamp(P, 3);
     // ---- this range's denominator rows, error exponents, spill, arrival
     {
       double* den = R.den + ((int64_t)(U.chunk * P.Hkv + U.kvh) * R.nranges + U.range) * kN;
+      if (tid < kN) {  // four partial sums, then in order
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int bl = 0; bl < kR3MaxSpr; bl += 4)
 #pragma unroll
-      for (int z = 0; z < kN / kWarps; ++z) {
-        const int j = warp + z * kWarps;
-        const double v = warp_sum_d(g[j * kR3MaxSpr + lane] + g[j * kR3MaxSpr + lane + 32]);
-        if (lane == 0) den[j] = v;
+          for (int z = 0; z < 4; ++z) v[z] += g[(bl + z) * kGS + tid];
+        den[tid] = (v[0] + v[1]) + (v[2] + v[3]);
       }
       if (tid < U.nrows) {
         const int ex = m.flag ? kExpoFlag : m.qexp[tid] + m.kemax + kExpoBias;
         atomicMax(&R.cnt[kCntExpo + U.s0 + tid / P.G], ex);
       }
       if (u + nctas < units) {  // not this CTA's last unit: phase 2 reloads g from L2
-        double* sp = R.gspill + (int64_t)U.lu * kN * kR3MaxSpr;
-        for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) sp[e] = g[e];
+        double* sp = R.gspill + (int64_t)U.lu * kR3MaxSpr * kGS;
+        for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) sp[e] = g[e];
       }
     }
     tc_fence_before();
@@ -808,8 +834,8 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const double* src = R.den + (int64_t)(U.chunk * P.Hkv + U.kvh) * R.nranges * kN;
     for (int e = tid; e < R.nranges * kN; e += kThreads) st[e] = __ldcg(src + e);
     if (!last) {
-      const double* sp = R.gspill + (int64_t)U.lu * kN * kR3MaxSpr;
-      for (int e = tid; e < kN * kR3MaxSpr; e += kThreads) gs[e] = __ldcg(sp + e);
+      const double* sp = R.gspill + (int64_t)U.lu * kR3MaxSpr * kGS;
+      for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) gs[e] = __ldcg(sp + e);
     }
     __syncthreads();
     if (tid < kN) {
@@ -824,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     for (int e = tid; e < U.nslots * nsel; e += kThreads) {
       const int sl = e / nsel, bl = e % nsel;
       double c = 0.0;
-      for (int h = 0; h < P.G; ++h) c = fma(gs[(sl * P.G + h) * kR3MaxSpr + bl], m.invD[sl * P.G + h], c);
+      for (int h = 0; h < P.G; ++h) c = fma(gs[bl * kGS + sl * P.G + h], m.invD[sl * P.G + h], c);
       R.contrib[((int64_t)(U.s0 + sl) * P.Hkv + U.kvh) * R.sel_pad + U.b0 + bl] = c;
     }
     __syncthreads();
@@ -871,7 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     // relative score error <= 2 ln2 delta (+ fp64 exp / summation rounding), with margin
     const bool flagged = ex >= kExpoFlag;
     const double delta = flagged ? 0.0 : P.c_sl * pow2i(max(-1000, min(1000, ex - kExpoBias - 22)));
-    const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-12;
+    const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-10;
     select_topn(sel, surv, avail, P.n, eps, m);
     stamp(P, 15);
     if (flagged || !m.certified || P.force_exact) {
