@@ -213,7 +213,7 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
     L.r3_spill_off = off;
     off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * (kR3Rows + 1) * kR3MaxSpr * 8), 256);
     L.r3_contrib_off = off;
-    off = align_up(off + (size_t)(nq * c.n_kv_heads * L.sel_pad * 8), 256);
+    off = align_up(off + (size_t)(nq * L.sel_pad * 8), 256);
   }
   L.total = off;
   return L;
@@ -465,6 +465,8 @@ void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, R
   P.fallbacks = cnt + 4;
   const char* fe = std::getenv("SPECSV_ROUTE3_FORCE_EXACT");  // tests: the exact re-scoring path
   P.force_exact = (fe != nullptr && fe[0] == '1') ? 1 : 0;
+  const char* dbg = std::getenv("SPECSV_ROUTE3_DEBUG");
+  P.debug = dbg != nullptr ? std::atoi(dbg) : 0;
   P.trace = g_trace;
   if (c.d_head != kR3Tile) throw Error(SPECSV_EUNSUPPORTED, "route3: d_head must be 128");
 }
@@ -516,6 +518,7 @@ void fill_attend_params(AttendParams& p, const specsv_nsa_config& c, const specs
   p.idx_count = a.idx_count;
   p.trace = g_trace;
   p.debug_flags = std::getenv("SPECSV_ATTEND_FORCE_ROBUST") != nullptr ? 1 : 0;
+  if (const char* e = std::getenv("SPECSV_ATTEND_DEBUG")) p.debug_flags |= std::atoi(e);  // timing experiments
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
   p.nq = a.n_queries;

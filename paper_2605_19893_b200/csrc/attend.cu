@@ -160,8 +160,10 @@ __device__ void group_barrier(int* cnt, int* gen, int S, int tid) {
     // bar.sync above orders them before thread 0) and acquire the others'
     const int g = sm100::ld_acquire_gpu(gen);
     if (sm100::atom_add_acq_rel_gpu(cnt, 1) == S - 1) {
-      atomicExch(cnt, 0);
-      sm100::atom_add_acq_rel_gpu(gen, 1);
+      // the last arrival: plain stores (no round trip before the others see
+      // the new generation); the release orders the reset before it
+      *reinterpret_cast<volatile int*>(cnt) = 0;
+      sm100::st_release_gpu(gen, g + 1);
     } else {
       while (sm100::ld_acquire_gpu(gen) == g) __nanosleep(32);
     }
@@ -382,15 +384,16 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     const CUtensorMap *tk, *tv;
     int r0, r1;
     tile_rows(t, tk, tv, r0, r1);
+    const uint64_t pol = l2_evict_first_policy();  // each tile is read once per launch
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      tma_load_3d(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st]);
-      tma_load_3d(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st]);
+      tma_load_3d_hint(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st], pol);
+      tma_load_3d_hint(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st], pol);
     }
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      tma_load_3d(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st]);
-      tma_load_3d(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st]);
+      tma_load_3d_hint(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st], pol);
+      tma_load_3d_hint(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st], pol);
     }
   };
   // stages issued before the CTA-wide barrier (compressed tiles only)
@@ -908,7 +911,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         asm volatile("prefetch.global.L2 [%0];" ::"l"(bv + off));
       }
     };
-    for (int j = 2; split + j * S < n_cmp; ++j) prefetch_tile(split + j * S);
+    if (!(p.debug_flags & 2))  // bit 1 (timing experiments): no L2 prefetch of the compressed tiles
+      for (int j = 2; split + j * S < n_cmp; ++j) prefetch_tile(split + j * S);
     // the index rows may come from the routing launch just before this one
     // (programmatic dependent launch: the rest of this CTA -- q, the
     // compressed tiles -- does not wait for it)
@@ -920,8 +924,9 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     if (trace && lane == 0) p.trace[cta_id * 64 + 1] = globaltimer();
     const int T = tile_count();
     const int n_tok_end = n_cmp + m.n_tok_tiles;
-    for (int j = 2; j < T; ++j)
-      if (split + j * S >= n_cmp && split + j * S < n_tok_end) prefetch_tile(split + j * S);
+    if (!(p.debug_flags & 4))  // bit 2 (timing experiments): no L2 prefetch of the token tiles
+      for (int j = 2; j < T; ++j)
+        if (split + j * S >= n_cmp && split + j * S < n_tok_end) prefetch_tile(split + j * S);
     if (trace && lane == 0) p.trace[cta_id * 64 + 60] = globaltimer();
     named_bar_sync(kBarPassEnd, kThreads);
     if (m.flag) {

@@ -142,7 +142,8 @@ struct Route3Req {
   uint32_t* idx_forced;  // [nq]
   double* den;           // [nchunks][Hkv][nranges][kR3Rows] per-range denominators (token-weighted)
   double* gspill;        // [units][kR3MaxSpr][kR3Rows + 1] selection-block sums of a CTA's earlier units
-  double* contrib;       // [nr][Hkv][sel_pad] normalised per-KV-head score shares
+  double* contrib;       // [nr][sel_pad] selection scores x Hq (the KV heads' shares, fp64 atomics;
+                         // zero between launches)
   int32_t* cnt;          // [kR3CntPerReq] this request's counter set (zero-initialised, self-resetting)
   int32_t nr, nchunks, nranges, spr, blocks, avail_max, sel_pad;
   int32_t slot_q[kMaxQueries];
@@ -161,9 +162,11 @@ struct Route3Launch {
   int32_t bps;         // compressed blocks overlapping one selection block (at most)
   double scale;        // 1 / sqrt(dh)
   double c_sl;         // log2(e) / sqrt(dh): logits in log2 units
-  int32_t* exit_cnt;   // [1] CTAs done (the last one resets every request's counter set)
+  int32_t* exit_cnt;   // [2] CTAs through phase 2, tasks through their wait (the last of each
+                       // resets the counters nobody polls any more); self-resetting
   int32_t* fallbacks;  // cumulative count of exact re-scorings (diagnostics; never reset)
   int32_t force_exact; // tests: re-score every query in fp64
+  int32_t debug;       // diagnostics (SPECSV_ROUTE3_DEBUG): bit 0 runs the selection twice
   unsigned long long* trace;  // diagnostics: per-CTA stamps at kRouteTraceBase + cta * 16
 };
 cudaError_t launch_route3(Route3Launch& p, cudaStream_t stream);

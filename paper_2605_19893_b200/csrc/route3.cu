@@ -642,13 +642,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const bool has_ke = tid < U.nblk;  // the exponent load is in flight across the setup
     const int ke = has_ke ? __ldg(R.ckexp + (int64_t)(U.row0 + tid) * P.Hkv + U.kvh) : 0;
     if (tid == 0) {
+      const uint64_t pol = l2_evict_first_policy();  // the digit planes are read once per launch
       for (int t = 0; t < 2; ++t) {
         if (t < ntile) {
           mbar_expect_tx(&m.tma_full[t], kTileBytes);
 #pragma unroll
           for (int s = 0; s < 4; ++s)
-            tma_load_4d(smem + t * kTileBytes + s * kPlaneBytes, &R.tm_ckd, 0, s, U.kvh, U.row0 + t * kTB,
-                        &m.tma_full[t]);
+            tma_load_4d_hint(smem + t * kTileBytes + s * kPlaneBytes, &R.tm_ckd, 0, s, U.kvh, U.row0 + t * kTB,
+                             &m.tma_full[t], pol);
         } else {
           mbar_arrive(&m.tma_full[t]);
         }
@@ -851,12 +852,21 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       const int sl = e / nsel, bl = e % nsel;
       double c = 0.0;
       for (int h = 0; h < P.G; ++h) c = fma(gs[bl * kGS + sl * P.G + h], m.invD[sl * P.G + h], c);
-      R.contrib[((int64_t)(U.s0 + sl) * P.Hkv + U.kvh) * R.sel_pad + U.b0 + bl] = c;
+      // the KV heads' shares meet in one score row per slot (fp64 atomics: the
+      // summation order varies, inside the certified bound; the Top-n task
+      // reads the row and zeroes it for the next launch)
+      atomicAdd(R.contrib + (int64_t)(U.s0 + sl) * R.sel_pad + U.b0 + bl, c);
     }
     __syncthreads();
     if (tid == 0) red_add_release_gpu(&R.cnt[kCntTop + U.chunk], 1);
   }
   stamp(P, 6);
+  if (tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt, 1) == nctas - 1) {
+    // the last CTA through phase 2: no unit polls a denominator counter any more
+    for (int r = 0; r < P.n_req; ++r)
+      for (int i = 0; i < P.req[r].nchunks * P.Hkv; ++i) P.req[r].cnt[kCntDen + i] = 0;
+    st_release_gpu(P.exit_cnt, 0);
+  }
 
   // ================= phase 3: one Top-n task per routed slot =================
   griddep_launch();  // the next launch may start placing CTAs as this grid drains
@@ -879,16 +889,16 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     stamp(P, 7);
     const int avail = R.slot_avail[slot];
     const double inv = 1.0 / (double)P.Hq;
-    const double* cb = R.contrib + (int64_t)slot * P.Hkv * R.sel_pad;
+    if (tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt + 1, 1) == tasks - 1) {
+      // the last task through its wait: no task polls a chunk counter any more
+      for (int rr = 0; rr < P.n_req; ++rr)
+        for (int i = 0; i < P.req[rr].nchunks; ++i) P.req[rr].cnt[kCntTop + i] = 0;
+      st_release_gpu(P.exit_cnt + 1, 0);
+    }
+    double* sc = R.contrib + (int64_t)slot * R.sel_pad;
     for (int b = tid; b < avail; b += kThreads) {
-      double v[8];
-#pragma unroll
-      for (int h = 0; h < 8; ++h) v[h] = h < P.Hkv ? __ldcg(cb + (int64_t)h * R.sel_pad + b) : 0.0;
-      double s = 0.0;  // KV heads ascending
-#pragma unroll
-      for (int h = 0; h < 8; ++h) s += v[h];
-      for (int h = 8; h < P.Hkv; ++h) s += __ldcg(cb + (int64_t)h * R.sel_pad + b);
-      sel[b] = s * inv;
+      sel[b] = __ldcg(sc + b) * inv;
+      sc[b] = 0.0;
     }
     const int ex = __ldcg(&R.cnt[kCntExpo + slot]);
     __syncthreads();
@@ -898,8 +908,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const bool flagged = ex >= kExpoFlag;
     const double delta = flagged ? 0.0 : P.c_sl * pow2i(max(-1000, min(1000, ex - kExpoBias - 22)));
     const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-10;
+    const long long c0 = clock64();
     select_topn(sel, surv, avail, P.n, eps, m);
     stamp(P, 15);
+    if (P.trace != nullptr && tid == 0) P.trace[kRouteTraceBase + blockIdx.x * 16 + 12] = clock64() - c0;
+    if (P.debug & 1) {  // diagnostics: the selection again (warm instruction cache)
+      select_topn(sel, surv, avail, P.n, eps, m);
+      stamp(P, 13);
+    }
     if (flagged || !m.certified || P.force_exact) {
       if (tid == 0 && P.fallbacks != nullptr) atomicAdd(P.fallbacks, 1);
       exact_scores(P, R, slot, sel, qrows, m);
@@ -910,16 +926,6 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     __syncthreads();
   }
   stamp(P, 8);
-  __syncthreads();
-  if (tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt, 1) == nctas - 1) {  // the last CTA out resets
-    for (int r = 0; r < P.n_req; ++r) {
-      const Route3Req& R = P.req[r];
-      for (int i = 0; i < R.nchunks * P.Hkv; ++i) R.cnt[kCntDen + i] = 0;
-      for (int i = 0; i < R.nchunks; ++i) R.cnt[kCntTop + i] = 0;
-    }
-    __threadfence();
-    atomicExch(P.exit_cnt, 0);
-  }
 }
 
 int sm_count3() {

@@ -86,19 +86,25 @@ def main():
     for j in range(L):
         t = bufs[j][:RBASE].view(-1, 64).cpu().numpy()
         t = t[t[:, 0] > 0]
-        r = bufs[j][RBASE:RBASE + 1024 * 64].view(-1, 64).cpu().numpy()
+        r = bufs[j][RBASE:RBASE + 1024 * 16].view(-1, 16).cpu().numpy()
         r = r[r[:, 0] > 0]
         if t_first is None:
             t_first = (r[:, 0].min() if len(r) else t[:, 0].min())
         line = f"layer {j:2d} {'R' if j % 2 == 0 else 'U'}"
-        if len(r):
+        if len(r):  # route3 stamps: 0 start, 4 phase 1 done, 6 shares written, 8 done
             r0 = r[:, 0].min()
-            rend = r[:, 5][r[:, 5] > 0].max() if (r[:, 5] > 0).any() else r[:, 1].max()
+            rend = r[:, 8].max()
             gap = (r0 - prev_end) / 1e3 if prev_end is not None else 0.0
-            tiles = (np.median(r[:, 1]) - r0) / 1e3
-            bar = (np.median(r[:, 4][r[:, 4] > 0]) - r0) / 1e3 if (r[:, 4] > 0).any() else -1
-            line += (f" | route start {(r0 - t_first) / 1e3:8.2f} gap {gap:5.2f} tiles(med) {tiles:5.2f}"
-                     f" barrier {bar:5.2f} end {(rend - r0) / 1e3:5.2f}")
+            p1 = (np.median(r[:, 4][r[:, 4] > 0]) - r0) / 1e3
+            sh = (np.median(r[:, 6][r[:, 6] > 0]) - r0) / 1e3
+            tk = r[r[:, 7] > 0]  # the Top-n task CTAs: start, scores in, selected, done
+
+            def tcol(c):
+                return (np.median(tk[:, c]) - r0) / 1e3 if len(tk) else -1
+            line += (f" | route start {(r0 - t_first) / 1e3:8.2f} gap {gap:5.2f} phase1(med) {p1:5.2f}"
+                     f" shares {sh:5.2f} topn {tcol(7):5.2f}/{tcol(14):5.2f}/{tcol(15):5.2f}/{tcol(8):5.2f}"
+                     f" select {np.median(tk[:, 12]) if len(tk) else -1:.0f} clk"
+                     f" end {(rend - r0) / 1e3:5.2f}")
             prev_end = rend
         t0 = t[:, 0].min()
         gap = (t0 - prev_end) / 1e3 if prev_end is not None else 0.0
@@ -110,6 +116,7 @@ def main():
 
         end = t[:, 4].max()
         line += (f" | attend start {(t0 - t_first) / 1e3:8.2f} gap {gap:5.2f} spread {(t[:, 0].max() - t0) / 1e3:4.2f}"
+                 f" idx in {ph(59)[0]:5.2f}/{ph(59)[1]:5.2f} u {ph(56)[0]:5.2f}/{ph(57)[0]:5.2f}/{ph(58)[0]:5.2f}"
                  f" union {ph(1)[0]:5.2f} loop {ph(2)[0]:5.2f}/{ph(2)[1]:5.2f} part {ph(3)[0]:5.2f}/{ph(3)[1]:5.2f}"
                  f" bar {ph(6)[0]:5.2f} merge {ph(4)[0]:5.2f}/{ph(4)[1]:5.2f} ctas {len(t)}")
         prev_end = end
