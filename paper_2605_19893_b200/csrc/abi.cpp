@@ -517,6 +517,7 @@ void fill_attend_params(AttendParams& p, const specsv_nsa_config& c, const specs
   p.idx = a.idx;
   p.idx_count = a.idx_count;
   p.trace = g_trace;
+  p.idx_early = a.role == SPECSV_ROLE_REUSE ? 1 : 0;
   p.debug_flags = std::getenv("SPECSV_ATTEND_FORCE_ROBUST") != nullptr ? 1 : 0;
   if (const char* e = std::getenv("SPECSV_ATTEND_DEBUG")) p.debug_flags |= std::atoi(e);  // timing experiments
   const int qc = qc_size_for(c);

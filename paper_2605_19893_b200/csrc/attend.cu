@@ -67,6 +67,8 @@ constexpr int kBarSoft = 1;         // named barriers: softmax warps
 constexpr int kBarChunk0 = 3;       // 3..5: the 4 warps of one column chunk
 constexpr int kBarPassEnd = 7;
 constexpr int kBarRedo = 8;
+constexpr int kBarUnion = 9;        // the 12 softmax warps + the union warp build the union
+constexpr int kUnionThreads = kSoftThreads + 32;
 
 // shared memory map (bytes from the 1024-aligned base)
 constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P^T of branch A)
@@ -129,6 +131,13 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) 
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// a wait that may be long (the union, built by one warp from index rows that
+// may still be in flight): back off between probes so the waiting warps leave
+// the union warp the issue slots
+__device__ __forceinline__ void mbar_backoff_wait(uint64_t* bar, uint32_t parity, bool backoff) {
+  while (!mbar_try_wait(bar, parity))
+    if (backoff) __nanosleep(256);
+}
 
 // transpose-reduce of 16 columns across the warp: returns, in lanes 2c and
 // 2c+1, the reduction over all 32 lanes of column c (16 shuffles)
@@ -177,36 +186,64 @@ __device__ void group_barrier(int* cnt, int* gen, int S, int tid) {
 // bound, layer_roles.cpp:37-50).  Built by the union warp while the
 // compressed tiles (which do not need it) are already in flight; the index
 // rows are staged with fire-and-forget cp.async (one round trip).
-// index rows of the chunk's queries -> smem, fire-and-forget (one round trip)
-__device__ __forceinline__ void stage_index_rows(const AttendParams& p, Misc& m, int q0, int nqc, int lane) {
-  const int n = p.n_sel;
-  for (int e = lane; e < nqc * n; e += 32) {
-    const int i = e / n, k = e - i * n;
-    const int r = p.src_row[q0 + i];
-    cp_async4(&m.qsel[e], p.idx + r * n + k);
-    if (k == 0) cp_async4(&m.qcount[i], p.idx_count + r);
+// index rows of the chunk's queries -> smem, fire-and-forget (one round trip).
+// Per-query kernel parameters are read once, lane q holding query q's (a
+// divergent read of the parameter space serialises per distinct address).
+// The union warp's kernel parameters, read into registers before it waits
+// for the routing launch: a first read of the parameter bank misses the
+// constant cache, and one serialised miss per line after the wait would sit
+// on the critical path.
+struct UnionArgs {
+  const int32_t* idx;
+  const int32_t* idx_count;
+  int n, l_sel, rows;
+  int my_src;  // lane q: query q's index-set row
+};
+
+__device__ __forceinline__ UnionArgs union_args(const AttendParams& p, int q0, int nqc, int lane) {
+  UnionArgs u;
+  u.idx = p.idx;
+  u.idx_count = p.idx_count;
+  u.n = p.n_sel;
+  u.l_sel = p.l_sel;
+  u.rows = p.rows;
+  u.my_src = lane < nqc ? p.src_row[q0 + lane] : 0;
+  // materialise every value now (the loads must not sink below the wait)
+  asm volatile("" ::"l"(u.idx), "l"(u.idx_count), "r"(u.n), "r"(u.l_sel), "r"(u.rows), "r"(u.my_src));
+  return u;
+}
+
+__device__ __forceinline__ void stage_index_rows(const UnionArgs& u, Misc& m, int nqc, int lane) {
+  const int n = u.n;
+  if (lane < nqc) cp_async4(&m.qcount[lane], u.idx_count + u.my_src);
+  for (int i = 0; i < nqc; ++i) {
+    const int r = __shfl_sync(0xffffffffu, u.my_src, i);
+    for (int k = lane; k < n; k += 32) cp_async4(&m.qsel[i * n + k], u.idx + r * n + k);
   }
 }
 
-__device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc, int lane, int wlo,
-                                 int whi, unsigned long long* tr) {
-  const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
+// The union of selected + window blocks with per-block query ownership, built
+// by the 12 softmax warps and the union warp together (kUnionThreads
+// participants, `pt` = this thread's index among them) once the index rows
+// are staged: five short parallel steps between named barriers.  (One warp
+// alone took ~6 us for it under the step's load; the softmax warps reach this
+// point with nothing else to do, their compressed tiles done.)
+__device__ void coop_union(Misc& m, int pt, int nqc, int n, int l_sel, int rows, int wlo, int whi) {
+  const int nsel = (rows + l_sel - 1) / l_sel;
   const int words = (nsel + 31) >> 5;
-  const int n = p.n_sel;
-  for (int w = lane; w < words; w += 32) m.bitmap[w] = 0u;
-  cp_async_wait_all();
-  __syncwarp();
-  if (tr && lane == 0) tr[56] = globaltimer();
-  for (int b = wlo / p.l_sel + lane; b <= whi / p.l_sel; b += 32) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
-  for (int e = lane; e < nqc * n; e += 32) {
+  for (int w = pt; w < words; w += kUnionThreads) m.bitmap[w] = 0u;
+  named_bar_sync(kBarUnion, kUnionThreads);
+  for (int b = wlo / l_sel + pt; b <= whi / l_sel; b += kUnionThreads) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
+  for (int e = pt; e < nqc * n; e += kUnionThreads) {
     const int i = e / n, k = e - i * n;
     int b = m.qsel[e];
-    if (k >= m.qcount[i] || b < 0 || (int64_t)b * p.l_sel >= p.qbound[q0 + i] || b >= nsel) b = -1;
+    if (k >= m.qcount[i] || b < 0 || (int64_t)b * l_sel >= m.qbound[i] || b >= nsel) b = -1;
     m.qsel[e] = b;
     if (b >= 0) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
   }
-  __syncwarp();
-  {  // exclusive prefix of popcounts, contiguous word ranges per lane
+  named_bar_sync(kBarUnion, kUnionThreads);
+  if (pt >= kSoftThreads) {  // one warp: exclusive prefix of popcounts over contiguous word ranges
+    const int lane = pt - kSoftThreads;
     const int per = (words + 31) >> 5;
     const int w0 = lane * per;
     int local = 0;
@@ -228,9 +265,8 @@ __device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc
       m.n_tok_tiles = (min(total, kMaxUnion) + 1) / 2;
     }
   }
-  __syncwarp();
-  if (tr && lane == 0) tr[57] = globaltimer();
-  for (int w = lane; w < words; w += 32) {
+  named_bar_sync(kBarUnion, kUnionThreads);
+  for (int w = pt; w < words; w += kUnionThreads) {
     uint32_t bits = m.bitmap[w];
     int r = m.word_prefix[w];
     while (bits) {
@@ -243,16 +279,15 @@ __device__ void build_union_warp(const AttendParams& p, Misc& m, int q0, int nqc
       ++r;
     }
   }
-  __syncwarp();
-  if (tr && lane == 0) tr[58] = globaltimer();
-  for (int e = lane; e < nqc * n; e += 32) {
+  named_bar_sync(kBarUnion, kUnionThreads);
+  for (int e = pt; e < nqc * n; e += kUnionThreads) {
     const int b = m.qsel[e];
     if (b < 0) continue;
     const int w = b >> 5;
     const int r = m.word_prefix[w] + __popc(m.bitmap[w] & ((1u << (b & 31)) - 1u));
     if (r < kMaxUnion) atomicOr(&m.union_own[r], 1u << (e / n));
   }
-  __syncwarp();
+  named_bar_sync(kBarUnion, kUnionThreads);
 }
 
 struct TileInfo {
@@ -559,7 +594,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       for (int j = 0; active; ++j) {
         const int t = split + j * S;
         if (!union_seen && t >= n_cmp) {
-          mbar_sleep_wait(&m.union_ready, 0);
+          coop_union(m, tid, nqc, p.n_sel, p.l_sel, p.rows, cwlo, cwhi);
+          if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
           union_seen = true;
           T = tile_count();
         }
@@ -725,6 +761,11 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         if (lane == 0) mbar_arrive(&m.p_full[J & 1]);
         if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 32 + j] = globaltimer();
       }
+      if (!union_seen) {  // a warp without columns: it still takes part in the union build, once
+        coop_union(m, tid, nqc, p.n_sel, p.l_sel, p.rows, cwlo, cwhi);
+        union_seen = true;
+        T = tile_count();
+      }
       if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 2] = globaltimer();
       // ---- end of pass: branch row sums, then the fast-pass check ----
       if ((lane & 1) == 0) {
@@ -791,7 +832,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     if (lane == 0) {
       for (int j = pre;; ++j) {
         if (T == 0x7fffffff && split + j * S >= n_cmp) {
-          mbar_sleep_wait(&m.union_ready, 0);
+          mbar_backoff_wait(&m.union_ready, 0, !(p.debug_flags & 8));
           T = tile_count();
         }
         if (j >= T) break;
@@ -816,7 +857,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     int T = 0x7fffffff;
     auto tiles = [&](int j) {
       if (split + j * S >= n_cmp && !union_seen) {
-        mbar_sleep_wait(&m.union_ready, 0);
+        mbar_backoff_wait(&m.union_ready, 0, !(p.debug_flags & 8));
         union_seen = true;
         T = tile_count();
       }
@@ -911,17 +952,26 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         asm volatile("prefetch.global.L2 [%0];" ::"l"(bv + off));
       }
     };
+    const UnionArgs ua = union_args(p, q0, nqc, lane);
+    const bool early = p.idx_early != 0 && !(p.debug_flags & 8);
+    if (early) stage_index_rows(ua, m, nqc, lane);  // (in flight across the prefetches)
     if (!(p.debug_flags & 2))  // bit 1 (timing experiments): no L2 prefetch of the compressed tiles
       for (int j = 2; split + j * S < n_cmp; ++j) prefetch_tile(split + j * S);
-    // the index rows may come from the routing launch just before this one
-    // (programmatic dependent launch: the rest of this CTA -- q, the
-    // compressed tiles -- does not wait for it)
-    griddep_wait();
-    stage_index_rows(p, m, q0, nqc, lane);
+    // REFRESH: the index rows come from the routing launch just before this
+    // one (programmatic dependent launch: the rest of this CTA -- q, the
+    // compressed tiles -- does not wait for it).  REUSE: they were complete
+    // before the previous launch started, and this launch writes nothing the
+    // previous one still reads (it triggers after its last workspace read),
+    // so the union is built at once, under the compressed tiles.
+    if (!early) {
+      griddep_wait();
+      stage_index_rows(ua, m, nqc, lane);
+    }
+    cp_async_wait_all();
+    __syncwarp();
     if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
-    build_union_warp(p, m, q0, nqc, lane, cwlo, cwhi, trace ? p.trace + cta_id * 64 : nullptr);
-    mbar_arrive(&m.union_ready);  // every lane: releases its own union writes
-    if (trace && lane == 0) p.trace[cta_id * 64 + 1] = globaltimer();
+    coop_union(m, kSoftThreads + lane, nqc, ua.n, ua.l_sel, ua.rows, cwlo, cwhi);
+    mbar_arrive(&m.union_ready);  // the TMA and MMA warps wait for this
     const int T = tile_count();
     const int n_tok_end = n_cmp + m.n_tok_tiles;
     if (!(p.debug_flags & 4))  // bit 2 (timing experiments): no L2 prefetch of the token tiles

@@ -37,6 +37,9 @@ struct AttendParams {
   int32_t rows, blocks, l, d, l_sel, w, lag;
   int32_t qc_size, n_splits;
   int32_t kvh0, nkvh;            // KV heads [kvh0, kvh0 + nkvh) of this call (head-group shard)
+  int32_t idx_early;             // 1 (REUSE): the index rows predate the previous launch, so the
+                                 // union is built without waiting for it; 0 (REFRESH): they come
+                                 // from the routing launch just before (programmatic dependent launch)
   float scale_log2;
   int32_t pos[kMaxQueries];
   int32_t src_row[kMaxQueries];  // index-set row each query attends with

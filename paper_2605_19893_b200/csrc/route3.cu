@@ -93,7 +93,7 @@ constexpr uint32_t kOffG = kOffQs + 4 * kQsSlice;          // g [kR3MaxSpr][kGS]
 constexpr uint32_t kOffMisc = kOffG + kR3MaxSpr * kGS * 8;
 static_assert(kTB * kES * 8 == kTileBytes, "e values: tile t's rows alias tile t's planes");
 static_assert(kQsSlice % 1024 == 0, "SW128 atoms");
-static_assert((size_t)kMaxAvail * 12 + 4 * kDh * 8 <= 2 * kTileBytes, "Top-n arrays alias the planes");
+static_assert((size_t)kMaxAvail * 12 + 4 * kDh * 8 + 66 * 4 <= 2 * kTileBytes, "Top-n arrays alias the planes");
 
 struct Misc {
   uint64_t tma_full[2], mma_done[2];

@@ -116,7 +116,7 @@ def main():
 
         end = t[:, 4].max()
         line += (f" | attend start {(t0 - t_first) / 1e3:8.2f} gap {gap:5.2f} spread {(t[:, 0].max() - t0) / 1e3:4.2f}"
-                 f" idx in {ph(59)[0]:5.2f}/{ph(59)[1]:5.2f} u {ph(56)[0]:5.2f}/{ph(57)[0]:5.2f}/{ph(58)[0]:5.2f}"
+                 f" idx in {ph(59)[0]:5.2f}/{ph(59)[1]:5.2f}"
                  f" union {ph(1)[0]:5.2f} loop {ph(2)[0]:5.2f}/{ph(2)[1]:5.2f} part {ph(3)[0]:5.2f}/{ph(3)[1]:5.2f}"
                  f" bar {ph(6)[0]:5.2f} merge {ph(4)[0]:5.2f}/{ph(4)[1]:5.2f} ctas {len(t)}")
         prev_end = end
