@@ -657,17 +657,28 @@ def run_ours(a, world: int, rank: int, local: int):
         groups.append((j0, min(L, j0 + max(1, j0))))
         j0 = groups[-1][1]
 
+    commits = [TR.PreparedCommit(cfg, caches[r], [batches[r][j].tree_k for j in range(L)],
+                                 [batches[r][j].tree_v for j in range(L)], slots, pes[r])
+               for r in range(R)] if slots else []
+    host_parts = {"copies": 0.0, "verify_calls": 0.0, "readback": 0.0, "commit": 0.0}
+    host_role = {int(V.ROLE_REFRESH): 0.0, int(V.ROLE_REUSE): 0.0}
+
+    variant = os.environ.get("SPECSV_E2E_VARIANT", "")  # diagnostics only: drop one part of the step
+
     def e2e_step():
+        tA = time.perf_counter()
         cur = torch.cuda.current_stream()
         copy_stream.wait_stream(cur)  # the previous step's readers of the inputs are done
         ready = []
         with torch.cuda.stream(copy_stream):
             for g0, g1 in groups:
-                for r in range(R):
-                    inbufs[r][g0:g1].copy_(hin[r][g0:g1], non_blocking=True)
+                if variant != "nocopy":
+                    for r in range(R):
+                        inbufs[r][g0:g1].copy_(hin[r][g0:g1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
                 ready.append(ev)
+        tB = time.perf_counter()
         gi = 0
         for j in range(L):
             if gi < len(groups) and j == groups[gi][0]:
@@ -675,22 +686,34 @@ def run_ours(a, world: int, rank: int, local: int):
                 gi += 1
             t0 = time.perf_counter()
             prepared[j].run()
-            host_s[0] += time.perf_counter() - t0
+            dt = time.perf_counter() - t0
+            host_s[0] += dt
             n_calls[0] += 1
-        for r in range(R):
-            hout[r].copy_(outs[r][L - 1], non_blocking=True)
-        if slots:  # commit: rows + positions advance for the next step
+            host_role[int(roles[j])] += dt
+        tC = time.perf_counter()
+        if variant != "nod2h":
             for r in range(R):
-                TR.commit_accepted(cfg, caches[r], [batches[r][j].tree_k for j in range(L)],
-                                   [batches[r][j].tree_v for j in range(L)], slots, pes[r], cur)
-                new_pos = np.array([caches[r][0].rows - 1 + i for i in range(nq)], np.int64)
-                for j in range(L):
-                    batches[r][j].pos = new_pos
+                hout[r].copy_(outs[r][L - 1], non_blocking=True)
+        tD = time.perf_counter()
+        for r, pc in enumerate(commits if variant != "nocommit" else []):  # commit: rows + positions advance
+            pc.run(cur)
+            new_pos = np.array([caches[r][0].rows - 1 + i for i in range(nq)], np.int64)
+            for j in range(L):
+                batches[r][j].pos = new_pos
+        tE = time.perf_counter()
+        host_parts["copies"] += tB - tA
+        host_parts["verify_calls"] += tC - tB
+        host_parts["readback"] += tD - tC
+        host_parts["commit"] += tE - tD
 
     for _ in range(max(3, a.warmup)):
         e2e_step()
     barrier()
     host_s[0], n_calls[0] = 0.0, 0
+    for k in host_parts:
+        host_parts[k] = 0.0
+    for k in host_role:
+        host_role[k] = 0.0
     t0w = time.perf_counter()
     ev0.record(stream)
     for _ in range(a.steps):
@@ -725,6 +748,10 @@ def run_ours(a, world: int, rank: int, local: int):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "advancing": True, "ms_per_step": e2e_ms,
                 "host_us_per_call": host_us, "accepted_rows_per_step": len(slots),
+                "host_us_per_step": {k: v / a.steps * 1e6 for k, v in host_parts.items()},
+                "host_us_per_call_by_role": {
+                    "refresh": host_role[int(V.ROLE_REFRESH)] / max(1, a.steps * n_refresh) * 1e6,
+                    "reuse": host_role[int(V.ROLE_REUSE)] / max(1, a.steps * (L - n_refresh)) * 1e6},
                 "what": "eager C-ABI calls per layer with each step's positions/rows, pinned "
                         "host->device inputs, accepted-row commit + compressed append, "
                         "last layer's output device->host"},
@@ -751,6 +778,7 @@ def run_ours(a, world: int, rank: int, local: int):
             "step_frac_of_peak": step_bytes / (ms_rank * 1e-3) / 1e9 / peak,
             "unique_selected_blocks_per_layer": float(np.mean(uniq)),
             "refresh_layers": n_refresh, "reuse_layers": L - n_refresh,
+            "route_exact_rescorings": ws.route_fallbacks(),
             "requests_this_rank": R, "graph": graph is not None,
             "shards_rank0": [(s.request, s.head_begin, s.head_count) for s in shards],
         },

@@ -393,10 +393,7 @@ void run_route_batched(const specsv_nsa_config& c, const specsv_layer_kv* kvs,
 // the routing kernel of a call: route3_kernel (integer tensor pipe, certified
 // Top-n) whenever the cache carries digit planes; route_fused_kernel (fp64
 // DMMA over ck) otherwise or with SPECSV_ROUTE_LEGACY=1
-bool use_route3(const specsv_layer_kv& kv) {
-  const char* e = std::getenv("SPECSV_ROUTE_LEGACY");
-  return kv.ckd != nullptr && (e == nullptr || e[0] != '1');
-}
+bool use_route3(const specsv_layer_kv& kv) { return kv.ckd != nullptr && !debug_env().route_legacy; }
 
 // one request's route3 parameters; `base` is its routing region (E_off-relative
 // offsets of the layout apply); `spread`: ranges per (chunk, KV head) may grow
@@ -463,10 +460,8 @@ void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, R
   int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.r3cnt_off);
   P.exit_cnt = cnt;
   P.fallbacks = cnt + 4;
-  const char* fe = std::getenv("SPECSV_ROUTE3_FORCE_EXACT");  // tests: the exact re-scoring path
-  P.force_exact = (fe != nullptr && fe[0] == '1') ? 1 : 0;
-  const char* dbg = std::getenv("SPECSV_ROUTE3_DEBUG");
-  P.debug = dbg != nullptr ? std::atoi(dbg) : 0;
+  P.force_exact = debug_env().force_exact ? 1 : 0;  // tests: the exact re-scoring path
+  P.debug = debug_env().route3_debug;
   P.trace = g_trace;
   if (c.d_head != kR3Tile) throw Error(SPECSV_EUNSUPPORTED, "route3: d_head must be 128");
 }
@@ -508,9 +503,6 @@ void fill_attend_params(AttendParams& p, const specsv_nsa_config& c, const specs
   encode_rows_map(&p.tm_tk, gamma > 0 ? a.tree_k : kv.k, std::max(gamma, 1), H, dh);
   encode_rows_map(&p.tm_tv, gamma > 0 ? a.tree_v : kv.v, std::max(gamma, 1), H, dh);
   p.k_raw = static_cast<const uint16_t*>(kv.k);
-  p.v_raw = static_cast<const uint16_t*>(kv.v);
-  p.ck_raw = static_cast<const uint16_t*>(kv.ck16);
-  p.cv_raw = static_cast<const uint16_t*>(kv.cv);
   p.q = a.q;
   p.gates = a.gates;
   p.out = a.out;
@@ -518,8 +510,7 @@ void fill_attend_params(AttendParams& p, const specsv_nsa_config& c, const specs
   p.idx_count = a.idx_count;
   p.trace = g_trace;
   p.idx_early = a.role == SPECSV_ROLE_REUSE ? 1 : 0;
-  p.debug_flags = std::getenv("SPECSV_ATTEND_FORCE_ROBUST") != nullptr ? 1 : 0;
-  if (const char* e = std::getenv("SPECSV_ATTEND_DEBUG")) p.debug_flags |= std::atoi(e);  // timing experiments
+  p.debug_flags = (debug_env().force_robust ? 1 : 0) | debug_env().attend_debug;  // tests / timing experiments
   const int qc = qc_size_for(c);
   const int nchunks = (a.n_queries + qc - 1) / qc;
   p.nq = a.n_queries;

@@ -34,10 +34,12 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
 #include "attend.h"
+#include "policy.h"
 #include "sm100.cuh"
 
 namespace specsv_b200 {
@@ -929,34 +931,12 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       named_bar_sync(kBarPassEnd, kThreads);
     }
   } else {
-    // =================== union warp: block union, then L2 prefetch ===================
-    // L2 prefetch of this CTA's tiles beyond the two smem stages (LSU
-    // prefetches: they do not occupy the TMA unit the stage loads use)
-    auto prefetch_tile = [&](int t) {
-      const uint16_t *bk, *bv;
-      int r0, r1, lim;
-      if (t < n_cmp) {
-        bk = p.ck_raw; bv = p.cv_raw; r0 = t * kTile; r1 = r0 + 64; lim = p.blocks - 1;
-      } else {
-        const int u0 = 2 * (t - n_cmp);
-        bk = p.k_raw; bv = p.v_raw; lim = p.rows - 1;
-        r0 = m.union_blk[u0] * p.l_sel;
-        r1 = (u0 + 1 < m.n_union ? m.union_blk[u0 + 1] : m.union_blk[u0]) * p.l_sel;
-      }
-#pragma unroll 4
-      for (int i = lane; i < 256; i += 32) {  // 128 rows x 2 lines of 128 B, K and V
-        const int rr = i >> 1;
-        const int r = min(rr < 64 ? r0 + rr : r1 + rr - 64, lim);
-        const int64_t off = ((int64_t)r * p.Hkv + kvh) * kDh + (i & 1) * 64;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(bk + off));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(bv + off));
-      }
-    };
+    // =================== union warp: index rows, then the union (with the softmax warps) ===================
+    // (an L2 prefetch of this CTA's later tiles from here was measured and
+    // removed: with the evict-first stage loads it cost ~4% of the step)
     const UnionArgs ua = union_args(p, q0, nqc, lane);
     const bool early = p.idx_early != 0 && !(p.debug_flags & 8);
-    if (early) stage_index_rows(ua, m, nqc, lane);  // (in flight across the prefetches)
-    if (!(p.debug_flags & 2))  // bit 1 (timing experiments): no L2 prefetch of the compressed tiles
-      for (int j = 2; split + j * S < n_cmp; ++j) prefetch_tile(split + j * S);
+    if (early) stage_index_rows(ua, m, nqc, lane);
     // REFRESH: the index rows come from the routing launch just before this
     // one (programmatic dependent launch: the rest of this CTA -- q, the
     // compressed tiles -- does not wait for it).  REUSE: they were complete
@@ -972,12 +952,6 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
     coop_union(m, kSoftThreads + lane, nqc, ua.n, ua.l_sel, ua.rows, cwlo, cwhi);
     mbar_arrive(&m.union_ready);  // the TMA and MMA warps wait for this
-    const int T = tile_count();
-    const int n_tok_end = n_cmp + m.n_tok_tiles;
-    if (!(p.debug_flags & 4))  // bit 2 (timing experiments): no L2 prefetch of the token tiles
-      for (int j = 2; j < T; ++j)
-        if (split + j * S >= n_cmp && split + j * S < n_tok_end) prefetch_tile(split + j * S);
-    if (trace && lane == 0) p.trace[cta_id * 64 + 60] = globaltimer();
     named_bar_sync(kBarPassEnd, kThreads);
     if (m.flag) {
       named_bar_sync(kBarRedo, kThreads);
@@ -1095,20 +1069,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t attend_smem_bytes() { return kOffMisc + sizeof(Misc) + 1024; }
 
-bool pdl_enabled() {
-  const char* e = std::getenv("SPECSV_NO_PDL");
-  return e == nullptr || e[0] != '1';
-}
+bool pdl_enabled() { return !debug_env().no_pdl; }
 
 size_t attend_workspace_floats(int n_chunks, int hkv, int n_splits) {
   const size_t units = (size_t)n_chunks * hkv * n_splits;
   return units * (3 * kCols * 2) + units * (3 * kCols * kDh);  // split partials (m, l), O
 }
 
+// the dynamic shared-memory opt-in of a kernel, once per device
+template <class K>
+cudaError_t smem_opt_in(K* kernel, size_t bytes, std::atomic<int>* done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& d = done[dev < 64 ? dev : 63];
+  if (d.load(std::memory_order_acquire)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) d.store(1, std::memory_order_release);
+  return e;
+}
+std::atomic<int> g_attend_batch_smem[64], g_attend_smem[64];
+
 cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, int n_heads, bool cooperative,
                                 cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(nsa_attend_batch_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attend_smem_bytes());
+  cudaError_t e = smem_opt_in(nsa_attend_batch_kernel, attend_smem_bytes(), g_attend_batch_smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_splits, n_heads, b.n_req * b.n_chunks);
@@ -1132,8 +1115,7 @@ cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, int n_heads,
 
 cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stream) {
   static_assert(kDh == 128, "d_head");
-  cudaError_t e = cudaFuncSetAttribute(nsa_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)attend_smem_bytes());
+  cudaError_t e = smem_opt_in(nsa_attend_kernel, attend_smem_bytes(), g_attend_smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.n_splits, p.nkvh, n_chunks);
@@ -1148,8 +1130,7 @@ cudaError_t launch_attend(const AttendParams& p, int n_chunks, cudaStream_t stre
   // CTAs retire (a refresh layer's attend streams its compressed tiles under
   // the routing tail), and every CTA still becomes resident because nothing
   // the previous launch waits on depends on this grid.
-  const char* coop_env = std::getenv("SPECSV_ATTEND_COOP");
-  const bool coop = p.n_splits > 1 && (!pdl_enabled() || (coop_env != nullptr && coop_env[0] == '1'));
+  const bool coop = p.n_splits > 1 && (!pdl_enabled() || debug_env().attend_coop);
   if (coop) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na++].val.cooperative = 1;

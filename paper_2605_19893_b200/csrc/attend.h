@@ -19,10 +19,7 @@ struct AttendParams {
   CUtensorMap tm_k, tm_v;    // committed K/V bf16, dims (dh, Hkv, rows)
   CUtensorMap tm_ck, tm_cv;  // compressed K (bf16 copy) / V bf16, dims (dh, Hkv, blocks)
   CUtensorMap tm_tk, tm_tv;  // draft rows bf16, dims (dh, Hkv, max(gamma, 1))
-  const uint16_t* k_raw;     // committed K bf16 (the fast-pass reference key row; L2 prefetch)
-  const uint16_t* v_raw;     // committed V bf16 (L2 prefetch)
-  const uint16_t* ck_raw;    // compressed K bf16 copy (L2 prefetch)
-  const uint16_t* cv_raw;    // compressed V bf16 (L2 prefetch)
+  const uint16_t* k_raw;     // committed K bf16 (the fast-pass reference key row)
   const float* q;            // [nq][Hq][dh]
   const float* gates;        // [nq][Hq][3]
   float* out;                // [nq][Hq][dh]

@@ -9,13 +9,44 @@
 #include "policy.h"
 #include "attend.h"
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 namespace specsv_b200 {
+
+namespace {
+thread_local DebugEnv g_env;
+}  // namespace
+
+const DebugEnv& debug_env() { return g_env; }
+
+void refresh_debug_env() {
+  DebugEnv e;
+  for (char** p = environ; p != nullptr && *p != nullptr; ++p) {
+    const char* v = *p;
+    if (std::strncmp(v, "SPECSV_", 7) != 0) continue;
+    v += 7;
+    const char* eq = std::strchr(v, '=');
+    if (eq == nullptr) continue;
+    const std::string name(v, eq - v);
+    const char* val = eq + 1;
+    const bool one = val[0] == '1';
+    if (name == "ROUTE_LEGACY") e.route_legacy = one;
+    else if (name == "ROUTE3_FORCE_EXACT") e.force_exact = one;
+    else if (name == "ATTEND_FORCE_ROBUST") e.force_robust = true;
+    else if (name == "NO_PDL") e.no_pdl = one;
+    else if (name == "ATTEND_COOP") e.attend_coop = one;
+    else if (name == "ROUTE3_DEBUG") e.route3_debug = std::atoi(val);
+    else if (name == "ATTEND_DEBUG") e.attend_debug = std::atoi(val);
+  }
+  g_env = e;
+}
 
 std::string& last_error() {
   thread_local std::string msg;

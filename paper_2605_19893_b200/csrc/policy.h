@@ -17,10 +17,26 @@ struct Error : std::runtime_error {
 // thread-local message behind specsv_last_error()
 std::string& last_error();
 
+// Diagnostic / test switches (SPECSV_* environment variables), read in one
+// pass over the environment at the start of every C-ABI call (getenv per use
+// cost ~1 us each on the per-call host path).  Thread-local.
+struct DebugEnv {
+  bool route_legacy = false;    // SPECSV_ROUTE_LEGACY=1: fp64-DMMA routing kernel
+  bool force_exact = false;     // SPECSV_ROUTE3_FORCE_EXACT=1: every query through the exact path
+  bool force_robust = false;    // SPECSV_ATTEND_FORCE_ROBUST: the attend robust redo pass
+  bool no_pdl = false;          // SPECSV_NO_PDL=1: no programmatic dependent launch
+  bool attend_coop = false;     // SPECSV_ATTEND_COOP=1: cooperative attend launches under PDL
+  int route3_debug = 0;         // SPECSV_ROUTE3_DEBUG
+  int attend_debug = 0;         // SPECSV_ATTEND_DEBUG
+};
+const DebugEnv& debug_env();
+void refresh_debug_env();
+
 // runs a C-ABI body: exceptions become a status code plus the thread-local message
 template <class F>
 specsv_status guarded(F&& f) {
   try {
+    refresh_debug_env();
     f();
     last_error().clear();
     return SPECSV_OK;

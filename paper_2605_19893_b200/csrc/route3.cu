@@ -955,8 +955,16 @@ cudaError_t launch_route3(Route3Launch& p, cudaStream_t s) {
   }
   const int work = std::max(p.unit_start[p.n_req], p.task_start[p.n_req]);
   const int ctas = std::max(1, std::min(sm_count3(), work));
-  cudaError_t e = cudaFuncSetAttribute(route3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-  if (e != cudaSuccess) return e;
+  static std::atomic<int> done[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& d = done[dev < 64 ? dev : 63];
+  if (!d.load(std::memory_order_acquire)) {  // the shared-memory opt-in, once per device
+    const cudaError_t e = cudaFuncSetAttribute(route3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
+    d.store(1, std::memory_order_release);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(kThreads);

@@ -290,3 +290,38 @@ def commit_accepted(cfg, caches, tree_ks, tree_vs, slots: Sequence[int], pos_emb
     for cache in caches:
         cache.rows += int(s.shape[0])
         cache.blocks = cfg.compressed_block_count(cache.rows)
+
+
+class PreparedCommit:
+    """commit_accepted for a fixed set of caches and draft-row buffers with the
+    ctypes arguments built once: run() refreshes the committed rows and blocks
+    and calls specsv_commit_rows_compress (the form an engine issues every
+    step; same entry point and semantics as commit_accepted)."""
+
+    def __init__(self, cfg, caches, tree_ks, tree_vs, slots: Sequence[int], pos_embed=None):
+        n = len(caches)
+        if not (len(tree_ks) == len(tree_vs) == n):
+            raise ValueError("caches, tree_ks and tree_vs must have the same length")
+        self.cfg, self.caches, self.n = cfg, list(caches), n
+        self.s = np.ascontiguousarray(np.asarray(slots, np.int32))
+        self.kvs = (abi.LayerKvC * max(n, 1))(*[c.c() for c in caches])
+        self.tk = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in tree_ks])
+        self.tv = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in tree_vs])
+        pes = list(pos_embed) if isinstance(pos_embed, (list, tuple)) else [pos_embed] * n
+        self.pe = (C.c_void_p * max(n, 1))(*[None if x is None else x.data_ptr() for x in pes])
+        self.cfgc = cfg.c()
+        self.fn = _lib().specsv_commit_rows_compress
+
+    def run(self, stream=None) -> None:
+        from .verify import _stream  # noqa: PLC0415
+        k = int(self.s.shape[0])
+        for i, c in enumerate(self.caches):
+            if c.rows + k > c.capacity:
+                raise SpecsvError(abi.EINVAL, "commit exceeds the cache capacity")
+            self.kvs[i].rows = c.rows
+            self.kvs[i].blocks = c.blocks
+        check(self.fn(C.byref(self.cfgc), self.kvs, self.tk, self.tv, self.n, _p(self.s, C.c_int32), k,
+                      self.pe, _stream(stream)))
+        for c in self.caches:
+            c.rows += k
+            c.blocks = self.cfg.compressed_block_count(c.rows)

@@ -117,11 +117,28 @@ def main():
         end = t[:, 4].max()
         line += (f" | attend start {(t0 - t_first) / 1e3:8.2f} gap {gap:5.2f} spread {(t[:, 0].max() - t0) / 1e3:4.2f}"
                  f" idx in {ph(59)[0]:5.2f}/{ph(59)[1]:5.2f}"
-                 f" union {ph(1)[0]:5.2f} loop {ph(2)[0]:5.2f}/{ph(2)[1]:5.2f} part {ph(3)[0]:5.2f}/{ph(3)[1]:5.2f}"
+                 f" union {ph(1)[0]:5.2f} loop {ph(2)[0]:5.2f}/{ph(2)[1]:5.2f} pv {ph(7)[0]:5.2f}/{ph(7)[1]:5.2f} part {ph(3)[0]:5.2f}/{ph(3)[1]:5.2f}"
                  f" bar {ph(6)[0]:5.2f} merge {ph(4)[0]:5.2f}/{ph(4)[1]:5.2f} ctas {len(t)}")
         prev_end = end
         print(line)
+        if os.environ.get("TRACE_SPLITS"):
+            print("   split: loop end / partials written (median over heads): " +
+                  " ".join(f"{sp}:{a:.1f}/{b:.1f}" for sp, a, b in per_split(bufs[j])))
+
+
+def per_split(buf, S=18):
+    """loop-end time per split index (median over KV heads) of one attend trace buffer"""
+    t = buf[:RBASE].view(-1, 64).cpu().numpy()
+    n = (t[:, 0] > 0).sum()
+    t = t[:n]
+    t0 = t[:, 0].min()
+    rows = []
+    for s in range(S):
+        sel = t[s::S]
+        rows.append((s, np.median((sel[:, 2] - t0) / 1e3), np.median((sel[:, 3] - t0) / 1e3)))
+    return rows
 
 
 if __name__ == "__main__":
     main()
+
