@@ -632,9 +632,25 @@ def run_ours(a, world: int, rank: int, local: int):
     # step's positions and rows (eager: host work in the timed region), commits
     # `accept` draft rows + the next root into every layer (the context grows)
     # and reads the last layer's output back
-    hin = [t.cpu().pin_memory() for t in inbufs]
+    # every step verifies new draft queries: a ring of input sets (q, gates, draft
+    # rows), each copied host->device by the step that uses it
+    ring = 4
+    hin_ring = []
+    for k in range(ring):
+        if k > 0:
+            gen.manual_seed(sharding.request_seed(shards[0].request) + 7919 * k)
+            for r in range(R):  # the same distributions as the first set
+                for j in range(L):
+                    b = batches[r][j]
+                    b.q.copy_(urand(*b.q.shape))
+                    b.gates.copy_(torch.rand(*b.gates.shape, generator=gen, device=dev) * 0.6 + 0.2)
+                    b.tree_k.copy_(urand(*b.tree_k.shape, dtype=torch.bfloat16))
+                    b.tree_v.copy_(urand(*b.tree_v.shape, dtype=torch.bfloat16))
+        hin_ring.append([t.cpu().pin_memory() for t in inbufs])
+    hin = hin_ring[0]
+    step_no = [0]
     hout = [torch.empty(nq, Hq, dh, pin_memory=True) for _ in range(R)]
-    h2d = sum(t.numel() * t.element_size() for t in hin)
+    h2d = sum(t.numel() * t.element_size() for t in hin_ring[0])
     d2h = sum(t.numel() * t.element_size() for t in hout)
     acc = max(0, min(a.accept, g))
     slots = list(range(acc)) + ([acc] if acc < g else [])  # accepted drafts, then the bonus root's row
@@ -667,6 +683,8 @@ def run_ours(a, world: int, rank: int, local: int):
 
     def e2e_step():
         tA = time.perf_counter()
+        hin = hin_ring[step_no[0] % ring]
+        step_no[0] += 1
         cur = torch.cuda.current_stream()
         copy_stream.wait_stream(cur)  # the previous step's readers of the inputs are done
         ready = []

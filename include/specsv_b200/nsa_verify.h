@@ -94,8 +94,10 @@ typedef struct specsv_layer_kv {
                            in [-128, 127].  Written by specsv_compress_append next to ck;
                            the integer tensor-pipe routing kernel streams these planes
                            (NULL selects the fp64 routing kernel over ck) */
-  int32_t* ckexp;       /* device [>= blocks][Hkv]: e with max_x |ck[x]| < 2^e (0 for an
-                           all-zero row); NULL iff ckd is NULL */
+  int32_t* ckexp;       /* device [>= blocks][Hkv]: bits 0-15 (signed) e with max_x |ck[x]| <
+                           2^e (0 for an all-zero row), bits 16-23 how many of the row's
+                           elements the 2^(e-30) grid rounds (the routing error bound);
+                           NULL iff ckd is NULL */
 } specsv_layer_kv;
 
 /* One verify call: one layer x one request, root + gamma draft queries in

@@ -129,7 +129,7 @@ struct Layout {
   int max_chunks = 1;                   // query chunks of the widest call (kMaxQueries)
   size_t r3cnt_off = 0;                 // route3 words: [0] exit count, [4] fallbacks, then one
                                         // counter set per request of a launch (fixed position)
-  size_t r3_den_off = 0, r3_spill_off = 0, r3_contrib_off = 0;  // route3 regions (per request)
+  size_t r3_den_off = 0, r3_spill_off = 0, r3_contrib_off = 0, r3_exact_off = 0;  // route3 regions (per request)
   size_t attend_off = 0, attend_bytes = 0;
   size_t E_off = 0, TM_off = 0, TD_off = 0, F_off = 0, sel_off = 0, cnt_off = 0;
   int64_t sel_pad = 0;
@@ -214,6 +214,8 @@ Layout layout_for(const specsv_nsa_config& c, int32_t nq, int64_t max_rows) {
     off = align_up(off + (size_t)(chunks * c.n_kv_heads * nranges * (kR3Rows + 1) * kR3MaxSpr * 8), 256);
     L.r3_contrib_off = off;
     off = align_up(off + (size_t)(nq * L.sel_pad * 8), 256);
+    L.r3_exact_off = off;  // the exact path's scratch, one slot at a time
+    off = align_up(off + (size_t)c.n_q_heads * std::max<int64_t>(maxblk, 1) * 8, 256);
   }
   L.total = off;
   return L;
@@ -442,6 +444,7 @@ void make_route3_req(const specsv_nsa_config& c, const specsv_layer_kv& kv, cons
   R.den = reinterpret_cast<double*>(base + (L.r3_den_off - rel));
   R.gspill = reinterpret_cast<double*>(base + (L.r3_spill_off - rel));
   R.contrib = reinterpret_cast<double*>(base + (L.r3_contrib_off - rel));
+  R.exact = reinterpret_cast<double*>(base + (L.r3_exact_off - rel));
 }
 
 void fill_route3_common(const specsv_nsa_config& c, const Layout& L, char* ws, Route3Launch& P) {

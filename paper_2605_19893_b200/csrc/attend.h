@@ -131,7 +131,7 @@ constexpr int kR3MaxBlk = 256;   // compressed blocks per unit (two tiles)
 constexpr int kR3MaxSpr = 64;    // selection blocks per unit
 constexpr int kR3MaxBps = 16;    // compressed blocks overlapping one selection block (host-checked)
 constexpr int kR3Batch = 16;     // requests per launch
-constexpr int kR3CntPerReq = 448;  // counter words per request (den arrivals, top arrivals, expo)
+constexpr int kR3CntPerReq = 512;  // counter words per request (den arrivals, top arrivals, bounds, lock)
 struct Route3Req {
   CUtensorMap tm_ckd;    // int8 digit planes, dims (dh, 4, Hkv, blocks), box 128 x 1 x 1 x 128, SW128
   const int32_t* ckexp;  // [blocks][Hkv] row exponents of the digit planes
@@ -142,6 +142,7 @@ struct Route3Req {
   uint32_t* idx_forced;  // [nq]
   double* den;           // [nchunks][Hkv][nranges][kR3Rows] per-range denominators (token-weighted)
   double* gspill;        // [units][kR3MaxSpr][kR3Rows + 1] selection-block sums of a CTA's earlier units
+  double* exact;         // [Hq][blocks] the exact path's logits / e values (scratch, one slot at a time)
   double* contrib;       // [nr][sel_pad] selection scores x Hq (the KV heads' shares, fp64 atomics;
                          // zero between launches)
   int32_t* cnt;          // [kR3CntPerReq] this request's counter set (zero-initialised, self-resetting)

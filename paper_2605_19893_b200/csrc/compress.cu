@@ -41,28 +41,38 @@ __device__ __forceinline__ uint32_t digits4(float x, int e) {
   return (static_cast<uint32_t>(X) + 0x80808080u) ^ 0x80808080u;
 }
 
-// the digit planes of one (block, head) row: fk[r] is element threadIdx.x + r blockDim
+// the digit planes of one (block, head) row: fk[r] is element threadIdx.x + r blockDim.
+// ckexp packs the row exponent e (low 16 bits, signed) and, in bits 16..23, how many
+// elements the 31-bit grid rounds (the others it represents exactly: the routing
+// kernel's error bound counts only the rounded ones)
 template <int kPer>
 __device__ void write_digit_row(const float (&fk)[kPer], int dh, int8_t* ckd, int32_t* ckexp,
                                 int64_t row) {
   __shared__ float red[32];
+  __shared__ int inexact;
   float a = 0.f;
 #pragma unroll
   for (int r = 0; r < kPer; ++r)
     if (threadIdx.x + r * blockDim.x < dh) a = fmaxf(a, fabsf(fk[r]));
-  const float mx = row_absmax(a, red);
+  if (threadIdx.x == 0) inexact = 0;
+  const float mx = row_absmax(a, red);  // (its barriers order the reset)
   int e = 0;
   if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
   int8_t* dst = ckd + row * 4 * dh;
+  int cnt = 0;
 #pragma unroll
   for (int r = 0; r < kPer; ++r) {
     const int x = threadIdx.x + r * blockDim.x;
     if (x >= dh) break;
+    const float sx = ldexpf(fk[r], 30 - e);
+    cnt += (float)__float2int_rn(sx) != sx ? 1 : 0;
     const uint32_t w = digits4(fk[r], e);
 #pragma unroll
     for (int s = 0; s < 4; ++s) dst[s * dh + x] = static_cast<int8_t>((w >> (8 * s)) & 0xFFu);
   }
-  if (threadIdx.x == 0) ckexp[row] = e;
+  if (cnt) atomicAdd(&inexact, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) ckexp[row] = (e & 0xFFFF) | (min(inexact, 255) << 16);
 }
 
 __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,

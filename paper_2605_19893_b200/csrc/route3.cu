@@ -70,16 +70,21 @@ constexpr int kAcc = 5;       // digit-pair weight classes 256^2 .. 256^6
 constexpr int kWarpMma = 12;
 constexpr uint32_t kTmemCols = 512;  // 2 tiles x 5 classes x 48 columns
 constexpr int kTopnGroups = kThreads / 4;
+constexpr uint32_t kExStage = 32768;  // exact path: bytes per key stage (whole blocks, all KV heads)
+constexpr int kMaxHq = 128;           // q heads (build limit)
+constexpr uint32_t kExQOff = 3 * kExStage;  // exact path: fp64 q of every head, after three stages
+constexpr int kExQS = kDh + 4;               // its row stride in doubles (KV heads' rows on other banks)
 static_assert(kN == 4 * 12, "epilogue: 4 TMEM lane quadrants x 4 column groups of 12 (16 warps)");
 static_assert(kR3MaxSpr == 64, "two selection blocks per lane in the row sums");
 
 // counter words of one request (Route3Req::cnt)
 constexpr int kCntDen = 0;     // [nchunks x Hkv] arrivals of a (chunk, KV head)'s ranges
 constexpr int kCntTop = 272;   // [nchunks] arrivals of a chunk's units after their shares
-constexpr int kCntExpo = 352;  // [nr] max (qe + ke) + kExpoBias per slot (kExpoFlag: exact path)
-static_assert(kCntExpo + kMaxQueries <= kR3CntPerReq, "counter set");
-constexpr int kExpoBias = 4096;
-constexpr int kExpoFlag = 1 << 24;
+constexpr int kCntBound = 352;  // [nr] 64-bit: the slot's logit error bound (log2 units, fp64 bits;
+                                //      +inf: exact path), max over its rows and units
+constexpr int kCntLock = 496;   // the exact path's scratch lock
+static_assert(kCntBound + 2 * kMaxQueries <= kCntLock && kCntLock < kR3CntPerReq, "counter set");
+constexpr unsigned long long kBoundFlag = 0x7FF0000000000000ULL;  // +inf
 
 // shared memory map (bytes from the 1024-aligned base)
 constexpr uint32_t kPlaneBytes = kTB * 128;                // one digit plane of one tile (SW128)
@@ -96,10 +101,11 @@ static_assert(kQsSlice % 1024 == 0, "SW128 atoms");
 static_assert((size_t)kMaxAvail * 12 + 4 * kDh * 8 + 66 * 4 <= 2 * kTileBytes, "Top-n arrays alias the planes");
 
 struct Misc {
-  uint64_t tma_full[2], mma_done[2];
+  uint64_t tma_full[2], mma_done[2], ex_full[3];
   uint32_t tmem_base;
-  int32_t flag, kemax;
+  int32_t flag, kemax, nkmax;
   int32_t qexp[kN];
+  int32_t qinex[kN];    // q elements the grid rounds, per row
   int32_t colmvis[kN];  // visible compressed blocks of the column's slot (0: no column)
   double qsc[kN];       // c_sl 2^(qe - 44): logit (log2 units) per unit of h 2^ke
   double invD[kN];
@@ -145,27 +151,6 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   r = fma(n, -1.90821492927058770002e-10, r);
   double p = 2.08767569878680989792e-09;
   p = fma(p, r, 2.50521083854417187751e-08);
-  p = fma(p, r, 2.75573192239858906526e-07);
-  p = fma(p, r, 2.75573192239858906526e-06);
-  p = fma(p, r, 2.48015873015873015873e-05);
-  p = fma(p, r, 1.98412698412698412698e-04);
-  p = fma(p, r, 1.38888888888888888889e-03);
-  p = fma(p, r, 8.33333333333333333333e-03);
-  p = fma(p, r, 4.16666666666666666667e-02);
-  p = fma(p, r, 1.66666666666666666667e-01);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  return __hiloint2double(__double2hiint(p) + (static_cast<int>(n) << 20), __double2loint(p));
-}
-
-// 2^x for x <= 0 (x in log2 units), ~2 ulp: x = n + f, f in [-1/2, 1/2],
-// 2^f = e^(f ln2) by Taylor to degree 11 (|f ln2| <= 0.347: < 1e-17)
-__device__ __forceinline__ double exp2_nonpos(double x) {
-  if (!(x >= -1020.0)) return 0.0;
-  const double n = rint(x);
-  const double r = (x - n) * 6.93147180559945309417e-01;
-  double p = 2.50521083854417187751e-08;
   p = fma(p, r, 2.75573192239858906526e-07);
   p = fma(p, r, 2.75573192239858906526e-06);
   p = fma(p, r, 2.48015873015873015873e-05);
@@ -323,7 +308,19 @@ __device__ __forceinline__ void digit_q(const Route3Launch& P, const Route3Req& 
     int e = 0;
     if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
     write_digit_row(smem + kOffQs, kQsSlice, j, lane, v[z], e);
+    int inex = 0;  // elements the 31-bit grid rounds (the rest it represents exactly)
+    {
+      const float xs[4] = {v[z].x, v[z].y, v[z].z, v[z].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float sx = ldexpf(xs[c], 30 - e);
+        inex += (float)__float2int_rn(sx) != sx ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) inex += __shfl_xor_sync(0xffffffffu, inex, o);
     if (lane == 0) {
+      m.qinex[j] = inex;
       m.qexp[j] = e;
       m.qsc[j] = P.c_sl * pow2i(e - 44);
       m.colmvis[j] = j < U.nrows ? R.slot_mvis[U.s0 + j / P.G] : 0;
@@ -489,104 +486,136 @@ __device__ void write_row(const Misc& cm, Misc& m, int avail, int n, int32_t* id
 
 // ------------------------------------------------------------------ exact path
 // fp64 scores of one slot, the reference's arithmetic (nsa_attention.cpp:38-80)
-// regrouped: per KV head, up to four of its q heads at a time, a pass for the
-// softmax maximum and denominator, then per selection block the overlapping
-// blocks' probabilities.  One CTA; only for queries the certified path cannot
-// decide (or forced by tests).
-__device__ void exact_scores(const Route3Launch& P, const Route3Req& R, int slot, double* sel,
-                             double* qrows, Misc& m) {
+// regrouped, for queries the certified path cannot decide (or forced by
+// tests).  One CTA: (1) every visible block's logit for every q head (fp32
+// operands, fp64 products and sums) from the compressed keys streamed as
+// contiguous 32 KB chunks (all KV heads of whole blocks) by bulk copies
+// through kExStages shared-memory stages, stored once to the request's scratch
+// [Hq][blocks] in L2, per-head running maxima; (2) e = exp(logit - max) stored
+// back, denominators in a fixed order; (3) per selection block the overlapping
+// blocks' probabilities.  The scratch is one per request: slots that fall
+// back take it in turn (a spin lock; the path is rare).
+constexpr int kExStages = 3;
+__device__ __forceinline__ uint32_t ex_stage_off(int s) { return (uint32_t)s * kExStage; }  // over the idle sel/surv arrays
+
+__device__ void exact_scores(const Route3Launch& P, const Route3Req& R, int slot, double* sel, uint8_t* smem,
+                             Misc& m, int& ex_seq) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qi = R.slot_q[slot], mv = R.slot_mvis[slot], avail = R.slot_avail[slot];
-  const int G = P.G, Hkv = P.Hkv;
-  const double inv = 1.0 / ((double)P.Hq * (double)P.l);
-  for (int b = tid; b < avail; b += kThreads) sel[b] = 0.0;
-  for (int kvh = 0; kvh < Hkv; ++kvh) {
-    for (int g0 = 0; g0 < G; g0 += 4) {
-      const int ng = min(4, G - g0);
-      __syncthreads();
-      for (int e = tid; e < ng * kDh; e += kThreads)
-        qrows[e] = (double)R.q[((int64_t)qi * P.Hq + kvh * G + g0 + e / kDh) * kDh + e % kDh];
-      __syncthreads();
-      auto logits = [&](int i, double (&l)[4]) {
-        const float4* kr = reinterpret_cast<const float4*>(R.ck + ((int64_t)i * Hkv + kvh) * kDh);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int x4 = 0; x4 < kDh / 4; ++x4) {
-          const float4 k4 = __ldg(kr + x4);
-          const double kx[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int gg = 0; gg < 4; ++gg)
-              if (gg < ng) acc[gg] = fma(qrows[gg * kDh + 4 * x4 + c], kx[c], acc[gg]);
-        }
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg) l[gg] = acc[gg] * P.scale;
-      };
-      double mx[4], sm[4];
-#pragma unroll
-      for (int gg = 0; gg < 4; ++gg) {
-        mx[gg] = -INFINITY;
-        sm[gg] = 0.0;
-      }
-      for (int i = tid; i < mv; i += kThreads) {  // pass 1: running (max, sum) per head
-        double l[4];
-        logits(i, l);
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-          if (l[gg] > mx[gg]) {
-            sm[gg] = sm[gg] * exp_nonpos(mx[gg] - l[gg]) + 1.0;
-            mx[gg] = l[gg];
-          } else {
-            sm[gg] += exp_nonpos(l[gg] - mx[gg]);
-          }
-        }
-      }
-#pragma unroll
-      for (int gg = 0; gg < 4; ++gg) {  // fixed-order reduction: xor tree, then warps in order
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          const double om = __shfl_xor_sync(0xffffffffu, mx[gg], o);
-          const double os = __shfl_xor_sync(0xffffffffu, sm[gg], o);
-          const double M = fmax(mx[gg], om);
-          sm[gg] = (M == -INFINITY) ? 0.0 : sm[gg] * exp_nonpos(mx[gg] - M) + os * exp_nonpos(om - M);
-          mx[gg] = M;
-        }
-        if (lane == 0) {
-          m.red_m[warp][gg] = mx[gg];
-          m.red_s[warp][gg] = sm[gg];
-        }
-      }
-      __syncthreads();
-      if (tid < 4) {
-        double M = -INFINITY, S = 0.0;
-        for (int w = 0; w < kWarps; ++w) {
-          const double wm = m.red_m[w][tid], ws = m.red_s[w][tid];
-          const double nm = fmax(M, wm);
-          S = (nm == -INFINITY) ? 0.0 : S * exp_nonpos(M - nm) + ws * exp_nonpos(wm - nm);
-          M = nm;
-        }
-        m.fin_m[tid] = M;
-        m.fin_s[tid] = S;
-      }
-      __syncthreads();
-      for (int b = tid; b < avail; b += kThreads) {  // pass 2: per selection block
-        int lo, hi;
-        blocks_of(b, P.d, P.l, P.l_sel, lo, hi);
-        hi = min(hi, mv - 1);
-        double s = 0.0;
-        for (int i = lo; i <= hi; ++i) {
-          double l[4];
-          logits(i, l);
-          const double w = (double)overlap(i, b, P.d, P.l, P.l_sel);
-#pragma unroll
-          for (int gg = 0; gg < 4; ++gg)
-            if (gg < ng && m.fin_s[gg] > 0.0) s += exp_nonpos(l[gg] - m.fin_m[gg]) / m.fin_s[gg] * w;
-        }
-        sel[b] += s * inv;
-      }
-    }
+  const int Hq = P.Hq, Hkv = P.Hkv, G = P.G;
+  const double inv = 1.0 / ((double)Hq * (double)P.l);
+  const int bpc = max(1, (int)(kExStage / ((uint32_t)Hkv * kDh * 4)));  // blocks per chunk
+  const int nch = (mv + bpc - 1) / bpc;
+  double* q64 = reinterpret_cast<double*>(smem + kExQOff);  // [Hq][kExQS] fp64 (exact copies)
+  double* Lg = R.exact;                                      // [Hq][blocks]
+  if (tid == 0) {  // the request's scratch, one fallback at a time
+    while (atomicCAS(&R.cnt[kCntLock], 0, 1) != 0) __nanosleep(1000);
+    __threadfence();
   }
   __syncthreads();
+  stamp(P, 9);
+  auto issue = [&](int c) {  // chunk c -> stage (ex_seq + c) % kExStages
+    const int sq = ex_seq + c, st = sq % kExStages;
+    const int i0 = c * bpc, nb = min(bpc, mv - i0);
+    const uint32_t bytes = (uint32_t)nb * Hkv * kDh * 4;
+    mbar_expect_tx(&m.ex_full[st], bytes);
+    bulk_g2s(smem + ex_stage_off(st), R.ck + (int64_t)i0 * Hkv * kDh, bytes, &m.ex_full[st]);
+  };
+  // KV-head groups whose q heads (<= 64) fit the fp64 q rows; the keys stream once per group
+  const int kvg = max(1, 64 / G);
+  for (int kv0 = 0; kv0 < Hkv; kv0 += kvg) {
+    const int kv1 = min(Hkv, kv0 + kvg);
+    __syncthreads();  // the previous group's q rows and stages are consumed
+    for (int e = tid; e < (kv1 - kv0) * G * kDh; e += kThreads)
+      q64[(e / kDh) * kExQS + e % kDh] = (double)R.q[((int64_t)qi * Hq + kv0 * G) * kDh + e];
+    if (tid == 0)
+      for (int c = 0; c < min(kExStages, nch); ++c) issue(c);
+    __syncthreads();  // q visible
+    // ---- pass 1: item = (block of the chunk, KV head, 8-way dims part): each key element
+    // is converted to fp64 once and meets the G q heads of its KV head; the 8 parts of a
+    // (block, KV head) are 8 consecutive lanes (fixed-order shuffle sum)
+    const int part = tid & 7;
+    const int nkv = kv1 - kv0;
+    for (int c = 0; c < nch; ++c) {
+      const int sq = ex_seq + c, st = sq % kExStages;
+      mbar_wait(&m.ex_full[st], (sq / kExStages) & 1);
+      const float* kst = reinterpret_cast<const float*>(smem + ex_stage_off(st));
+      const int i0 = c * bpc, nb = min(bpc, mv - i0);
+      for (int item = tid >> 3; item < nb * nkv; item += kThreads / 8) {
+        const int it = item / nkv, kvl = item % nkv, kvh = kv0 + kvl;
+        // dims part + 8 x: the 8 parts read consecutive words (no bank conflicts)
+        const float* kr = kst + ((int64_t)it * Hkv + kvh) * kDh + part;
+        double kx[16];
+#pragma unroll
+        for (int x = 0; x < 16; ++x) kx[x] = (double)kr[8 * x];
+        for (int g0 = 0; g0 < G; g0 += 4) {
+          double acc[4];
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) {
+            acc[gg] = 0.0;
+            if (g0 + gg < G) {
+              const double* qr = q64 + (kvl * G + g0 + gg) * kExQS + part;
+#pragma unroll
+              for (int x = 0; x < 16; ++x) acc[gg] = fma(qr[8 * x], kx[x], acc[gg]);
+            }
+          }
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg)
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) acc[gg] += __shfl_xor_sync(0xffffffffu, acc[gg], o);
+          if (part == 0)
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg)
+              if (g0 + gg < G) Lg[(int64_t)(kvh * G + g0 + gg) * R.blocks + i0 + it] = acc[gg] * P.scale;
+        }
+      }
+      __syncthreads();  // the stage is consumed
+      if (tid == 0 && c + kExStages < nch) issue(c + kExStages);
+    }
+    ex_seq += nch;
+  }
+  double* Mh = reinterpret_cast<double*>(smem + kExQOff);  // q no longer needed: [kMaxHq] den
+  __syncthreads();
+  stamp(P, 10);
+  // ---- pass 2 (warp w: heads w, w + 16, ..): the head's maximum, then e = exp(logit - max)
+  // stored back and the denominator (lanes, then the warp tree: a fixed order)
+  for (int h = warp; h < Hq; h += kWarps) {
+    double* lh = Lg + (int64_t)h * R.blocks;
+    double M = -INFINITY;
+    for (int i = lane; i < mv; i += 32) M = fmax(M, __ldcg(lh + i));
+    M = warp_max_d(M);
+    double sm = 0.0;
+    for (int i = lane; i < mv; i += 32) {
+      const double e = exp_nonpos(__ldcg(lh + i) - M);
+      lh[i] = e;
+      sm += e;
+    }
+    sm = warp_sum_d(sm);
+    if (lane == 0) Mh[kMaxHq + h] = sm;
+  }
+  __syncthreads();
+  stamp(P, 11);
+  // ---- pass 3: per selection block
+  for (int b = tid; b < avail; b += kThreads) {
+    int lo, hi;
+    blocks_of(b, P.d, P.l, P.l_sel, lo, hi);
+    hi = min(hi, mv - 1);
+    double acc = 0.0;
+    for (int h = 0; h < Hq; ++h) {
+      const double D = Mh[kMaxHq + h];
+      if (!(D > 0.0)) continue;
+      double sh = 0.0;
+      for (int i = lo; i <= hi; ++i)
+        sh += __ldcg(Lg + (int64_t)h * R.blocks + i) * (double)overlap(i, b, P.d, P.l, P.l_sel);
+      acc += sh / D;
+    }
+    sel[b] = acc * inv;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicExch(&R.cnt[kCntLock], 0);
+  }
 }
 
 // ------------------------------------------------------------------ kernel
@@ -606,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       mbar_init(&m.tma_full[t], 1);
       mbar_init(&m.mma_done[t], 1);
     }
+    for (int t = 0; t < 3; ++t) mbar_init(&m.ex_full[t], 1);
     fence_mbar_init();
   }
   if (tid < 16) m.T16[tid] = exp2((double)tid * 0.0625);
@@ -640,7 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     load_q(P, R, U, qv);
     static_assert(kR3MaxBlk <= kThreads, "one block exponent per thread");
     const bool has_ke = tid < U.nblk;  // the exponent load is in flight across the setup
-    const int ke = has_ke ? __ldg(R.ckexp + (int64_t)(U.row0 + tid) * P.Hkv + U.kvh) : 0;
+    const int kpack = has_ke ? __ldg(R.ckexp + (int64_t)(U.row0 + tid) * P.Hkv + U.kvh) : 0;
+    const int ke = (int)(int16_t)(kpack & 0xFFFF), knx = (kpack >> 16) & 0xFF;  // exponent, rounded elements
     if (tid == 0) {
       const uint64_t pol = l2_evict_first_policy();  // the digit planes are read once per launch
       for (int t = 0; t < 2; ++t) {
@@ -656,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       }
       m.flag = 0;
       m.kemax = -100000;
+      m.nkmax = 0;
     }
     {  // compressed blocks overlapping each selection block of the range, and their token overlaps
       const int bl = tid & (kR3MaxSpr - 1), kg = tid / kR3MaxSpr;
@@ -671,7 +703,10 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     __syncthreads();  // flag / kemax reset before the block exponents
     if (tid < kR3MaxBlk) {
       m.kexp[tid] = has_ke ? ke : 0;
-      if (has_ke) atomicMax(&m.kemax, ke);
+      if (has_ke) {
+        atomicMax(&m.kemax, ke);
+        if (knx) atomicMax(&m.nkmax, knx);
+      }
     }
     for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) g[e] = 0.0;  // (selection blocks past nsel stay 0)
     fence_proxy_async_smem();  // q digits: generic-proxy writes read by the MMA
@@ -802,8 +837,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
         den[tid] = (v[0] + v[1]) + (v[2] + v[3]);
       }
       if (tid < U.nrows) {
-        const int ex = m.flag ? kExpoFlag : m.qexp[tid] + m.kemax + kExpoBias;
-        atomicMax(&R.cnt[kCntExpo + U.s0 + tid / P.G], ex);
+        // |logit error| <= 2^(eq + ek - 31) (rounded q elements + rounded k elements + 2.01):
+        // grid rounding of the rounded elements only, plus the three dropped low digit
+        // pairs (< 2^(eq + ek - 29.99)); per unit the largest ek and k count, x2 margin
+        const double bnd = m.flag ? __longlong_as_double((long long)kBoundFlag)
+                                  : P.c_sl * pow2i(max(-1000, min(1000, m.qexp[tid] + m.kemax - 30))) *
+                                        ((double)(m.nkmax + m.qinex[tid]) + 2.01);
+        atomicMax(reinterpret_cast<unsigned long long*>(R.cnt + kCntBound) + U.s0 + tid / P.G,
+                  (unsigned long long)__double_as_longlong(bnd));
       }
       if (u + nctas < units) {  // not this CTA's last unit: phase 2 reloads g from L2
         double* sp = R.gspill + (int64_t)U.lu * kR3MaxSpr * kGS;
@@ -844,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       for (int r = 0; r < R.nranges; ++r) D += st[r * kN + tid];
       m.invD[tid] = D > 0.0 ? 1.0 / D : 0.0;
       if (tid < U.nrows && D > 0.0 && D < 0x1p-900)  // e values may have lost bits: exact path
-        atomicMax(&R.cnt[kCntExpo + U.s0 + tid / P.G], kExpoFlag);
+        atomicMax(reinterpret_cast<unsigned long long*>(R.cnt + kCntBound) + U.s0 + tid / P.G, kBoundFlag);
     }
     __syncthreads();
     const int nsel = U.b1 - U.b0;
@@ -873,7 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
   const int tasks = P.task_start[P.n_req];
   double* sel = reinterpret_cast<double*>(smem);                          // [kMaxAvail]
   int* surv = reinterpret_cast<int*>(smem + 8 * kMaxAvail);                // [kMaxAvail]
-  double* qrows = reinterpret_cast<double*>(smem + 12 * kMaxAvail);        // [4][128]
+  int ex_seq = 0;  // exact-path chunks loaded by this CTA so far (the stage barriers' phases)
   for (int t = nctas - 1 - cta; t < tasks; t += nctas) {
     int r = 0;
     while (r + 1 < P.n_req && t >= P.task_start[r + 1]) ++r;
@@ -900,13 +941,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       sel[b] = __ldcg(sc + b) * inv;
       sc[b] = 0.0;
     }
-    const int ex = __ldcg(&R.cnt[kCntExpo + slot]);
+    unsigned long long* bslot = reinterpret_cast<unsigned long long*>(R.cnt + kCntBound) + slot;
+    const unsigned long long bb = __ldcg(bslot);
     __syncthreads();
     stamp(P, 14);
-    if (tid == 0) R.cnt[kCntExpo + slot] = 0;  // every atomicMax of this launch is in
+    if (tid == 0) *bslot = 0ull;  // every atomicMax of this launch is in
     // relative score error <= 2 ln2 delta (+ fp64 exp / summation rounding), with margin
-    const bool flagged = ex >= kExpoFlag;
-    const double delta = flagged ? 0.0 : P.c_sl * pow2i(max(-1000, min(1000, ex - kExpoBias - 22)));
+    const bool flagged = bb >= kBoundFlag;
+    const double delta = flagged ? 0.0 : __longlong_as_double((long long)bb);
     const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-10;
     const long long c0 = clock64();
     select_topn(sel, surv, avail, P.n, eps, m);
@@ -918,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     }
     if (flagged || !m.certified || P.force_exact) {
       if (tid == 0 && P.fallbacks != nullptr) atomicAdd(P.fallbacks, 1);
-      exact_scores(P, R, slot, sel, qrows, m);
+      exact_scores(P, R, slot, sel, smem, m, ex_seq);
       select_topn(sel, surv, avail, P.n, 0.0, m);
     }
     const int q = R.slot_q[slot];

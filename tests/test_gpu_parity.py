@@ -71,21 +71,26 @@ def test_compress_append_bit_exact(oracle_lib):
 
 def test_compress_digit_planes():
     """The routing keys' digit planes (ABI v3) written by the compressed append:
-    per (block, head) row, e is the smallest power of two above max |ck|, and
-    the four signed base-256 digits recombine to round(ck 2^(30 - e))."""
+    per (block, head) row, e is the smallest power of two above max |ck|, the
+    four signed base-256 digits recombine to round(ck 2^(30 - e)), and ckexp
+    also counts the elements that rounding changed."""
     cfg = O.llama_config(4)
     x = LayerInputs(cfg, 3000, 2, 77)
     case = DeviceCase(cfg, x)
     c = case.cache
     nb = c.blocks
     ck = c.ck[:nb].cpu().numpy().astype(np.float64)
-    e = c.ckexp[:nb].cpu().numpy().astype(np.int64)
+    packed = c.ckexp[:nb].cpu().numpy().astype(np.int64)
+    e = ((packed & 0xFFFF) ^ 0x8000) - 0x8000  # low 16 bits, signed
+    nrounded = (packed >> 16) & 0xFF
     dg = c.ckd[:nb].cpu().numpy().astype(np.int64)  # [nb][H][4][dh]
     X = dg[:, :, 0] + 256 * dg[:, :, 1] + 65536 * dg[:, :, 2] + 16777216 * dg[:, :, 3]
     mx = np.abs(ck).max(-1)
     assert (mx < np.ldexp(1.0, e)).all() and (mx >= np.ldexp(1.0, e - 1)).all()
-    want = np.rint(ck * np.ldexp(1.0, 30 - e)[..., None])
+    scaled = ck * np.ldexp(1.0, 30 - e)[..., None]
+    want = np.rint(scaled)
     assert np.array_equal(X, want.astype(np.int64))
+    assert np.array_equal(nrounded, (want != scaled).sum(-1))  # the elements the grid rounds
     assert dg.min() >= -128 and dg.max() <= 127
 
 
