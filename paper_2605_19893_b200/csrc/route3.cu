@@ -216,6 +216,12 @@ __device__ __forceinline__ void write_digit_row(uint8_t* base, uint32_t slice_by
 }
 
 
+// 2^(k/16), k = 0..15, correctly rounded
+__constant__ double kT16[16] = {1.0, 1.0442737824274138, 1.0905077326652577, 1.1387886347566916,
+                                1.189207115002721, 1.241857812073484, 1.2968395546510096, 1.3542555469368927,
+                                1.4142135623730951, 1.4768261459394993, 1.5422108254079407, 1.6104903319492543,
+                                1.681792830507429, 1.7562521603732995, 1.8340080864093424, 1.9152065613971474};
+
 // 2^L for |L| < 512 in fp64 (relative error < 5e-11, inside the 2e-10 term of
 // the certification bound): 16 L rounded to an integer k16 by the
 // 1.5 2^52 shifter, 2^(k16 / 16) from the table and the exponent field,
@@ -311,9 +317,12 @@ __device__ __forceinline__ void digit_q(const Route3Launch& P, const Route3Req& 
     int inex = 0;  // elements the 31-bit grid rounds (the rest it represents exactly)
     {
       const float xs[4] = {v[z].x, v[z].y, v[z].z, v[z].w};
+      const int shift = 30 - e;
+      const bool plain = shift >= -126 && shift <= 127;
+      const float sc = plain ? __int_as_float((127 + shift) << 23) : 1.0f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const float sx = ldexpf(xs[c], 30 - e);
+        const float sx = plain ? xs[c] * sc : ldexpf(xs[c], shift);  // exact (a power of two)
         inex += (float)__float2int_rn(sx) != sx ? 1 : 0;
       }
     }
@@ -324,6 +333,23 @@ __device__ __forceinline__ void digit_q(const Route3Launch& P, const Route3Req& 
       m.qexp[j] = e;
       m.qsc[j] = P.c_sl * pow2i(e - 44);
       m.colmvis[j] = j < U.nrows ? R.slot_mvis[U.s0 + j / P.G] : 0;
+    }
+  }
+}
+
+// one unit's key digit planes -> the two tile stages (an empty second tile just arrives)
+__device__ __forceinline__ void issue_unit_tma(const Route3Req& R, const Unit& U, uint8_t* smem, Misc& m) {
+  const uint64_t pol = l2_evict_first_policy();  // the digit planes are read once per launch
+  const int ntile = U.nblk > kTB ? 2 : 1;
+  for (int t = 0; t < 2; ++t) {
+    if (t < ntile) {
+      mbar_expect_tx(&m.tma_full[t], kTileBytes);
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        tma_load_4d_hint(smem + t * kTileBytes + s * kPlaneBytes, &R.tm_ckd, 0, s, U.kvh, U.row0 + t * kTB,
+                         &m.tma_full[t], pol);
+    } else {
+      mbar_arrive(&m.tma_full[t]);
     }
   }
 }
@@ -391,7 +417,8 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
       m.gbest_i[tid >> 2] = bi;
     }
     __syncthreads();
-    {  // 2. the group maximum of rank want-1: a lower bound of the want-th best
+    {  // 2. the group maximum of rank `want`: at least want + 1 candidates rank at or
+       //    before it, so the survivors hold the picks AND the best non-pick
       const int g = tid >> 2, part = tid & 3;
       const double ms = m.gbest_s[g];
       const int mi = m.gbest_i[g];
@@ -400,7 +427,7 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
         rank += ranks_before(m.gbest_s[o], m.gbest_i[o], ms, mi) ? 1 : 0;
       rank += __shfl_xor_sync(0xffffffffu, rank, 1);
       rank += __shfl_xor_sync(0xffffffffu, rank, 2);
-      if (part == 0 && want <= kTopnGroups && rank == want - 1 && ms != -INFINITY) {
+      if (part == 0 && want < kTopnGroups && rank == want && ms != -INFINITY) {
         m.lb_s = ms;
         m.lb_i = mi;
       }
@@ -427,7 +454,7 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
       if (rank == want) m.sk1 = sb;
     }
     __syncthreads();
-    if (ns <= want && ncand > want) {  // 5. the best non-survivor is the best non-pick
+    if (ns <= want && ncand > want) {  // 5. (a survivor set without a non-pick: the best non-survivor)
       double bo = -INFINITY;
       for (int b = tid; b < avail; b += kThreads) {
         double sc;
@@ -627,8 +654,6 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x, nctas = gridDim.x;
   double* g = reinterpret_cast<double*>(smem + kOffG);  // [kR3MaxSpr][kGS]
-  griddep_wait();  // inputs (q) may come from the launch just before (PDL)
-  stamp(P, 0);
   const int units = P.unit_start[P.n_req];
   if (tid == 0) {
     for (int t = 0; t < 2; ++t) {
@@ -638,7 +663,53 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     for (int t = 0; t < 3; ++t) mbar_init(&m.ex_full[t], 1);
     fence_mbar_init();
   }
-  if (tid < 16) m.T16[tid] = exp2((double)tid * 0.0625);
+  // The first unit's key planes and block exponents are cache data (complete in
+  // stream order before this call): they go out before the wait for the
+  // previous launch, so they stream under its tail.  q comes after the wait.
+  // a unit's setup that needs no q: counters, selection-block weights, zeroed sums,
+  // block exponents (issue_unit_tma goes first, by thread 0)
+  auto setup_unit = [&](const Unit& U, const Route3Req& R) {
+    const int kpack = tid < U.nblk ? __ldg(R.ckexp + (int64_t)(U.row0 + tid) * P.Hkv + U.kvh) : 0;
+    if (tid == 0) {
+      m.flag = 0;
+      m.kemax = -100000;
+      m.nkmax = 0;
+    }
+    {  // compressed blocks overlapping each selection block of the range, and their token overlaps
+      const int bl = tid & (kR3MaxSpr - 1), kg = tid / kR3MaxSpr;
+      const int b = U.b0 + bl;
+      int lo, hi;
+      blocks_of(b, P.d, P.l, P.l_sel, lo, hi);
+      hi = min(hi, U.row0 + U.nblk - 1);
+      if (kg == 0) m.glo[bl] = lo;
+      for (int kq = kg; kq < kR3MaxBps; kq += kThreads / kR3MaxSpr)
+        m.gw[kq][bl] = lo + kq <= hi ? (double)overlap(lo + kq, b, P.d, P.l, P.l_sel) : 0.0;
+    }
+    for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) g[e] = 0.0;  // (selection blocks past nsel stay 0)
+    __syncthreads();  // counter resets before the exponent maxima
+    static_assert(kR3MaxBlk <= kThreads, "one block exponent per thread");
+    if (tid < kR3MaxBlk) {
+      const bool has = tid < U.nblk;
+      const int ke = (int)(int16_t)(kpack & 0xFFFF), knx = (kpack >> 16) & 0xFF;  // exponent, rounded elements
+      m.kexp[tid] = has ? ke : 0;
+      if (has) {
+        atomicMax(&m.kemax, ke);
+        if (knx) atomicMax(&m.nkmax, knx);
+      }
+    }
+  };
+  // The first unit's key planes, block exponents and weights are cache data
+  // (complete in stream order before this call): they go out before the wait
+  // for the previous launch, under its tail.  q comes after the wait.
+  if (tid < 16) m.T16[tid] = kT16[tid];
+  if (cta < units) {
+    const Unit U = unit_of(P, cta);
+    const Route3Req& R = P.req[U.req];
+    if (tid == 0) issue_unit_tma(R, U, smem, m);
+    setup_unit(U, R);
+  }
+  griddep_wait();  // inputs (q) may come from the launch just before (PDL)
+  stamp(P, 0);
   if (cta == nctas - 1) {  // queries that reuse a representative's set get count -1
     for (int r = 0; r < P.n_req; ++r) {
       const Route3Req& R = P.req[r];
@@ -666,49 +737,13 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const Route3Req& R = P.req[U.req];
     const uint32_t par = k & 1;
     const int ntile = U.nblk > kTB ? 2 : 1;
+    if (k > 0) {
+      if (tid == 0) issue_unit_tma(R, U, smem, m);
+      setup_unit(U, R);
+    }
     float4 qv[3];
     load_q(P, R, U, qv);
-    static_assert(kR3MaxBlk <= kThreads, "one block exponent per thread");
-    const bool has_ke = tid < U.nblk;  // the exponent load is in flight across the setup
-    const int kpack = has_ke ? __ldg(R.ckexp + (int64_t)(U.row0 + tid) * P.Hkv + U.kvh) : 0;
-    const int ke = (int)(int16_t)(kpack & 0xFFFF), knx = (kpack >> 16) & 0xFF;  // exponent, rounded elements
-    if (tid == 0) {
-      const uint64_t pol = l2_evict_first_policy();  // the digit planes are read once per launch
-      for (int t = 0; t < 2; ++t) {
-        if (t < ntile) {
-          mbar_expect_tx(&m.tma_full[t], kTileBytes);
-#pragma unroll
-          for (int s = 0; s < 4; ++s)
-            tma_load_4d_hint(smem + t * kTileBytes + s * kPlaneBytes, &R.tm_ckd, 0, s, U.kvh, U.row0 + t * kTB,
-                             &m.tma_full[t], pol);
-        } else {
-          mbar_arrive(&m.tma_full[t]);
-        }
-      }
-      m.flag = 0;
-      m.kemax = -100000;
-      m.nkmax = 0;
-    }
-    {  // compressed blocks overlapping each selection block of the range, and their token overlaps
-      const int bl = tid & (kR3MaxSpr - 1), kg = tid / kR3MaxSpr;
-      const int b = U.b0 + bl;
-      int lo, hi;
-      blocks_of(b, P.d, P.l, P.l_sel, lo, hi);
-      hi = min(hi, U.row0 + U.nblk - 1);
-      if (kg == 0) m.glo[bl] = lo;
-      for (int kq = kg; kq < kR3MaxBps; kq += kThreads / kR3MaxSpr)
-        m.gw[kq][bl] = lo + kq <= hi ? (double)overlap(lo + kq, b, P.d, P.l, P.l_sel) : 0.0;
-    }
     digit_q(P, R, U, qv, smem, m);
-    __syncthreads();  // flag / kemax reset before the block exponents
-    if (tid < kR3MaxBlk) {
-      m.kexp[tid] = has_ke ? ke : 0;
-      if (has_ke) {
-        atomicMax(&m.kemax, ke);
-        if (knx) atomicMax(&m.nkmax, knx);
-      }
-    }
-    for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) g[e] = 0.0;  // (selection blocks past nsel stay 0)
     fence_proxy_async_smem();  // q digits: generic-proxy writes read by the MMA
     tc_fence_before();
     __syncthreads();

@@ -19,7 +19,7 @@ from paper_2605_19893_b200 import abi  # noqa: E402
 from paper_2605_19893_b200 import verify as V  # noqa: E402
 
 BASE = 196608
-PHASES = {9: "exact: lock held", 10: "exact: logits", 11: "exact: exps", 1: "q digits staged", 9: "tile 0 MMAs done", 10: "tile 1 MMAs done", 2: "e values done",
+PHASES = {1: "q digits staged", 9: "tile 0 MMAs done", 10: "tile 1 MMAs done", 2: "e values done",
           3: "unit sums done", 4: "phase 1 done",
           5: "den rows in", 6: "shares written", 7: "top-n start", 14: "top-n scores in", 15: "top-n selected",
           8: "done"}
