@@ -322,7 +322,7 @@ class ClockSampler:
 def ncu_traffic(workload: str, n_req_launch: int):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     capture of the SAME workload (profiles/), or None."""
-    name = "r02_attend_ncu_summary.json" if n_req_launch == 1 else "attend_batch_c4_ncu_summary.json"
+    name = "r02_attend_ncu_summary.json" if n_req_launch == 1 else "r02_attend_batch_c4_ncu_summary.json"
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", name)))
     except (OSError, ValueError):
