@@ -153,11 +153,9 @@ struct Route3Req {
   int32_t unrouted[kMaxQueries];
   int32_t n_unrouted;
 };
-struct Route3Launch {
-  Route3Req req[kR3Batch];
+// the launch-wide fields; the request table follows in Route3LaunchT
+struct Route3Common {
   int32_t n_req;
-  int32_t unit_start[kR3Batch + 1];  // units of requests < r (set at launch)
-  int32_t task_start[kR3Batch + 1];  // (request, slot) Top-n tasks of requests < r
   int32_t Hq, Hkv, G, n, l, d, l_sel;
   int32_t spc;         // slots per row chunk (chunk rows = spc x G <= kR3Rows)
   int32_t bps;         // compressed blocks overlapping one selection block (at most)
@@ -170,6 +168,16 @@ struct Route3Launch {
   int32_t debug;       // diagnostics (SPECSV_ROUTE3_DEBUG): bit 0 runs the selection twice
   unsigned long long* trace;  // diagnostics: per-CTA stamps at kRouteTraceBase + cta * 16
 };
+// The kernel parameters of a launch over up to NR requests.  A one-request
+// launch passes ~1.9 KB instead of ~33 KB: the command processor copies every
+// launch's parameters, and eager per-layer calls issue one per refresh layer.
+template <int NR>
+struct Route3LaunchT : Route3Common {
+  Route3Req req[NR];
+  int32_t unit_start[NR + 1];  // units of requests < r (set at launch)
+  int32_t task_start[NR + 1];  // (request, slot) Top-n tasks of requests < r
+};
+using Route3Launch = Route3LaunchT<kR3Batch>;  // the host's staging of any launch
 cudaError_t launch_route3(Route3Launch& p, cudaStream_t stream);
 int route3_grid();  // CTAs of a route3 launch on this device (one per SM)
 

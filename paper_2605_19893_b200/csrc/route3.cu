@@ -262,7 +262,8 @@ struct Unit {
   int row0, nblk;         // compressed blocks [row0, row0 + nblk)
 };
 
-__device__ __forceinline__ Unit unit_of(const Route3Launch& P, int u) {
+template <class LaunchT>
+__device__ __forceinline__ Unit unit_of(const LaunchT& P, int u) {
   int r = 0;
   while (r + 1 < P.n_req && u >= P.unit_start[r + 1]) ++r;
   const Route3Req& R = P.req[r];
@@ -289,7 +290,8 @@ __device__ __forceinline__ Unit unit_of(const Route3Launch& P, int u) {
 
 // the unit's q rows (16 warps, three rows each), loaded first so the loads are
 // in flight across the rest of the unit's setup
-__device__ __forceinline__ void load_q(const Route3Launch& P, const Route3Req& R, const Unit& U, float4 (&v)[3]) {
+template <class LaunchT>
+__device__ __forceinline__ void load_q(const LaunchT& P, const Route3Req& R, const Unit& U, float4 (&v)[3]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int z = 0; z < 3; ++z) {
@@ -303,7 +305,8 @@ __device__ __forceinline__ void load_q(const Route3Launch& P, const Route3Req& R
 }
 
 // ... -> digit slices, plus per-column tables
-__device__ __forceinline__ void digit_q(const Route3Launch& P, const Route3Req& R, const Unit& U,
+template <class LaunchT>
+__device__ __forceinline__ void digit_q(const LaunchT& P, const Route3Req& R, const Unit& U,
                                         const float4 (&v)[3], uint8_t* smem, Misc& m) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   static_assert(kN == 3 * kWarps, "three q rows per warp");
@@ -354,7 +357,8 @@ __device__ __forceinline__ void issue_unit_tma(const Route3Req& R, const Unit& U
   }
 }
 
-__device__ __forceinline__ void stamp(const Route3Launch& P, int k) {
+template <class LaunchT>
+__device__ __forceinline__ void stamp(const LaunchT& P, int k) {
   if (P.trace != nullptr && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -372,8 +376,10 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
 // then the `want` best others into m.picks.  Also records the last pick's
 // score (m.sk) and the best non-pick's (m.sk1, -inf if none) and sets
 // m.certified = the two are separated by more than eps (relative).
-__device__ void select_topn(const double* sel, int* surv, int avail, int n, double eps, Misc& m) {
+__device__ void select_topn(const double* sel, int* surv, int avail, int n, double eps, Misc& m,
+                            unsigned long long* tr = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long c0 = clock64();
   const int f1 = avail - 2 > 0 ? avail - 2 : -1;
   const int f2 = avail - 1 > 0 ? avail - 1 : -1;
   const int nforced = avail > 0 ? 1 + (f1 > 0) + (f2 > 0 && f2 != f1) : 0;
@@ -433,6 +439,7 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
       }
     }
     __syncthreads();
+    if (tr != nullptr && tid == 0) tr[11] = clock64() - c0;
     const double ls = m.lb_s;  // 3. survivors: a prefix of the global order
     const int li = m.lb_i;
     for (int b = tid; b < avail; b += kThreads) {
@@ -525,7 +532,8 @@ __device__ void write_row(const Misc& cm, Misc& m, int avail, int n, int32_t* id
 constexpr int kExStages = 3;
 __device__ __forceinline__ uint32_t ex_stage_off(int s) { return (uint32_t)s * kExStage; }  // over the idle sel/surv arrays
 
-__device__ void exact_scores(const Route3Launch& P, const Route3Req& R, int slot, double* sel, uint8_t* smem,
+template <class LaunchT>
+__device__ void exact_scores(const LaunchT& P, const Route3Req& R, int slot, double* sel, uint8_t* smem,
                              Misc& m, int& ex_seq) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qi = R.slot_q[slot], mv = R.slot_mvis[slot], avail = R.slot_avail[slot];
@@ -646,7 +654,8 @@ __device__ void exact_scores(const Route3Launch& P, const Route3Req& R, int slot
 }
 
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_constant__ Route3Launch P) {
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_constant__ Route3LaunchT<NR> P) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
@@ -986,7 +995,8 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const double delta = flagged ? 0.0 : __longlong_as_double((long long)bb);
     const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-10;
     const long long c0 = clock64();
-    select_topn(sel, surv, avail, P.n, eps, m);
+    select_topn(sel, surv, avail, P.n, eps, m,
+                P.trace != nullptr ? P.trace + kRouteTraceBase + blockIdx.x * 16 : nullptr);
     stamp(P, 15);
     if (P.trace != nullptr && tid == 0) P.trace[kRouteTraceBase + blockIdx.x * 16 + 12] = clock64() - c0;
     if (P.debug & 1) {  // diagnostics: the selection again (warm instruction cache)
@@ -1018,26 +1028,14 @@ int sm_count3() {
   return sms;
 }
 
-}  // namespace
-
-int route3_grid() { return sm_count3(); }
-
-cudaError_t launch_route3(Route3Launch& p, cudaStream_t s) {
-  p.unit_start[0] = 0;
-  p.task_start[0] = 0;
-  for (int r = 0; r < p.n_req; ++r) {
-    const Route3Req& R = p.req[r];
-    p.unit_start[r + 1] = p.unit_start[r] + p.Hkv * R.nchunks * R.nranges;
-    p.task_start[r + 1] = p.task_start[r] + R.nr;
-  }
-  const int work = std::max(p.unit_start[p.n_req], p.task_start[p.n_req]);
-  const int ctas = std::max(1, std::min(sm_count3(), work));
+template <int NR>
+cudaError_t launch_route3_n(const Route3LaunchT<NR>& p, int ctas, cudaStream_t s) {
   static std::atomic<int> done[64];
   int dev = 0;
   cudaGetDevice(&dev);
   std::atomic<int>& d = done[dev < 64 ? dev : 63];
   if (!d.load(std::memory_order_acquire)) {  // the shared-memory opt-in, once per device
-    const cudaError_t e = cudaFuncSetAttribute(route3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t e = cudaFuncSetAttribute(route3_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)kSmemBytes);
     if (e != cudaSuccess) return e;
     d.store(1, std::memory_order_release);
@@ -1057,7 +1055,34 @@ cudaError_t launch_route3(Route3Launch& p, cudaStream_t s) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, route3_kernel, p);
+  return cudaLaunchKernelEx(&cfg, route3_kernel<NR>, p);
+}
+
+}  // namespace
+
+int route3_grid() { return sm_count3(); }
+
+cudaError_t launch_route3(Route3Launch& p, cudaStream_t s) {
+  p.unit_start[0] = 0;
+  p.task_start[0] = 0;
+  for (int r = 0; r < p.n_req; ++r) {
+    const Route3Req& R = p.req[r];
+    p.unit_start[r + 1] = p.unit_start[r] + p.Hkv * R.nchunks * R.nranges;
+    p.task_start[r + 1] = p.task_start[r] + R.nr;
+  }
+  const int work = std::max(p.unit_start[p.n_req], p.task_start[p.n_req]);
+  const int ctas = std::max(1, std::min(sm_count3(), work));
+  if (p.n_req == 1 && !(p.debug & 4)) {  // the one-request parameter block (debug bit 2: the full one)
+    thread_local Route3LaunchT<1> one;
+    static_cast<Route3Common&>(one) = static_cast<const Route3Common&>(p);
+    one.req[0] = p.req[0];
+    one.unit_start[0] = p.unit_start[0];
+    one.unit_start[1] = p.unit_start[1];
+    one.task_start[0] = p.task_start[0];
+    one.task_start[1] = p.task_start[1];
+    return launch_route3_n(one, ctas, s);
+  }
+  return launch_route3_n(p, ctas, s);
 }
 
 }  // namespace specsv_b200

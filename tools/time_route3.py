@@ -91,7 +91,8 @@ def main():
             print(f"  {name:22s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}  (n={len(d)})")
     tk = t[t[:, 12] > 0]
     if len(tk):
-        print(f"  select: {np.median(tk[:, 12]):.0f} SM cycles (median over {len(tk)} tasks)")
+        print(f"  select: {np.median(tk[:, 12]):.0f} SM cycles (median over {len(tk)} tasks), "
+              f"of which steps 1-2 {np.median(tk[:, 11]):.0f}")
     d = (t[:, 0] - t0) / 1e3
     print(f"  {'start':22s} min {d.min():7.2f} med {np.median(d):7.2f} max {d.max():7.2f}")
     print("exact re-scorings:", sum(cs[-1].route_fallbacks() for cs in cases), "over all launches")
