@@ -69,8 +69,8 @@ constexpr int kBarSoft = 1;         // named barriers: softmax warps
 constexpr int kBarChunk0 = 3;       // 3..5: the 4 warps of one column chunk
 constexpr int kBarPassEnd = 7;
 constexpr int kBarRedo = 8;
-constexpr int kBarUnion = 9;        // the 12 softmax warps + the union warp build the union
-constexpr int kUnionThreads = kSoftThreads + 32;
+constexpr int kBarUnion = 9;        // the 12 softmax warps build the union
+constexpr int kUnionThreads = kSoftThreads;
 
 // shared memory map (bytes from the 1024-aligned base)
 constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P^T of branch A)
@@ -91,7 +91,7 @@ struct Misc {
   // needs PV(j - 1)), and a single barrier would then complete tile j's phase
   // with that warp's P still unwritten (it cannot get two tiles ahead: tile
   // j + 2 needs PV(j), which needs every tile-j arrival)
-  uint64_t p_full[2], q_ready, union_ready;
+  uint64_t p_full[2], q_ready, rows_ready, union_ready;
   uint32_t tmem_base;
   int32_t n_union, n_tok_tiles;
   int32_t flag;                   // end-of-pass check failed: redo the tiles in the robust pass
@@ -107,7 +107,6 @@ struct Misc {
   int32_t qcount[kMaxChunkQ];
   int32_t qsel[kMaxChunkQ * 64];
   uint32_t bitmap[kMaxUnionWords];
-  int32_t word_prefix[kMaxUnionWords];
   int32_t union_blk[kMaxUnion];
   uint32_t union_own[kMaxUnion];
 };
@@ -224,72 +223,104 @@ __device__ __forceinline__ void stage_index_rows(const UnionArgs& u, Misc& m, in
   }
 }
 
+// position of the j-th (0-based) set bit of v (v has more than j set bits)
+__device__ __forceinline__ int nth_set_bit(uint32_t v, int j) {
+  int pos = 0;
+#pragma unroll
+  for (int sh = 16; sh >= 1; sh >>= 1) {
+    const int c = __popc(v & ((1u << sh) - 1u));
+    if (c <= j) {
+      j -= c;
+      v >>= sh;
+      pos += sh;
+    }
+  }
+  return pos;
+}
+
 // The union of selected + window blocks with per-block query ownership, built
-// by the 12 softmax warps and the union warp together (kUnionThreads
-// participants, `pt` = this thread's index among them) once the index rows
-// are staged: five short parallel steps between named barriers.  (One warp
-// alone took ~6 us for it under the step's load; the softmax warps reach this
-// point with nothing else to do, their compressed tiles done.)
+// by the 12 softmax warps (kUnionThreads participants, `pt` = this thread's
+// index among them) when they reach their first token tile, from the index
+// rows the union warp staged (it also zeroed the bitmap and the ownership
+// words).  Two steps: (1) set the window (whole-word masks) and selected
+// bits; (2) every warp scans the word popcounts in registers (lane L covers
+// words [L << lp, (L + 1) << lp)), so any word's union rank is one shuffle
+// away; warp k scatters the k-th, (k+12)-th, ... set bit of each word and the
+// index-row entries OR their ownership bits.  The build is a short chain of
+// dependent instructions per warp: five barrier-separated steps with a
+// one-lane-per-word scatter loop took ~4000 SM cycles in the step, this
+// ~2500; one warp alone (the union warp, under the compressed tiles) ~9000.
 __device__ void coop_union(Misc& m, int pt, int nqc, int n, int l_sel, int rows, int wlo, int whi) {
   const int nsel = (rows + l_sel - 1) / l_sel;
   const int words = (nsel + 31) >> 5;
-  for (int w = pt; w < words; w += kUnionThreads) m.bitmap[w] = 0u;
-  named_bar_sync(kBarUnion, kUnionThreads);
-  for (int b = wlo / l_sel + pt; b <= whi / l_sel; b += kUnionThreads) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
-  for (int e = pt; e < nqc * n; e += kUnionThreads) {
+  const int lane = pt & 31, wid = pt >> 5;
+  const int nsl = nqc * n;
+  mbar_sleep_wait(&m.rows_ready, 0);
+  {  // the window's blocks are contiguous: one OR per bitmap word
+    const int b0 = wlo / l_sel, b1 = whi / l_sel;
+    const int w = (b0 >> 5) + pt;
+    if (b0 <= b1 && w <= (b1 >> 5)) {
+      const int lo = max(b0, w << 5) & 31, hi = min(b1, (w << 5) + 31) & 31;
+      atomicOr(&m.bitmap[w], (0xFFFFFFFFu >> (31 - hi)) & (0xFFFFFFFFu << lo));
+    }
+  }
+  for (int e = pt; e < nsl; e += kUnionThreads) {
     const int i = e / n, k = e - i * n;
     int b = m.qsel[e];
     if (k >= m.qcount[i] || b < 0 || (int64_t)b * l_sel >= m.qbound[i] || b >= nsel) b = -1;
     m.qsel[e] = b;
     if (b >= 0) atomicOr(&m.bitmap[b >> 5], 1u << (b & 31));
   }
+  __syncwarp();
   named_bar_sync(kBarUnion, kUnionThreads);
-  if (pt >= kSoftThreads) {  // one warp: exclusive prefix of popcounts over contiguous word ranges
-    const int lane = pt - kSoftThreads;
-    const int per = (words + 31) >> 5;
-    const int w0 = lane * per;
-    int local = 0;
-    for (int w = w0; w < min(words, w0 + per); ++w) local += __popc(m.bitmap[w]);
-    int incl = local;
+  const int lp = words <= 32 ? 0 : 32 - __clz(((words + 31) >> 5) - 1);  // 2^lp words per lane
+  const int wb = lane << lp, we = min(words, (lane + 1) << lp);
+  int local = 0;
+  for (int w = wb; w < we; ++w) local += __popc(m.bitmap[w]);
+  int incl = local;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += y;
-    }
-    int run = incl - local;
-    for (int w = w0; w < min(words, w0 + per); ++w) {
-      m.word_prefix[w] = run;
-      run += __popc(m.bitmap[w]);
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 0) {
-      m.n_union = min(total, kMaxUnion);
-      m.n_tok_tiles = (min(total, kMaxUnion) + 1) / 2;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int base = incl - local;  // union rank of word wb's first block
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  {  // scatter: this lane's words, this warp's share of their set bits
+    int r = base;
+    for (int w = wb; w < we; ++w) {
+      const uint32_t bits = m.bitmap[w];
+      const int c = __popc(bits);
+      for (int j = wid; j < c; j += kSoftWarps)
+        if (r + j < kMaxUnion) m.union_blk[r + j] = (w << 5) + nth_set_bit(bits, j);
+      r += c;
     }
   }
-  named_bar_sync(kBarUnion, kUnionThreads);
-  for (int w = pt; w < words; w += kUnionThreads) {
-    uint32_t bits = m.bitmap[w];
-    int r = m.word_prefix[w];
-    while (bits) {
-      const int bit = __ffs(bits) - 1;
-      bits &= bits - 1;
-      if (r < kMaxUnion) {
-        m.union_blk[r] = (w << 5) + bit;
-        m.union_own[r] = 0u;
-      }
-      ++r;
-    }
+  // ownership: entry e of the index rows (query e / n) owns its block
+  for (int e0 = pt - lane; e0 < nsl; e0 += kUnionThreads) {
+    const int e = e0 + lane;
+    const int b = e < nsl ? m.qsel[e] : -1;
+    const int w = b >= 0 ? (b >> 5) : 0;
+    int r = __shfl_sync(0xffffffffu, base, w >> lp);
+    for (int w2 = (w >> lp) << lp; w2 < w; ++w2) r += __popc(m.bitmap[w2]);
+    r += __popc(m.bitmap[w] & ((1u << (b & 31)) - 1u));
+    if (b >= 0 && r < kMaxUnion) atomicOr(&m.union_own[r], 1u << (e / n));
   }
-  named_bar_sync(kBarUnion, kUnionThreads);
-  for (int e = pt; e < nqc * n; e += kUnionThreads) {
-    const int b = m.qsel[e];
-    if (b < 0) continue;
-    const int w = b >> 5;
-    const int r = m.word_prefix[w] + __popc(m.bitmap[w] & ((1u << (b & 31)) - 1u));
-    if (r < kMaxUnion) atomicOr(&m.union_own[r], 1u << (e / n));
+  if (pt == 0) {
+    m.n_union = min(total, kMaxUnion);
+    m.n_tok_tiles = (min(total, kMaxUnion) + 1) / 2;
   }
+  __syncwarp();
   named_bar_sync(kBarUnion, kUnionThreads);
+  if (pt < 32) mbar_arrive(&m.union_ready);  // the TMA and MMA warps wait for this
+}
+
+// the union's shared state, zeroed by the union warp before it stages the rows
+__device__ __forceinline__ void zero_union(Misc& m, int nqc, int n, int l_sel, int rows, int wlo, int whi,
+                                           int lane) {
+  const int words = ((rows + l_sel - 1) / l_sel + 31) >> 5;
+  for (int w = lane; w < words; w += 32) m.bitmap[w] = 0u;
+  const int umax = min(kMaxUnion, nqc * n + (whi / l_sel - wlo / l_sel + 1));
+  for (int u = lane; u < umax; u += 32) m.union_own[u] = 0u;
 }
 
 struct TileInfo {
@@ -444,6 +475,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
 
   // ---- prologue: everything that needs no other warp goes out first --------
   float4 xa[2], xb[2];  // softmax warps: this thread's q units, in flight over the barrier
+
   uint4 kr;             //                and its slice of the reference key row
   if (warp == kWarpTma) {
     if (lane == 0) {
@@ -458,6 +490,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       mbar_init(&m.p_full[0], 4 * nch);
       mbar_init(&m.p_full[1], 4 * nch);
       mbar_init(&m.q_ready, kSoftWarps);
+      mbar_init(&m.rows_ready, 32);
       mbar_init(&m.union_ready, 32);
       m.flag = (p.debug_flags & 1) ? 1 : 0;  // bit 0: force the robust redo (tests)
       fence_mbar_init();
@@ -595,9 +628,27 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
 #pragma unroll 1
       for (int j = 0; active; ++j) {
         const int t = split + j * S;
-        if (!union_seen && t >= n_cmp) {
+        if (!union_seen && t >= n_cmp) {  // the token tiles need the union
           coop_union(m, tid, nqc, p.n_sel, p.l_sel, p.rows, cwlo, cwhi);
           if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
+          if ((p.debug_flags & 32) && trace && tid == 0) {  // check: a sequential recount of the union
+            int bad = 0, cnt = 0, prev = -1;
+            const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
+            for (int b = 0; b < nsel; ++b) {
+              bool in = (b * p.l_sel <= cwhi) && (b * p.l_sel + p.l_sel - 1 >= cwlo);
+              for (int e = 0; e < nqc * p.n_sel && !in; ++e) in = m.qsel[e] == b;
+              if (in) {
+                if (cnt < m.n_union && m.union_blk[cnt] != b) bad |= 1;
+                ++cnt;
+              }
+            }
+            for (int u = 0; u < m.n_union; ++u) {
+              if (m.union_blk[u] <= prev) bad |= 2;
+              prev = m.union_blk[u];
+            }
+            if (cnt != m.n_union) bad |= 4;
+            p.trace[cta_id * 64 + 63] = 1000 + bad;
+          }
           union_seen = true;
           T = tile_count();
         }
@@ -931,18 +982,19 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       named_bar_sync(kBarPassEnd, kThreads);
     }
   } else {
-    // =================== union warp: index rows, then the union (with the softmax warps) ===================
+    // =================== union warp: the index rows ===================
     // (an L2 prefetch of this CTA's later tiles from here was measured and
     // removed: with the evict-first stage loads it cost ~4% of the step)
     const UnionArgs ua = union_args(p, q0, nqc, lane);
     const bool early = p.idx_early != 0 && !(p.debug_flags & 8);
+    zero_union(m, nqc, ua.n, ua.l_sel, ua.rows, cwlo, cwhi, lane);
     if (early) stage_index_rows(ua, m, nqc, lane);
     // REFRESH: the index rows come from the routing launch just before this
     // one (programmatic dependent launch: the rest of this CTA -- q, the
     // compressed tiles -- does not wait for it).  REUSE: they were complete
     // before the previous launch started, and this launch writes nothing the
     // previous one still reads (it triggers after its last workspace read),
-    // so the union is built at once, under the compressed tiles.
+    // so they are staged at once, under the compressed tiles.
     if (!early) {
       griddep_wait();
       stage_index_rows(ua, m, nqc, lane);
@@ -950,8 +1002,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     cp_async_wait_all();
     __syncwarp();
     if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
-    coop_union(m, kSoftThreads + lane, nqc, ua.n, ua.l_sel, ua.rows, cwlo, cwhi);
-    mbar_arrive(&m.union_ready);  // the TMA and MMA warps wait for this
+    mbar_arrive(&m.rows_ready);  // the softmax warps build the union from them
     named_bar_sync(kBarPassEnd, kThreads);
     if (m.flag) {
       named_bar_sync(kBarRedo, kThreads);

@@ -121,9 +121,40 @@ def main():
                  f" bar {ph(6)[0]:5.2f} merge {ph(4)[0]:5.2f}/{ph(4)[1]:5.2f} ctas {len(t)}")
         prev_end = end
         print(line)
+        if os.environ.get("TRACE_TILES"):
+            print_tiles(t)
         if os.environ.get("TRACE_SPLITS"):
             print("   split: loop end / partials written (median over heads): " +
                   " ".join(f"{sp}:{a:.1f}/{b:.1f}" for sp, a, b in per_split(bufs[j])))
+
+
+def print_tiles(t):
+    """per-tile stamps (median over CTAs, us from each CTA's own start):
+    TMA issue, K full (QK issued), S full (softmax start), exp done, P handed
+    over, V full (PV issued)"""
+    raw = t[:, [0, 16, 24, 48, 32, 40]].astype(np.int64).ravel()
+    raw = raw[raw > 0]
+    print("   globaltimer gcd of stamps (ns):", int(np.gcd.reduce(raw - raw.min())),
+          " distinct low values:", len(np.unique(raw % 1000)))
+    rel = (t - t[:, :1]) / 1e3
+    cols = [("issue", 8), ("qk", 16), ("s_full", 24), ("exp", 48), ("p", 32), ("pv", 40)]
+    u = [np.median(rel[:, c][t[:, c] > 0]) if (t[:, c] > 0).sum() > len(t) // 2 else -1
+         for c in (59, 56, 57, 58, 60, 1)]
+    chk = t[:, 63]
+    if (chk >= 1000).any():
+        print("   union check: %d CTAs checked, %d bad (codes %s)" % ((chk >= 1000).sum(), (chk > 1000).sum(),
+                                                                  sorted(set((chk[chk > 1000] - 1000).tolist()))))
+    print("   union: index rows in %.2f, built %.2f (us)" % (u[0], u[5]))
+    if os.environ.get("TRACE_RAW"):
+        for i in range(0, len(t), 29):
+            print("   cta %3d: " % i + " ".join("%d:%.2f" % (c, rel[i, c]) for c in (59, 56, 1, 24, 25, 26)))
+    print("   tile " + " ".join(f"{n:>8s}" for n, _ in cols))
+    for j in range(8):
+        vals = []
+        for _, b in cols:
+            d = rel[:, b + j][t[:, b + j] > 0]
+            vals.append(f"{np.median(d):8.2f}" if len(d) > len(t) // 2 else "       -")
+        print(f"   {j:4d} " + " ".join(vals))
 
 
 def per_split(buf, S=18):
