@@ -28,6 +28,19 @@
  * specsv_status; specsv_last_error() gives a thread-local message (the
  * reference throws std::invalid_argument for the same conditions,
  * config.hpp:39-50, group_attend.cpp:12,94,126, layer_roles.cpp:20-22).
+ *
+ * Programmatic dependent launch: the routing and attend kernels are enqueued
+ * with programmatic stream serialization, so a call's first kernel may start
+ * -- and read its inputs (q, gates, the KV caches, the draft rows, on REUSE
+ * the index sets) -- as soon as the kernel enqueued just before it has
+ * triggered programmatic completion (griddepcontrol.launch_dependents), not
+ * only once it has finished.  This library's own kernels trigger only after
+ * their last write a later call reads (attend: after its output; routing:
+ * before its index-set writes, which the attend launch of the same call
+ * waits for).  Kernels that never trigger (ordinary CUDA/PyTorch kernels)
+ * complete first, as usual.  A caller whose own producer kernel triggers
+ * early, before writing a verify input, must not enqueue it directly before
+ * a verify call -- or set SPECSV_NO_PDL=1, which turns the attribute off.
  */
 #ifndef SPECSV_B200_NSA_VERIFY_H
 #define SPECSV_B200_NSA_VERIFY_H
