@@ -73,19 +73,22 @@ constexpr int kBarUnion = 9;        // the 12 softmax warps build the union
 constexpr int kUnionThreads = kSoftThreads;
 
 // shared memory map (bytes from the 1024-aligned base)
-constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tile; then P^T of branch A)
+constexpr uint32_t kOffK = 0;        // 2 stages x 32 KB (K tiles: free once their QK is done)
 constexpr uint32_t kOffV = 65536;    // 2 stages x 32 KB
 constexpr uint32_t kOffQ = 131072;   // Q^T [hi | lo] rows, two 64-element K halves of 96 x 128 B
 constexpr uint32_t kQHalf = 2 * kCols * 128;
-constexpr uint32_t kOffPB = kOffQ + 2 * kQHalf;  // P^T of branch B (window): 2 MN atoms x 16 KB
-constexpr uint32_t kOffMisc = kOffPB + 32768;
+// P^T of the tile, N = [first active branch hi | lo | second hi | lo] x 48 columns:
+// 3 MN atoms x 16 KB, so a tile with both token branches (selected + window,
+// whose O accumulators are adjacent in TMEM) is ONE set of N = 192 MMAs
+constexpr uint32_t kOffP = kOffQ + 2 * kQHalf;
+constexpr uint32_t kOffMisc = kOffP + 49152;
 constexpr uint32_t kStageBytes = 32768;
 
 enum Branch { kCmp = 0, kSlc = 1, kWin = 2 };
 enum TileKind { kTileCmp = 0, kTileTok = 1, kTileTree = 2 };
 
 struct Misc {
-  uint64_t k_full[2], v_full[2], kv_empty[2], s_full[2], s_free[2], pv_done[2];
+  uint64_t k_full[2], v_full[2], k_empty[2], v_empty[2], s_full[2], s_free[2], pv_done[2];
   // p_full is double-buffered by tile parity like s_full: a softmax warp may
   // finish tile j + 1 before a slower warp arrives for tile j (tile j + 1 only
   // needs PV(j - 1)), and a single barrier would then complete tile j's phase
@@ -370,9 +373,9 @@ __device__ __forceinline__ void store_cols(uint8_t* base, int row, int n0, const
 }
 
 // P^T of one branch for this warp's 16 columns x its 32 key rows: masked
-// probabilities -> hi at N = c0.., lo at N = nqk + c0.. (bf16), and the
-// warp's column sums added to lacc (lanes 2c, 2c+1 hold column c)
-__device__ __forceinline__ void write_p(uint8_t* pdst, int row, int c0, int nqk, uint32_t cm,
+// probabilities -> hi at N = nb + c0.., lo at N = nb + 48 + c0.. (bf16), and
+// the warp's column sums added to lacc (lanes 2c, 2c+1 hold column c)
+__device__ __forceinline__ void write_p(uint8_t* pdst, int row, int c0, int nb, uint32_t cm,
                                         const float (&pe)[16], float& lacc, int lane) {
   float pv[16];
 #pragma unroll
@@ -386,8 +389,8 @@ __device__ __forceinline__ void write_p(uint8_t* pdst, int row, int c0, int nqk,
     hi[e] = *reinterpret_cast<const uint32_t*>(&h2);
     lo[e] = pack_bf16(a - hf.x, b - hf.y);
   }
-  store_cols(pdst, row, c0, hi);
-  store_cols(pdst, row, nqk + c0, lo);
+  store_cols(pdst, row, nb + c0, hi);
+  store_cols(pdst, row, nb + kCols + c0, lo);
   lacc += reduce16<false>(pv, lane);
 }
 
@@ -441,27 +444,24 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       r0 = 0; r1 = 64;
     }
   };
-  auto issue = [&](int t, int J) {
+  // one K or V stage (v = 0 / 1); a stage is reused for tile J once tile J - 2
+  // released it: K after its QK, V after its PV
+  auto issue = [&](int t, int J, int v) {
     const int st = J & 1;
-    if (J >= 2) mbar_sleep_wait(&m.kv_empty[st], ((J >> 1) + 1) & 1);
-    uint8_t* kdst = smem + kOffK + st * kStageBytes;
-    uint8_t* vdst = smem + kOffV + st * kStageBytes;
-    if (trace && J < 8) p.trace[cta_id * 64 + 8 + J] = globaltimer();
-    mbar_expect_tx(&m.k_full[st], kStageBytes);
-    mbar_expect_tx(&m.v_full[st], kStageBytes);
+    if (J >= 2) mbar_sleep_wait(v ? &m.v_empty[st] : &m.k_empty[st], ((J >> 1) + 1) & 1);
+    uint8_t* dst = smem + (v ? kOffV : kOffK) + st * kStageBytes;
+    uint64_t* full = v ? &m.v_full[st] : &m.k_full[st];
+    if (trace && J < 8 && !v) p.trace[cta_id * 64 + 8 + J] = globaltimer();
+    mbar_expect_tx(full, kStageBytes);
     const CUtensorMap *tk, *tv;
     int r0, r1;
     tile_rows(t, tk, tv, r0, r1);
+    const CUtensorMap* tm = v ? tv : tk;
     const uint64_t pol = l2_evict_first_policy();  // each tile is read once per launch
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      tma_load_3d_hint(kdst + c * 16384, tk, c * 64, kvh, r0, &m.k_full[st], pol);
-      tma_load_3d_hint(kdst + c * 16384 + 8192, tk, c * 64, kvh, r1, &m.k_full[st], pol);
-    }
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      tma_load_3d_hint(vdst + c * 16384, tv, c * 64, kvh, r0, &m.v_full[st], pol);
-      tma_load_3d_hint(vdst + c * 16384 + 8192, tv, c * 64, kvh, r1, &m.v_full[st], pol);
+      tma_load_3d_hint(dst + c * 16384, tm, c * 64, kvh, r0, full, pol);
+      tma_load_3d_hint(dst + c * 16384 + 8192, tm, c * 64, kvh, r1, full, pol);
     }
   };
   // stages issued before the CTA-wide barrier (compressed tiles only)
@@ -482,7 +482,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       for (int i = 0; i < 2; ++i) {
         mbar_init(&m.k_full[i], 1);
         mbar_init(&m.v_full[i], 1);
-        mbar_init(&m.kv_empty[i], 1);
+        mbar_init(&m.k_empty[i], 1);
+        mbar_init(&m.v_empty[i], 1);
         mbar_init(&m.s_full[i], 1);
         mbar_init(&m.s_free[i], 4 * nch);  // the warps of the active column chunks
         mbar_init(&m.pv_done[i], 1);
@@ -494,7 +495,10 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       mbar_init(&m.union_ready, 32);
       m.flag = (p.debug_flags & 1) ? 1 : 0;  // bit 0: force the robust redo (tests)
       fence_mbar_init();
-      for (int j = 0; j < pre; ++j) issue(split + j * S, j);
+      for (int j = 0; j < pre; ++j) {
+        issue(split + j * S, j, 0);
+        issue(split + j * S, j, 1);
+      }
     }
     __syncwarp();
     tmem_alloc<kTmemCols>(&m.tmem_base);
@@ -587,6 +591,11 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     const uint32_t qmask_w = (gw == 32) ? 0xFFFFFFFFu : ((1u << gw) - 1u);
     const uint32_t colvalid = ncols - c0 >= 16 ? 0xFFFFu : (ncols > c0 ? ((1u << (ncols - c0)) - 1u) : 0u);
     const int bar_chunk = kBarChunk0 + ck;               // named barrier of this chunk's 4 warps
+    // REUSE: the index rows are staged at once, so the union is built after
+    // the first compressed tile (whose K and V stages are then free for the
+    // first token tiles) rather than after the last (debug bit 6: after the
+    // last, for A/B timing)
+    const bool union_early = p.idx_early != 0 && !(p.debug_flags & (8 | 64));
     bool union_seen = false;
     int T = 0x7fffffff;
     int J0 = 0;  // tiles of earlier passes (mbarrier phase base)
@@ -613,7 +622,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
 #pragma unroll
           for (int br = 0; br < 3; ++br) {
             tmem_st16(lanebase + kTmemO + kTmemStride * br + c0, z);
-            tmem_st16(lanebase + kTmemO + kTmemStride * br + nqk + c0, z);
+            tmem_st16(lanebase + kTmemO + kTmemStride * br + kCols + c0, z);
           }
         }
         tmem_wait_st();
@@ -624,11 +633,10 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       bool ovf = false;       // fast pass: an active logit above mref + kFastHi
       uint32_t act_ab = 0u;   // fast pass: active columns, cmp (bits 0-15) / slc (16-31)
       uint32_t act_w = 0u;    //            and win (bits 0-15), of this lane
-      bool prev_b = false;    // previous tile wrote the branch-B P region
 #pragma unroll 1
       for (int j = 0; active; ++j) {
         const int t = split + j * S;
-        if (!union_seen && t >= n_cmp) {  // the token tiles need the union
+        if (!union_seen && (t >= n_cmp || (union_early && j == 1))) {  // the token tiles need the union
           coop_union(m, tid, nqc, p.n_sel, p.l_sel, p.rows, cwlo, cwhi);
           if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
           if ((p.debug_flags & 32) && trace && tid == 0) {  // check: a sequential recount of the union
@@ -729,15 +737,13 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
           if (ti.kind == kTileCmp) act_ab |= cm_a; else act_ab |= cm_a << 16;
           act_w |= cm_b;
           if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
+          // the P region is rewritten only after the previous tile's PV read it
+          if (J > 0 && (ti.act_a || ti.act_b)) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
+          if (trace && tid == 0 && j == 3) p.trace[cta_id * 64 + 57] = globaltimer();
           if (ti.act_a)
-            write_p(smem + kOffK + sb * kStageBytes, row, c0, nqk, cm_a, pe,
-                    lacc[ti.kind == kTileCmp ? kCmp : kSlc], lane);
-          if (ti.act_b) {
-            // the shared branch-B P region is rewritten only after the previous
-            // tile's MMAs read it (branch-A P lives in this tile's own K stage)
-            if (j > 0 && prev_b) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
-            write_p(smem + kOffPB, row, c0, nqk, cm_b, pe, lacc[kWin], lane);
-          }
+            write_p(smem + kOffP, row, c0, 0, cm_a, pe, lacc[ti.kind == kTileCmp ? kCmp : kSlc], lane);
+          if (ti.act_b) write_p(smem + kOffP, row, c0, ti.act_a ? 2 * kCols : 0, cm_b, pe, lacc[kWin], lane);
+          if (trace && tid == 0 && j == 3) p.trace[cta_id * 64 + 58] = globaltimer();
         } else {
           // ---- robust pass: lazy running max per active branch; the 4 warps
           // sharing this column chunk vote (columns are independent across chunks)
@@ -782,7 +788,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
             for (int e = 0; e < 16; ++e) al[e] = m.alpha[c0 + e];
 #pragma unroll
             for (int hl = 0; hl < 2; ++hl) {
-              const uint32_t ta = lanebase + kTmemO + kTmemStride * br + (hl ? nqk : 0) + c0;
+              const uint32_t ta = lanebase + kTmemO + kTmemStride * br + (hl ? kCols : 0) + c0;
               uint32_t r[16];
               tmem_ld16(ta, r);
               tmem_wait_ld();
@@ -794,7 +800,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
             lacc[br] *= m.alpha[c0 + (lane >> 1)];
             named_bar_sync(bar_chunk, 128);  // alpha is reused by the other side
           }
-          if (j > 0 && ti.act_b && prev_b && !resc[0] && !resc[1])
+          if (J > 0 && (ti.act_a || ti.act_b) && !resc[0] && !resc[1])  // the P region is free
             mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
 #pragma unroll 1
           for (int side = 0; side < 2; ++side) {
@@ -803,14 +809,14 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
             float pe[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) pe[e] = fast_exp2(s[e] - m.m2[br][c0 + e]);
-            write_p(side == 0 ? smem + kOffK + sb * kStageBytes : smem + kOffPB, row, c0, nqk,
-                    side == 0 ? cm_a : cm_b, pe, lacc[br], lane);
+            write_p(smem + kOffP, row, c0, (side == 1 && ti.act_a) ? 2 * kCols : 0, side == 0 ? cm_a : cm_b,
+                    pe, lacc[br], lane);
           }
         }
-        prev_b = ti.act_b;
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
+        if (trace && tid == 0 && j == 3) p.trace[cta_id * 64 + 60] = globaltimer();
         if (lane == 0) mbar_arrive(&m.p_full[J & 1]);
         if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 32 + j] = globaltimer();
       }
@@ -868,7 +874,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         uint32_t rh[16], rl[16];
         const uint32_t ta = lanebase + kTmemO + kTmemStride * br + c0;
         tmem_ld16(ta, rh);
-        tmem_ld16(ta + nqk, rl);
+        tmem_ld16(ta + kCols, rl);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 16; ++e)
@@ -879,26 +885,47 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
   } else if (warp == kWarpTma) {
     // =================== TMA producer ===================
-    // the first compressed stages went out in the prologue; token tiles wait
-    // for the union warp
+    // One thread polls: a K stage frees at its tile's QK, well before the V
+    // stage of the same tile frees at its PV, so K and V loads go out
+    // independently, each as soon as its stage is free (a blocking in-order
+    // issue would hold the next K behind the previous V).  The first stages
+    // went out in the prologue; token tiles wait for the union.
     int T = 0x7fffffff;
     if (lane == 0) {
-      for (int j = pre;; ++j) {
-        if (T == 0x7fffffff && split + j * S >= n_cmp) {
-          mbar_backoff_wait(&m.union_ready, 0, !(p.debug_flags & 8));
+      const int jtok = n_cmp > split ? (n_cmp - split + S - 1) / S : 0;  // first token tile
+      int nk = pre, nv = pre;
+      bool known = false;
+      for (;;) {
+        if (!known && (nk >= jtok || nv >= jtok) && mbar_test_wait(&m.union_ready, 0)) {
+          known = true;
           T = tile_count();
         }
-        if (j >= T) break;
-        issue(split + j * S, j);
+        const int lim = known ? T : jtok;
+        if (known && nk >= T && nv >= T) break;
+        bool any = false;
+        if (nk < lim && (nk < 2 || mbar_test_wait(&m.k_empty[nk & 1], ((nk >> 1) + 1) & 1))) {
+          issue(split + nk * S, nk, 0);
+          ++nk;
+          any = true;
+        }
+        if (nv < lim && (nv < 2 || mbar_test_wait(&m.v_empty[nv & 1], ((nv >> 1) + 1) & 1))) {
+          issue(split + nv * S, nv, 1);
+          ++nv;
+          any = true;
+        }
+        if (!any) __nanosleep(20);
       }
     }
-    T = __shfl_sync(0xffffffffu, T, 0);
     __syncwarp();
+    T = __shfl_sync(0xffffffffu, T, 0);
     named_bar_sync(kBarPassEnd, kThreads);
     if (m.flag) {  // robust redo: the same tiles again
       named_bar_sync(kBarRedo, kThreads);
       if (lane == 0)
-        for (int j = 0; j < T; ++j) issue(split + j * S, T + j);
+        for (int j = 0; j < T; ++j) {
+          issue(split + j * S, T + j, 0);
+          issue(split + j * S, T + j, 1);
+        }
       __syncwarp();
       named_bar_sync(kBarPassEnd, kThreads);
     }
@@ -916,9 +943,12 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       }
       return j < T;
     };
-    // one MMA per 16-element K step, hi and lo stacked along N
+    // one MMA per 16-element K step, hi and lo stacked along N; PV: one or two
+    // branches (N = 96 / 192, O_slc and O_win adjacent in TMEM)
     const uint32_t idesc_qk = idesc_bf16(128, 2 * nqk, 0, 0);
-    const uint32_t idesc_pv = idesc_bf16(128, 2 * nqk, 1, 1);
+    const uint32_t idesc_pv1 = idesc_bf16(128, 2 * kCols, 1, 1);
+    const uint32_t idesc_pv2 = idesc_bf16(128, 4 * kCols, 1, 1);
+    static_assert(kTmemO + kTmemStride * kSlc + kTmemStride == kTmemO + kTmemStride * kWin, "O_slc | O_win");
     auto qk_pass = [&](int J0) {
       for (int j = 0; tiles(j); ++j) {
         const int J = J0 + j;
@@ -938,6 +968,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
                    idesc_qk, kk != 0);
         }
         umma_commit(&m.s_full[sb]);
+        umma_commit(&m.k_empty[sb]);  // the K stage is free once its QK is done
       }
     };
     auto pv_pass = [&](int J0) {
@@ -950,19 +981,18 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         if (trace && J < 8) p.trace[cta_id * 64 + 40 + J] = globaltimer();
         tc_fence_after();
         const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
-#pragma unroll 1
-        for (int side = 0; side < 2; ++side) {
-          if (!(side == 0 ? ti.act_a : ti.act_b)) continue;
-          const uint32_t pa = side == 0 ? sbase + kOffK + st * kStageBytes : sbase + kOffPB;
-          const int br = side == 0 ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
+        if (ti.act_a || ti.act_b) {
+          const uint32_t pa = sbase + kOffP;
+          const int br = ti.act_a ? (ti.kind == kTileCmp ? kCmp : kSlc) : kWin;
           const uint32_t d = tmem + kTmemO + kTmemStride * br;
+          const uint32_t idesc = (ti.act_a && ti.act_b) ? idesc_pv2 : idesc_pv1;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             umma_f16(d, desc_sw128(vaddr + kk * 2048, 16384, 1024),
-                     desc_sw128(pa + kk * 2048, 16384, 1024), idesc_pv, 1u);
+                     desc_sw128(pa + kk * 2048, 16384, 1024), idesc, 1u);
         }
         umma_commit(&m.pv_done[J & 1]);
-        umma_commit(&m.kv_empty[st]);
+        umma_commit(&m.v_empty[st]);
       }
     };
     if (lane == 0) {

@@ -12,7 +12,7 @@ constexpr int kAttendCols = 48;     // query columns (queries x GQA heads) per a
 constexpr int kAttendDh = 128;      // d_head of this build (host-checked)
 constexpr int kMaxQueries = 65;      // 1 + gamma, gamma <= 64 (one mask word per row)
 constexpr int kMaxChunkQ = 32;       // queries per CTA column chunk (64 cols / G, G >= 2)
-constexpr int kMaxUnion = 1280;      // union blocks per chunk
+constexpr int kMaxUnion = 1024;      // union blocks per chunk
 constexpr int kMaxUnionWords = 1024; // selection-block bitmap words (32768 blocks)
 
 struct AttendParams {

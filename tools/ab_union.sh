@@ -1,5 +1,5 @@
-# A/B: reuse-layer union before the compressed tiles (default) vs after (SPECSV_ATTEND_DEBUG=64)
-TRACE_TILES=1 python tools/trace_step.py 2 2>&1 | grep -A6 "layer  1"
+# A/B: reuse-layer union after the first compressed tile (default) vs after the last (SPECSV_ATTEND_DEBUG=64)
+TRACE_TILES=1 python tools/trace_step.py 2 2>&1 | grep -A9 "layer  1"
 for v in 0 64 0 64; do
   SPECSV_ATTEND_DEBUG=$v timeout 600 python bench.py --steps 20 --warmup 5 --skip-cpu-baseline --skip-decode-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('debug=$v', d['value'], d['e2e']['value'], d['detail']['attend_us_per_launch'])"
 done

@@ -145,6 +145,9 @@ def print_tiles(t):
         print("   union check: %d CTAs checked, %d bad (codes %s)" % ((chk >= 1000).sum(), (chk > 1000).sum(),
                                                                   sorted(set((chk[chk > 1000] - 1000).tolist()))))
     print("   union: index rows in %.2f, built %.2f (us)" % (u[0], u[5]))
+    if (t[:, 57] > 0).sum() > len(t) // 2:
+        print("   tile 3 softmax: exp %.2f, P region free %.2f, P written %.2f, fenced %.2f" %
+              tuple(np.median(rel[:, c][t[:, c] > 0]) for c in (51, 57, 58, 60)))
     if os.environ.get("TRACE_RAW"):
         for i in range(0, len(t), 29):
             print("   cta %3d: " % i + " ".join("%d:%.2f" % (c, rel[i, c]) for c in (59, 56, 1, 24, 25, 26)))
