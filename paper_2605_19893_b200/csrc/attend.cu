@@ -661,6 +661,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
           T = tile_count();
         }
         if (union_seen && j >= T) break;
+        const bool cs = trace && tid == 0 && j == 3 && !robust;  // cycle stamps of one tile (debug)
+        const long long cb = cs ? clock64() : 0;
         const int J = J0 + j;
         const int sb = J & 1;
         const TileInfo ti = tile_info(m, n_cmp, t, cwlo, cwhi, p.l_sel);
@@ -700,7 +702,9 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         if (!ti.act_b) cm_b = 0u;
         // S^T rows of this quadrant, this warp's 16 columns (log2 units): hi + lo halves
         float s[16];
+        if (cs) p.trace[cta_id * 64 + 29] = clock64() - cb;
         mbar_sleep_wait(&m.s_full[sb], (J >> 1) & 1);
+        if (cs) p.trace[cta_id * 64 + 30] = clock64() - cb;
         if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 24 + j] = globaltimer();
         tc_fence_after();
         {
@@ -715,6 +719,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&m.s_free[sb]);
+        if (cs) p.trace[cta_id * 64 + 31] = clock64() - cb;
 
         if (!robust) {
           // ---- fast pass: one exp per element, shared by both branches ----
@@ -738,12 +743,13 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
           act_w |= cm_b;
           if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
           // the P region is rewritten only after the previous tile's PV read it
+          if (cs) p.trace[cta_id * 64 + 37] = clock64() - cb;
           if (J > 0 && (ti.act_a || ti.act_b)) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
-          if (trace && tid == 0 && j == 3) p.trace[cta_id * 64 + 57] = globaltimer();
+          if (cs) p.trace[cta_id * 64 + 38] = clock64() - cb;
           if (ti.act_a)
             write_p(smem + kOffP, row, c0, 0, cm_a, pe, lacc[ti.kind == kTileCmp ? kCmp : kSlc], lane);
           if (ti.act_b) write_p(smem + kOffP, row, c0, ti.act_a ? 2 * kCols : 0, cm_b, pe, lacc[kWin], lane);
-          if (trace && tid == 0 && j == 3) p.trace[cta_id * 64 + 58] = globaltimer();
+          if (cs) p.trace[cta_id * 64 + 39] = clock64() - cb;
         } else {
           // ---- robust pass: lazy running max per active branch; the 4 warps
           // sharing this column chunk vote (columns are independent across chunks)
@@ -816,8 +822,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (trace && tid == 0 && j == 3) p.trace[cta_id * 64 + 60] = globaltimer();
         if (lane == 0) mbar_arrive(&m.p_full[J & 1]);
+        if (cs) p.trace[cta_id * 64 + 47] = clock64() - cb;
         if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 32 + j] = globaltimer();
       }
       if (!union_seen) {  // a warp without columns: it still takes part in the union build, once
@@ -905,15 +911,18 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         bool any = false;
         if (nk < lim && (nk < 2 || mbar_test_wait(&m.k_empty[nk & 1], ((nk >> 1) + 1) & 1))) {
           issue(split + nk * S, nk, 0);
+          if (trace && (nk == 2 || nk == 3)) p.trace[cta_id * 64 + (nk == 2 ? 56 : 60)] = globaltimer();
           ++nk;
           any = true;
         }
         if (nv < lim && (nv < 2 || mbar_test_wait(&m.v_empty[nv & 1], ((nv >> 1) + 1) & 1))) {
+          if (trace && nv == 2) p.trace[cta_id * 64 + 57] = globaltimer();
           issue(split + nv * S, nv, 1);
+          if (trace && nv == 2) p.trace[cta_id * 64 + 58] = globaltimer();
           ++nv;
           any = true;
         }
-        if (!any) __nanosleep(20);
+        if (!any && (p.debug_flags & 128)) __nanosleep(20);
       }
     }
     __syncwarp();

@@ -146,11 +146,15 @@ def print_tiles(t):
                                                                   sorted(set((chk[chk > 1000] - 1000).tolist()))))
     print("   union: index rows in %.2f, built %.2f (us)" % (u[0], u[5]))
     if (t[:, 57] > 0).sum() > len(t) // 2:
-        print("   tile 3 softmax: exp %.2f, P region free %.2f, P written %.2f, fenced %.2f" %
-              tuple(np.median(rel[:, c][t[:, c] > 0]) for c in (51, 57, 58, 60)))
+        print("   producer: K2 %.2f-%.2f, V2 %.2f-%.2f, K3 %.2f-%.2f" %
+              tuple(np.median(rel[:, c][t[:, c] > 0]) for c in (10, 56, 57, 58, 11, 60)))
     if os.environ.get("TRACE_RAW"):
         for i in range(0, len(t), 29):
             print("   cta %3d: " % i + " ".join("%d:%.2f" % (c, rel[i, c]) for c in (59, 56, 1, 24, 25, 26)))
+    cyc = [int(np.median(t[:, c][t[:, c] > 0])) if (t[:, c] > 0).sum() > len(t) // 4 else -1
+           for c in (29, 30, 31, 37, 38, 39, 47)]
+    print("   softmax tile 3 (SM cycles from loop top): masks %d, S in %d, S read %d, exp %d, P free %d, "
+          "P written %d, handed over %d" % tuple(cyc))
     print("   tile " + " ".join(f"{n:>8s}" for n, _ in cols))
     for j in range(8):
         vals = []
