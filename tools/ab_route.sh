@@ -1,4 +1,3 @@
-# quick A/B of the routing kernel: timeline, timing, parity of the routing-heavy tests
-python tools/trace_route.py > gpurun_out/tr.log 2>&1
-python tools/time_route.py >> gpurun_out/tr.log 2>&1
-python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2 > gpurun_out/ab_tests.txt
+# route3 phases + step numbers
+python tools/time_route3.py 2>&1 | tail -16
+for i in 1 2 3; do timeout 600 python bench.py --steps 30 --warmup 5 --skip-cpu-baseline --skip-decode-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],1), round(d['e2e']['value'],1), round(d['detail']['route_us_per_launch'],2), round(d['detail']['attend_us_per_launch'],2))"; done
