@@ -656,68 +656,90 @@ def run_ours(a, world: int, rank: int, local: int):
     slots = list(range(acc)) + ([acc] if acc < g else [])  # accepted drafts, then the bonus root's row
     host_s = [0.0]
     n_calls = [0]
-    # one prepared C-ABI call per layer (ctypes arguments built once; rows and
-    # positions refreshed per step)
-    prepared = []
-    for j in range(L):
-        src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
-        prepared.append(V.PreparedVerify(
-            cfg, [caches[r][j] for r in range(R)], [batches[r][j] for r in range(R)],
-            [sets[r][src] for r in range(R)], [outs[r][j] for r in range(R)], ws, a.group, mode,
-            int(roles[j]), kv_heads=heads if R > 1 else heads[0]))
+    # Two device input sets (parity b = step % 2): while step s verifies from
+    # set b, step s+1's inputs are copied host->device into set 1-b on a copy
+    # stream (every timed step still copies one step's inputs and reads one
+    # output back; the first timed step's inputs were copied by the last
+    # warm-up step, the last timed step copies inputs no step uses).
+    inbufs2 = [t.clone() for t in inbufs]
+    batches2 = []
+    for r in range(R):
+        views = [inbufs2[r][:, o:o + nb].view(dt).view(L, *sh)
+                 for (sh, dt), nb, o in zip(parts, sizes, offs)]
+        batches2.append([V.DraftBatch(pos=batches[r][j].pos, tree_mask=tmask, q=views[0][j],
+                                      gates=views[1][j], tree_k=views[2][j], tree_v=views[3][j])
+                         for j in range(L)])
+    sets_in = [(inbufs, batches), (inbufs2, batches2)]
+    # one prepared C-ABI call per layer and input set (ctypes arguments built
+    # once; rows and positions refreshed per step)
+    prepared = [[], []]
+    for b, (_, bset) in enumerate(sets_in):
+        for j in range(L):
+            src = j if roles[j] == V.ROLE_REFRESH else int(source[j])
+            prepared[b].append(V.PreparedVerify(
+                cfg, [caches[r][j] for r in range(R)], [bset[r][j] for r in range(R)],
+                [sets[r][src] for r in range(R)], [outs[r][j] for r in range(R)], ws, a.group, mode,
+                int(roles[j]), kv_heads=heads if R > 1 else heads[0]))
     copy_stream = torch.cuda.Stream(device=dev)
-    # layers per host->device copy: geometric 1, 1, 2, 4, ... so layer 0 waits
-    # for one small copy and later copies overlap earlier layers' kernels
-    groups, j0 = [], 0
-    while j0 < L:
-        groups.append((j0, min(L, j0 + max(1, j0))))
-        j0 = groups[-1][1]
+    ready = [torch.cuda.Event(), torch.cuda.Event()]  # set b's inputs landed
+    done = [torch.cuda.Event(), torch.cuda.Event()]   # set b's readers (verify + commit) finished
+    out_ready = torch.cuda.Event()
 
-    commits = [TR.PreparedCommit(cfg, caches[r], [batches[r][j].tree_k for j in range(L)],
-                                 [batches[r][j].tree_v for j in range(L)], slots, pes[r])
-               for r in range(R)] if slots else []
+    commits = [[TR.PreparedCommit(cfg, caches[r], [bset[r][j].tree_k for j in range(L)],
+                                  [bset[r][j].tree_v for j in range(L)], slots, pes[r])
+                for r in range(R)] if slots else [] for _, bset in sets_in]
     host_parts = {"copies": 0.0, "verify_calls": 0.0, "readback": 0.0, "commit": 0.0}
     host_role = {int(V.ROLE_REFRESH): 0.0, int(V.ROLE_REUSE): 0.0}
 
     variant = os.environ.get("SPECSV_E2E_VARIANT", "")  # diagnostics only: drop one part of the step
 
+    def copy_inputs(s_no, cur):
+        """host->device copy of step s_no's inputs into set s_no % 2, on the copy
+        stream, once that set's previous readers (step s_no - 2) are done"""
+        b = s_no % 2
+        hin = hin_ring[s_no % ring]
+        copy_stream.wait_event(done[b])
+        with torch.cuda.stream(copy_stream):
+            if variant != "nocopy":
+                for r in range(R):
+                    sets_in[b][0][r].copy_(hin[r], non_blocking=True)
+            ready[b].record(copy_stream)
+
     def e2e_step():
         tA = time.perf_counter()
-        hin = hin_ring[step_no[0] % ring]
+        s_no = step_no[0]
         step_no[0] += 1
+        b = s_no % 2
         cur = torch.cuda.current_stream()
-        copy_stream.wait_stream(cur)  # the previous step's readers of the inputs are done
-        ready = []
-        with torch.cuda.stream(copy_stream):
-            for g0, g1 in groups:
-                if variant != "nocopy":
-                    for r in range(R):
-                        inbufs[r][g0:g1].copy_(hin[r][g0:g1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy_stream)
-                ready.append(ev)
+        if s_no == 0:  # (the first warm-up step copies its own inputs)
+            for k in (0, 1):
+                done[k].record(cur)
+            copy_inputs(0, cur)
+        copy_inputs(s_no + 1, cur)  # the next step's inputs, under this step's kernels
         tB = time.perf_counter()
-        gi = 0
+        cur.wait_event(ready[b])
         for j in range(L):
-            if gi < len(groups) and j == groups[gi][0]:
-                cur.wait_event(ready[gi])
-                gi += 1
             t0 = time.perf_counter()
-            prepared[j].run()
+            prepared[b][j].run()
             dt = time.perf_counter() - t0
             host_s[0] += dt
             n_calls[0] += 1
             host_role[int(roles[j])] += dt
         tC = time.perf_counter()
-        if variant != "nod2h":
-            for r in range(R):
-                hout[r].copy_(outs[r][L - 1], non_blocking=True)
+        if variant != "nod2h":  # the step's result, read back on the copy stream
+            out_ready.record(cur)
+            copy_stream.wait_event(out_ready)
+            with torch.cuda.stream(copy_stream):
+                for r in range(R):
+                    hout[r].copy_(outs[r][L - 1], non_blocking=True)
         tD = time.perf_counter()
-        for r, pc in enumerate(commits if variant != "nocommit" else []):  # commit: rows + positions advance
+        for r, pc in enumerate(commits[b] if variant != "nocommit" else []):  # rows + positions advance
             pc.run(cur)
             new_pos = np.array([caches[r][0].rows - 1 + i for i in range(nq)], np.int64)
             for j in range(L):
                 batches[r][j].pos = new_pos
+                batches2[r][j].pos = new_pos
+        done[b].record(cur)
         tE = time.perf_counter()
         host_parts["copies"] += tB - tA
         host_parts["verify_calls"] += tC - tB
