@@ -1050,8 +1050,17 @@ cudaError_t launch_route3_n(const Route3LaunchT<NR>& p, int ctas, cudaStream_t s
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  attr[na].id = cudaLaunchAttributeCooperative;  // arrival waits: every CTA co-resident
-  attr[na++].val.cooperative = 1;
+  // CTAs wait on each other's arrivals, so every CTA must be resident (the
+  // host sizes the grid to one CTA per SM).  Under programmatic dependent
+  // launch the cooperative attribute is dropped, as for the attend launch:
+  // CTAs are then placed as the previous launch's CTAs retire, and all of them
+  // become resident because nothing the previous launch waits on depends on
+  // this grid (with the attribute, eager launches started ~2-3 us later).
+  // (debug bit 4 keeps it, for A/B timing)
+  if (!pdl_enabled() || (p.debug & 16)) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
   if (pdl_enabled()) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na++].val.programmaticStreamSerializationAllowed = 1;

@@ -63,6 +63,20 @@ def main():
 
     step(False)
     torch.cuda.synchronize()
+    if os.environ.get("TRACE_EAGER"):  # the same calls issued eagerly (no graph)
+        for _ in range(3):
+            step(False)
+        torch.cuda.synchronize()
+        for bb in bufs:
+            bb.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(True)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"step of {L} layers: {e0.elapsed_time(e1) * 1e3:.1f} us (traced, eager)")
+        report(L, bufs)
+        return
     graph = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream(device=dev)
     s.wait_stream(torch.cuda.current_stream())
@@ -81,6 +95,10 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     print(f"step of {L} layers: {e0.elapsed_time(e1) * 1e3:.1f} us (traced)")
+    report(L, bufs)
+
+
+def report(L, bufs):
     t_first = None
     prev_end = None
     for j in range(L):
