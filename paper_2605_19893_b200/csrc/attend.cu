@@ -1190,7 +1190,10 @@ cudaError_t launch_attend_batch(const AttendBatch& b, int n_splits, int n_heads,
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (cooperative) {  // split CTAs of a head meet at a barrier
+  // split CTAs of a head meet at a barrier (the host checks the grid fits the
+  // device); under programmatic dependent launch the attribute is dropped as
+  // in launch_attend below
+  if (cooperative && (!pdl_enabled() || debug_env().attend_coop)) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na++].val.cooperative = 1;
   }
