@@ -43,6 +43,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
             cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+            if os.environ.get("SPECSV_TRACE_TILES"):  # diagnostics build: per-tile stamps (--force)
+                cmd.append("-DSPECSV_TRACE_TILES")
             if src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"] if verbose else []
             if verbose:

@@ -122,6 +122,21 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// per-tile trace stamps: compiled only into a diagnostics build
+// (SPECSV_TRACE_TILES=1 python -m paper_2605_19893_b200.build --force) -- even
+// untaken, their predicates and addresses cost ~15% of a softmax warp's
+// instructions per tile; the per-CTA stamps below stay in every build
+#ifdef SPECSV_TRACE_TILES
+#define TILE_STAMP(cond, slot, val)                            \
+  do {                                                         \
+    if (cond) p.trace[cta_id * 64 + (slot)] = (val);           \
+  } while (0)
+#else
+#define TILE_STAMP(cond, slot, val) \
+  do {                              \
+  } while (0)
+#endif
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -451,7 +466,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     if (J >= 2) mbar_sleep_wait(v ? &m.v_empty[st] : &m.k_empty[st], ((J >> 1) + 1) & 1);
     uint8_t* dst = smem + (v ? kOffV : kOffK) + st * kStageBytes;
     uint64_t* full = v ? &m.v_full[st] : &m.k_full[st];
-    if (trace && J < 8 && !v) p.trace[cta_id * 64 + 8 + J] = globaltimer();
+    TILE_STAMP(trace && J < 8 && !v, 8 + J, globaltimer());
     mbar_expect_tx(full, kStageBytes);
     const CUtensorMap *tk, *tv;
     int r0, r1;
@@ -661,8 +676,10 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
           T = tile_count();
         }
         if (union_seen && j >= T) break;
-        const bool cs = trace && tid == 0 && j == 3 && !robust;  // cycle stamps of one tile (debug)
+#ifdef SPECSV_TRACE_TILES
+        const bool cs = trace && tid == 0 && j == 3 && !robust;  // cycle stamps of one tile
         const long long cb = cs ? clock64() : 0;
+#endif
         const int J = J0 + j;
         const int sb = J & 1;
         const TileInfo ti = tile_info(m, n_cmp, t, cwlo, cwhi, p.l_sel);
@@ -702,10 +719,10 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         if (!ti.act_b) cm_b = 0u;
         // S^T rows of this quadrant, this warp's 16 columns (log2 units): hi + lo halves
         float s[16];
-        if (cs) p.trace[cta_id * 64 + 29] = clock64() - cb;
+        TILE_STAMP(cs, 29, clock64() - cb);
         mbar_sleep_wait(&m.s_full[sb], (J >> 1) & 1);
-        if (cs) p.trace[cta_id * 64 + 30] = clock64() - cb;
-        if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 24 + j] = globaltimer();
+        TILE_STAMP(cs, 30, clock64() - cb);
+        TILE_STAMP(trace && tid == 0 && j < 8 && !robust, 24 + j, globaltimer());
         tc_fence_after();
         {
           uint32_t rh[16], rl[16];
@@ -719,7 +736,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&m.s_free[sb]);
-        if (cs) p.trace[cta_id * 64 + 31] = clock64() - cb;
+        TILE_STAMP(cs, 31, clock64() - cb);
 
         if (!robust) {
           // ---- fast pass: one exp per element, shared by both branches ----
@@ -741,15 +758,15 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
           ovf |= mx > kFastHi;
           if (ti.kind == kTileCmp) act_ab |= cm_a; else act_ab |= cm_a << 16;
           act_w |= cm_b;
-          if (trace && tid == 0 && j < 8) p.trace[cta_id * 64 + 48 + j] = globaltimer();
+          TILE_STAMP(trace && tid == 0 && j < 8, 48 + j, globaltimer());
           // the P region is rewritten only after the previous tile's PV read it
-          if (cs) p.trace[cta_id * 64 + 37] = clock64() - cb;
+          TILE_STAMP(cs, 37, clock64() - cb);
           if (J > 0 && (ti.act_a || ti.act_b)) mbar_sleep_wait(&m.pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
-          if (cs) p.trace[cta_id * 64 + 38] = clock64() - cb;
+          TILE_STAMP(cs, 38, clock64() - cb);
           if (ti.act_a)
             write_p(smem + kOffP, row, c0, 0, cm_a, pe, lacc[ti.kind == kTileCmp ? kCmp : kSlc], lane);
           if (ti.act_b) write_p(smem + kOffP, row, c0, ti.act_a ? 2 * kCols : 0, cm_b, pe, lacc[kWin], lane);
-          if (cs) p.trace[cta_id * 64 + 39] = clock64() - cb;
+          TILE_STAMP(cs, 39, clock64() - cb);
         } else {
           // ---- robust pass: lazy running max per active branch; the 4 warps
           // sharing this column chunk vote (columns are independent across chunks)
@@ -823,8 +840,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&m.p_full[J & 1]);
-        if (cs) p.trace[cta_id * 64 + 47] = clock64() - cb;
-        if (trace && tid == 0 && j < 8 && !robust) p.trace[cta_id * 64 + 32 + j] = globaltimer();
+        TILE_STAMP(cs, 47, clock64() - cb);
+        TILE_STAMP(trace && tid == 0 && j < 8 && !robust, 32 + j, globaltimer());
       }
       if (!union_seen) {  // a warp without columns: it still takes part in the union build, once
         coop_union(m, tid, nqc, p.n_sel, p.l_sel, p.rows, cwlo, cwhi);
@@ -911,14 +928,14 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         bool any = false;
         if (nk < lim && (nk < 2 || mbar_test_wait(&m.k_empty[nk & 1], ((nk >> 1) + 1) & 1))) {
           issue(split + nk * S, nk, 0);
-          if (trace && (nk == 2 || nk == 3)) p.trace[cta_id * 64 + (nk == 2 ? 56 : 60)] = globaltimer();
+          TILE_STAMP(trace && (nk == 2 || nk == 3), nk == 2 ? 56 : 60, globaltimer());
           ++nk;
           any = true;
         }
         if (nv < lim && (nv < 2 || mbar_test_wait(&m.v_empty[nv & 1], ((nv >> 1) + 1) & 1))) {
-          if (trace && nv == 2) p.trace[cta_id * 64 + 57] = globaltimer();
+          TILE_STAMP(trace && nv == 2, 57, globaltimer());
           issue(split + nv * S, nv, 1);
-          if (trace && nv == 2) p.trace[cta_id * 64 + 58] = globaltimer();
+          TILE_STAMP(trace && nv == 2, 58, globaltimer());
           ++nv;
           any = true;
         }
@@ -964,7 +981,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         const int sb = J & 1;
         if (J >= 2) mbar_sleep_wait(&m.s_free[sb], ((J >> 1) + 1) & 1);
         mbar_sleep_wait(&m.k_full[sb], (J >> 1) & 1);
-        if (trace && J < 8) p.trace[cta_id * 64 + 16 + J] = globaltimer();
+        TILE_STAMP(trace && J < 8, 16 + J, globaltimer());
         tc_fence_after();
         const uint32_t kaddr = sbase + kOffK + sb * kStageBytes;
         const uint32_t qaddr = sbase + kOffQ;
@@ -987,7 +1004,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         mbar_sleep_wait(&m.p_full[J & 1], (J >> 1) & 1);
         const TileInfo ti = tile_info(m, n_cmp, split + j * S, cwlo, cwhi, p.l_sel);
         mbar_sleep_wait(&m.v_full[st], (J >> 1) & 1);
-        if (trace && J < 8) p.trace[cta_id * 64 + 40 + J] = globaltimer();
+        TILE_STAMP(trace && J < 8, 40 + J, globaltimer());
         tc_fence_after();
         const uint32_t vaddr = sbase + kOffV + st * kStageBytes;
         if (ti.act_a || ti.act_b) {
