@@ -359,11 +359,13 @@ __device__ __forceinline__ void issue_unit_tma(const Route3Req& R, const Unit& U
 
 template <class LaunchT>
 __device__ __forceinline__ void stamp(const LaunchT& P, int k) {
+#ifdef SPECSV_TRACE_TILES  // phase stamps: diagnostics build only (see attend.cu)
   if (P.trace != nullptr && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     P.trace[kRouteTraceBase + blockIdx.x * 16 + k] = t;
   }
+#endif
 }
 
 // ------------------------------------------------------------------ Top-n
@@ -997,6 +999,7 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const bool flagged = bb >= kBoundFlag;
     const double delta = flagged ? 0.0 : __longlong_as_double((long long)bb);
     const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-10;
+#ifdef SPECSV_TRACE_TILES
     const long long c0 = clock64();
     select_topn(sel, surv, avail, P.n, eps, m,
                 P.trace != nullptr ? P.trace + kRouteTraceBase + blockIdx.x * 16 : nullptr);
@@ -1006,6 +1009,9 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       select_topn(sel, surv, avail, P.n, eps, m);
       stamp(P, 13);
     }
+#else
+    select_topn(sel, surv, avail, P.n, eps, m);
+#endif
     if (flagged || !m.certified || P.force_exact) {
       if (tid == 0 && P.fallbacks != nullptr) atomicAdd(P.fallbacks, 1);
       exact_scores(P, R, slot, sel, smem, m, ex_seq);

@@ -1,9 +1,11 @@
-# same-box A/B of the working attend.cu against .ab/attend_base.cu (two builds)
-b() { timeout 600 python bench.py --steps 30 --warmup 5 --skip-cpu-baseline --skip-decode-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['value'],1), round(d['e2e']['value'],1), round(d['detail']['attend_us_per_launch'],2))"; }
-F=paper_2605_19893_b200/csrc/attend.cu
-cp $F /tmp/attend_new.cu
+# same-box A/B of a working source file against .ab/<name>_base.cu (two builds):
+#   bash tools/ab_src.sh attend|route3
+N=${1:-attend}
+b() { timeout 600 python bench.py --steps 30 --warmup 5 --skip-cpu-baseline --skip-decode-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['value'],1), round(d['e2e']['value'],1), round(d['detail']['route_us_per_launch'],2), round(d['detail']['attend_us_per_launch'],2))"; }
+F=paper_2605_19893_b200/csrc/$N.cu
+cp $F /tmp/new.cu
 for i in 1 2; do
-  cp /tmp/attend_new.cu $F; python -m paper_2605_19893_b200.build > /dev/null 2>&1; b new
-  cp .ab/attend_base.cu $F; python -m paper_2605_19893_b200.build > /dev/null 2>&1; b base
+  cp /tmp/new.cu $F; python -m paper_2605_19893_b200.build > /dev/null 2>&1; b new
+  cp .ab/${N}_base.cu $F; python -m paper_2605_19893_b200.build > /dev/null 2>&1; b base
 done
-cp /tmp/attend_new.cu $F; python -m paper_2605_19893_b200.build > /dev/null 2>&1
+cp /tmp/new.cu $F; python -m paper_2605_19893_b200.build > /dev/null 2>&1

@@ -4,6 +4,10 @@ shape -- route3_kernel (default) vs route_fused_kernel (SPECSV_ROUTE_LEGACY=1)
 plus route3's exact re-scoring count and per-phase stamps.
 
     python tools/time_route3.py [ctx] [gamma]
+
+The per-phase stamps need the diagnostics build
+(SPECSV_TRACE_TILES=1 python -m paper_2605_19893_b200.build --force);
+the default build prints the launch timings only.
 """
 import os
 import sys

@@ -5,6 +5,11 @@ stamps (specsv_debug_attend_trace; one trace buffer per layer).
 
     python tools/trace_step.py [layers] [ctx] [gamma]
 
+Per-tile columns (TRACE_TILES=1), the routing phases and the union / producer
+stamps need the diagnostics build (SPECSV_TRACE_TILES=1 python -m
+paper_2605_19893_b200.build --force); the per-CTA attend phases are in every
+build.
+
 Prints, per layer, the attend kernel's first-CTA start, the median/max CTA
 phase times (union built, tile loop done, partials written, barrier passed,
 merge done, relative to the first CTA start) and the gap to the previous
