@@ -116,16 +116,17 @@ struct Misc {
 static_assert(sizeof(Misc) + kOffMisc + 1024 <= 232448, "shared memory budget");
 static_assert(kTmemO + 3 * kTmemStride <= (int)kTmemCols, "TMEM budget");
 
-__device__ __forceinline__ uint64_t globaltimer() {
+[[maybe_unused]] __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
-// per-tile trace stamps: compiled only into a diagnostics build
-// (SPECSV_TRACE_TILES=1 python -m paper_2605_19893_b200.build --force) -- even
-// untaken, their predicates and addresses cost ~15% of a softmax warp's
-// instructions per tile; the per-CTA stamps below stay in every build
+// trace stamps (specsv_debug_attend_trace): compiled only into a diagnostics
+// build (SPECSV_TRACE_TILES=1 python -m paper_2605_19893_b200.build --force)
+// -- even untaken, the per-tile ones cost ~15% of a softmax warp's
+// instructions per tile, and the trace pointer and CTA id they keep live cost
+// registers in the tile loop
 #ifdef SPECSV_TRACE_TILES
 #define TILE_STAMP(cond, slot, val)                            \
   do {                                                         \
@@ -439,7 +440,9 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
   const int nqk = (ncols + 15) & ~15;  // hi columns; lo columns follow at nqk
   const int nch = nqk >> 4;            // 16-column chunks holding valid columns
   const int gshift = __ffs(p.G) - 1;
+#ifdef SPECSV_TRACE_TILES
   const bool trace = p.trace != nullptr;
+#endif
   const int n_cmp = p.ch_ncmp[chunk];  // compressed tiles do not depend on the union
   const int cwlo = p.ch_wlo[chunk], cwhi = p.ch_whi[chunk];
   const bool has_tree = (p.gamma > 0) && (q0 + nqc > 1);
@@ -548,7 +551,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = m.tmem_base;
-  if (trace && tid == 0) p.trace[cta_id * 64 + 0] = globaltimer();
+  TILE_STAMP(trace && tid == 0, 0, globaltimer());
 
   if (warp < kSoftWarps) {
     const int qd = warp & 3, ck = warp >> 2;  // TMEM lane quadrant, column chunk
@@ -591,11 +594,11 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
           *reinterpret_cast<uint4*>(half + sw128_off(nqk + c, u16 & 7)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
       }
-      if (trace && tid == 0) p.trace[cta_id * 64 + 61] = globaltimer();
+      TILE_STAMP(trace && tid == 0, 61, globaltimer());
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&m.q_ready);
-      if (trace && tid == 0) p.trace[cta_id * 64 + 5] = globaltimer();
+      TILE_STAMP(trace && tid == 0, 5, globaltimer());
     }
 
     // =================== passes over this CTA's tiles ===================
@@ -653,7 +656,8 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         const int t = split + j * S;
         if (!union_seen && (t >= n_cmp || (union_early && j == 1))) {  // the token tiles need the union
           coop_union(m, tid, nqc, p.n_sel, p.l_sel, p.rows, cwlo, cwhi);
-          if (trace && tid == 0) p.trace[cta_id * 64 + 1] = globaltimer();
+          TILE_STAMP(trace && tid == 0, 1, globaltimer());
+#ifdef SPECSV_TRACE_TILES
           if ((p.debug_flags & 32) && trace && tid == 0) {  // check: a sequential recount of the union
             int bad = 0, cnt = 0, prev = -1;
             const int nsel = (p.rows + p.l_sel - 1) / p.l_sel;
@@ -672,6 +676,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
             if (cnt != m.n_union) bad |= 4;
             p.trace[cta_id * 64 + 63] = 1000 + bad;
           }
+#endif
           union_seen = true;
           T = tile_count();
         }
@@ -848,7 +853,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
         union_seen = true;
         T = tile_count();
       }
-      if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 2] = globaltimer();
+      TILE_STAMP(trace && tid == 0 && !robust, 2, globaltimer());
       // ---- end of pass: branch row sums, then the fast-pass check ----
       if ((lane & 1) == 0) {
 #pragma unroll
@@ -875,9 +880,9 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       }
       // the O accumulators are final once the last PV of the pass completed
       if (active && T > 0) mbar_sleep_wait(&m.pv_done[(J0 + T - 1) & 1], ((J0 + T - 1) >> 1) & 1);
-      if (trace && tid == 0 && !robust) p.trace[cta_id * 64 + 7] = globaltimer();
+      TILE_STAMP(trace && tid == 0 && !robust, 7, globaltimer());
       named_bar_sync(kBarPassEnd, kThreads);  // pass end: the redo decision is visible to every role
-      if (trace && tid == 0) p.trace[cta_id * 64 + 62 + pass] = (unsigned long long)m.flag;
+      TILE_STAMP(trace && tid == 0, 62 + pass, (unsigned long long)m.flag);
       if (!m.flag) break;
       J0 += T;
     }
@@ -905,7 +910,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
             ws_o[((int64_t)br * kCols + c0 + e) * kDh + row] = __uint_as_float(rh[e]) + __uint_as_float(rl[e]);
       }
     }
-    if (trace && tid == 0) p.trace[cta_id * 64 + 3] = globaltimer();
+    TILE_STAMP(trace && tid == 0, 3, globaltimer());
   } else if (warp == kWarpTma) {
     // =================== TMA producer ===================
     // One thread polls: a K stage frees at its tile's QK, well before the V
@@ -1057,7 +1062,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
     }
     cp_async_wait_all();
     __syncwarp();
-    if (trace && lane == 0) p.trace[cta_id * 64 + 59] = globaltimer();
+    TILE_STAMP(trace && lane == 0, 59, globaltimer());
     mbar_arrive(&m.rows_ready);  // the softmax warps build the union from them
     named_bar_sync(kBarPassEnd, kThreads);
     if (m.flag) {
@@ -1071,7 +1076,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
   if (S > 1) {
     int* sync = reinterpret_cast<int*>(p.ws + p.ws_sync_offset) + 2 * (chunk * p.Hkv + kvh);
     group_barrier(sync, sync + 1, S, tid);
-    if (trace && tid == 0) p.trace[cta_id * 64 + 6] = globaltimer();
+    TILE_STAMP(trace && tid == 0, 6, globaltimer());
   } else {
     __syncthreads();
   }
@@ -1138,7 +1143,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
             make_float2((a0.x + a1.x) + a2.x, (a0.y + a1.y) + a2.y);
       }
     }
-    if (trace && tid == 0) p.trace[cta_id * 64 + 4] = globaltimer();
+    TILE_STAMP(trace && tid == 0, 4, globaltimer());
   }
   tc_fence_before();
   __syncthreads();
