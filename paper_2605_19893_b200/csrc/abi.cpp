@@ -103,7 +103,8 @@ int qc_size_for(const specsv_nsa_config& c);
 int splits_for(const specsv_nsa_config& c, int32_t nq, int n_heads) {
   const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
   const int groups = n_heads * nchunks;
-  return std::max(1, std::min(18, coresident_for_device() / groups));
+  const int cap = debug_env().attend_splits > 0 ? std::min(18, debug_env().attend_splits) : 18;
+  return std::max(1, std::min(cap, coresident_for_device() / groups));
 }
 
 // KV heads of a call: [begin, begin + count), count 0 = all

@@ -44,6 +44,7 @@ void refresh_debug_env() {
     else if (name == "ATTEND_COOP") e.attend_coop = one;
     else if (name == "ROUTE3_DEBUG") e.route3_debug = std::atoi(val);
     else if (name == "ATTEND_DEBUG") e.attend_debug = std::atoi(val);
+    else if (name == "ATTEND_SPLITS") e.attend_splits = std::atoi(val);
   }
   g_env = e;
 }

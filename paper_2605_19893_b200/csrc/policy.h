@@ -28,6 +28,7 @@ struct DebugEnv {
   bool attend_coop = false;     // SPECSV_ATTEND_COOP=1: cooperative attend launches under PDL
   int route3_debug = 0;         // SPECSV_ROUTE3_DEBUG
   int attend_debug = 0;         // SPECSV_ATTEND_DEBUG
+  int attend_splits = 0;        // SPECSV_ATTEND_SPLITS=k: at most k split CTAs per head (timing)
 };
 const DebugEnv& debug_env();
 void refresh_debug_env();
