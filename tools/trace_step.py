@@ -144,6 +144,13 @@ def report(L, bufs):
                  f" bar {ph(6)[0]:5.2f} merge {ph(4)[0]:5.2f}/{ph(4)[1]:5.2f} ctas {len(t)}")
         prev_end = end
         print(line)
+        if os.environ.get("TRACE_HEADS"):  # per KV head (CTA id = head * 18 + split)
+            full = bufs[j][:RBASE].view(-1, 64).cpu().numpy()[:144]
+            for h in range(8):
+                hb = full[h * 18:(h + 1) * 18]
+                st, le = (hb[:, 0] - t0) / 1e3, (hb[:, 2] - t0) / 1e3
+                print(f"   head {h}: start {st.min():5.2f}-{st.max():5.2f} loop end med {np.median(le):5.2f} "
+                      f"max {le.max():5.2f} (split {int(le.argmax())}) merge {((hb[:, 4] - t0) / 1e3).max():5.2f}")
         if os.environ.get("TRACE_TILES"):
             print_tiles(t)
         if os.environ.get("TRACE_SPLITS"):
