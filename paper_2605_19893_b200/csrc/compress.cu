@@ -75,6 +75,36 @@ __device__ void write_digit_row(const float (&fk)[kPer], int dh, int8_t* ckd, in
   if (threadIdx.x == 0) ckexp[row] = (e & 0xFFFF) | (min(inexact, 255) << 16);
 }
 
+// fp64 sums of one compressed block's l rows (key + positional embedding,
+// value) for element x, in the reference's order (nsa_cache.cpp); the loads of
+// eight rows go out together ahead of their (ordered) adds
+__device__ __forceinline__ void pool_rows(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                                          const float* __restrict__ pe, int64_t b, int h, int x, int hkv,
+                                          int dh, int l, int d, double& acc_k, double& acc_v) {
+  for (int o0 = 0; o0 < l; o0 += 8) {
+    float kk[8], vv[8], pp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int o = o0 + u;
+      kk[u] = vv[u] = pp[u] = 0.f;
+      if (o < l) {
+        const int64_t off = ((b * d + o) * hkv + h) * dh + x;
+        kk[u] = __bfloat162float(k[off]);
+        vv[u] = __bfloat162float(v[off]);
+        if (pe != nullptr) pp[u] = pe[o * dh + x];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (o0 + u < l) {
+        acc_k = __dadd_rn(acc_k, (double)kk[u]);
+        if (pe != nullptr) acc_k = __dadd_rn(acc_k, (double)pp[u]);
+        acc_v = __dadd_rn(acc_v, (double)vv[u]);
+      }
+    }
+  }
+}
+
 __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,
                                 const __nv_bfloat16* __restrict__ v, const float* __restrict__ pe,
                                 float* __restrict__ ck, __nv_bfloat16* __restrict__ ck16,
@@ -91,12 +121,7 @@ __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,
     fkr[r] = 0.f;
     if (x >= dh) continue;
     double acc_k = 0.0, acc_v = 0.0;
-    for (int o = 0; o < l; ++o) {
-      const int64_t off = ((b * d + o) * hkv + h) * dh + x;
-      acc_k = __dadd_rn(acc_k, (double)__bfloat162float(k[off]));
-      if (pe != nullptr) acc_k = __dadd_rn(acc_k, (double)pe[o * dh + x]);
-      acc_v = __dadd_rn(acc_v, (double)__bfloat162float(v[off]));
-    }
+    pool_rows(k, v, pe, b, h, x, hkv, dh, l, d, acc_k, acc_v);
     const float fk = (float)__dmul_rn(acc_k, inv_l);
     const float fv = (float)__dmul_rn(acc_v, inv_l);
     const int64_t o = (b * hkv + h) * dh + x;
@@ -127,12 +152,7 @@ __global__ void compress_layers_kernel(const __grid_constant__ CompressLayers c)
     fkr[r] = 0.f;
     if (x >= dh) continue;
     double acc_k = 0.0, acc_v = 0.0;
-    for (int o = 0; o < l; ++o) {
-      const int64_t off = ((b * d + o) * hkv + h) * dh + x;
-      acc_k = __dadd_rn(acc_k, (double)__bfloat162float(k[off]));
-      if (pe != nullptr) acc_k = __dadd_rn(acc_k, (double)pe[o * dh + x]);
-      acc_v = __dadd_rn(acc_v, (double)__bfloat162float(v[off]));
-    }
+    pool_rows(k, v, pe, b, h, x, hkv, dh, l, d, acc_k, acc_v);
     const float fk = (float)__dmul_rn(acc_k, inv_l);
     const float fv = (float)__dmul_rn(acc_v, inv_l);
     const int64_t o = (b * hkv + h) * dh + x;
