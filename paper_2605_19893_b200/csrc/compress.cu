@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "attend.h"
+#include "sm100.cuh"
 
 namespace specsv_b200 {
 namespace {
@@ -136,6 +137,7 @@ __global__ void compress_kernel(const __nv_bfloat16* __restrict__ k,
 // the blocks a commit completed, in every layer at once: grid (block, head,
 // layer); the same pooling as compress_kernel
 __global__ void compress_layers_kernel(const __grid_constant__ CompressLayers c) {
+  sm100::griddep_wait();  // (programmatic dependent launch) the committed rows are in
   const int j = blockIdx.z;
   if ((int64_t)blockIdx.x >= c.count[j]) return;
   const int64_t b = c.first[j] + blockIdx.x;
@@ -170,8 +172,16 @@ cudaError_t launch_compress_layers(const CompressLayers& c, int n_layers, int64_
                                    cudaStream_t stream) {
   if (n_layers <= 0 || max_count <= 0) return cudaSuccess;
   if (max_count > 65535) return cudaErrorInvalidValue;
-  compress_layers_kernel<<<dim3((unsigned)max_count, c.hkv, n_layers), c.dh < 256 ? c.dh : 256, 0,
-                           stream>>>(c);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)max_count, c.hkv, n_layers);
+  lc.blockDim = dim3(c.dh < 256 ? c.dh : 256);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&lc, compress_layers_kernel, c);
   return cudaGetLastError();
 }
 

@@ -16,6 +16,7 @@
 
 #include "attend.h"
 #include "policy.h"
+#include "sm100.cuh"
 #include "specsv_b200/draft_tree.h"
 
 namespace specsv_b200 {
@@ -95,6 +96,9 @@ struct CommitParams {
 // grid (accepted row, layer): one CTA copies one K row and one V row; 16-byte
 // coalesced loads and stores, one pass over 2 x Hkv x dh x 2 bytes
 __global__ void __launch_bounds__(128) commit_rows_kernel(const __grid_constant__ CommitParams p) {
+  // (launched with programmatic dependent launch: resident under the previous
+  // launch's tail, then in stream order for its inputs and the rows it writes)
+  sm100::griddep_wait();
   const int i = blockIdx.x, j = blockIdx.y;
   const int64_t src = (int64_t)p.slots[i] * p.units, dst = (p.rows[j] + i) * p.units;
   for (int u = threadIdx.x; u < p.units; u += blockDim.x) {
@@ -275,7 +279,16 @@ specsv_status specsv_commit_rows(const specsv_nsa_config* cfg, const specsv_laye
         p.tk[jj] = reinterpret_cast<const uint4*>(tree_k[j0 + jj]);
         p.tv[jj] = reinterpret_cast<const uint4*>(tree_v[j0 + jj]);
       }
-      commit_rows_kernel<<<dim3(n_accepted, p.n_layers), 128, 0, st>>>(p);
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(n_accepted, p.n_layers);
+      lc.blockDim = dim3(128);
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = pdl_enabled() ? 1 : 0;
+      cudaLaunchKernelEx(&lc, commit_rows_kernel, p);
       const cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) throw Error(SPECSV_ECUDA, std::string("commit launch: ") + cudaGetErrorString(e));
     }
