@@ -685,9 +685,13 @@ def run_ours(a, world: int, rank: int, local: int):
     done = [torch.cuda.Event(), torch.cuda.Event()]   # set b's readers (verify + commit) finished
     out_ready = torch.cuda.Event()
 
-    commits = [[TR.PreparedCommit(cfg, caches[r], [bset[r][j].tree_k for j in range(L)],
-                                  [bset[r][j].tree_v for j in range(L)], slots, pes[r])
-                for r in range(R)] if slots else [] for _, bset in sets_in]
+    # one commit call over every request's layers (the entry point takes a list
+    # of independent caches), per input set
+    commits = [[TR.PreparedCommit(cfg, [caches[r][j] for r in range(R) for j in range(L)],
+                                  [bset[r][j].tree_k for r in range(R) for j in range(L)],
+                                  [bset[r][j].tree_v for r in range(R) for j in range(L)], slots,
+                                  [pes[r] for r in range(R) for j in range(L)])]
+               if slots else [] for _, bset in sets_in]
     host_parts = {"copies": 0.0, "verify_calls": 0.0, "readback": 0.0, "commit": 0.0}
     host_role = {int(V.ROLE_REFRESH): 0.0, int(V.ROLE_REUSE): 0.0}
 
@@ -733,12 +737,13 @@ def run_ours(a, world: int, rank: int, local: int):
                 for r in range(R):
                     hout[r].copy_(outs[r][L - 1], non_blocking=True)
         tD = time.perf_counter()
-        for r, pc in enumerate(commits[b] if variant != "nocommit" else []):  # rows + positions advance
+        for pc in commits[b] if variant != "nocommit" else []:  # rows + positions advance
             pc.run(cur)
-            new_pos = np.array([caches[r][0].rows - 1 + i for i in range(nq)], np.int64)
-            for j in range(L):
-                batches[r][j].pos = new_pos
-                batches2[r][j].pos = new_pos
+            for r in range(R):
+                new_pos = np.array([caches[r][0].rows - 1 + i for i in range(nq)], np.int64)
+                for j in range(L):
+                    batches[r][j].pos = new_pos
+                    batches2[r][j].pos = new_pos
         done[b].record(cur)
         tE = time.perf_counter()
         host_parts["copies"] += tB - tA
