@@ -986,12 +986,20 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
       st_release_gpu(P.exit_cnt + 1, 0);
     }
     double* sc = R.contrib + (int64_t)slot * R.sel_pad;
-    for (int b = tid; b < avail; b += kThreads) {
-      sel[b] = __ldcg(sc + b) * inv;
-      sc[b] = 0.0;
-    }
     unsigned long long* bslot = reinterpret_cast<unsigned long long*>(R.cnt + kCntBound) + slot;
     const unsigned long long bb = __ldcg(bslot);
+    // the score row in one round trip: every load of this thread before any store
+    for (int b0 = tid; b0 < avail; b0 += 4 * kThreads) {
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = b0 + u * kThreads < avail ? __ldcg(sc + b0 + u * kThreads) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b0 + u * kThreads < avail) {
+          sel[b0 + u * kThreads] = x[u] * inv;
+          sc[b0 + u * kThreads] = 0.0;
+        }
+    }
     __syncthreads();
     stamp(P, 14);
     if (tid == 0) *bslot = 0ull;  // every atomicMax of this launch is in
