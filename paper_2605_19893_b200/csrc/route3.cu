@@ -923,7 +923,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     double* st = reinterpret_cast<double*>(smem);                // [nranges][48] den rows
     double* gs = last ? g : reinterpret_cast<double*>(smem + kTileBytes);  // this unit's g
     const double* src = R.den + (int64_t)(U.chunk * P.Hkv + U.kvh) * R.nranges * kN;
-    for (int e = tid; e < R.nranges * kN; e += kThreads) st[e] = __ldcg(src + e);
+    for (int e0 = tid; e0 < R.nranges * kN; e0 += 4 * kThreads) {  // loads first: one round trip
+      double x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = e0 + u * kThreads < R.nranges * kN ? __ldcg(src + e0 + u * kThreads) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e0 + u * kThreads < R.nranges * kN) st[e0 + u * kThreads] = x[u];
+    }
     if (!last) {
       const double* sp = R.gspill + (int64_t)U.lu * kR3MaxSpr * kGS;
       for (int e = tid; e < kR3MaxSpr * kGS; e += kThreads) gs[e] = __ldcg(sp + e);
