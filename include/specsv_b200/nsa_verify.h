@@ -34,13 +34,19 @@
  * -- and read its inputs (q, gates, the KV caches, the draft rows, on REUSE
  * the index sets) -- as soon as the kernel enqueued just before it has
  * triggered programmatic completion (griddepcontrol.launch_dependents), not
- * only once it has finished.  This library's own kernels trigger only after
- * their last write a later call reads (attend: after its output; routing:
- * before its index-set writes, which the attend launch of the same call
- * waits for).  Kernels that never trigger (ordinary CUDA/PyTorch kernels)
- * complete first, as usual.  A caller whose own producer kernel triggers
- * early, before writing a verify input, must not enqueue it directly before
- * a verify call -- or set SPECSV_NO_PDL=1, which turns the attribute off.
+ * only once it has finished.  This library's own kernels trigger before
+ * their last writes and every kernel of it waits (griddepcontrol.wait) for
+ * its predecessor's completion before writing anything a predecessor may
+ * still touch: routing triggers before its index-set writes, which the
+ * attend launch of the same call waits for; attend triggers after its tile
+ * loop, before its split merge and its OUTPUT writes.  So a verify call's
+ * inputs must not be the output of the verify call enqueued just before it
+ * (a kernel or event in between -- e.g. the next layer's projection --
+ * orders them as usual).  Kernels that never trigger (ordinary CUDA/PyTorch
+ * kernels) complete first, as usual.  A caller whose own producer kernel
+ * triggers early, before writing a verify input, must not enqueue it
+ * directly before a verify call -- or set SPECSV_NO_PDL=1, which turns the
+ * attribute off.
  */
 #ifndef SPECSV_B200_NSA_VERIFY_H
 #define SPECSV_B200_NSA_VERIFY_H

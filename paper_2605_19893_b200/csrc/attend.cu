@@ -887,6 +887,11 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
       J0 += T;
     }
     // ---- epilogue: partial (m, l, O = O_hi + O_lo) of this split -> workspace ----
+    // The previous launch triggers its dependents after its tile loop, so it
+    // may still be merging out of the workspace (and counters) this launch
+    // writes from here on: wait for it to complete.  Its completion implies
+    // its own predecessor's (it waited here too), so the chain is ordered.
+    griddep_wait();
     tc_fence_after();
     const int64_t unit = ((int64_t)chunk * p.Hkv + kvh) * S + split;  // partial slot
     float* ws_ml = p.ws + unit * (3 * kCols * 2);
@@ -1072,6 +1077,12 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
   }
 
   // ---- merge of the split partials (per-head barrier) + gated combine ----
+  // Every CTA past its tile loop: the next launch may start placing CTAs (its
+  // launch latency and prologue run under this merge).  It reads only its
+  // inputs before its own epilogue's wait (nsa_verify.h, programmatic
+  // dependent launch).  Debug bit 8 (256): trigger after the merge instead.
+  const bool late_trigger = (p.debug_flags & 256) != 0;
+  if (!late_trigger) griddep_launch();
   tc_fence_before();
   if (S > 1) {
     int* sync = reinterpret_cast<int*>(p.ws + p.ws_sync_offset) + 2 * (chunk * p.Hkv + kvh);
@@ -1147,9 +1158,7 @@ __device__ __forceinline__ void attend_cta(const AttendParams& p, const int spli
   }
   tc_fence_before();
   __syncthreads();
-  // every read of this launch's workspace partials is done: the next launch
-  // (which may reuse them) can start placing CTAs
-  griddep_launch();
+  if (late_trigger) griddep_launch();
   if (warp == kWarpTma) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
