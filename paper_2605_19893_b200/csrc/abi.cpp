@@ -100,10 +100,11 @@ int coresident_for_device() {
 int qc_size_for(const specsv_nsa_config& c);
 
 // split CTAs per (KV head, query chunk): all of them must be co-resident
-int splits_for(const specsv_nsa_config& c, int32_t nq, int n_heads) {
+int splits_for(const specsv_nsa_config& c, int32_t nq, int n_heads, int cap_override = 0) {
   const int nchunks = (nq + qc_size_for(c) - 1) / qc_size_for(c);
   const int groups = n_heads * nchunks;
-  const int cap = debug_env().attend_splits > 0 ? std::min(18, debug_env().attend_splits) : 18;
+  int cap = debug_env().attend_splits > 0 ? std::min(18, debug_env().attend_splits) : 18;
+  if (cap_override > 0) cap = std::min(cap, cap_override);
   return std::max(1, std::min(cap, coresident_for_device() / groups));
 }
 
@@ -571,8 +572,9 @@ void set_attend_ws(AttendParams& p, const Layout& L, char* ws, int r, int chunks
 }
 
 void run_attend(const specsv_nsa_config& c, const specsv_layer_kv& kv, const specsv_verify_args& a,
-                void* ws, size_t ws_bytes, cudaStream_t stream) {
-  const int S = splits_for(c, a.n_queries, head_count(c, a));
+                void* ws, size_t ws_bytes, cudaStream_t stream, bool after_route = false) {
+  const int S = splits_for(c, a.n_queries, head_count(c, a),
+                           after_route ? debug_env().attend_splits_refresh : 0);
   const Layout L = layout_for(c, a.n_queries, kv.rows);
   if (ws == nullptr || ws_bytes < L.total) throw Error(SPECSV_ENOSPACE, "workspace too small");
   AttendParams p;
@@ -696,8 +698,9 @@ specsv_status specsv_nsa_verify(const specsv_nsa_config* cfg, const specsv_layer
     check_build_limits(*cfg);
     validate_args(*cfg, *kv, *args);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (args->role == SPECSV_ROLE_REFRESH) run_route(*cfg, *kv, *args, ws, ws_bytes, s);
-    run_attend(*cfg, *kv, *args, ws, ws_bytes, s);
+    const bool refresh = args->role == SPECSV_ROLE_REFRESH;
+    if (refresh) run_route(*cfg, *kv, *args, ws, ws_bytes, s);
+    run_attend(*cfg, *kv, *args, ws, ws_bytes, s, refresh);
   });
 }
 

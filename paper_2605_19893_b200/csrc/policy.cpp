@@ -45,6 +45,7 @@ void refresh_debug_env() {
     else if (name == "ROUTE3_DEBUG") e.route3_debug = std::atoi(val);
     else if (name == "ATTEND_DEBUG") e.attend_debug = std::atoi(val);
     else if (name == "ATTEND_SPLITS") e.attend_splits = std::atoi(val);
+    else if (name == "ATTEND_SPLITS_REFRESH") e.attend_splits_refresh = std::atoi(val);
   }
   g_env = e;
 }

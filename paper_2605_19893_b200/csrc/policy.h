@@ -29,6 +29,7 @@ struct DebugEnv {
   int route3_debug = 0;         // SPECSV_ROUTE3_DEBUG
   int attend_debug = 0;         // SPECSV_ATTEND_DEBUG
   int attend_splits = 0;        // SPECSV_ATTEND_SPLITS=k: at most k split CTAs per head (timing)
+  int attend_splits_refresh = 0;  // SPECSV_ATTEND_SPLITS_REFRESH=k: the same, refresh layers only
 };
 const DebugEnv& debug_env();
 void refresh_debug_env();
