@@ -99,6 +99,7 @@ constexpr uint32_t kOffMisc = kOffG + kR3MaxSpr * kGS * 8;
 static_assert(kTB * kES * 8 == kTileBytes, "e values: tile t's rows alias tile t's planes");
 static_assert(kQsSlice % 1024 == 0, "SW128 atoms");
 static_assert((size_t)kMaxAvail * 12 + 4 * kDh * 8 + 66 * 4 <= 2 * kTileBytes, "Top-n arrays alias the planes");
+static_assert((size_t)kMaxAvail * 12 + 2048 * 8 <= 2 * kTileBytes, "survivor scores after sel and surv");
 
 struct Misc {
   uint64_t tma_full[2], mma_done[2], ex_full[3];
@@ -378,8 +379,18 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
 // then the `want` best others into m.picks.  Also records the last pick's
 // score (m.sk) and the best non-pick's (m.sk1, -inf if none) and sets
 // m.certified = the two are separated by more than eps (relative).
-__device__ void select_topn(const double* sel, int* surv, int avail, int n, double eps, Misc& m,
-                            unsigned long long* tr = nullptr) {
+// GL lanes per group (2 candidates each at avail <= 2 x kThreads): groups of
+// 8 lanes rank 64 group bests (8 comparisons per thread; groups of 4: 128
+// bests, 32 comparisons).  want <= n - 1 <= 63 < 64 groups (check_build_limits).
+// The survivors' scores are copied next to their ids (surv_s, up to
+// kSurvCap), so the exact ranking reads two independent arrays instead of
+// sel[surv[o]]; with COMPACT false it reads sel[surv[o]] (the earlier form).
+constexpr int kSurvCap = 2048;
+template <int GL, bool COMPACT>
+__device__ void select_topn_impl(const double* sel, int* surv, double* surv_s, int avail, int n, double eps,
+                                 Misc& m, unsigned long long* tr) {
+  constexpr int kGroups = kThreads / GL;
+  static_assert(kGroups <= kTopnGroups, "group bests");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long c0 = clock64();
   const int f1 = avail - 2 > 0 ? avail - 2 : -1;
@@ -412,7 +423,7 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
       }
     }
 #pragma unroll
-    for (int off = 1; off <= 2; off <<= 1) {
+    for (int off = 1; off < GL; off <<= 1) {
       const double os = __shfl_xor_sync(0xffffffffu, bs, off);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (ranks_before(os, oi, bs, bi)) {
@@ -420,22 +431,23 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
         bi = oi;
       }
     }
-    if ((lane & 3) == 0) {
-      m.gbest_s[tid >> 2] = bs;
-      m.gbest_i[tid >> 2] = bi;
+    if ((lane & (GL - 1)) == 0) {
+      m.gbest_s[tid / GL] = bs;
+      m.gbest_i[tid / GL] = bi;
     }
     __syncthreads();
     {  // 2. the group maximum of rank `want`: at least want + 1 candidates rank at or
        //    before it, so the survivors hold the picks AND the best non-pick
-      const int g = tid >> 2, part = tid & 3;
+      const int g = tid / GL, part = tid & (GL - 1);
       const double ms = m.gbest_s[g];
       const int mi = m.gbest_i[g];
       int rank = 0;
-      for (int o = part; o < kTopnGroups; o += 4)
+#pragma unroll
+      for (int o = part; o < kGroups; o += GL)
         rank += ranks_before(m.gbest_s[o], m.gbest_i[o], ms, mi) ? 1 : 0;
-      rank += __shfl_xor_sync(0xffffffffu, rank, 1);
-      rank += __shfl_xor_sync(0xffffffffu, rank, 2);
-      if (part == 0 && want < kTopnGroups && rank == want && ms != -INFINITY) {
+#pragma unroll
+      for (int off = 1; off < GL; off <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, off);
+      if (part == 0 && want < kGroups && rank == want && ms != -INFINITY) {
         m.lb_s = ms;
         m.lb_i = mi;
       }
@@ -446,21 +458,38 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
     const int li = m.lb_i;
     for (int b = tid; b < avail; b += kThreads) {
       double sc;
-      if (cand(b, sc) && (ranks_before(sc, b, ls, li) || (sc == ls && b == li))) surv[atomicAdd(&m.nsurv, 1)] = b;
+      if (cand(b, sc) && (ranks_before(sc, b, ls, li) || (sc == ls && b == li))) {
+        const int slot = atomicAdd(&m.nsurv, 1);
+        surv[slot] = b;
+        if (COMPACT && slot < kSurvCap) surv_s[slot] = sc;
+      }
     }
     __syncthreads();
     const int ns = m.nsurv;  // 4. exact ranks among the survivors
-    for (int k = tid; k < ns; k += kThreads) {
-      const int b = surv[k];
-      const double sb = sel[b];
-      int rank = 0;
-      for (int o = 0; o < ns; ++o) {
-        const int c = surv[o];
-        rank += ranks_before(sel[c], c, sb, b) ? 1 : 0;
+    if (COMPACT && ns <= kSurvCap) {
+      for (int k = tid; k < ns; k += kThreads) {
+        const int b = surv[k];
+        const double sb = surv_s[k];
+        int rank = 0;
+#pragma unroll 4
+        for (int o = 0; o < ns; ++o) rank += ranks_before(surv_s[o], surv[o], sb, b) ? 1 : 0;
+        if (rank < want) m.picks[nforced + rank] = b;
+        if (rank == want - 1) m.sk = sb;
+        if (rank == want) m.sk1 = sb;
       }
-      if (rank < want) m.picks[nforced + rank] = b;
-      if (rank == want - 1) m.sk = sb;
-      if (rank == want) m.sk1 = sb;
+    } else {
+      for (int k = tid; k < ns; k += kThreads) {
+        const int b = surv[k];
+        const double sb = sel[b];
+        int rank = 0;
+        for (int o = 0; o < ns; ++o) {
+          const int c = surv[o];
+          rank += ranks_before(sel[c], c, sb, b) ? 1 : 0;
+        }
+        if (rank < want) m.picks[nforced + rank] = b;
+        if (rank == want - 1) m.sk = sb;
+        if (rank == want) m.sk1 = sb;
+      }
     }
     __syncthreads();
     if (ns <= want && ncand > want) {  // 5. (a survivor set without a non-pick: the best non-survivor)
@@ -485,6 +514,16 @@ __device__ void select_topn(const double* sel, int* surv, int avail, int n, doub
     m.certified = (want <= 0 || ncand <= want || b == -INFINITY || (a - b) > eps * (a + b)) ? 1 : 0;
   }
   __syncthreads();
+}
+
+// route3 debug bit 5 (32): the earlier form (groups of 4 lanes, sel[surv[o]])
+__device__ __forceinline__ void select_topn(const double* sel, int* surv, int avail, int n, double eps, Misc& m,
+                                            int debug, unsigned long long* tr = nullptr) {
+  double* surv_s = const_cast<double*>(sel) + 12 * kMaxAvail / 8;  // after sel and surv
+  if (debug & 32)
+    select_topn_impl<4, false>(sel, surv, surv_s, avail, n, eps, m, tr);
+  else
+    select_topn_impl<8, true>(sel, surv, surv_s, avail, n, eps, m, tr);
 }
 
 // the selected row, ascending (a rank-and-scatter over distinct block ids)
@@ -1016,21 +1055,21 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const double eps = 1.5 * 2.0 * 0.6931471805599453 * delta + 2e-10;
 #ifdef SPECSV_TRACE_TILES
     const long long c0 = clock64();
-    select_topn(sel, surv, avail, P.n, eps, m,
+    select_topn(sel, surv, avail, P.n, eps, m, P.debug,
                 P.trace != nullptr ? P.trace + kRouteTraceBase + blockIdx.x * 16 : nullptr);
     stamp(P, 15);
     if (P.trace != nullptr && tid == 0) P.trace[kRouteTraceBase + blockIdx.x * 16 + 12] = clock64() - c0;
     if (P.debug & 1) {  // diagnostics: the selection again (warm instruction cache)
-      select_topn(sel, surv, avail, P.n, eps, m);
+      select_topn(sel, surv, avail, P.n, eps, m, P.debug);
       stamp(P, 13);
     }
 #else
-    select_topn(sel, surv, avail, P.n, eps, m);
+    select_topn(sel, surv, avail, P.n, eps, m, P.debug);
 #endif
     if (flagged || !m.certified || P.force_exact) {
       if (tid == 0 && P.fallbacks != nullptr) atomicAdd(P.fallbacks, 1);
       exact_scores(P, R, slot, sel, smem, m, ex_seq);
-      select_topn(sel, surv, avail, P.n, 0.0, m);
+      select_topn(sel, surv, avail, P.n, 0.0, m, P.debug);
     }
     const int q = R.slot_q[slot];
     write_row(m, m, avail, P.n, R.idx + (int64_t)q * P.n, R.idx_count + q, R.idx_forced + q);
