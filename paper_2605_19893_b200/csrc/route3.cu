@@ -997,7 +997,14 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     if (tid == 0) red_add_release_gpu(&R.cnt[kCntTop + U.chunk], 1);
   }
   stamp(P, 6);
-  if (tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt, 1) == nctas - 1) {
+  const int tasks = P.task_start[P.n_req];
+  // The denominator counters are reset once no unit polls them: by the last
+  // Top-n task through its wait below (every unit of every chunk has then
+  // published its shares, after its denominator wait), so no CTA spends an
+  // atomic round trip here.  Without tasks (or debug bit 6 (64)): by the
+  // last CTA through phase 2.
+  const bool den_by_tasks = tasks > 0 && !(P.debug & 64);
+  if (!den_by_tasks && tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt, 1) == nctas - 1) {
     // the last CTA through phase 2: no unit polls a denominator counter any more
     for (int r = 0; r < P.n_req; ++r)
       for (int i = 0; i < P.req[r].nchunks * P.Hkv; ++i) P.req[r].cnt[kCntDen + i] = 0;
@@ -1006,7 +1013,6 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
 
   // ================= phase 3: one Top-n task per routed slot =================
   griddep_launch();  // the next launch may start placing CTAs as this grid drains
-  const int tasks = P.task_start[P.n_req];
   double* sel = reinterpret_cast<double*>(smem);                          // [kMaxAvail]
   int* surv = reinterpret_cast<int*>(smem + 8 * kMaxAvail);                // [kMaxAvail]
   int ex_seq = 0;  // exact-path chunks loaded by this CTA so far (the stage barriers' phases)
@@ -1027,8 +1033,12 @@ __global__ void __launch_bounds__(kThreads, 1) route3_kernel(const __grid_consta
     const double inv = 1.0 / (double)P.Hq;
     if (tid == 0 && atom_add_acq_rel_gpu(P.exit_cnt + 1, 1) == tasks - 1) {
       // the last task through its wait: no task polls a chunk counter any more
-      for (int rr = 0; rr < P.n_req; ++rr)
+      // (nor any unit a denominator counter: every chunk has a task)
+      for (int rr = 0; rr < P.n_req; ++rr) {
         for (int i = 0; i < P.req[rr].nchunks; ++i) P.req[rr].cnt[kCntTop + i] = 0;
+        if (den_by_tasks)
+          for (int i = 0; i < P.req[rr].nchunks * P.Hkv; ++i) P.req[rr].cnt[kCntDen + i] = 0;
+      }
       st_release_gpu(P.exit_cnt + 1, 0);
     }
     double* sc = R.contrib + (int64_t)slot * R.sel_pad;
