@@ -137,7 +137,9 @@ typedef struct specsv_verify_args {
   int32_t* idx;               /* device [nq][n] ascending, -1 padded.  REFRESH: written.
                                  REUSE: read (the source layer's sets, unclamped) */
   int32_t* idx_count;         /* device [nq]; -1 = no set (approx non-representatives) */
-  uint32_t* idx_forced;       /* device [nq]; bit i = idx[q][i] is a forced block */
+  uint32_t* idx_forced;       /* device [nq]; bit i = idx[q][i] is a forced block (i < 32:
+                                 with n > 32 later positions are not flagged; the attend
+                                 path does not read the mask) */
   float* out;                 /* device fp32 [nq][Hq][dh] gated-combine output */
   int32_t kv_head_begin;      /* KV-head group sharding: attend only KV heads
                                  [kv_head_begin, kv_head_begin + kv_head_count) and write

@@ -380,8 +380,10 @@ __device__ __forceinline__ bool ranks_before(double sa, int ia, double sb, int i
 // score (m.sk) and the best non-pick's (m.sk1, -inf if none) and sets
 // m.certified = the two are separated by more than eps (relative).
 // GL lanes per group (2 candidates each at avail <= 2 x kThreads): groups of
-// 8 lanes rank 64 group bests (8 comparisons per thread; groups of 4: 128
-// bests, 32 comparisons).  want <= n - 1 <= 63 < 64 groups (check_build_limits).
+// 16 lanes rank 32 group bests (2 comparisons per thread), groups of 8 rank
+// 64 (8 comparisons; groups of 4: 128 bests, 32 comparisons).  The bound needs
+// want < groups: want <= n - 1, so 16 lanes for n <= 32 and 8 lanes up to the
+// build limit n <= 64 (check_build_limits).
 // The survivors' scores are copied next to their ids (surv_s, up to
 // kSurvCap), so the exact ranking reads two independent arrays instead of
 // sel[surv[o]]; with COMPACT false it reads sel[surv[o]] (the earlier form).
@@ -522,7 +524,9 @@ __device__ __forceinline__ void select_topn(const double* sel, int* surv, int av
   double* surv_s = const_cast<double*>(sel) + 12 * kMaxAvail / 8;  // after sel and surv
   if (debug & 32)
     select_topn_impl<4, false>(sel, surv, surv_s, avail, n, eps, m, tr);
-  else
+  else if (n <= 32)  // want <= n - 1 < 32 groups of 16 lanes
+    select_topn_impl<16, true>(sel, surv, surv_s, avail, n, eps, m, tr);
+  else  // want <= 63 < 64 groups of 8 lanes
     select_topn_impl<8, true>(sel, surv, surv_s, avail, n, eps, m, tr);
 }
 
